@@ -1,0 +1,134 @@
+"""Byte simulator and sequential definition (test infrastructure; oracle).
+
+simulate(): executes an instruction log in iid order — a topological order,
+so sequential execution trivially satisfies every dependency (P:L518,
+§4.1) — over per-allocation arrays (R15: an allocation is a dense row-major
+array over its box; a copy moves exactly its region's bytes; a kernel
+addresses its bound allocations at buffer coordinates).  Fresh allocations
+are filled with a garbage pattern so a missing coherence copy shows up.
+
+sequential(): the plain definition the instruction graph must reproduce
+(semantic transparency): every task applied, in submission
+order, to ONE global array per buffer over the whole kernel range — no
+split, no allocations, no copies.
+"""
+
+import numpy as np
+
+from . import geometry as g
+from .kernels import Acc, run_kernel
+from .program import apply_mapper
+from .scheduler import HOST_AID, USER_AID, _norm_mapper
+
+GARBAGE = np.uint32(0x7FC00BAD)      # a float32 NaN payload; never produced by a kernel
+
+
+def _words(elem_size):
+    assert elem_size % 4 == 0, "the simulator models 4-byte words"
+    return elem_size // 4
+
+
+def host_array(data, extent, elem_size):
+    sh = g.shape(extent) + (_words(elem_size),)
+    a = np.ascontiguousarray(data).reshape(-1).view(np.uint32)
+    return a.reshape(sh).copy()
+
+
+def _tobox(jb):
+    return (tuple(jb[0]), tuple(jb[1]))
+
+
+def _view(arr, abox, bx):
+    b = abox[0]
+    return arr[bx[0][0] - b[0]:bx[1][0] - b[0], bx[0][1] - b[1]:bx[1][1] - b[1],
+               bx[0][2] - b[2]:bx[1][2] - b[2]]
+
+
+def simulate(rt):
+    """Run rt.log over arrays.  Returns {readback id: uint32 array}."""
+    meta = rt.buf_meta
+    arrays = {}
+    boxes = {}
+    host = {}
+    for bid, m in meta.items():
+        if m["host_init"] is not None:
+            host[bid] = host_array(m["host_init"], m["extent"], m["elem_size"])
+    results = {}
+    for rb, (bid, rbox) in rt.readbacks.items():
+        results[rb] = np.full(g.shape(rbox) + (_words(meta[bid]["elem_size"]),), GARBAGE, dtype=np.uint32)
+    for rec in rt.log:
+        k = rec["kind"]
+        if k == "alloc":
+            bx = _tobox(rec["box"])
+            words = _words(meta[rec["buffer"]]["elem_size"])
+            arrays[rec["aid"]] = np.full(g.shape(bx) + (words,), GARBAGE, dtype=np.uint32)
+            boxes[rec["aid"]] = bx
+        elif k == "free":
+            del arrays[rec["aid"]]
+        elif k == "copy":
+            bid = rec["buffer"]
+            if rec["src_aid"] == HOST_AID:
+                src, sbox = host[bid], meta[bid]["extent"]
+            else:
+                src, sbox = arrays[rec["src_aid"]], boxes[rec["src_aid"]]
+            if rec["dst_aid"] == USER_AID:
+                dst, dbox = results[rec["readback"]], rt.readbacks[rec["readback"]][1]
+            else:
+                dst, dbox = arrays[rec["dst_aid"]], boxes[rec["dst_aid"]]
+            for jb in rec["region"]:
+                bx = _tobox(jb)
+                _view(dst, dbox, bx)[...] = _view(src, sbox, bx)
+        elif k == "kernel":
+            spec = rt.tasks[rec["task"]]
+            chunk = _tobox(rec["chunk"])
+            bxs, accs = [], []
+            for (bid, mode, mapper), aid in zip(spec["accesses"], rec["bindings"]):
+                ext = meta[bid]["extent"]
+                bxs.append(apply_mapper(mapper, chunk, ext))
+                accs.append(Acc(arrays[aid], boxes[aid], ext) if aid > 0 else None)
+            run_kernel(spec, bxs, accs)
+    return results
+
+
+def sequential(program):
+    """Apply the program's tasks in order to one global array per buffer.
+    Returns ({readback index: uint32 array}, {readback index: bool mask of
+    defined elements})."""
+    bufs, defined, meta = [], [], []
+    for b in program["buffers"]:
+        ext = g.box([0] * b["dims"], list(b["extent"]))
+        words = _words(b["elem_size"])
+        meta.append(ext)
+        if b.get("host_init") is not None:
+            bufs.append(host_array(b["host_init"], ext, b["elem_size"]))
+            defined.append(np.ones(g.shape(ext), dtype=bool))
+        else:
+            bufs.append(np.full(g.shape(ext) + (words,), GARBAGE, dtype=np.uint32))
+            defined.append(np.zeros(g.shape(ext), dtype=bool))
+    results, masks = {}, {}
+    rb = 0
+    for op in program["ops"]:
+        if op[0] == "task":
+            spec = dict(op[1])
+            spec["accesses"] = [(bid, mode, _norm_mapper(mp)) for (bid, mode, mp) in spec["accesses"]]
+            rng = g.box(spec["range"][0], spec["range"][1])
+            if g.is_empty(rng):
+                continue
+            bxs, accs = [], []
+            ok = True
+            for (bid, mode, mapper) in spec["accesses"]:
+                bx = apply_mapper(mapper, rng, meta[bid])
+                bxs.append(bx)
+                accs.append(Acc(bufs[bid], meta[bid], meta[bid]))
+                if mode in ("read", "read_write") and not g.is_empty(bx):
+                    ok = ok and bool(_view(defined[bid], meta[bid], bx).all())
+            run_kernel(spec, bxs, accs)
+            for (bid, mode, mapper), bx in zip(spec["accesses"], bxs):
+                if mode in ("write", "read_write") and not g.is_empty(bx):
+                    _view(defined[bid], meta[bid], bx)[...] = ok
+        elif op[0] == "read":
+            bid, rbox = op[1], g.box(op[2][0], op[2][1])
+            results[rb] = _view(bufs[bid], meta[bid], rbox).copy()
+            masks[rb] = _view(defined[bid], meta[bid], rbox).copy()
+            rb += 1
+    return results, masks
