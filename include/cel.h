@@ -1,0 +1,208 @@
+/*
+ * cel.h — C-ABI of the B200-native Celerity instruction-graph coherence path
+ * (Knorr et al., "Concurrent Scheduling of High-Level Parallel Programs on
+ * Multi-GPU Systems", arXiv 2503.10516).
+ *
+ * The calls follow the paper's user model (§2): a
+ * queue to which tasks are submitted; each task launches one kernel over an
+ * index space and declares accesses to virtual buffers through range mappers;
+ * epochs synchronise with the caller.  Behind the calls the library
+ * splits each task over the devices (§3.1), evaluates the range
+ * mappers, diffs the per-device read/write regions against the buffers'
+ * up-to-date / original-producer region maps (§3.3), generates
+ * alloc / resize-copy / copy / free / kernel / horizon / epoch instructions
+ * (Table 1; §3.2; §3.5) with the lookahead
+ * of §4.3, and executes them on B200 (sm_100a): copies by SM
+ * kernels (peer pushes over NVLink/NVSwitch), kernels on per-device streams.
+ *
+ * Conventions
+ *   - Boxes are half-open [min, max) in 3 dimensions; dimensions beyond a
+ *     buffer's `dims` are [0, 1).  Dimension 0 is the slowest (row-major).
+ *   - Buffers are dense row-major arrays of `elem_size`-byte elements.
+ *   - Status: 0 = OK; > 0 = warning (the call took effect); < 0 = error (the
+ *     call had no effect, except CEL_E_CUDA / CEL_E_OOM during execution,
+ *     which poison the runtime: every later call except cel_runtime_destroy
+ *     returns the same error).  cel_last_error() gives a thread-local message.
+ *   - All calls on one runtime come from one thread (Celerity's single user
+ *     thread).  Pointers passed in are only read during the call
+ *     unless stated otherwise.
+ */
+#ifndef CEL_H
+#define CEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CEL_OK 0
+#define CEL_W_UNINIT_READ 1          /* §4.4 uninitialised-read warning */
+#define CEL_E_INVALID (-1)           /* malformed argument */
+#define CEL_E_OUT_OF_BOUNDS (-2)     /* one_to_one chunk / fixed / remap box outside the buffer */
+#define CEL_E_OVERLAPPING_WRITE (-3) /* §4.4 overlapping-write error */
+#define CEL_E_OOM (-4)               /* device arena or pinned host memory exhausted (sticky) */
+#define CEL_E_CUDA (-5)              /* CUDA error, or no GPU (sticky) */
+#define CEL_E_NCCL (-6)
+#define CEL_E_STATE (-7)             /* call not valid in this state (e.g. after shutdown) */
+
+typedef struct cel_runtime cel_runtime; /* opaque: owns all device memory, streams, events */
+typedef uint32_t cel_buffer;
+typedef uint64_t cel_task;
+
+typedef struct {
+    uint64_t min[3];
+    uint64_t max[3];
+} cel_box;
+
+/* Range mappers (R5 of DESIGN.md):
+ *   ONE_TO_ONE   buffer region = kernel chunk (error if outside the buffer)
+ *   NEIGHBORHOOD chunk inflated by border[d] per dim, clamped to the buffer
+ *   ALL          the whole buffer ("always spans the entire buffer range")
+ *   FIXED        the box `fixed` regardless of the chunk
+ *   REMAP        buffer dim k takes the chunk's interval of kernel dim
+ *                from_kernel_dim[k], or fixed's interval if that is -1
+ *                (e.g. RSim "append row t": fixed=[t,t+1)x., map={-1,0,-1}) */
+typedef enum { CEL_ONE_TO_ONE = 0, CEL_NEIGHBORHOOD = 1, CEL_ALL = 2, CEL_FIXED = 3, CEL_REMAP = 4 } cel_mapper_kind;
+
+typedef struct {
+    int32_t kind;              /* cel_mapper_kind */
+    uint32_t border[3];        /* NEIGHBORHOOD */
+    cel_box fixed;             /* FIXED, REMAP */
+    int32_t from_kernel_dim[3];/* REMAP */
+} cel_range_mapper;
+
+typedef enum { CEL_READ = 1, CEL_WRITE = 2, CEL_READ_WRITE = 3 } cel_mode;
+typedef enum { CEL_SPLIT_1D = 0, CEL_SPLIT_2D = 1 } cel_split; /* §3.1 split along dim 0, or dims 0 and 1 */
+
+typedef struct {
+    cel_buffer buf;
+    int32_t mode;              /* cel_mode */
+    cel_range_mapper map;
+} cel_access;
+
+/* Built-in sm_100a device kernels (synthetic workloads); the
+ * accessor order each expects is given in brackets.  CALLBACK calls `fn`. */
+typedef enum {
+    CEL_K_FILL_HASH = 0,   /* [write]               word w of element x = init(seed, lin(x)*words+w) */
+    CEL_K_FILL_CONST = 1,  /* [write]               every 32-bit word = value */
+    CEL_K_STENCIL3 = 2,    /* [read nbhd(1), write]  1-D 3-point (Listing 5 shape) */
+    CEL_K_WAVE5 = 3,       /* [read u nbhd(1,1), read_write up] WaveSim 5-point leapfrog */
+    CEL_K_JACOBI7 = 4,     /* [read nbhd(1,1,1), write] 3-D 7-point */
+    CEL_K_NBODY_STEP = 5,  /* [read P all, read_write V] float4 bodies */
+    CEL_K_NBODY_UPDATE = 6,/* [read V, read_write P] */
+    CEL_K_RSIM_ROW = 7,    /* [read fixed rows [0,t), write remap row t] */
+    CEL_K_PROBE = 8,       /* u32 coherence probe, any accessors, one written */
+    CEL_K_CALLBACK = 9
+} cel_kernel;
+
+/* What a kernel sees of one accessor: its backing allocation. */
+typedef struct {
+    void* base;                /* device pointer of the allocation (element alloc_box.min) */
+    cel_box alloc_box;         /* buffer box the allocation covers, dense row-major */
+    uint32_t elem_size;
+} cel_accessor;
+
+/* User kernel: called on the scheduling thread with the device's stream; it
+ * must only enqueue work on `cuda_stream` (a cudaStream_t). */
+typedef void (*cel_kernel_fn)(void* user, int device, const cel_box* chunk, const cel_accessor* acc, int n_acc,
+                              void* cuda_stream);
+
+typedef struct {
+    uint64_t seed;             /* FILL_HASH */
+    float value;               /* FILL_CONST */
+    uint32_t t;                /* RSIM_ROW: row index */
+    uint32_t salt;             /* PROBE */
+} cel_kernel_params;
+
+typedef struct {
+    int32_t dims;              /* kernel index space dimensionality 1..3 */
+    cel_box range;             /* kernel index space */
+    int32_t split;             /* cel_split */
+    int32_t kernel;            /* cel_kernel */
+    cel_kernel_params params;
+    cel_kernel_fn fn;          /* CALLBACK only; must outlive the task */
+    void* fn_user;
+    const cel_access* acc;     /* n_acc accessors, copied during the call */
+    int32_t n_acc;
+} cel_task_desc;
+
+typedef struct {
+    const int* cuda_devices;   /* physical CUDA device of each virtual device; repeats allowed
+                                  (several virtual devices on one GPU); NULL = 0..n_devices-1 */
+    int32_t n_devices;         /* G: devices the work is split over */
+    int32_t execute;           /* 0 = generate the instruction graph only (no GPU touched) */
+    int32_t lookahead;         /* 0 none, 1 auto (default), 2 infinite */
+    int32_t horizon_step;      /* critical-path horizon step (R7), default 4 */
+    int32_t checks;            /* §4.4 checks (uninitialised read, overlapping write) */
+    const char* instr_log_path;/* JSONL instruction log (one record per instruction) or NULL */
+    uint64_t arena_bytes;      /* device memory reserved per device; 0 = 16 GiB */
+    int32_t rank;              /* multi-process: this process's rank; device `rank` is its own */
+    int32_t world;             /* multi-process: number of processes (= n_devices), 1 = single process */
+} cel_config;
+
+typedef struct {
+    uint64_t n_alloc, n_free, n_copy, n_kernel, n_horizon, n_epoch;
+    uint64_t copies_resize, copies_coherence, copies_readback;
+    uint64_t bytes_resize, bytes_coherence, bytes_readback, bytes_d2d_peer;
+    uint64_t alloc_bytes_peak;
+    uint64_t flushes;          /* lookahead queue flushes */
+    uint64_t kernel_launches;  /* CUDA kernels launched by this process (workload + copy) */
+    uint64_t copy_launches, memcpy_calls, event_waits, remote_waits, signals, host_syncs;
+    uint64_t gen_ns;           /* host time spent in scheduling + issue */
+} cel_stats;
+
+/* Create a runtime.  With execute != 0 every device reserves arena_bytes of
+ * device memory and gets its own streams; peer access is enabled between
+ * distinct GPUs.  Fails with CEL_E_CUDA if no GPU is visible. */
+int cel_runtime_create(const cel_config* cfg, cel_runtime** out);
+
+/* Multi-process (world > 1, one process per GPU): export this rank's arena
+ * handle (cel_ipc_blob_size() bytes into blob), import every other rank's,
+ * then cel_ipc_connect.  Copies into another rank's memory are pushed by SM
+ * stores over NVLink; cross-process dependencies are flags in GPU memory. */
+size_t cel_ipc_blob_size(void);
+int cel_ipc_export(cel_runtime* rt, void* blob);
+int cel_ipc_import(cel_runtime* rt, int32_t rank, const void* blob);
+
+/* Virtual buffer: only the parts the devices access are ever
+ * allocated.  host_init (nullable) holds extent[0]*..*extent[dims-1]*elem_size
+ * bytes and is copied before the call returns. */
+int cel_buffer_create(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
+                      const void* host_init, cel_buffer* out);
+
+/* Submit a task: returns after its instructions are generated and enqueued
+ * (asynchronous).  >0: uninitialised-read warning; <0: rejected, no effect. */
+int cel_task_submit(cel_runtime* rt, const cel_task_desc* desc, cel_task* out);
+
+/* Epoch: flush the lookahead queue, block until all work is done. */
+int cel_wait(cel_runtime* rt);
+
+/* Read back `box` of a buffer into host_dst (dense over box): coherence copies
+ * to host followed by an epoch; blocking.  Elements never written and not
+ * host-initialised are left untouched.  Multi-process: only the elements
+ * whose up-to-date copy lives on this rank's device are written. */
+int cel_buffer_read(cel_runtime* rt, cel_buffer buf, const cel_box* box, void* host_dst);
+
+/* Drop the buffer: its allocations are freed once the last user has finished. */
+int cel_buffer_destroy(cel_runtime* rt, cel_buffer buf);
+
+int cel_stats_get(cel_runtime* rt, cel_stats* out);
+
+/* Device-time profile of the kernels this process launched, measured with
+ * CUDA events on the launching streams: ms[k], count[k] for k = cel_kernel
+ * kinds 0..9 and k = 10 for the copy kernel.  n = array length (11). */
+int cel_profile_enable(cel_runtime* rt, int32_t on);
+int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n);
+
+/* Shutdown epoch, free everything. */
+int cel_runtime_destroy(cel_runtime* rt);
+
+const char* cel_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CEL_H */

@@ -1,0 +1,277 @@
+// C-ABI (include/cel.h) over the scheduler and executor.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/cel.h"
+#include "exec.hpp"
+#include "sched.hpp"
+
+using namespace cel;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int rc, const std::string& msg) {
+    g_err = msg;
+    return rc;
+}
+
+Box to_box(const cel_box& b) {
+    int64_t lo[3], hi[3];
+    for (int d = 0; d < 3; ++d) {
+        lo[d] = int64_t(b.min[d]);
+        hi[d] = int64_t(b.max[d]);
+    }
+    return Box::make(lo, hi);
+}
+
+uint64_t now_ns() {
+    return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now().time_since_epoch())
+                        .count());
+}
+}  // namespace
+
+struct cel_runtime {
+    cel_config cfg;
+    FILE* log = nullptr;
+    std::unique_ptr<Executor> exec;
+    std::unique_ptr<Scheduler> sched;
+    uint64_t gen_ns = 0;
+    int poisoned = 0;
+    bool destroyed = false;
+};
+
+namespace {
+int check_poison(cel_runtime* rt) {
+    if (!rt) return fail(CEL_E_INVALID, "null runtime");
+    if (rt->poisoned) return rt->poisoned;
+    if (rt->exec && rt->exec->error()) {
+        rt->poisoned = rt->exec->error();
+        return fail(rt->poisoned, rt->exec->error_msg());
+    }
+    return 0;
+}
+int after(cel_runtime* rt, int rc) {
+    if (rt->exec && rt->exec->error()) {
+        rt->poisoned = rt->exec->error();
+        return fail(rt->poisoned, rt->exec->error_msg());
+    }
+    return rc;
+}
+}  // namespace
+
+extern "C" {
+
+const char* cel_last_error(void) { return g_err.c_str(); }
+
+size_t cel_ipc_blob_size(void) { return 64; }
+
+int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
+    if (!cfg || !out) return fail(CEL_E_INVALID, "null argument");
+    if (cfg->n_devices < 1 || cfg->n_devices > 30) return fail(CEL_E_INVALID, "n_devices must be 1..30");
+    if (cfg->lookahead < 0 || cfg->lookahead > 2) return fail(CEL_E_INVALID, "lookahead must be 0, 1 or 2");
+    const int world = cfg->world > 0 ? cfg->world : 1;
+    if (world > 1 && (cfg->rank < 0 || cfg->rank >= world || world != cfg->n_devices))
+        return fail(CEL_E_INVALID, "multi-process mode needs 0 <= rank < world == n_devices");
+    auto rt = std::make_unique<cel_runtime>();
+    rt->cfg = *cfg;
+    rt->cfg.world = world;
+    if (cfg->instr_log_path && cfg->instr_log_path[0]) {
+        rt->log = fopen(cfg->instr_log_path, "w");
+        if (!rt->log) return fail(CEL_E_INVALID, std::string("cannot open ") + cfg->instr_log_path);
+    }
+    if (cfg->execute) {
+        ExecConfig ec;
+        for (int d = 0; d < cfg->n_devices; ++d) ec.cuda_devices.push_back(cfg->cuda_devices ? cfg->cuda_devices[d] : d);
+        ec.rank = world > 1 ? cfg->rank : 0;
+        ec.world = world;
+        ec.arena_bytes = cfg->arena_bytes;
+        rt->exec = std::make_unique<Executor>(ec, nullptr);
+        std::string err;
+        const int rc = rt->exec->init(&err);
+        if (rc != 0) {
+            if (rt->log) fclose(rt->log);
+            return fail(rc, err.empty() ? rt->exec->error_msg() : err);
+        }
+    }
+    const int step = cfg->horizon_step > 0 ? cfg->horizon_step : 4;
+    rt->sched = std::make_unique<Scheduler>(cfg->n_devices, cfg->lookahead, step, cfg->checks != 0, rt->exec.get(),
+                                            rt->log);
+    if (rt->exec) rt->exec->set_scheduler(rt->sched.get());
+    *out = rt.release();
+    return CEL_OK;
+}
+
+int cel_ipc_export(cel_runtime* rt, void* blob) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!rt->exec) return fail(CEL_E_STATE, "runtime does not execute");
+    return after(rt, rt->exec->ipc_export(blob));
+}
+
+int cel_ipc_import(cel_runtime* rt, int32_t rank, const void* blob) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!rt->exec) return fail(CEL_E_STATE, "runtime does not execute");
+    return after(rt, rt->exec->ipc_import(rank, blob));
+}
+
+int cel_buffer_create(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
+                      const void* host_init, cel_buffer* out) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!extent || !out) return fail(CEL_E_INVALID, "null argument");
+    int64_t ext[3] = {1, 1, 1};
+    uint64_t n = 1;
+    for (int d = 0; d < dims && d < 3; ++d) {
+        ext[d] = int64_t(extent[d]);
+        n *= extent[d];
+    }
+    uint32_t bid = 0;
+    const int rc = rt->sched->buffer_create(dims, ext, elem_size, host_init != nullptr, &bid);
+    if (rc != 0) return fail(rc, "invalid buffer (dims 1..3, extents > 0, elem_size > 0)");
+    if (host_init && rt->exec) {
+        const int r2 = rt->exec->set_host_init(bid, host_init, size_t(n) * elem_size);
+        if (r2 != 0) return fail(r2, "cannot pin host memory for host_init");
+    }
+    *out = bid;
+    return CEL_OK;
+}
+
+int cel_task_submit(cel_runtime* rt, const cel_task_desc* d, cel_task* out) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!d || (d->n_acc > 0 && !d->acc) || d->n_acc < 0) return fail(CEL_E_INVALID, "null argument");
+    if (d->kernel < 0 || d->kernel > CEL_K_CALLBACK) return fail(CEL_E_INVALID, "unknown kernel");
+    if (d->kernel == CEL_K_CALLBACK && !d->fn) return fail(CEL_E_INVALID, "CALLBACK kernel without fn");
+    if (d->n_acc > kMaxAcc) return fail(CEL_E_INVALID, "too many accessors");
+    TaskDesc t;
+    t.dims = d->dims;
+    t.range = to_box(d->range);
+    t.split = d->split;
+    t.kernel = d->kernel;
+    t.params.seed = d->params.seed;
+    t.params.value = d->params.value;
+    t.params.t = d->params.t;
+    t.params.salt = d->params.salt;
+    t.fn = reinterpret_cast<KernelFn>(d->fn);
+    t.fn_user = d->fn_user;
+    for (int i = 0; i < d->n_acc; ++i) {
+        const cel_access& a = d->acc[i];
+        Access x;
+        x.buf = a.buf;
+        x.mode = a.mode;
+        x.map.kind = MapKind(a.map.kind);
+        for (int k = 0; k < 3; ++k) {
+            x.map.border[k] = a.map.border[k];
+            x.map.fixed.lo[k] = int64_t(a.map.fixed.min[k]);
+            x.map.fixed.hi[k] = int64_t(a.map.fixed.max[k]);
+            x.map.from_kernel_dim[k] = a.map.from_kernel_dim[k];
+        }
+        t.acc.push_back(x);
+    }
+    std::string err;
+    uint64_t tid = 0;
+    const uint64_t t0 = now_ns();
+    const int rc = rt->sched->task_submit(t, &tid, &err);
+    rt->gen_ns += now_ns() - t0;
+    if (rc < 0) return fail(rc, err);
+    if (out) *out = tid;
+    return after(rt, rc);
+}
+
+int cel_wait(cel_runtime* rt) {
+    if (int rc = check_poison(rt)) return rc;
+    const uint64_t t0 = now_ns();
+    rt->sched->wait();
+    rt->gen_ns += now_ns() - t0;
+    return after(rt, CEL_OK);
+}
+
+int cel_buffer_read(cel_runtime* rt, cel_buffer buf, const cel_box* box, void* host_dst) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!box || !host_dst) return fail(CEL_E_INVALID, "null argument");
+    if (!rt->sched->has_buffer(buf)) return fail(CEL_E_INVALID, "unknown buffer");
+    const Box b = to_box(*box);
+    if (rt->exec) rt->exec->set_readback(rt->sched->next_readback_id(), host_dst, b, rt->sched->elem_size(buf));
+    std::string err;
+    int64_t rb = 0;
+    const int rc = rt->sched->readback(buf, b, &rb, &err);
+    if (rc < 0) return fail(rc, err);
+    return after(rt, CEL_OK);
+}
+
+int cel_buffer_destroy(cel_runtime* rt, cel_buffer buf) {
+    if (int rc = check_poison(rt)) return rc;
+    std::string err;
+    const int rc = rt->sched->destroy(buf, &err);
+    if (rc < 0) return fail(rc, err);
+    if (rt->exec) rt->exec->drop_host_init_later(buf);
+    return after(rt, CEL_OK);
+}
+
+int cel_stats_get(cel_runtime* rt, cel_stats* o) {
+    if (!rt || !o) return fail(CEL_E_INVALID, "null argument");
+    memset(o, 0, sizeof *o);
+    const SchedStats& s = rt->sched->stats();
+    o->n_alloc = s.n_by_kind[int(IKind::Alloc)];
+    o->n_free = s.n_by_kind[int(IKind::Free)];
+    o->n_copy = s.n_by_kind[int(IKind::Copy)];
+    o->n_kernel = s.n_by_kind[int(IKind::Kernel)];
+    o->n_horizon = s.n_by_kind[int(IKind::Horizon)];
+    o->n_epoch = s.n_by_kind[int(IKind::Epoch)];
+    o->copies_resize = s.copies_by_reason[REASON_RESIZE];
+    o->copies_coherence = s.copies_by_reason[REASON_COHERENCE];
+    o->copies_readback = s.copies_by_reason[REASON_READBACK];
+    o->bytes_resize = s.bytes_by_reason[REASON_RESIZE];
+    o->bytes_coherence = s.bytes_by_reason[REASON_COHERENCE];
+    o->bytes_readback = s.bytes_by_reason[REASON_READBACK];
+    o->bytes_d2d_peer = s.bytes_d2d_peer;
+    o->alloc_bytes_peak = s.alloc_bytes_peak;
+    o->flushes = s.flushes;
+    o->gen_ns = rt->gen_ns;
+    if (rt->exec) {
+        const ExecStats& e = rt->exec->stats();
+        o->kernel_launches = e.kernel_launches;
+        o->copy_launches = e.copy_launches;
+        o->memcpy_calls = e.memcpy_calls;
+        o->event_waits = e.event_waits;
+        o->remote_waits = e.remote_waits;
+        o->signals = e.signals;
+        o->host_syncs = e.host_syncs;
+    }
+    return CEL_OK;
+}
+
+int cel_profile_enable(cel_runtime* rt, int32_t on) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!rt->exec) return fail(CEL_E_STATE, "runtime does not execute");
+    rt->exec->set_profile(on != 0);
+    if (on) rt->exec->profile_reset();
+    return CEL_OK;
+}
+
+int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!rt->exec) return fail(CEL_E_STATE, "runtime does not execute");
+    if (!ms || !count) return fail(CEL_E_INVALID, "null argument");
+    return after(rt, rt->exec->profile_read(ms, count, n));
+}
+
+int cel_runtime_destroy(cel_runtime* rt) {
+    if (!rt) return fail(CEL_E_INVALID, "null runtime");
+    int rc = CEL_OK;
+    if (!rt->poisoned && !(rt->exec && rt->exec->error())) {
+        rt->sched->shutdown();
+        if (rt->exec && rt->exec->error()) rc = fail(rt->exec->error(), rt->exec->error_msg());
+    } else {
+        rc = rt->poisoned ? rt->poisoned : rt->exec->error();
+    }
+    rt->sched.reset();
+    rt->exec.reset();
+    if (rt->log) fclose(rt->log);
+    delete rt;
+    return rc;
+}
+
+}  // extern "C"

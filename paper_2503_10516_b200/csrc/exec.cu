@@ -1,0 +1,859 @@
+// Executor implementation (see exec.hpp).  Paper: §4.1 out-of-order dispatch
+// (P:L515-530), allocation instructions, copy instructions
+// (P:L292), epochs, horizons.
+#include "exec.hpp"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/cel.h"
+
+namespace cel {
+
+Box map_access(const Mapper& m, const Box& chunk, const Box& ext);  // sched.cpp
+
+namespace {
+// Driver-API entry points resolved through the runtime (no link-time libcuda
+// dependency, so the library also loads on a host without a driver for the
+// execute=0 scheduling mode).
+struct Drv {
+    CUresult (*wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+    CUresult (*write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
+    CUresult (*errstr)(CUresult, const char**) = nullptr;
+    CUresult (*devattr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+    bool loaded = false;
+    void load() {
+        if (loaded) return;
+        loaded = true;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuStreamWaitValue64", reinterpret_cast<void**>(&wait64), cudaEnableDefault, &q);
+        cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&write64), cudaEnableDefault, &q);
+        cudaGetDriverEntryPoint("cuGetErrorString", reinterpret_cast<void**>(&errstr), cudaEnableDefault, &q);
+        cudaGetDriverEntryPoint("cuDeviceGetAttribute", reinterpret_cast<void**>(&devattr), cudaEnableDefault, &q);
+    }
+} g_drv;
+
+constexpr int kStreamsPerDev = 4;
+enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3 };
+constexpr uint64_t kAlign = 512;
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+}  // namespace
+
+// ------------------------------------------------------------ arena (allocation manager)
+// Deterministic first-fit sub-allocator over one pre-reserved device range per
+// device.  Every process of a multi-process run replays the same alloc/free
+// sequence for every device, so it knows every allocation's address without
+// communication; a freed range carries the completion token of its free
+// instruction, and a new allocation that reuses it inherits that token.
+bool Executor::Arena::alloc(uint64_t bytes, uint64_t* off, Token* tok) {
+    bytes = round_up(std::max<uint64_t>(bytes, 1), kAlign);
+    for (auto it = free_.begin(); it != free_.end(); ++it) {
+        if (it->second.len < bytes) continue;
+        *off = it->first;
+        *tok = it->second.tok;
+        FreeRange rest{it->second.len - bytes, it->second.tok};
+        const uint64_t o = it->first;
+        free_.erase(it);
+        if (rest.len) free_[o + bytes] = rest;
+        return true;
+    }
+    return false;
+}
+
+void Executor::Arena::release(uint64_t off, uint64_t bytes, Token tok) {
+    bytes = round_up(std::max<uint64_t>(bytes, 1), kAlign);
+    auto nx = free_.lower_bound(off);
+    // coalesce with the successor
+    if (nx != free_.end() && off + bytes == nx->first) {
+        bytes += nx->second.len;
+        for (auto& e : nx->second.tok.local) tok.local.push_back(e);
+        for (auto& e : nx->second.tok.remote) tok.remote.push_back(e);
+        nx = free_.erase(nx);
+    }
+    // coalesce with the predecessor
+    if (nx != free_.begin()) {
+        auto pv = std::prev(nx);
+        if (pv->first + pv->second.len == off) {
+            pv->second.len += bytes;
+            for (auto& e : tok.local) pv->second.tok.local.push_back(e);
+            for (auto& e : tok.remote) pv->second.tok.remote.push_back(e);
+            return;
+        }
+    }
+    free_[off] = FreeRange{bytes, std::move(tok)};
+}
+
+// ------------------------------------------------------------ setup
+Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(sched) {
+    G_ = int(cfg_.cuda_devices.size());
+}
+
+Executor::~Executor() {
+    if (err_ == 0) sync_all();
+    for (auto& p : prof_pending_) {
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    for (int d = 0; d < int(arenas_.size()); ++d) {
+        if (!owned(d)) {
+            if (cfg_.world > 1 && arenas_[d].base) cudaIpcCloseMemHandle(arenas_[d].base);
+            continue;
+        }
+        set_dev(d);
+        for (int k = 0; k < kStreamsPerDev; ++k) {
+            Stream& s = streams_[d * kStreamsPerDev + k];
+            for (auto& p : s.inflight) cudaEventDestroy(p.second);
+            if (s.s) cudaStreamDestroy(s.s);
+        }
+        for (cudaEvent_t e : pool_[d]) cudaEventDestroy(e);
+        // one cudaMalloc per physical device+virtual device
+        if (arenas_[d].base) cudaFree(arenas_[d].base);
+    }
+    for (auto& kv : host_init_) cudaFreeHost(kv.second.first);
+}
+
+void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
+
+void Executor::check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess || err_) return;
+    err_ = E_CUDA;
+    errmsg_ = std::string(what) + ": " + cudaGetErrorString(e);
+}
+
+void Executor::checkd(CUresult e, const char* what) {
+    if (e == CUDA_SUCCESS || err_) return;
+    const char* s = nullptr;
+    if (g_drv.errstr) g_drv.errstr(e, &s);
+    err_ = E_CUDA;
+    errmsg_ = std::string(what) + ": " + (s ? s : "driver error");
+}
+
+int Executor::init(std::string* err) {
+    phys_ = cfg_.cuda_devices;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        *err = "no CUDA device visible (the coherence path has no CPU fallback)";
+        return E_CUDA;
+    }
+    for (int p : phys_)
+        if (p < 0 || p >= ndev) {
+            *err = "cuda_devices names a device that does not exist";
+            return E_INVALID;
+        }
+    if (cfg_.world > 1 && cfg_.world != G_) {
+        *err = "multi-process mode needs n_devices == world (one device per rank)";
+        return E_INVALID;
+    }
+    streams_.resize(size_t(G_) * kStreamsPerDev);
+    pool_.resize(G_);
+    arenas_.resize(G_);
+    uint64_t arena = cfg_.arena_bytes ? cfg_.arena_bytes : (16ull << 30);
+    const uint64_t sig_bytes = cfg_.world > 1 ? uint64_t(cfg_.world) * kRing * 8 : 0;
+    const uint64_t data_off = round_up(sig_bytes, 2u << 20);
+    // peer access between distinct physical devices (NVLink 5 / NVSwitch)
+    for (int a = 0; a < G_; ++a) {
+        if (!owned(a)) continue;
+        for (int b = 0; b < G_; ++b) {
+            if (phys_[a] == phys_[b]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, phys_[a], phys_[b]);
+            if (can) {
+                cudaSetDevice(phys_[a]);
+                cudaError_t e = cudaDeviceEnablePeerAccess(phys_[b], 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            }
+        }
+    }
+    for (int d = 0; d < G_; ++d) {
+        Arena& A = arenas_[d];
+        A.size = arena;
+        A.data_off = data_off;
+        A.free_[data_off] = FreeRange{arena - data_off, Token{}};
+        if (!owned(d)) continue;
+        set_dev(d);
+        for (int k = 0; k < kStreamsPerDev; ++k) {
+            Stream& s = streams_[d * kStreamsPerDev + k];
+            s.dev = d;
+            if (cudaStreamCreateWithFlags(&s.s, cudaStreamNonBlocking) != cudaSuccess) {
+                *err = "cudaStreamCreate failed";
+                return E_CUDA;
+            }
+        }
+        cudaError_t e = cudaMalloc(&A.base, arena);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            char buf[200];
+            snprintf(buf, sizeof buf, "cannot reserve a %.1f GiB arena on device %d (set arena_bytes)",
+                     double(arena) / double(1ull << 30), phys_[d]);
+            *err = buf;
+            return E_OOM;
+        }
+        if (sig_bytes) cudaMemset(A.base, 0, sig_bytes);
+    }
+    if (cfg_.world > 1) {
+        int v = 0;
+        g_drv.load();
+        if (g_drv.devattr)
+            g_drv.devattr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, CUdevice(phys_[cfg_.rank]));
+        memops64_ = v != 0 && g_drv.wait64 && g_drv.write64;
+        if (!memops64_) {
+            *err = "multi-process mode needs 64-bit stream memory operations";
+            return E_CUDA;
+        }
+    }
+    cudaDeviceSynchronize();
+    return err_;
+}
+
+size_t Executor::ipc_blob_size() const { return sizeof(cudaIpcMemHandle_t); }
+
+int Executor::ipc_export(void* blob) const {
+    if (cfg_.world <= 1) return E_STATE;
+    cudaIpcMemHandle_t h;
+    cudaSetDevice(phys_[cfg_.rank]);
+    if (cudaIpcGetMemHandle(&h, arenas_[cfg_.rank].base) != cudaSuccess) return E_CUDA;
+    memcpy(blob, &h, sizeof h);
+    return E_OK;
+}
+
+int Executor::ipc_import(int rank, const void* blob) {
+    if (cfg_.world <= 1 || rank < 0 || rank >= G_) return E_INVALID;
+    if (rank == cfg_.rank) return E_OK;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, blob, sizeof h);
+    void* p = nullptr;
+    set_dev(cfg_.rank);
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        check(e, "cudaIpcOpenMemHandle");
+        return E_CUDA;
+    }
+    arenas_[rank].base = static_cast<char*>(p);
+    return E_OK;
+}
+
+int Executor::set_host_init(uint32_t bid, const void* data, size_t bytes) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return E_OOM;
+    }
+    memcpy(p, data, bytes);
+    host_init_[bid] = {static_cast<char*>(p), bytes};
+    return E_OK;
+}
+
+void Executor::drop_host_init(uint32_t bid) {
+    auto it = host_init_.find(bid);
+    if (it == host_init_.end()) return;
+    sync_all();
+    cudaFreeHost(it->second.first);
+    host_init_.erase(it);
+}
+
+void Executor::set_readback(int64_t rb, void* dst, const Box& box, uint32_t es) {
+    readbacks_[rb] = Readback{static_cast<char*>(dst), box, es};
+}
+
+// ------------------------------------------------------------ events / tokens
+cudaEvent_t Executor::get_event(int dev) {
+    auto& p = pool_[dev];
+    if (!p.empty()) {
+        cudaEvent_t e = p.back();
+        p.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    return e;
+}
+
+void Executor::put_event(int dev, cudaEvent_t e) { pool_[dev].push_back(e); }
+
+void Executor::poll(bool prune) {
+    for (auto& s : streams_) {
+        while (!s.inflight.empty()) {
+            cudaError_t q = cudaEventQuery(s.inflight.front().second);
+            if (q == cudaErrorNotReady) break;
+            if (q != cudaSuccess) {
+                check(q, "asynchronous CUDA error");
+                return;
+            }
+            s.done = s.inflight.front().first;
+            put_event(s.dev, s.inflight.front().second);
+            s.inflight.pop_front();
+        }
+    }
+    (void)prune;
+}
+
+Token Executor::dep_token(uint64_t j) const {
+    auto it = tok_.find(j);
+    return it == tok_.end() ? Token{} : it->second;
+}
+
+void Executor::merge(Token& into, const Token& t) const {
+    for (const TokEntry& e : t.local) {
+        if (e.seq <= streams_[e.stream].done) continue;
+        bool found = false;
+        for (TokEntry& x : into.local)
+            if (x.stream == e.stream) {
+                if (e.seq > x.seq) x = e;
+                found = true;
+                break;
+            }
+        if (!found) into.local.push_back(e);
+    }
+    for (auto& r : t.remote)
+        if (std::find(into.remote.begin(), into.remote.end(), r) == into.remote.end()) into.remote.push_back(r);
+}
+
+uint64_t* Executor::sig_slot(int dev, int from_rank, uint64_t iid) {
+    return reinterpret_cast<uint64_t*>(arenas_[dev].base) + (uint64_t(from_rank) * kRing + (iid % kRing));
+}
+
+void Executor::wait_token(int sidx, const Token& t) {
+    Stream& s = streams_[sidx];
+    for (const TokEntry& e : t.local) {
+        if (e.stream == sidx || e.seq <= streams_[e.stream].done) continue;
+        check(cudaStreamWaitEvent(s.s, e.ev, 0), "cudaStreamWaitEvent");
+        st_.event_waits++;
+    }
+    for (auto& r : t.remote) {
+        // the producer's process writes iid into this GPU's slot when done
+        checkd(g_drv.wait64(reinterpret_cast<CUstream>(s.s),
+                                   reinterpret_cast<CUdeviceptr>(sig_slot(s.dev, r.first, r.second)), r.second,
+                                   CU_STREAM_WAIT_VALUE_GEQ),
+               "cuStreamWaitValue64");
+        st_.remote_waits++;
+    }
+}
+
+Token Executor::record(int sidx) {
+    Stream& s = streams_[sidx];
+    cudaEvent_t e = get_event(s.dev);
+    check(cudaEventRecord(e, s.s), "cudaEventRecord");
+    const uint64_t seq = ++s.seq;
+    s.inflight.push_back({seq, e});
+    Token t;
+    t.local.push_back({sidx, seq, e});
+    return t;
+}
+
+Token Executor::materialize(int dev, const Token& t) {
+    const int sidx = dev * kStreamsPerDev + S_SYNC;
+    wait_token(sidx, t);
+    return record(sidx);
+}
+
+void Executor::throttle() {
+    for (auto& s : streams_) {
+        while (s.inflight.size() > 2048) {
+            check(cudaEventSynchronize(s.inflight.front().second), "cudaEventSynchronize");
+            st_.host_syncs++;
+            s.done = s.inflight.front().first;
+            put_event(s.dev, s.inflight.front().second);
+            s.inflight.pop_front();
+        }
+    }
+}
+
+void Executor::sync_all() {
+    for (auto& s : streams_)
+        if (s.s) cudaStreamSynchronize(s.s);
+    poll(true);
+}
+
+void Executor::prune_tokens(uint64_t below) {
+    for (auto it = tok_.begin(); it != tok_.end();) {
+        if (it->first < below && !live_alloc_iid_.count(it->first))
+            it = tok_.erase(it);
+        else
+            ++it;
+    }
+}
+
+// ------------------------------------------------------------ ownership
+int Executor::instr_owner(const Instr& ins) const {
+    switch (ins.kind) {
+    case IKind::Alloc:
+    case IKind::Free:
+        return ins.mem - 2;
+    case IKind::Kernel:
+        return ins.device;
+    case IKind::Copy:
+        return ins.src_mem >= 2 ? ins.src_mem - 2 : ins.dst_mem - 2;   // push model: the producer's GPU
+    default:
+        return -1;
+    }
+}
+
+// Local part of a set of dependencies: tokens of the deps this process executes
+// (or multi-owner horizons/epochs); deps executed elsewhere appear as remote
+// markers that their owner signals to us.
+Token Executor::local_part(const std::vector<uint64_t>& deps) const {
+    Token t;
+    for (uint64_t j : deps) merge(t, dep_token(j));
+    return t;
+}
+
+// Called on a process that does NOT execute `ins`: signal to the executing
+// process every dependency whose (local part of the) completion lives here.
+void Executor::signal_deps(const Instr& ins, int owner_dev) {
+    const int o = owner_rank(owner_dev);
+    for (uint64_t j : ins.deps) {
+        auto kit = kind_of_.find(j);
+        if (kit == kind_of_.end()) continue;  // complete before any remote dependent existed
+        const int jo = kit->second;           // owner device, -1 = all
+        if (jo >= 0 && owner_rank(jo) != cfg_.rank) continue;
+        const uint64_t key = j * uint64_t(cfg_.world) + uint64_t(o);
+        if (!signalled_.insert(key).second) continue;
+        const int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
+        wait_token(sidx, dep_token(j));
+        checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
+                                    reinterpret_cast<CUdeviceptr>(sig_slot(o, cfg_.rank, j)), j,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT),
+               "cuStreamWriteValue64");
+        st_.signals++;
+    }
+}
+
+char* Executor::alloc_ptr(int64_t aid) {
+    auto it = allocs_.find(aid);
+    if (it == allocs_.end()) return nullptr;
+    const AllocRec& r = it->second;
+    return arenas_[r.dev].base + r.off;
+}
+
+// ------------------------------------------------------------ dispatch
+void Executor::on_instr(const Instr& ins) {
+    if (err_) return;
+    const int od = instr_owner(ins);
+    const bool mine = od < 0 || owner_rank(od) == cfg_.rank;
+    if (cfg_.world > 1) {
+        if (od >= 0) kind_of_[ins.iid] = od;
+        else kind_of_[ins.iid] = -1;
+        if (!mine && ins.kind != IKind::Alloc) signal_deps(ins, od);
+    }
+    switch (ins.kind) {
+    case IKind::Alloc: {
+        const int dev = ins.mem - 2;
+        const uint32_t es = sched_->elem_size(ins.buffer);
+        const uint64_t bytes = ins.box.volume() * es;
+        uint64_t off = 0;
+        Token t;
+        if (!arenas_[dev].alloc(bytes, &off, &t)) {
+            err_ = E_OOM;
+            char buf[200];
+            snprintf(buf, sizeof buf, "device %d arena exhausted allocating %.3f GiB", dev, double(bytes) / (1ull << 30));
+            errmsg_ = buf;
+            return;
+        }
+        allocs_[ins.aid] = AllocRec{dev, off, bytes, ins.box, es, ins.iid};
+        live_alloc_iid_.insert(ins.iid);
+        Token mt;
+        if (mine) merge(mt, t);
+        else mt.remote.push_back({owner_rank(dev), ins.iid});
+        if (mt.remote.size() > 8) mt = materialize(dev, mt);
+        tok_[ins.iid] = mt;
+        return;
+    }
+    case IKind::Free: {
+        auto it = allocs_.find(ins.aid);
+        if (it == allocs_.end()) {
+            err_ = E_STATE;
+            errmsg_ = "free of an unknown allocation";
+            return;
+        }
+        const AllocRec r = it->second;
+        Token t;
+        if (mine) {
+            t = local_part(ins.deps);
+            for (uint64_t j : ins.deps) {
+                auto kit = kind_of_.find(j);
+                if (cfg_.world > 1 && kit != kind_of_.end() && kit->second >= 0 &&
+                    owner_rank(kit->second) != cfg_.rank)
+                    t.remote.push_back({owner_rank(kit->second), j});
+            }
+            if (t.remote.size() > 8) t = materialize(r.dev, t);
+        } else {
+            t.remote.push_back({owner_rank(r.dev), ins.iid});
+        }
+        arenas_[r.dev].release(r.off, r.bytes, t);
+        tok_[ins.iid] = t;
+        live_alloc_iid_.erase(r.iid);
+        allocs_.erase(it);
+        return;
+    }
+    case IKind::Copy:
+        if (!mine) {
+            tok_[ins.iid] = Token{{}, {{owner_rank(od), ins.iid}}};
+            return;
+        }
+        exec_copy(ins);
+        break;
+    case IKind::Kernel:
+        if (!mine) {
+            tok_[ins.iid] = Token{{}, {{owner_rank(od), ins.iid}}};
+            return;
+        }
+        exec_kernel(ins);
+        break;
+    case IKind::Horizon: {
+        // completion of a horizon tells us everything before it is done;
+        // deps older than the applied (previous) horizon are never referenced again.
+        Token t;
+        for (uint64_t j : ins.deps) {
+            auto kit = kind_of_.find(j);
+            const bool remote_only = cfg_.world > 1 && kit != kind_of_.end() && kit->second >= 0 &&
+                                     owner_rank(kit->second) != cfg_.rank;
+            if (!remote_only) merge(t, dep_token(j));
+        }
+        for (int r = 0; r < cfg_.world; ++r)
+            if (r != cfg_.rank) t.remote.push_back({r, ins.iid});
+        tok_[ins.iid] = t;
+        poll(false);
+        throttle();
+        // prune tokens below the previously emitted horizon (allocation tokens stay)
+        if (prev_horizon_) prune_tokens(prev_horizon_);
+        prev_horizon_ = ins.iid;
+        return;
+    }
+    case IKind::Epoch:
+        exec_epoch(ins);
+        return;
+    }
+    if (++since_poll_ >= 64) {
+        since_poll_ = 0;
+        poll(false);
+        throttle();
+    }
+}
+
+void Executor::exec_epoch(const Instr& ins) {
+    Token t;
+    for (uint64_t j : ins.deps) {
+        auto kit = kind_of_.find(j);
+        const bool remote_only = cfg_.world > 1 && kit != kind_of_.end() && kit->second >= 0 &&
+                                 owner_rank(kit->second) != cfg_.rank;
+        if (!remote_only) merge(t, dep_token(j));
+    }
+    // an epoch synchronises with the main thread
+    if (cfg_.world > 1) {
+        const int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
+        wait_token(sidx, t);
+        check(cudaStreamSynchronize(streams_[sidx].s), "epoch synchronize");
+    } else {
+        for (const TokEntry& e : t.local)
+            if (e.seq > streams_[e.stream].done) check(cudaEventSynchronize(e.ev), "epoch synchronize");
+    }
+    st_.host_syncs++;
+    poll(true);
+    for (uint32_t bid : host_drop_) {
+        auto it = host_init_.find(bid);
+        if (it != host_init_.end()) {
+            cudaFreeHost(it->second.first);
+            host_init_.erase(it);
+        }
+    }
+    host_drop_.clear();
+    Token mine;
+    for (int r = 0; r < cfg_.world; ++r)
+        if (r != cfg_.rank) mine.remote.push_back({r, ins.iid});
+    // everything before the epoch is complete locally: drop old tokens
+    prune_tokens(ins.iid);
+    prev_horizon_ = 0;
+    tok_[ins.iid] = mine;
+    if (cfg_.world > 1) {
+        // remote markers older than the epoch stay valid (their slots keep the value)
+        for (auto it = kind_of_.begin(); it != kind_of_.end();) {
+            if (it->first + kRing / 2 < ins.iid) it = kind_of_.erase(it);
+            else ++it;
+        }
+    }
+}
+
+void Executor::exec_copy(const Instr& ins) {
+    const uint32_t es = sched_->elem_size(ins.buffer);
+    Token deps;
+    for (uint64_t j : ins.deps) merge(deps, dep_token(j));
+    if (ins.src_mem >= 2 && ins.dst_mem >= 2) {
+        const AllocRec& S = allocs_.at(ins.src_aid);
+        const AllocRec& D = allocs_.at(ins.dst_aid);
+        const int dev = S.dev;
+        const bool peer = S.dev != D.dev;
+        const int sidx = dev * kStreamsPerDev + (peer ? S_PUSH : S_COPY);
+        set_dev(dev);
+        wait_token(sidx, deps);
+        const char* sb = arenas_[S.dev].base + S.off;
+        char* db = arenas_[D.dev].base + D.off;
+        CopyArgs args;
+        args.nseg = 0;
+        args.total_units = 0;
+        const int64_t sn1 = S.box.extent(1), sn2 = S.box.extent(2);
+        const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
+        uint64_t bytes = 0;
+        auto flush = [&]() {
+            if (args.nseg == 0) return;
+            if (cfg_.profile) {
+                Prof p{K_NUM, nullptr, nullptr};
+                cudaEventCreate(&p.a);
+                cudaEventCreate(&p.b);
+                cudaEventRecord(p.a, streams_[sidx].s);
+                st_.kernel_launches += launch_copy(args, streams_[sidx].s);
+                cudaEventRecord(p.b, streams_[sidx].s);
+                prof_pending_.push_back(p);
+            } else {
+                st_.kernel_launches += launch_copy(args, streams_[sidx].s);
+            }
+            st_.copy_launches++;
+            args.nseg = 0;
+            args.total_units = 0;
+        };
+        for (const Box& b : ins.region) {
+            CopySeg g;
+            const int64_t so = ((b.lo[0] - S.box.lo[0]) * sn1 + (b.lo[1] - S.box.lo[1])) * sn2 + (b.lo[2] - S.box.lo[2]);
+            const int64_t dof = ((b.lo[0] - D.box.lo[0]) * dn1 + (b.lo[1] - D.box.lo[1])) * dn2 + (b.lo[2] - D.box.lo[2]);
+            g.src = sb + so * es;
+            g.dst = db + dof * es;
+            g.row_bytes = uint64_t(b.extent(2)) * es;
+            g.rows = uint32_t(b.extent(1));
+            g.planes = uint32_t(b.extent(0));
+            g.src_row_stride = uint64_t(sn2) * es;
+            g.dst_row_stride = uint64_t(dn2) * es;
+            g.src_plane_stride = uint64_t(sn1 * sn2) * es;
+            g.dst_plane_stride = uint64_t(dn1 * dn2) * es;
+            if (g.row_bytes == g.src_row_stride && g.row_bytes == g.dst_row_stride) {
+                g.row_bytes *= g.rows;
+                g.rows = 1;
+                if (g.row_bytes == g.src_plane_stride && g.row_bytes == g.dst_plane_stride) {
+                    g.row_bytes *= g.planes;
+                    g.planes = 1;
+                }
+            }
+            uint64_t a = uintptr_t(g.src) | uintptr_t(g.dst) | g.row_bytes;
+            if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
+            if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
+            g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
+            g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
+            // huge planes x rows: split so that units stay below 2^63 (never in practice)
+            if (args.nseg == kMaxSegs) flush();
+            g.units_begin = args.total_units;
+            args.seg[args.nseg++] = g;
+            args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
+            bytes += b.volume() * es;
+        }
+        flush();
+        const int kind = ins.reason == REASON_RESIZE ? 0 : (peer ? (phys_[S.dev] == phys_[D.dev] ? 1 : 2) : 1);
+        st_.bytes_copy[kind] += bytes;
+        tok_[ins.iid] = record(sidx);
+        return;
+    }
+    // host <-> device: DMA (cudaMemcpy3DAsync per box)
+    const bool h2d = ins.src_mem == 0 && ins.dst_mem >= 2;
+    const bool d2h = ins.src_mem >= 2 && ins.dst_aid == USER_AID;
+    if (!h2d && !d2h) {
+        // host implicit allocation -> user pointer: plain host copy
+        auto hi = host_init_.find(ins.buffer);
+        auto rb = readbacks_.find(ins.readback);
+        if (hi == host_init_.end() || rb == readbacks_.end()) {
+            err_ = E_STATE;
+            errmsg_ = "host copy without source or destination";
+            return;
+        }
+        const Box E = sched_->extent(ins.buffer);
+        const Box& R = rb->second.box;
+        for (const Box& b : ins.region)
+            for (int64_t z = b.lo[0]; z < b.hi[0]; ++z)
+                for (int64_t y = b.lo[1]; y < b.hi[1]; ++y) {
+                    const int64_t so = ((z * E.extent(1)) + y) * E.extent(2) + b.lo[2];
+                    const int64_t dof = (((z - R.lo[0]) * R.extent(1)) + (y - R.lo[1])) * R.extent(2) + (b.lo[2] - R.lo[2]);
+                    memcpy(rb->second.dst + dof * es, hi->second.first + so * es, size_t(b.extent(2)) * es);
+                }
+        st_.bytes_copy[5] += rvolume(ins.region) * es;
+        tok_[ins.iid] = Token{};
+        return;
+    }
+    const int dev = h2d ? ins.dst_mem - 2 : ins.src_mem - 2;
+    const int sidx = dev * kStreamsPerDev + S_COPY;
+    set_dev(dev);
+    wait_token(sidx, deps);
+    char* hbase;
+    Box hbox;
+    char* dbase;
+    Box dbox;
+    if (h2d) {
+        auto hi = host_init_.find(ins.buffer);
+        if (hi == host_init_.end()) {
+            err_ = E_STATE;
+            errmsg_ = "H2D copy of a buffer without host data";
+            return;
+        }
+        hbase = hi->second.first;
+        hbox = sched_->extent(ins.buffer);
+        const AllocRec& D = allocs_.at(ins.dst_aid);
+        dbase = arenas_[D.dev].base + D.off;
+        dbox = D.box;
+    } else {
+        auto rb = readbacks_.find(ins.readback);
+        if (rb == readbacks_.end()) {
+            err_ = E_STATE;
+            errmsg_ = "readback copy without a destination";
+            return;
+        }
+        hbase = rb->second.dst;
+        hbox = rb->second.box;
+        const AllocRec& S = allocs_.at(ins.src_aid);
+        dbase = arenas_[S.dev].base + S.off;
+        dbox = S.box;
+    }
+    for (const Box& b : ins.region) {
+        cudaMemcpy3DParms p;
+        memset(&p, 0, sizeof p);
+        cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, size_t(hbox.extent(2)) * es, size_t(hbox.extent(2)) * es,
+                                                size_t(hbox.extent(1)));
+        cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, size_t(dbox.extent(2)) * es, size_t(dbox.extent(2)) * es,
+                                                size_t(dbox.extent(1)));
+        cudaPos hpos = make_cudaPos(size_t(b.lo[2] - hbox.lo[2]) * es, size_t(b.lo[1] - hbox.lo[1]),
+                                    size_t(b.lo[0] - hbox.lo[0]));
+        cudaPos dpos = make_cudaPos(size_t(b.lo[2] - dbox.lo[2]) * es, size_t(b.lo[1] - dbox.lo[1]),
+                                    size_t(b.lo[0] - dbox.lo[0]));
+        if (h2d) {
+            p.srcPtr = hp;
+            p.srcPos = hpos;
+            p.dstPtr = dp;
+            p.dstPos = dpos;
+            p.kind = cudaMemcpyHostToDevice;
+        } else {
+            p.srcPtr = dp;
+            p.srcPos = dpos;
+            p.dstPtr = hp;
+            p.dstPos = hpos;
+            p.kind = cudaMemcpyDeviceToHost;
+        }
+        p.extent = make_cudaExtent(size_t(b.extent(2)) * es, size_t(b.extent(1)), size_t(b.extent(0)));
+        check(cudaMemcpy3DAsync(&p, streams_[sidx].s), "cudaMemcpy3DAsync");
+        st_.memcpy_calls++;
+    }
+    st_.bytes_copy[h2d ? 3 : 4] += rvolume(ins.region) * es;
+    tok_[ins.iid] = record(sidx);
+}
+
+void Executor::exec_kernel(const Instr& ins) {
+    const TaskDesc& d = *ins.desc;
+    const int dev = ins.device;
+    const int sidx = dev * kStreamsPerDev + S_COMPUTE;
+    set_dev(dev);
+    Token deps;
+    for (uint64_t j : ins.deps) merge(deps, dep_token(j));
+    wait_token(sidx, deps);
+    if (d.kernel == K_CALLBACK) {
+        std::vector<cel_accessor> acc(d.acc.size());
+        for (size_t i = 0; i < d.acc.size(); ++i) {
+            const int64_t aid = ins.bindings[i];
+            auto it = allocs_.find(aid);
+            memset(&acc[i], 0, sizeof acc[i]);
+            if (it == allocs_.end()) continue;
+            acc[i].base = arenas_[it->second.dev].base + it->second.off;
+            for (int k = 0; k < 3; ++k) {
+                acc[i].alloc_box.min[k] = uint64_t(it->second.box.lo[k]);
+                acc[i].alloc_box.max[k] = uint64_t(it->second.box.hi[k]);
+            }
+            acc[i].elem_size = it->second.es;
+        }
+        cel_box ch;
+        for (int k = 0; k < 3; ++k) {
+            ch.min[k] = uint64_t(ins.chunk.lo[k]);
+            ch.max[k] = uint64_t(ins.chunk.hi[k]);
+        }
+        if (d.fn) d.fn(d.fn_user, dev, &ch, acc.data(), int(acc.size()), streams_[sidx].s);
+        tok_[ins.iid] = record(sidx);
+        return;
+    }
+    KArgs a;
+    memset(&a, 0, sizeof a);
+    a.kind = d.kernel;
+    a.n_acc = int(std::min<size_t>(d.acc.size(), kMaxAcc));
+    for (int k = 0; k < 3; ++k) {
+        a.chunk.lo[k] = ins.chunk.lo[k];
+        a.chunk.hi[k] = ins.chunk.hi[k];
+    }
+    a.seed = d.params.seed;
+    a.value = d.params.value;
+    a.t = d.params.t;
+    a.salt = d.params.salt;
+    for (int i = 0; i < a.n_acc; ++i) {
+        const Access& ac = d.acc[i];
+        DAcc& A = a.acc[i];
+        const Box ext = sched_->extent(ac.buf);
+        for (int k = 0; k < 3; ++k) A.ext[k] = ext.hi[k];
+        A.es = sched_->elem_size(ac.buf);
+        A.mode = ac.mode;
+        A.map = int(ac.map.kind);
+        for (int k = 0; k < 3; ++k) {
+            A.border[k] = ac.map.border[k];
+            A.fixed.lo[k] = ac.map.fixed.lo[k];
+            A.fixed.hi[k] = ac.map.fixed.hi[k];
+        }
+        const Box mb = map_access(ac.map, ins.chunk, ext);
+        for (int k = 0; k < 3; ++k) {
+            A.box.lo[k] = mb.lo[k];
+            A.box.hi[k] = mb.hi[k];
+        }
+        auto it = allocs_.find(ins.bindings[i]);
+        if (it != allocs_.end()) {
+            A.base = arenas_[it->second.dev].base + it->second.off;
+            for (int k = 0; k < 3; ++k) {
+                A.lo[k] = it->second.box.lo[k];
+                A.n[k] = it->second.box.extent(k);
+            }
+        }
+    }
+    int n;
+    if (cfg_.profile) {
+        Prof p{d.kernel, nullptr, nullptr};
+        cudaEventCreate(&p.a);
+        cudaEventCreate(&p.b);
+        cudaEventRecord(p.a, streams_[sidx].s);
+        n = launch_workload(a, streams_[sidx].s);
+        cudaEventRecord(p.b, streams_[sidx].s);
+        prof_pending_.push_back(p);
+    } else {
+        n = launch_workload(a, streams_[sidx].s);
+    }
+    check(cudaGetLastError(), "kernel launch");
+    st_.kernel_launches += n;
+    st_.workload_launches += n;
+    tok_[ins.iid] = record(sidx);
+}
+
+int Executor::profile_read(double* ms, uint64_t* count, int n) {
+    for (auto& p : prof_pending_) {
+        float t = 0.f;
+        cudaEventSynchronize(p.b);
+        cudaEventElapsedTime(&t, p.a, p.b);
+        prof_ms_[p.kind] += t;
+        prof_n_[p.kind]++;
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    prof_pending_.clear();
+    for (int i = 0; i < n && i <= K_NUM; ++i) {
+        ms[i] = prof_ms_[i];
+        count[i] = prof_n_[i];
+    }
+    return E_OK;
+}
+
+void Executor::profile_reset() {
+    double ms[K_NUM + 1];
+    uint64_t c[K_NUM + 1];
+    profile_read(ms, c, K_NUM + 1);
+    for (int i = 0; i <= K_NUM; ++i) {
+        prof_ms_[i] = 0;
+        prof_n_[i] = 0;
+    }
+}
+
+}  // namespace cel

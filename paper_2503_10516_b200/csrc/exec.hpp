@@ -1,0 +1,182 @@
+// Instruction executor (§4.1 "Out-of-Order Instruction Dispatch").
+//
+// The paper's out-of-order engine issues an instruction *directly* when its
+// dependencies are complete or *eagerly* when all incomplete dependencies sit
+// on the same in-order queue.  On B200 the in-order queues are CUDA streams and
+// cross-queue dependencies become cudaStreamWaitEvent, so every instruction is
+// issued eagerly at generation time: a dependency on the same stream costs
+// nothing, one on another stream of this process costs one event wait, one on
+// a device owned by another process (one process per GPU) costs a stream
+// memory-op wait on a flag that the producer's process writes into this GPU's
+// memory over NVLink.  The host only blocks at epochs and when too
+// many events are in flight.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "kernels.cuh"
+#include "sched.hpp"
+
+namespace cel {
+
+// completion token of an instruction: per local stream the sequence number of
+// the event recorded after it, plus (rank, iid) pairs whose completion another
+// process signals.
+struct TokEntry {
+    int stream;
+    uint64_t seq;
+    cudaEvent_t ev;
+};
+struct Token {
+    std::vector<TokEntry> local;
+    std::vector<std::pair<int, uint64_t>> remote;
+    bool empty() const { return local.empty() && remote.empty(); }
+};
+
+struct ExecConfig {
+    std::vector<int> cuda_devices;     // physical device of each virtual device
+    int rank = 0, world = 1;           // world > 1: device d is owned by rank d
+    uint64_t arena_bytes = 0;          // per device; 0 = auto
+    bool profile = false;
+};
+
+struct ExecStats {
+    uint64_t kernel_launches = 0;      // our CUDA kernels (workload + copy + signal)
+    uint64_t workload_launches = 0;
+    uint64_t copy_launches = 0;
+    uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
+    uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
+    uint64_t event_waits = 0, remote_waits = 0, signals = 0;
+    uint64_t host_syncs = 0;
+};
+
+class Executor : public InstrSink {
+public:
+    Executor(const ExecConfig& cfg, Scheduler* sched);
+    ~Executor() override;
+
+    int init(std::string* err);
+    void on_instr(const Instr& ins) override;
+
+    // host data of a host-initialised buffer (copied, pinned)
+    int set_host_init(uint32_t bid, const void* data, size_t bytes);
+    void drop_host_init(uint32_t bid);
+    void drop_host_init_later(uint32_t bid) { host_drop_.push_back(bid); }
+    void set_scheduler(Scheduler* s) { sched_ = s; }
+    void set_readback(int64_t rb, void* dst, const Box& box, uint32_t elem_size);
+
+    // multi-process plumbing
+    size_t ipc_blob_size() const;
+    int ipc_export(void* blob) const;
+    int ipc_import(int rank, const void* blob);
+
+    int error() const { return err_; }
+    const std::string& error_msg() const { return errmsg_; }
+    const ExecStats& stats() const { return st_; }
+
+    // profiling: per kernel kind, accumulated device ms and launch count
+    void set_profile(bool on) { cfg_.profile = on; }
+    int profile_read(double* ms, uint64_t* count, int n);
+    void profile_reset();
+    int device_count() const { return G_; }
+    int owned(int d) const { return owner_rank(d) == cfg_.rank; }
+    void sync_all();
+
+private:
+    struct Stream {
+        cudaStream_t s = nullptr;
+        int dev = 0;
+        uint64_t seq = 0;
+        uint64_t done = 0;
+        std::deque<std::pair<uint64_t, cudaEvent_t>> inflight;
+    };
+    struct FreeRange {
+        uint64_t len;
+        Token tok;
+    };
+    struct Arena {
+        char* base = nullptr;          // local mapping (owned device) or IPC mapping
+        uint64_t size = 0;
+        uint64_t data_off = 0;         // after the signal area
+        std::map<uint64_t, FreeRange> free_;
+        bool alloc(uint64_t bytes, uint64_t* off, Token* tok);
+        void release(uint64_t off, uint64_t bytes, Token tok);
+    };
+    struct AllocRec {
+        int dev;
+        uint64_t off;
+        uint64_t bytes;
+        Box box;
+        uint32_t es;
+        uint64_t iid;
+    };
+    struct Prof {
+        int kind;
+        cudaEvent_t a, b;
+    };
+    struct Readback {
+        char* dst;
+        Box box;
+        uint32_t es;
+    };
+
+    int owner_rank(int dev) const { return cfg_.world > 1 ? dev : 0; }
+    int instr_owner(const Instr& ins) const;        // device that executes it, -1 = all
+    cudaEvent_t get_event(int dev);
+    void put_event(int dev, cudaEvent_t e);
+    void poll(bool prune);
+    Token dep_token(uint64_t j) const;
+    void merge(Token& into, const Token& t) const;
+    void wait_token(int sidx, const Token& t);
+    Token record(int sidx);
+    void set_dev(int dev);
+    void check(cudaError_t e, const char* what);
+    void checkd(CUresult e, const char* what);
+    void signal_deps(const Instr& ins, int owner_dev);
+    Token local_part(const std::vector<uint64_t>& deps) const;
+    char* alloc_ptr(int64_t aid);
+    void exec_copy(const Instr& ins);
+    void exec_kernel(const Instr& ins);
+    void exec_epoch(const Instr& ins);
+    void throttle();
+    void prune_tokens(uint64_t below);
+    Token materialize(int dev, const Token& t);
+    uint64_t* sig_slot(int dev, int from_rank, uint64_t iid);
+
+    ExecConfig cfg_;
+    Scheduler* sched_;
+    int G_ = 0;
+    std::vector<Stream> streams_;                  // dev*4 + {0 compute, 1 copy, 2 push, 3 sync}
+    std::vector<std::vector<cudaEvent_t>> pool_;
+    std::vector<Arena> arenas_;
+    std::unordered_map<uint64_t, Token> tok_;
+    std::unordered_map<uint64_t, int> kind_of_;    // iid -> owner device for event-only instrs (-1 all)
+    std::unordered_map<int64_t, AllocRec> allocs_;
+    std::unordered_map<uint32_t, std::pair<char*, size_t>> host_init_;
+    std::unordered_map<int64_t, Readback> readbacks_;
+    std::unordered_set<uint64_t> signalled_;       // (iid * world + target) already signalled
+    std::vector<Prof> prof_pending_;
+    double prof_ms_[K_NUM + 1] = {};
+    uint64_t prof_n_[K_NUM + 1] = {};
+    std::vector<int> phys_;
+    bool memops64_ = false;
+    int err_ = 0;
+    std::string errmsg_;
+    ExecStats st_;
+    uint64_t since_poll_ = 0;
+    uint64_t prev_horizon_ = 0;
+    std::unordered_set<uint64_t> live_alloc_iid_;
+    std::vector<uint32_t> host_drop_;
+    static constexpr uint64_t kRing = 1u << 16;
+};
+
+}  // namespace cel

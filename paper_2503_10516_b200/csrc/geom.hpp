@@ -1,0 +1,309 @@
+// Box / Region / RegionMap for the host scheduler.
+//
+// Paper basis: buffer state is tracked per "subregion" (§3.3) and
+// transfers per "rectangular region" (§3.4).  Representation follows
+// DESIGN.md R1-R3: half-open 3-D boxes (unused dims [0,1)), regions as
+// disjoint boxes in maximal-slab canonical form (dim 0 cut exactly where the
+// (dim1, dim2) cross-section changes, recursively; sorted by min), region
+// maps as value -> canonical region.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+namespace cel {
+
+struct Box {
+    int64_t lo[3] = {0, 0, 0};
+    int64_t hi[3] = {0, 0, 0};
+
+    static Box make(const int64_t* l, const int64_t* h) {
+        Box b;
+        for (int d = 0; d < 3; ++d) { b.lo[d] = l[d]; b.hi[d] = h[d]; }
+        return b.normalized();
+    }
+    bool empty() const { return hi[0] <= lo[0] || hi[1] <= lo[1] || hi[2] <= lo[2]; }
+    Box normalized() const { return empty() ? Box{} : *this; }
+    int64_t extent(int d) const { return hi[d] - lo[d]; }
+    uint64_t volume() const {
+        return empty() ? 0 : uint64_t(hi[0] - lo[0]) * uint64_t(hi[1] - lo[1]) * uint64_t(hi[2] - lo[2]);
+    }
+    bool operator==(const Box& o) const {
+        for (int d = 0; d < 3; ++d)
+            if (lo[d] != o.lo[d] || hi[d] != o.hi[d]) return false;
+        return true;
+    }
+    bool operator!=(const Box& o) const { return !(*this == o); }
+    bool contains(const Box& in) const {
+        if (in.empty()) return true;
+        if (empty()) return false;
+        for (int d = 0; d < 3; ++d)
+            if (in.lo[d] < lo[d] || in.hi[d] > hi[d]) return false;
+        return true;
+    }
+    Box with_dim(int d, int64_t l, int64_t h) const {
+        Box b = *this;
+        b.lo[d] = l;
+        b.hi[d] = h;
+        return b;
+    }
+};
+
+inline bool lex_less(const Box& a, const Box& b) {
+    for (int d = 0; d < 3; ++d)
+        if (a.lo[d] != b.lo[d]) return a.lo[d] < b.lo[d];
+    for (int d = 0; d < 3; ++d)
+        if (a.hi[d] != b.hi[d]) return a.hi[d] < b.hi[d];
+    return false;
+}
+
+inline Box intersect(const Box& a, const Box& b) {
+    Box r;
+    for (int d = 0; d < 3; ++d) {
+        r.lo[d] = std::max(a.lo[d], b.lo[d]);
+        r.hi[d] = std::min(a.hi[d], b.hi[d]);
+    }
+    return r.normalized();
+}
+
+inline Box bbox(const Box& a, const Box& b) {
+    if (a.empty()) return b.normalized();
+    if (b.empty()) return a;
+    Box r;
+    for (int d = 0; d < 3; ++d) {
+        r.lo[d] = std::min(a.lo[d], b.lo[d]);
+        r.hi[d] = std::max(a.hi[d], b.hi[d]);
+    }
+    return r;
+}
+
+using Region = std::vector<Box>;  // canonical (R2) unless stated otherwise
+
+// a \ b as disjoint boxes appended to out (peel slabs off dim 0, 1, 2).
+inline void subtract_into(const Box& a, const Box& b, std::vector<Box>& out) {
+    Box i = intersect(a, b);
+    if (i.empty()) {
+        if (!a.empty()) out.push_back(a);
+        return;
+    }
+    Box cur = a;
+    for (int d = 0; d < 3; ++d) {
+        if (cur.lo[d] < i.lo[d]) out.push_back(cur.with_dim(d, cur.lo[d], i.lo[d]));
+        if (i.hi[d] < cur.hi[d]) out.push_back(cur.with_dim(d, i.hi[d], cur.hi[d]));
+        cur = cur.with_dim(d, i.lo[d], i.hi[d]);
+    }
+}
+
+namespace detail {
+// Canonical boxes for the union of `bs` over dims d..2 (dims < d identical).
+inline void canon_dim(std::vector<Box>& bs, int d, std::vector<Box>& out) {
+    if (d == 2) {
+        std::sort(bs.begin(), bs.end(), [](const Box& a, const Box& b) {
+            return a.lo[2] != b.lo[2] ? a.lo[2] < b.lo[2] : a.hi[2] < b.hi[2];
+        });
+        int64_t cl = 0, ch = 0;
+        bool open = false;
+        const Box proto = bs[0];
+        for (const Box& b : bs) {
+            if (open && b.lo[2] <= ch) {
+                ch = std::max(ch, b.hi[2]);
+            } else {
+                if (open) out.push_back(proto.with_dim(2, cl, ch));
+                cl = b.lo[2];
+                ch = b.hi[2];
+                open = true;
+            }
+        }
+        if (open) out.push_back(proto.with_dim(2, cl, ch));
+        return;
+    }
+    std::vector<int64_t> cuts;
+    cuts.reserve(bs.size() * 2);
+    for (const Box& b : bs) {
+        cuts.push_back(b.lo[d]);
+        cuts.push_back(b.hi[d]);
+    }
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    // slabs: [lo, hi) with their canonical cross-section
+    std::vector<std::pair<std::pair<int64_t, int64_t>, std::vector<Box>>> slabs;
+    std::vector<Box> cover, sub;
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+        const int64_t lo = cuts[k], hi = cuts[k + 1];
+        cover.clear();
+        for (const Box& b : bs)
+            if (b.lo[d] <= lo && hi <= b.hi[d]) cover.push_back(b.with_dim(d, 0, 1));
+        if (cover.empty()) continue;
+        sub.clear();
+        canon_dim(cover, d + 1, sub);
+        if (!slabs.empty() && slabs.back().first.second == lo && slabs.back().second == sub) {
+            slabs.back().first.second = hi;
+        } else {
+            slabs.push_back({{lo, hi}, sub});
+        }
+    }
+    for (auto& s : slabs)
+        for (const Box& b : s.second) out.push_back(b.with_dim(d, s.first.first, s.first.second));
+}
+}  // namespace detail
+
+inline Region canon(std::vector<Box> boxes) {
+    boxes.erase(std::remove_if(boxes.begin(), boxes.end(), [](const Box& b) { return b.empty(); }), boxes.end());
+    Region out;
+    if (boxes.empty()) return out;
+    if (boxes.size() == 1) {
+        out.push_back(boxes[0]);
+        return out;
+    }
+    detail::canon_dim(boxes, 0, out);
+    return out;
+}
+
+inline Region region_of(const Box& b) { return b.empty() ? Region{} : Region{b}; }
+
+inline Region runion(const Region& a, const Region& b) {
+    if (a.empty()) return b;
+    if (b.empty()) return a;
+    std::vector<Box> all(a);
+    all.insert(all.end(), b.begin(), b.end());
+    return canon(std::move(all));
+}
+
+inline Region rinter(const Region& a, const Region& b) {
+    std::vector<Box> out;
+    for (const Box& x : a)
+        for (const Box& y : b) {
+            Box i = intersect(x, y);
+            if (!i.empty()) out.push_back(i);
+        }
+    if (out.size() <= 1) return out;
+    return canon(std::move(out));
+}
+
+inline Region rinter(const Region& a, const Box& b) { return rinter(a, region_of(b)); }
+
+inline Region rdiff(const Region& a, const Region& b) {
+    if (a.empty() || b.empty()) return a;
+    std::vector<Box> cur(a), nxt;
+    bool changed = false;
+    for (const Box& y : b) {
+        nxt.clear();
+        for (const Box& x : cur) {
+            Box i = intersect(x, y);
+            if (i.empty()) {
+                nxt.push_back(x);
+            } else {
+                changed = true;
+                subtract_into(x, y, nxt);
+            }
+        }
+        cur.swap(nxt);
+        if (cur.empty()) break;
+    }
+    if (!changed) return a;
+    return canon(std::move(cur));
+}
+
+inline uint64_t rvolume(const Region& r) {
+    uint64_t v = 0;
+    for (const Box& b : r) v += b.volume();
+    return v;
+}
+
+inline Box rbbox(const Region& r) {
+    Box out;
+    for (const Box& b : r) out = bbox(out, b);
+    return out;
+}
+
+inline bool rintersects(const Region& a, const Box& b) {
+    for (const Box& x : a)
+        if (!intersect(x, b).empty()) return true;
+    return false;
+}
+
+// Total map extent -> V (R3).  Entries sorted by value; regions canonical and
+// pairwise disjoint; their union is the extent.
+template <class V>
+struct RegionMap {
+    Box extent;
+    std::vector<std::pair<V, Region>> e;
+
+    RegionMap() = default;
+    RegionMap(const Box& ext, const V& dflt) : extent(ext) {
+        if (!ext.empty()) e.push_back({dflt, Region{ext}});
+    }
+
+    void put(const V& v, const Region& r) {
+        if (r.empty()) return;
+        auto it = std::lower_bound(e.begin(), e.end(), v,
+                                   [](const std::pair<V, Region>& p, const V& x) { return p.first < x; });
+        if (it != e.end() && it->first == v)
+            it->second = runion(it->second, r);
+        else
+            e.insert(it, {v, r});
+    }
+
+    void update(const Region& reg0, const V& v) {
+        Region reg = rinter(reg0, extent);
+        if (reg.empty()) return;
+        std::vector<std::pair<V, Region>> ne;
+        ne.reserve(e.size() + 1);
+        for (auto& p : e) {
+            Region rr = rdiff(p.second, reg);
+            if (!rr.empty()) ne.push_back({p.first, std::move(rr)});
+        }
+        e.swap(ne);
+        put(v, reg);
+    }
+
+    template <class F>
+    void apply(const Region& reg0, F fn) {
+        Region reg = rinter(reg0, extent);
+        if (reg.empty()) return;
+        std::vector<std::pair<V, Region>> old;
+        old.swap(e);
+        std::vector<std::pair<V, Region>> inside;
+        for (auto& p : old) {
+            Region in = rinter(p.second, reg);
+            if (in.empty()) {
+                put(p.first, p.second);
+                continue;
+            }
+            Region out = rdiff(p.second, reg);
+            if (!out.empty()) put(p.first, out);
+            inside.push_back({fn(p.first), std::move(in)});
+        }
+        for (auto& p : inside) put(p.first, p.second);
+    }
+
+    template <class F>
+    void map_values(F fn) {
+        std::vector<std::pair<V, Region>> old;
+        old.swap(e);
+        for (auto& p : old) put(fn(p.first), p.second);
+    }
+
+    // Partition of reg by value, sorted by value.
+    std::vector<std::pair<Region, V>> query(const Region& reg) const {
+        std::vector<std::pair<Region, V>> out;
+        if (reg.empty()) return out;
+        for (auto& p : e) {
+            Region i = rinter(p.second, reg);
+            if (!i.empty()) out.push_back({std::move(i), p.first});
+        }
+        return out;
+    }
+
+    template <class P>
+    Region where(P pred) const {
+        Region out;
+        for (auto& p : e)
+            if (pred(p.first)) out = runion(out, p.second);
+        return out;
+    }
+};
+
+}  // namespace cel

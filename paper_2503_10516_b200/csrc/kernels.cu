@@ -1,0 +1,578 @@
+// sm_100a kernels of the coherence path.
+//
+//  * copy_kernel   — Table 1 `copy`: one launch moves every box of a
+//    copy instruction's region (resize copies P:L351, coherence / d2d halo
+//    copies P:L371-378).  Persistent grid, 16 KiB row chunks per CTA
+//    iteration, 128-bit non-allocating loads/stores when the segment is
+//    16-byte aligned.  Destination pointers may be peer (NVLink) addresses:
+//    the copy then is an SM-driven push over NVSwitch.
+//  * workload kernels — the synthetic device-kernel instructions:
+//    fill, 1-D 3-point (Listing 5 shape), WaveSim 5-point,
+//    3-D 7-point, N-body timestep/update (Listing 1), RSim row
+//    (P:L632), integer probe.  Arithmetic order is exactly the oracle's
+//    (oracle/kernels.py); the library is built with -fmad=false (R16).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace cel {
+
+namespace {
+
+int g_copy_blocks_per_sm = 8;
+int g_num_sms = 0;
+
+int num_sms() {
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+// ------------------------------------------------------------------ copy
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void st_na_v4(void* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+template <class T>
+__device__ __forceinline__ void copy_span(const char* __restrict__ src, char* __restrict__ dst, uint32_t nbytes) {
+    const uint32_t n = nbytes / sizeof(T);
+    const T* s = reinterpret_cast<const T*>(src);
+    T* d = reinterpret_cast<T*>(dst);
+    uint32_t i = threadIdx.x;
+    constexpr int U = 4;
+    for (; i + (U - 1) * blockDim.x < n; i += U * blockDim.x) {
+        T v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) v[k] = s[i + k * blockDim.x];
+#pragma unroll
+        for (int k = 0; k < U; ++k) d[i + k * blockDim.x] = v[k];
+    }
+    for (; i < n; i += blockDim.x) d[i] = s[i];
+}
+
+template <>
+__device__ __forceinline__ void copy_span<uint4>(const char* __restrict__ src, char* __restrict__ dst, uint32_t nbytes) {
+    const uint32_t n = nbytes / 16;
+    uint32_t i = threadIdx.x;
+    constexpr int U = 4;
+    for (; i + (U - 1) * blockDim.x < n; i += U * blockDim.x) {
+        uint4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) v[k] = ld_nc_v4(src + 16ull * (i + k * blockDim.x));
+#pragma unroll
+        for (int k = 0; k < U; ++k) st_na_v4(dst + 16ull * (i + k * blockDim.x), v[k]);
+    }
+    for (; i < n; i += blockDim.x) st_na_v4(dst + 16ull * i, ld_nc_v4(src + 16ull * i));
+}
+
+__global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyArgs a) {
+    for (uint64_t u = blockIdx.x; u < a.total_units; u += gridDim.x) {
+        int s = 0;
+        while (s + 1 < a.nseg && a.seg[s + 1].units_begin <= u) ++s;
+        const CopySeg& g = a.seg[s];
+        const uint64_t lu = u - g.units_begin;
+        const uint64_t row_lin = lu / g.units_per_row;
+        const uint32_t chunk = uint32_t(lu - row_lin * g.units_per_row);
+        const uint64_t plane = row_lin / g.rows;
+        const uint64_t row = row_lin - plane * g.rows;
+        const uint64_t off = uint64_t(chunk) * kCopyUnit;
+        const char* src = g.src + plane * g.src_plane_stride + row * g.src_row_stride + off;
+        char* dst = g.dst + plane * g.dst_plane_stride + row * g.dst_row_stride + off;
+        const uint64_t rem = g.row_bytes - off;
+        const uint32_t nbytes = rem < kCopyUnit ? uint32_t(rem) : kCopyUnit;
+        switch (g.vec) {
+        case 16: copy_span<uint4>(src, dst, nbytes); break;
+        case 8: copy_span<uint2>(src, dst, nbytes); break;
+        case 4: copy_span<uint32_t>(src, dst, nbytes); break;
+        case 2: copy_span<uint16_t>(src, dst, nbytes); break;
+        default: copy_span<uint8_t>(src, dst, nbytes); break;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ int64_t off_of(const DAcc& A, int64_t z, int64_t y, int64_t x) {
+    return ((z - A.lo[0]) * A.n[1] + (y - A.lo[1])) * A.n[2] + (x - A.lo[2]);
+}
+template <class T>
+__device__ __forceinline__ T* ptr(const DAcc& A, int64_t z, int64_t y, int64_t x) {
+    return reinterpret_cast<T*>(A.base + off_of(A, z, y, x) * int64_t(A.es));
+}
+__device__ __forceinline__ int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+    h ^= h >> 16;
+    h *= 0x85EBCA6Bu;
+    h ^= h >> 13;
+    h *= 0xC2B2AE35u;
+    h ^= h >> 16;
+    return h;
+}
+
+__device__ __forceinline__ float init_value(uint64_t seed, uint64_t idx) {
+    const uint64_t h = splitmix64(seed + idx);
+    const float v = float(uint32_t(h >> 40));
+    return (2.0f * (v * 0x1p-24f)) - 1.0f;
+}
+
+// ------------------------------------------------------------------ fills
+__global__ void fill_hash_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& A = a.acc[0];
+    const DBox& b = A.box;
+    const int64_t n0 = b.hi[0] - b.lo[0], n1 = b.hi[1] - b.lo[1], n2 = b.hi[2] - b.lo[2];
+    const int64_t words = A.es / 4;
+    const int64_t total = n0 * n1 * n2 * words;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t w = t % words;
+        int64_t e = t / words;
+        const int64_t x = b.lo[2] + e % n2;
+        e /= n2;
+        const int64_t y = b.lo[1] + e % n1;
+        const int64_t z = b.lo[0] + e / n1;
+        const int64_t lin = (z * A.ext[1] + y) * A.ext[2] + x;
+        ptr<float>(A, z, y, x)[w] = init_value(a.seed, uint64_t(lin * words + w));
+    }
+}
+
+__global__ void fill_const_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& A = a.acc[0];
+    const DBox& b = A.box;
+    const int64_t n0 = b.hi[0] - b.lo[0], n1 = b.hi[1] - b.lo[1], n2 = b.hi[2] - b.lo[2];
+    const int64_t words = A.es / 4;
+    const int64_t total = n0 * n1 * n2 * words;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t w = t % words;
+        int64_t e = t / words;
+        const int64_t x = b.lo[2] + e % n2;
+        e /= n2;
+        const int64_t y = b.lo[1] + e % n1;
+        const int64_t z = b.lo[0] + e / n1;
+        ptr<float>(A, z, y, x)[w] = a.value;
+    }
+}
+
+// ------------------------------------------------------------------ C1 3-point
+__global__ void stencil3_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& S = a.acc[0];
+    const DAcc& D = a.acc[1];
+    const int64_t n = S.ext[0];
+    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const float xm = *ptr<const float>(S, clampi(i - 1, 0, n - 1), 0, 0);
+        const float xc = *ptr<const float>(S, i, 0, 0);
+        const float xp = *ptr<const float>(S, clampi(i + 1, 0, n - 1), 0, 0);
+        *ptr<float>(D, i, 0, 0) = (0.25f * xm + 0.5f * xc) + 0.25f * xp;
+    }
+}
+
+// ------------------------------------------------------------------ C2 WaveSim
+__device__ __forceinline__ float wave1(float uc, float up, float un, float us, float uw, float ue) {
+    const float lap = ((un + us) + (uw + ue)) - 4.0f * uc;
+    return (2.0f * uc - up) + 0.25f * lap;
+}
+
+// generic (scalar) path: any alignment
+__global__ void wave5_scalar(const __grid_constant__ KArgs a) {
+    const DAcc& U = a.acc[0];
+    const DAcc& P = a.acc[1];
+    const int64_t r0 = a.chunk.lo[0], c0 = a.chunk.lo[1];
+    const int64_t nr = a.chunk.hi[0] - r0, nc = a.chunk.hi[1] - c0;
+    const int64_t E0 = U.ext[0], E1 = U.ext[1];
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nr * nc; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = r0 + t / nc, c = c0 + t % nc;
+        const float uc = *ptr<const float>(U, r, c, 0);
+        const float un = *ptr<const float>(U, clampi(r - 1, 0, E0 - 1), c, 0);
+        const float us = *ptr<const float>(U, clampi(r + 1, 0, E0 - 1), c, 0);
+        const float uw = *ptr<const float>(U, r, clampi(c - 1, 0, E1 - 1), 0);
+        const float ue = *ptr<const float>(U, r, clampi(c + 1, 0, E1 - 1), 0);
+        float* pp = ptr<float>(P, r, c, 0);
+        *pp = wave1(uc, *pp, un, us, uw, ue);
+    }
+}
+
+constexpr int kWaveRows = 16;
+
+// vector path: 128 threads x float4 = 512 columns per CTA, a strip of kWaveRows
+// rows marched top to bottom with a 3-row register window; west/east
+// neighbours come from warp shuffles (scalar loads only at warp edges).
+__global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a) {
+    const DAcc& U = a.acc[0];
+    const DAcc& P = a.acc[1];
+    const int64_t r0 = a.chunk.lo[0], r1 = a.chunk.hi[0];
+    const int64_t c0 = a.chunk.lo[1], c1 = a.chunk.hi[1];
+    const int64_t E0 = U.ext[0], E1 = U.ext[1];
+    const int lane = threadIdx.x & 31;
+    const int64_t c = c0 + (int64_t(blockIdx.x) * 128 + threadIdx.x) * 4;
+    const bool valid = c < c1;
+    const int64_t rs = r0 + int64_t(blockIdx.y) * kWaveRows;
+    const int64_t re = rs + kWaveRows < r1 ? rs + kWaveRows : r1;
+    const float* ub = reinterpret_cast<const float*>(U.base);
+    float* pb = reinterpret_cast<float*>(P.base);
+    const int64_t uoff = c - U.lo[1];
+    const int64_t poff = c - P.lo[1];
+    auto urow = [&](int64_t r) { return ub + (r - U.lo[0]) * U.n[1]; };
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 prev = z4, cur = z4;
+    if (valid) {
+        prev = __ldg(reinterpret_cast<const float4*>(urow(rs > 0 ? rs - 1 : 0) + uoff));
+        cur = __ldg(reinterpret_cast<const float4*>(urow(rs) + uoff));
+    }
+    const bool need_e = valid && (lane == 31 || c + 4 >= c1);
+    const bool need_w = valid && lane == 0;
+    const int64_t cw = c > 0 ? c - 1 : 0;
+    const int64_t ce = c + 4 < E1 ? c + 4 : E1 - 1;
+#pragma unroll 2
+    for (int64_t r = rs; r < re; ++r) {
+        const int64_t rn = r + 1 < E0 ? r + 1 : E0 - 1;
+        float4 nxt = z4, up = z4;
+        float* prow = pb + (r - P.lo[0]) * P.n[1] + poff;
+        if (valid) {
+            nxt = __ldg(reinterpret_cast<const float4*>(urow(rn) + uoff));
+            up = *reinterpret_cast<const float4*>(prow);
+        }
+        float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
+        float e = __shfl_down_sync(0xffffffffu, cur.x, 1);
+        if (need_w) w = __ldg(urow(r) + (cw - U.lo[1]));
+        if (need_e) e = __ldg(urow(r) + (ce - U.lo[1]));
+        float4 o;
+        o.x = wave1(cur.x, up.x, prev.x, nxt.x, w, cur.y);
+        o.y = wave1(cur.y, up.y, prev.y, nxt.y, cur.x, cur.z);
+        o.z = wave1(cur.z, up.z, prev.z, nxt.z, cur.y, cur.w);
+        o.w = wave1(cur.w, up.w, prev.w, nxt.w, cur.z, e);
+        if (valid) *reinterpret_cast<float4*>(prow) = o;
+        prev = cur;
+        cur = nxt;
+    }
+}
+
+// ------------------------------------------------------------------ C5 Jacobi 7-point
+__device__ __forceinline__ float jac1(float c, float zm, float zp, float ym, float yp, float xm, float xp) {
+    return 0.25f * c + 0.125f * (((zm + zp) + (ym + yp)) + (xm + xp));
+}
+
+__global__ void jacobi7_scalar(const __grid_constant__ KArgs a) {
+    const DAcc& A = a.acc[0];
+    const DAcc& B = a.acc[1];
+    const DBox& ch = a.chunk;
+    const int64_t n0 = ch.hi[0] - ch.lo[0], n1 = ch.hi[1] - ch.lo[1], n2 = ch.hi[2] - ch.lo[2];
+    const int64_t E0 = A.ext[0], E1 = A.ext[1], E2 = A.ext[2];
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < n0 * n1 * n2; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t x = ch.lo[2] + t % n2;
+        const int64_t y = ch.lo[1] + (t / n2) % n1;
+        const int64_t z = ch.lo[0] + t / (n1 * n2);
+        const float c = *ptr<const float>(A, z, y, x);
+        const float zm = *ptr<const float>(A, clampi(z - 1, 0, E0 - 1), y, x);
+        const float zp = *ptr<const float>(A, clampi(z + 1, 0, E0 - 1), y, x);
+        const float ym = *ptr<const float>(A, z, clampi(y - 1, 0, E1 - 1), x);
+        const float yp = *ptr<const float>(A, z, clampi(y + 1, 0, E1 - 1), x);
+        const float xm = *ptr<const float>(A, z, y, clampi(x - 1, 0, E2 - 1));
+        const float xp = *ptr<const float>(A, z, y, clampi(x + 1, 0, E2 - 1));
+        *ptr<float>(B, z, y, x) = jac1(c, zm, zp, ym, yp, xm, xp);
+    }
+}
+
+constexpr int kJacZ = 16;
+
+__global__ void __launch_bounds__(128) jacobi7_vec(const __grid_constant__ KArgs a) {
+    const DAcc& A = a.acc[0];
+    const DAcc& B = a.acc[1];
+    const DBox& ch = a.chunk;
+    const int64_t E0 = A.ext[0], E1 = A.ext[1], E2 = A.ext[2];
+    const int lane = threadIdx.x & 31;
+    const int64_t x = ch.lo[2] + (int64_t(blockIdx.x) * 128 + threadIdx.x) * 4;
+    const bool valid = x < ch.hi[2];
+    const int64_t y = ch.lo[1] + blockIdx.y;
+    const int64_t zs = ch.lo[0] + int64_t(blockIdx.z) * kJacZ;
+    const int64_t ze = zs + kJacZ < ch.hi[0] ? zs + kJacZ : ch.hi[0];
+    const int64_t ym = y > 0 ? y - 1 : 0, yp = y + 1 < E1 ? y + 1 : E1 - 1;
+    const int64_t xw = x > 0 ? x - 1 : 0, xe = x + 4 < E2 ? x + 4 : E2 - 1;
+    const float* ab = reinterpret_cast<const float*>(A.base);
+    float* bb = reinterpret_cast<float*>(B.base);
+    auto arow = [&](int64_t z, int64_t yy) { return ab + ((z - A.lo[0]) * A.n[1] + (yy - A.lo[1])) * A.n[2] - A.lo[2]; };
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 prev = z4, cur = z4;
+    if (valid) {
+        prev = __ldg(reinterpret_cast<const float4*>(arow(zs > 0 ? zs - 1 : 0, y) + x));
+        cur = __ldg(reinterpret_cast<const float4*>(arow(zs, y) + x));
+    }
+    const bool need_e = valid && (lane == 31 || x + 4 >= ch.hi[2]);
+    const bool need_w = valid && lane == 0;
+    for (int64_t z = zs; z < ze; ++z) {
+        const int64_t zn = z + 1 < E0 ? z + 1 : E0 - 1;
+        float4 nxt = z4, fm = z4, fp = z4;
+        if (valid) {
+            nxt = __ldg(reinterpret_cast<const float4*>(arow(zn, y) + x));
+            fm = __ldg(reinterpret_cast<const float4*>(arow(z, ym) + x));
+            fp = __ldg(reinterpret_cast<const float4*>(arow(z, yp) + x));
+        }
+        float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
+        float e = __shfl_down_sync(0xffffffffu, cur.x, 1);
+        if (need_w) w = __ldg(arow(z, y) + xw);
+        if (need_e) e = __ldg(arow(z, y) + xe);
+        float4 o;
+        o.x = jac1(cur.x, prev.x, nxt.x, fm.x, fp.x, w, cur.y);
+        o.y = jac1(cur.y, prev.y, nxt.y, fm.y, fp.y, cur.x, cur.z);
+        o.z = jac1(cur.z, prev.z, nxt.z, fm.z, fp.z, cur.y, cur.w);
+        o.w = jac1(cur.w, prev.w, nxt.w, fm.w, fp.w, cur.z, e);
+        if (valid)
+            *reinterpret_cast<float4*>(bb + ((z - B.lo[0]) * B.n[1] + (y - B.lo[1])) * B.n[2] + (x - B.lo[2])) = o;
+        prev = cur;
+        cur = nxt;
+    }
+}
+
+// ------------------------------------------------------------------ C3 N-body
+constexpr float NB_DT = 0x1p-7f;
+constexpr float NB_MASS = 0x1p-20f;
+constexpr float NB_EPS2 = 0x1p-10f;
+constexpr int kNbTile = 256;
+
+__global__ void __launch_bounds__(kNbTile) nbody_step_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& P = a.acc[0];
+    const DAcc& V = a.acc[1];
+    __shared__ float4 sp[kNbTile];
+    const int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * kNbTile + threadIdx.x;
+    const bool valid = i < a.chunk.hi[0];
+    const int64_t N = P.ext[0];
+    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) pi = *ptr<const float4>(P, i, 0, 0);
+    float ax = 0.f, ay = 0.f, az = 0.f;
+    for (int64_t j0 = 0; j0 < N; j0 += kNbTile) {
+        const int64_t j = j0 + threadIdx.x;
+        sp[threadIdx.x] = j < N ? *ptr<const float4>(P, j, 0, 0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        const int jn = N - j0 < kNbTile ? int(N - j0) : kNbTile;
+        for (int k = 0; k < jn; ++k) {
+            const float4 pj = sp[k];
+            const float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+            const float r2 = ((dx * dx + dy * dy) + dz * dz) + NB_EPS2;
+            const float inv = 1.0f / sqrtf(r2);
+            const float s = (inv * inv) * inv;
+            ax = ax + dx * s;
+            ay = ay + dy * s;
+            az = az + dz * s;
+        }
+        __syncthreads();
+    }
+    if (valid) {
+        float4* vp = ptr<float4>(V, i, 0, 0);
+        float4 v = *vp;
+        const float c = NB_DT * NB_MASS;
+        v.x = v.x + c * ax;
+        v.y = v.y + c * ay;
+        v.z = v.z + c * az;
+        *vp = v;
+    }
+}
+
+__global__ void nbody_update_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& V = a.acc[0];
+    const DAcc& P = a.acc[1];
+    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = *ptr<const float4>(V, i, 0, 0);
+        float4* pp = ptr<float4>(P, i, 0, 0);
+        float4 p = *pp;
+        p.x = p.x + NB_DT * v.x;
+        p.y = p.y + NB_DT * v.y;
+        p.z = p.z + NB_DT * v.z;
+        *pp = p;
+    }
+}
+
+// ------------------------------------------------------------------ C4 RSim row
+__global__ void rsim_row_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& R = a.acc[0];
+    const DAcc& Wr = a.acc[1];
+    const int64_t t = a.t;
+    const int64_t W = R.ext[1];
+    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
+         i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        int64_t col = i;
+        for (int64_t s = 0; s < t; ++s) {
+            acc = acc + *ptr<const float>(R, s, col, 0);
+            col = col + 1 == W ? 0 : col + 1;
+        }
+        const float prev = *ptr<const float>(R, t - 1, i, 0);
+        const float coef = 0.5f / float(t);
+        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
+    }
+}
+
+// ------------------------------------------------------------------ integer probe
+__device__ uint32_t probe_sum(const DAcc& A, int64_t z, int64_t y, int64_t x) {
+    if (A.mode == 3 || A.map == 0)  // read_write or one_to_one: the element itself
+        return *ptr<const uint32_t>(A, z, y, x);
+    int64_t lo[3], hi[3];
+    if (A.map == 2) {  // all
+        for (int d = 0; d < 3; ++d) { lo[d] = 0; hi[d] = A.ext[d]; }
+    } else if (A.map == 3) {  // fixed
+        for (int d = 0; d < 3; ++d) { lo[d] = A.fixed.lo[d]; hi[d] = A.fixed.hi[d]; }
+    } else {  // neighborhood
+        const int64_t p[3] = {z, y, x};
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = p[d] - A.border[d] < 0 ? 0 : p[d] - A.border[d];
+            hi[d] = p[d] + A.border[d] + 1 > A.ext[d] ? A.ext[d] : p[d] + A.border[d] + 1;
+        }
+    }
+    uint32_t s = 0;
+    for (int64_t a0 = lo[0]; a0 < hi[0]; ++a0)
+        for (int64_t a1 = lo[1]; a1 < hi[1]; ++a1)
+            for (int64_t a2 = lo[2]; a2 < hi[2]; ++a2) s += *ptr<const uint32_t>(A, a0, a1, a2);
+    return s;
+}
+
+__global__ void probe_kernel(const __grid_constant__ KArgs a, int w) {
+    const DAcc& O = a.acc[w];
+    const DBox& b = O.box;
+    const int64_t n1 = b.hi[1] - b.lo[1], n2 = b.hi[2] - b.lo[2];
+    const int64_t total = (b.hi[0] - b.lo[0]) * n1 * n2;
+    for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t x = b.lo[2] + t % n2;
+        const int64_t y = b.lo[1] + (t / n2) % n1;
+        const int64_t z = b.lo[0] + t / (n1 * n2);
+        const uint32_t lin = uint32_t((z * O.ext[1] + y) * O.ext[2] + x);
+        uint32_t h = fmix32((a.salt + uint32_t(w)) ^ fmix32(lin));
+        for (int i = 0; i < a.n_acc; ++i) {
+            const DAcc& A = a.acc[i];
+            if (A.mode != 1 && A.mode != 3) continue;
+            h = fmix32(h ^ probe_sum(A, z, y, x));
+        }
+        *ptr<uint32_t>(O, z, y, x) = h;
+    }
+}
+
+int grid_for(int64_t work, int threads) {
+    int64_t g = (work + threads - 1) / threads;
+    const int64_t cap = int64_t(num_sms()) * 16;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return int(g);
+}
+
+int64_t vol(const DBox& b) {
+    int64_t v = 1;
+    for (int d = 0; d < 3; ++d) {
+        const int64_t e = b.hi[d] - b.lo[d];
+        if (e <= 0) return 0;
+        v *= e;
+    }
+    return v;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+void set_copy_blocks_per_sm(int n) { g_copy_blocks_per_sm = n > 0 ? n : 8; }
+
+int launch_copy(const CopyArgs& a, cudaStream_t s) {
+    if (a.total_units == 0 || a.nseg == 0) return 0;
+    int64_t grid = int64_t(num_sms()) * g_copy_blocks_per_sm;
+    if (int64_t(a.total_units) < grid) grid = int64_t(a.total_units);
+    copy_kernel<<<unsigned(grid), 256, 0, s>>>(a);
+    return 1;
+}
+
+int launch_workload(const KArgs& a, cudaStream_t s) {
+    const int64_t cv = vol(a.chunk);
+    switch (a.kind) {
+    case K_FILL_HASH:
+    case K_FILL_CONST: {
+        const int64_t work = vol(a.acc[0].box) * (a.acc[0].es / 4);
+        if (work == 0) return 0;
+        if (a.kind == K_FILL_HASH)
+            fill_hash_kernel<<<grid_for(work, 256), 256, 0, s>>>(a);
+        else
+            fill_const_kernel<<<grid_for(work, 256), 256, 0, s>>>(a);
+        return 1;
+    }
+    case K_STENCIL3:
+        if (cv == 0) return 0;
+        stencil3_kernel<<<grid_for(cv, 256), 256, 0, s>>>(a);
+        return 1;
+    case K_WAVE5: {
+        if (cv == 0) return 0;
+        const DAcc& U = a.acc[0];
+        const DAcc& P = a.acc[1];
+        const int64_t c0 = a.chunk.lo[1], w = a.chunk.hi[1] - c0;
+        const bool vec = U.es == 4 && P.es == 4 && U.n[2] == 1 && P.n[2] == 1 && U.n[1] % 4 == 0 &&
+                         P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
+                         aligned16(U.base) && aligned16(P.base);
+        if (vec) {
+            dim3 grid(unsigned((w / 4 + 127) / 128), unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kWaveRows - 1) / kWaveRows));
+            wave5_vec<<<grid, 128, 0, s>>>(a);
+        } else {
+            wave5_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);
+        }
+        return 1;
+    }
+    case K_JACOBI7: {
+        if (cv == 0) return 0;
+        const DAcc& A = a.acc[0];
+        const DAcc& B = a.acc[1];
+        const int64_t x0 = a.chunk.lo[2], w = a.chunk.hi[2] - x0;
+        const bool vec = A.es == 4 && B.es == 4 && A.n[2] % 4 == 0 && B.n[2] % 4 == 0 && (x0 - A.lo[2]) % 4 == 0 &&
+                         (x0 - B.lo[2]) % 4 == 0 && w % 4 == 0 && aligned16(A.base) && aligned16(B.base);
+        if (vec) {
+            dim3 grid(unsigned((w / 4 + 127) / 128), unsigned(a.chunk.hi[1] - a.chunk.lo[1]),
+                      unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kJacZ - 1) / kJacZ));
+            jacobi7_vec<<<grid, 128, 0, s>>>(a);
+        } else {
+            jacobi7_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);
+        }
+        return 1;
+    }
+    case K_NBODY_STEP: {
+        if (cv == 0) return 0;
+        const int64_t n = a.chunk.hi[0] - a.chunk.lo[0];
+        nbody_step_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
+        return 1;
+    }
+    case K_NBODY_UPDATE:
+        if (cv == 0) return 0;
+        nbody_update_kernel<<<grid_for(cv, 256), 256, 0, s>>>(a);
+        return 1;
+    case K_RSIM_ROW:
+        if (cv == 0) return 0;
+        rsim_row_kernel<<<grid_for(cv, 128), 128, 0, s>>>(a);
+        return 1;
+    case K_PROBE: {
+        int n = 0;
+        for (int w = 0; w < a.n_acc; ++w) {
+            if (a.acc[w].mode != 2 && a.acc[w].mode != 3) continue;
+            const int64_t work = vol(a.acc[w].box);
+            if (work == 0) continue;
+            probe_kernel<<<grid_for(work, 128), 128, 0, s>>>(a, w);
+            ++n;
+        }
+        return n;
+    }
+    default:
+        return 0;
+    }
+}
+
+}  // namespace cel

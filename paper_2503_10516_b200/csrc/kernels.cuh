@@ -1,0 +1,85 @@
+// Device kernels of the coherence path (sm_100a).  Launch wrappers are
+// called by the executor; no torch types anywhere.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace cel {
+
+// ---- copy instruction (Table 1 `copy`): a region = several boxes,
+// each lowered to a strided segment  planes x rows x row_bytes.
+struct CopySeg {
+    const char* src;
+    char* dst;
+    uint64_t row_bytes;
+    uint64_t src_row_stride, dst_row_stride;
+    uint64_t src_plane_stride, dst_plane_stride;
+    uint32_t rows, planes;
+    uint64_t units_begin;      // prefix sum of work units (exclusive)
+    uint32_t units_per_row;
+    uint32_t vec;              // 16, 8, 4, 2 or 1 byte accesses
+};
+
+constexpr int kMaxSegs = 24;
+constexpr uint32_t kCopyUnit = 16384;     // bytes of one row chunk per CTA iteration
+
+struct CopyArgs {
+    CopySeg seg[kMaxSegs];
+    int nseg;
+    uint64_t total_units;
+};
+
+// ---- accessor (allocation pointer interpolated into the accessor)
+struct DBox {
+    int64_t lo[3], hi[3];
+};
+
+struct DAcc {
+    char* base;                // allocation base
+    int64_t lo[3];             // allocation box min
+    int64_t n[3];              // allocation box extent
+    int64_t ext[3];            // buffer extent
+    uint32_t es;               // element size in bytes
+    int mode;                  // 1 read, 2 write, 3 read_write
+    int map;                   // mapper kind
+    int64_t border[3];
+    DBox fixed;
+    DBox box;                  // mapped box of this access for the chunk
+};
+
+constexpr int kMaxAcc = 6;
+
+struct KArgs {
+    int kind;
+    int n_acc;
+    DBox chunk;
+    uint64_t seed;
+    float value;
+    uint32_t t;
+    uint32_t salt;
+    DAcc acc[kMaxAcc];
+};
+
+// kernel kinds (mirror include/cel.h cel_kernel)
+enum : int {
+    K_FILL_HASH = 0,
+    K_FILL_CONST = 1,
+    K_STENCIL3 = 2,
+    K_WAVE5 = 3,
+    K_JACOBI7 = 4,
+    K_NBODY_STEP = 5,
+    K_NBODY_UPDATE = 6,
+    K_RSIM_ROW = 7,
+    K_PROBE = 8,
+    K_CALLBACK = 9,
+    K_NUM = 10,
+};
+
+// Returns the number of kernel launches issued (0 if nothing to do).
+int launch_copy(const CopyArgs& a, cudaStream_t s);
+int launch_workload(const KArgs& a, cudaStream_t s);
+
+void set_copy_blocks_per_sm(int n);
+
+}  // namespace cel

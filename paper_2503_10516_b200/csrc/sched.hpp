@@ -1,0 +1,229 @@
+// Host scheduler: task tracking + horizons, lookahead, instruction-graph (IDAG)
+// generation.  One node, G local devices ("manage all devices of a
+// multi-GPU node within a single process").  Rules R0-R14 of DESIGN.md.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "geom.hpp"
+
+namespace cel {
+
+// ---- error codes (mirror include/cel.h)
+enum : int {
+    E_OK = 0,
+    W_UNINIT_READ = 1,
+    E_INVALID = -1,
+    E_OUT_OF_BOUNDS = -2,
+    E_OVERLAPPING_WRITE = -3,
+    E_OOM = -4,
+    E_CUDA = -5,
+    E_NCCL = -6,
+    E_STATE = -7,
+};
+
+enum class MapKind : int { OneToOne = 0, Neighborhood = 1, All = 2, Fixed = 3, Remap = 4 };
+
+struct Mapper {
+    MapKind kind = MapKind::OneToOne;
+    int64_t border[3] = {0, 0, 0};
+    Box fixed;                        // Fixed / Remap (not normalised for Remap)
+    int from_kernel_dim[3] = {-1, -1, -1};
+};
+
+enum Mode : int { MODE_READ = 1, MODE_WRITE = 2, MODE_READ_WRITE = 3 };
+
+struct Access {
+    uint32_t buf = 0;
+    int mode = MODE_READ;
+    Mapper map;
+};
+
+struct KParams {                      // workload kernel parameters (see include/cel.h)
+    uint64_t seed = 0;
+    float value = 0.f;
+    uint32_t t = 0;
+    uint32_t salt = 0;
+};
+
+using KernelFn = void (*)(void* user, int device, const void* chunk, const void* acc, int n_acc, void* stream);
+
+struct TaskDesc {
+    int dims = 1;
+    Box range;
+    int split = 0;                    // 0 = 1D, 1 = 2D
+    int kernel = 0;
+    KParams params;
+    KernelFn fn = nullptr;
+    void* fn_user = nullptr;
+    std::vector<Access> acc;
+};
+
+enum class IKind : uint8_t { Alloc, Free, Copy, Kernel, Horizon, Epoch };
+enum CopyReason : int { REASON_RESIZE = 0, REASON_COHERENCE = 1, REASON_READBACK = 2 };
+
+constexpr int64_t NONE = -1;          // no writer (uninitialised)
+constexpr int64_t HOST_AID = -1;      // implicit M0 allocation of a host-initialised buffer
+constexpr int64_t USER_AID = -2;      // user pointer of a readback
+
+struct Instr {
+    uint64_t iid = 0;
+    IKind kind = IKind::Epoch;
+    int64_t task = -1;                // -1 = none
+    uint32_t buffer = 0;
+    // alloc / free
+    int64_t aid = 0;
+    int mem = 0;
+    Box box;
+    // copy
+    int reason = 0;
+    int64_t src_aid = 0, dst_aid = 0;
+    int src_mem = 0, dst_mem = 0;
+    Region region;
+    int64_t readback = -1;
+    // kernel
+    int device = -1;
+    Box chunk;
+    std::vector<int64_t> bindings;
+    std::shared_ptr<const TaskDesc> desc;
+    // all
+    std::vector<uint64_t> deps;
+};
+
+struct InstrSink {
+    virtual ~InstrSink() = default;
+    virtual void on_instr(const Instr& ins) = 0;   // called in iid (topological) order
+};
+
+struct SchedStats {
+    uint64_t n_by_kind[8] = {};
+    uint64_t copies_by_reason[3] = {};
+    uint64_t bytes_by_reason[3] = {};
+    uint64_t bytes_d2d_peer = 0;
+    uint64_t alloc_bytes_live = 0, alloc_bytes_peak = 0;
+    uint64_t flushes = 0;
+};
+
+class Scheduler {
+public:
+    Scheduler(int n_devices, int lookahead, int horizon_step, bool checks, InstrSink* sink, FILE* log);
+    ~Scheduler();
+
+    int buffer_create(int dims, const int64_t extent[3], uint32_t elem_size, bool host_init, uint32_t* out);
+    int task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string* err);
+    void wait();
+    int readback(uint32_t bid, const Box& box, int64_t* rb_out, std::string* err);
+    int destroy(uint32_t bid, std::string* err);
+    void shutdown();
+
+    uint32_t elem_size(uint32_t bid) const;
+    Box extent(uint32_t bid) const;
+    bool has_buffer(uint32_t bid) const;
+    const SchedStats& stats() const { return st_; }
+    int64_t next_readback_id() const { return next_rb_; }
+    uint64_t next_iid() const { return next_iid_; }
+
+private:
+    struct Alloc {
+        int64_t aid;
+        uint32_t buffer;
+        int mem;
+        Box box;
+        int64_t iid;                                  // alloc instruction, -1 for HOST_AID
+        RegionMap<int64_t> last_writer;
+        RegionMap<std::vector<int64_t>> readers;
+    };
+    struct Buf {
+        uint32_t bid;
+        int dims;
+        Box extent;
+        uint32_t elem_size;
+        bool host_init;
+        RegionMap<int64_t> orig_writer;               // P:L372 "original producer"
+        RegionMap<uint32_t> uptodate;                 // P:L371 bit m = memory Mm
+        std::map<int, std::vector<Alloc*>> live;      // non-overlapping per memory
+        std::unique_ptr<Alloc> host;
+    };
+    struct TBuf {                                     // task-graph tracking
+        RegionMap<int64_t> last_writer;
+        RegionMap<std::vector<int64_t>> readers;
+        Region initialized;
+    };
+    using Key = std::pair<int, uint32_t>;             // (device, buffer)
+    struct Cmd {
+        int kind = 0;                                 // 0 task, 1 horizon, 2 epoch, 3 destroy
+        int64_t tid = -1;
+        std::shared_ptr<const TaskDesc> desc;
+        std::vector<Box> chunks;
+        std::map<Key, Region> reads, writes;
+        std::map<Key, Box> req;
+        int64_t rb = -1;
+        uint32_t rb_buf = 0;
+        Box rb_box;
+        std::vector<uint32_t> destroy;
+    };
+
+    // task graph (R7)
+    int64_t tdag_submit(const std::map<uint32_t, Region>& reads, const std::map<uint32_t, Region>& writes);
+    int64_t tdag_horizon();
+    int64_t tdag_epoch();
+    void tdag_subsume(int64_t h);
+    // lookahead (R8)
+    void push(Cmd&& c);
+    void flush();
+    bool is_allocating(const Cmd& c) const;
+    std::map<std::pair<uint32_t, int>, Box> anticipated(const std::vector<Cmd>& q) const;
+    void epoch_cmd(Cmd&& c);
+    // IDAG (R9-R14)
+    void compile(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant);
+    void compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant);
+    void compile_horizon(Cmd& c);
+    void compile_epoch(Cmd& c);
+    uint64_t emit(Instr& ins, std::vector<uint64_t>& deps);
+    Alloc* new_alloc(uint32_t bid, int mem, const Box& box, int64_t tid);
+    void free_alloc(Alloc* a, int64_t tid);
+    uint64_t copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Alloc* dst, const Region& reg, int64_t rb);
+    std::map<std::tuple<int64_t, int, int64_t>, Region> source_parts(Buf& buf, const Region& need, int m_dst);
+    void subsume(int64_t h);
+    void log_instr(const Instr& ins);
+    int prepare(const TaskDesc& d, Cmd& c, std::string* err) const;
+
+    int G_;
+    int mode_;
+    bool checks_;
+    InstrSink* sink_;
+    FILE* log_;
+    SchedStats st_;
+
+    // task graph
+    int64_t next_tid_ = 1;
+    std::unordered_map<int64_t, int64_t> cp_;
+    int64_t t_fallback_ = 0, t_pending_h_ = -1, max_cp_ = 0, cp_ref_ = 0;
+    int horizon_step_;
+    std::map<uint32_t, TBuf> tbufs_;
+
+    // lookahead
+    std::vector<Cmd> queue_;
+    int counter_ = 0;
+
+    // IDAG
+    std::map<uint32_t, std::unique_ptr<Buf>> bufs_;
+    std::unordered_map<int64_t, std::unique_ptr<Alloc>> allocs_;
+    std::vector<uint64_t> front_;                     // sorted
+    uint64_t next_iid_ = 1;
+    int64_t fallback_ = 0, pending_h_ = -1;
+    int64_t next_aid_ = 1;
+    int64_t next_rb_ = 0;
+    uint32_t next_bid_ = 0;
+    bool shut_ = false;
+};
+
+}  // namespace cel

@@ -1,0 +1,136 @@
+"""CPU tests of the C-ABI library (no GPU): it loads, exports every symbol
+include/cel.h declares, and its scheduler (execute=0: instruction graph only,
+no CUDA call) produces exactly the oracle's instruction log — record for
+record, dependencies included — on every config and on random programs."""
+
+import json
+import os
+import re
+
+import pytest
+
+from oracle.invariants import check
+from oracle.scheduler import Runtime as OracleRuntime
+from oracle.scheduler import run_program
+from workloads import programs as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def cel():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2503_10516_b200 import cel as c
+    return c
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "cel.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(cel_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol(cel):
+    names = header_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(cel.lib, n), n
+    assert sorted(cel.SYMBOLS) == names
+
+
+def test_no_gpu_means_loud_failure(cel):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(cel.CelError) as e:
+        cel.Runtime(1, execute=True)
+    assert e.value.code == cel.E_CUDA
+
+
+def both_logs(cel, prog, G, mode, step=4, tmp="/tmp/cel_cpu_log.jsonl"):
+    o = OracleRuntime(G, lookahead=mode, horizon_step=step)
+    run_program(o, prog)
+    r = cel.Runtime(G, execute=False, lookahead=mode, horizon_step=step, instr_log_path=tmp)
+    run_program(r, prog)
+    c = [json.loads(line) for line in open(tmp)]
+    return o, c
+
+
+def assert_same(o, c):
+    assert len(o.log) == len(c)
+    for a, b in zip(o.log, c):
+        assert a == b
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("mode", ["none", "auto", "infinite"])
+def test_config_logs_match_oracle(cel, G, mode):
+    for prog in (P.c1_chain(), P.wavesim(48, 9), P.nbody(40, 3, host_init=True), P.nbody(40, 2),
+                 P.rsim(30, 12), P.jacobi3d(10, 3), P.listing5(20)):
+        o, c = both_logs(cel, prog, G, mode)
+        assert_same(o, c)
+        check(c, o.buf_meta, o.tasks)          # the C++ graph passes the brute-force checker
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4, 8])
+def test_random_logs_match_oracle(cel, G):
+    for s in range(30):
+        prog = P.random_program(7000 + 31 * G + s)
+        for mode in ("none", "auto"):
+            o, c = both_logs(cel, prog, G, mode, step=2 + s % 3)
+            assert_same(o, c)
+
+
+def test_full_size_instruction_counts(cel):
+    """Instruction parity at BASELINE sizes (execute=0 is cheap: regions only)."""
+    for prog, G in ((P.wavesim(16384, 12), 8), (P.jacobi3d(1024, 4), 8), (P.nbody(1 << 20, 3), 8),
+                    (P.c1_chain(), 2)):
+        o, c = both_logs(cel, prog, G, "auto")
+        assert_same(o, c)
+
+
+def test_rsim_full_size_lookahead(cel):
+    """Config 4 at W=84,000, T=256: auto allocates once per memory, none resizes every step."""
+    prog = P.rsim(84000, 256)
+    o, c = both_logs(cel, prog, 4, "auto")
+    assert_same(o, c)
+    assert sum(1 for r in c if r["kind"] == "alloc") == 4
+    o, c = both_logs(cel, prog, 4, "none")
+    assert_same(o, c)
+    assert sum(1 for r in c if r["kind"] == "alloc") == 4 * 256
+
+
+def test_errors_and_warnings(cel):
+    r = cel.Runtime(2, execute=False)
+    a = r.buffer_create(1, [16], 4)
+    b = r.buffer_create(1, [16], 4)
+    full = ([0], [16])
+    with pytest.raises(cel.CelError) as e:       # writing accessor with an all mapper
+        r.task_submit({"dims": 1, "range": full, "kernel": "probe", "params": {"salt": 1},
+                       "accesses": [(a, "write", ("all",))]})
+    assert e.value.code == cel.E_OVERLAPPING_WRITE
+    with pytest.raises(cel.CelError) as e:
+        r.task_submit({"dims": 1, "range": ([0], [20]), "kernel": "probe", "params": {"salt": 1},
+                       "accesses": [(a, "write", ("one_to_one",))]})
+    assert e.value.code == cel.E_OUT_OF_BOUNDS
+    with pytest.raises(cel.CelError) as e:
+        r.task_submit({"dims": 1, "range": full, "kernel": "probe", "params": {"salt": 1},
+                       "accesses": [(a, "read", ("fixed", ([0], [40])))]})
+    assert e.value.code == cel.E_OUT_OF_BOUNDS
+    with pytest.raises(cel.CelError) as e:
+        r.task_submit({"dims": 1, "range": full, "kernel": "probe", "params": {"salt": 1},
+                       "accesses": [(99, "write", ("one_to_one",))]})
+    assert e.value.code == cel.E_INVALID
+    # rejected tasks left no trace: the first accepted task is tid 1
+    tid, st = r.task_submit({"dims": 1, "range": ([0], [8]), "kernel": "probe", "params": {"salt": 1},
+                             "accesses": [(a, "write", ("one_to_one",))]})
+    assert (tid, st) == (1, 0)
+    tid, st = r.task_submit({"dims": 1, "range": full, "kernel": "probe", "params": {"salt": 2},
+                             "accesses": [(a, "read", ("one_to_one",)), (b, "write", ("one_to_one",))]})
+    assert st == cel.W_UNINIT_READ
+    r.buffer_destroy(a)
+    with pytest.raises(cel.CelError):
+        r.task_submit({"dims": 1, "range": full, "kernel": "probe", "params": {"salt": 3},
+                       "accesses": [(a, "write", ("one_to_one",))]})
+    r.shutdown()

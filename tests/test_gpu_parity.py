@@ -1,0 +1,183 @@
+"""GPU parity: the CUDA path (C-ABI, sm_100a kernels) against the CPU oracle.
+
+Bit-exact for every readback (integer probes and fp32 under -fmad=false, R16)
+and record-for-record equality of the instruction logs.  Several virtual
+devices may share one physical GPU (the multi-device logic — separate
+allocations, streams, d2d copies — is exercised on one B200); with >= 2 GPUs
+the same programs also run across physical devices (peer copies over NVLink).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import geometry as g  # noqa: E402
+from oracle.kernels import Acc, init_value, k_wave5, nbody_accel_one  # noqa: E402
+from oracle.scheduler import Runtime as OracleRuntime  # noqa: E402
+from oracle.scheduler import run_program  # noqa: E402
+from oracle.simulate import simulate  # noqa: E402
+from workloads import programs as P  # noqa: E402
+
+LOG = "/tmp/cel_gpu_log.jsonl"
+
+
+@pytest.fixture(scope="module")
+def cel():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2503_10516_b200 import cel as c
+    return c
+
+
+def run_both(cel, prog, G, mode="auto", devices=None, arena=256 << 20, step=4):
+    devices = devices if devices is not None else [0] * G
+    rt = cel.Runtime(G, cuda_devices=devices, lookahead=mode, arena_bytes=arena, instr_log_path=LOG,
+                     horizon_step=step)
+    got = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
+    o = OracleRuntime(G, lookahead=mode, horizon_step=step)
+    run_program(o, prog)
+    exp = simulate(o)
+    log = [json.loads(line) for line in open(LOG)]
+    assert log == o.log, "instruction log differs from the oracle"
+    for k, arr in enumerate(got):
+        e = exp[k]
+        defined = e != np.uint32(0x7FC00BAD)      # never-written elements are not compared (R6)
+        if not np.array_equal(arr[defined], e[defined]):
+            bad = np.argwhere((arr != e) & defined)
+            raise AssertionError("readback %d: %d mismatches, first at %s" % (k, len(bad), bad[:3].tolist()))
+    return rt
+
+
+def test_smoke(cel):
+    import __graft_entry__
+    __graft_entry__.smoke()
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_random_programs(cel, G):
+    for s in range(12):
+        prog = P.random_program(9000 + 17 * G + s)
+        for mode in ("none", "auto"):
+            run_both(cel, prog, G, mode, arena=32 << 20, step=2 + s % 3)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4])
+@pytest.mark.parametrize("mode", ["none", "auto"])
+def test_c1_chain(cel, G, mode):
+    run_both(cel, P.c1_chain(4096), G, mode)
+
+
+@pytest.mark.parametrize("G,rows,cols", [(1, 64, 512), (2, 300, 1040), (3, 257, 2048), (4, 130, 516), (2, 77, 101)])
+def test_wavesim_ragged(cel, G, rows, cols):
+    # several strips and CTAs, ragged tails; cols=101 takes the scalar kernel
+    run_both(cel, P.wavesim(cols, 9, rows=rows), G)
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+def test_jacobi3d(cel, G):
+    run_both(cel, P.jacobi3d(36, 5), G)
+
+
+def test_jacobi3d_ragged(cel):
+    prog = P.jacobi3d(20, 3)
+    run_both(cel, prog, 6)
+
+
+@pytest.mark.parametrize("G", [1, 3])
+def test_nbody(cel, G):
+    run_both(cel, P.nbody(1000, 2), G)
+    run_both(cel, P.nbody(300, 2, host_init=True), G)
+
+
+@pytest.mark.parametrize("G,mode", [(1, "auto"), (2, "auto"), (2, "none"), (4, "none"), (3, "infinite")])
+def test_rsim(cel, G, mode):
+    run_both(cel, P.rsim(1000, 24), G, mode)
+
+
+def test_physical_multi_gpu(cel):
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    devs = list(range(n))
+    run_both(cel, P.wavesim(1024, 7, rows=600), n, devices=devs)
+    run_both(cel, P.nbody(2048, 2), n, devices=devs)
+    run_both(cel, P.jacobi3d(40, 3), n, devices=devs)
+    run_both(cel, P.rsim(2000, 16), n, "none", devices=devs)
+    for s in range(6):
+        run_both(cel, P.random_program(500 + s), n, devices=devs, arena=32 << 20)
+
+
+# ---------------------------------------------------------------- full size
+def light_cone_wave(rows_lo, rows_hi, n, steps, seed=2):
+    """Oracle values of rows [rows_lo, rows_hi) of the 16384^2 WaveSim after
+    `steps` steps, computed on the light cone only (rows +- steps)."""
+    a = max(0, rows_lo - steps - 1)
+    b = min(n, rows_hi + steps + 1)
+    ext = g.box([0, 0], [n, n])
+    box = g.box([a, 0], [b, n])
+    i0 = np.arange(a, b, dtype=np.uint64)[:, None] * np.uint64(n) + np.arange(n, dtype=np.uint64)[None, :]
+    f = init_value(seed, i0).reshape(b - a, n, 1, 1)
+    u = Acc(f.view(np.uint32).copy(), box, ext)
+    up = Acc(f.view(np.uint32).copy(), box, ext)
+    lo, hi = a, b
+    for k in range(steps):
+        lo2 = lo if lo == 0 else lo + 1
+        hi2 = hi if hi == n else hi - 1
+        wb = g.box([lo2, 0], [hi2, n])
+        if k % 2 == 0:
+            k_wave5({}, [wb, wb], [u, up])
+        else:
+            k_wave5({}, [wb, wb], [up, u])
+        lo, hi = lo2, hi2
+    last = up if steps % 2 == 1 else u
+    return last.arr[rows_lo - a:rows_hi - a]
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_wavesim_full_size_sampled(cel, G):
+    """BASELINE config 2 at full size (16384^2), the bench's launch
+    configuration: sampled rows at the global edges and device boundaries."""
+    n, steps = 16384, 5
+    rt = cel.Runtime(G, cuda_devices=[0] * G, arena_bytes=int(2 * (n // G + 2) * n * 4 * 1.05) + (256 << 20))
+    u = rt.buffer_create(2, [n, n], 4)
+    up = rt.buffer_create(2, [n, n], 4)
+    for op in P.wavesim_init(n):
+        rt.task_submit(op[1])
+    for k in range(steps):
+        rt.task_submit(P.wavesim_step(n, k)[1])
+    last = up if steps % 2 == 1 else u
+    samples = [(0, 8), (n // 2 - 4, n // 2 + 4), (n - 8, n), (5000, 5003)]
+    for lo, hi in samples:
+        got = rt.buffer_read(last, ([lo, 0], [hi, n]))
+        exp = light_cone_wave(lo, hi, n, steps)
+        assert np.array_equal(got, exp), (lo, hi)
+    rt.shutdown()
+
+
+def test_nbody_full_size_sampled(cel):
+    """BASELINE config 3 at 2^20 bodies: one timestep, 16 sampled bodies
+    bit-exact (sequential sum over 2^20 bodies in the oracle)."""
+    N = 1 << 20
+    rt = cel.Runtime(1, arena_bytes=256 << 20)
+    prog = P.nbody(N, steps=0)
+    Pb = rt.buffer_create(1, [N], 16)
+    Vb = rt.buffer_create(1, [N], 16)
+    for op in prog["ops"]:
+        if op[0] == "task":
+            rt.task_submit(op[1])
+    rt.task_submit(P.nbody(N, 1)["ops"][2][1])          # the timestep task
+    v = rt.buffer_read(Vb, ([0], [N])).view(np.float32)[:, 0, 0, :]
+    pos = init_value(3, np.arange(4 * N, dtype=np.uint64)).reshape(N, 4)[:, :3].astype(np.float32)
+    c = np.float32(2.0 ** -7) * np.float32(2.0 ** -20)
+    rng = np.random.default_rng(0)
+    for i in list(rng.integers(0, N, 14)) + [0, N - 1]:
+        a = nbody_accel_one(pos, pos[i])
+        assert np.array_equal(v[i, :3], np.float32(0) + c * a), i
+    rt.shutdown()
