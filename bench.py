@@ -163,7 +163,7 @@ def make_runtime(cel, G, rank, world, dist, arena):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_FIELD)
@@ -242,7 +242,7 @@ def main():
     traffic = None
     tp = os.path.join(ROOT, "profiles", "wave5_traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("bytes_per_launch")
+        traffic = json.load(open(tp)).get("bytes_per_cell") * rows_here * n
     step_ms = ms / args.steps
     value = 1e3 / step_ms
     kernel_share = (wms / (ms * (G if world == 1 else 1))) if ms else None

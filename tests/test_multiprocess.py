@@ -1,0 +1,39 @@
+"""N>1 path: one process per device (torchrun).  CPU: world-size-2 gloo run of
+the replicated scheduler (execute=0) — every rank's instruction log equals the
+oracle's.  GPU: the same programs executed with peer pushes over NVLink and
+cross-process flag waits, readbacks merged and compared bit-exactly."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def torchrun(n, *args, port=29533, timeout=600):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_check.py")]
+    cmd += list(args)
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    return subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, timeout=timeout, env=env, cwd=ROOT)
+
+
+def test_replicated_scheduler_gloo_world2():
+    import __graft_entry__
+    __graft_entry__.build()
+    r = torchrun(2, "--execute", "0", "--quick")
+    out = r.stdout.decode()
+    assert r.returncode == 0 and "MP_CHECK PASS" in out, out[-3000:]
+
+
+@pytest.mark.gpu
+def test_multiprocess_gpu():
+    torch = pytest.importorskip("torch")
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    r = torchrun(min(n, 4), "--execute", "1", port=29534)
+    out = r.stdout.decode()
+    assert r.returncode == 0 and "MP_CHECK PASS" in out, out[-3000:]
