@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/cel.h"
@@ -87,6 +88,8 @@ void Executor::Arena::release(uint64_t off, uint64_t bytes, Token tok) {
 // ------------------------------------------------------------ setup
 Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(sched) {
     G_ = int(cfg_.cuda_devices.size());
+    const char* tr = getenv("CEL_TRACE");
+    trace_ = tr && tr[0] == '1';
 }
 
 Executor::~Executor() {
@@ -321,6 +324,9 @@ void Executor::wait_token(int sidx, const Token& t) {
         st_.event_waits++;
     }
     for (auto& r : t.remote) {
+        if (trace_)
+            fprintf(stderr, "[cel r%d] stream %d waits for iid %llu from rank %d\n", cfg_.rank, sidx,
+                    (unsigned long long)r.second, r.first);
         // the producer's process writes iid into this GPU's slot when done
         checkd(g_drv.wait64(reinterpret_cast<CUstream>(s.s),
                                    reinterpret_cast<CUdeviceptr>(sig_slot(s.dev, r.first, r.second)), r.second,
@@ -372,6 +378,33 @@ void Executor::prune_tokens(uint64_t below) {
         else
             ++it;
     }
+    for (auto it = ltok_.begin(); it != ltok_.end();) {
+        if (it->first < below)
+            it = ltok_.erase(it);
+        else
+            ++it;
+    }
+}
+
+// Local part of a horizon / epoch (executed by every process): the full tokens
+// of dependencies this process executes, the local parts of earlier horizons /
+// epochs, nothing of dependencies executed elsewhere (their owners' parts are
+// covered by the owners' own parts of this horizon / epoch).
+Token Executor::multi_local_part(const std::vector<uint64_t>& deps) const {
+    Token t;
+    for (uint64_t j : deps) {
+        auto kit = kind_of_.find(j);
+        if (cfg_.world > 1 && kit != kind_of_.end()) {
+            if (kit->second < 0) {
+                auto lt = ltok_.find(j);
+                if (lt != ltok_.end()) merge(t, lt->second);
+                continue;
+            }
+            if (owner_rank(kit->second) != cfg_.rank) continue;
+        }
+        merge(t, dep_token(j));
+    }
+    return t;
 }
 
 // ------------------------------------------------------------ ownership
@@ -410,7 +443,14 @@ void Executor::signal_deps(const Instr& ins, int owner_dev) {
         const uint64_t key = j * uint64_t(cfg_.world) + uint64_t(o);
         if (!signalled_.insert(key).second) continue;
         const int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
-        wait_token(sidx, dep_token(j));
+        if (jo < 0) {
+            auto lt = ltok_.find(j);
+            if (lt != ltok_.end()) wait_token(sidx, lt->second);
+        } else {
+            wait_token(sidx, dep_token(j));
+        }
+        if (trace_)
+            fprintf(stderr, "[cel r%d] signal iid %llu -> rank %d\n", cfg_.rank, (unsigned long long)j, o);
         checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
                                     reinterpret_cast<CUdeviceptr>(sig_slot(o, cfg_.rank, j)), j,
                                     CU_STREAM_WRITE_VALUE_DEFAULT),
@@ -431,6 +471,9 @@ void Executor::on_instr(const Instr& ins) {
     if (err_) return;
     const int od = instr_owner(ins);
     const bool mine = od < 0 || owner_rank(od) == cfg_.rank;
+    if (trace_)
+        fprintf(stderr, "[cel r%d] iid %llu kind %d owner %d %s\n", cfg_.rank, (unsigned long long)ins.iid,
+                int(ins.kind), od, mine ? "exec" : "skip");
     if (cfg_.world > 1) {
         if (od >= 0) kind_of_[ins.iid] = od;
         else kind_of_[ins.iid] = -1;
@@ -503,13 +546,9 @@ void Executor::on_instr(const Instr& ins) {
     case IKind::Horizon: {
         // completion of a horizon tells us everything before it is done;
         // deps older than the applied (previous) horizon are never referenced again.
-        Token t;
-        for (uint64_t j : ins.deps) {
-            auto kit = kind_of_.find(j);
-            const bool remote_only = cfg_.world > 1 && kit != kind_of_.end() && kit->second >= 0 &&
-                                     owner_rank(kit->second) != cfg_.rank;
-            if (!remote_only) merge(t, dep_token(j));
-        }
+        Token lt = multi_local_part(ins.deps);
+        ltok_[ins.iid] = lt;
+        Token t = lt;
         for (int r = 0; r < cfg_.world; ++r)
             if (r != cfg_.rank) t.remote.push_back({r, ins.iid});
         tok_[ins.iid] = t;
@@ -532,13 +571,7 @@ void Executor::on_instr(const Instr& ins) {
 }
 
 void Executor::exec_epoch(const Instr& ins) {
-    Token t;
-    for (uint64_t j : ins.deps) {
-        auto kit = kind_of_.find(j);
-        const bool remote_only = cfg_.world > 1 && kit != kind_of_.end() && kit->second >= 0 &&
-                                 owner_rank(kit->second) != cfg_.rank;
-        if (!remote_only) merge(t, dep_token(j));
-    }
+    Token t = multi_local_part(ins.deps);
     // an epoch synchronises with the main thread
     if (cfg_.world > 1) {
         const int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
@@ -564,7 +597,15 @@ void Executor::exec_epoch(const Instr& ins) {
     // everything before the epoch is complete locally: drop old tokens
     prune_tokens(ins.iid);
     prev_horizon_ = 0;
+    for (auto it = signalled_.begin(); it != signalled_.end();) {
+        const uint64_t j = *it / uint64_t(cfg_.world);
+        if (j < ins.iid && !live_alloc_iid_.count(j))
+            it = signalled_.erase(it);
+        else
+            ++it;
+    }
     tok_[ins.iid] = mine;
+    ltok_[ins.iid] = Token{};
     if (cfg_.world > 1) {
         // remote markers older than the epoch stay valid (their slots keep the value)
         for (auto it = kind_of_.begin(); it != kind_of_.end();) {
@@ -591,6 +632,7 @@ void Executor::exec_copy(const Instr& ins) {
         CopyArgs args;
         args.nseg = 0;
         args.total_units = 0;
+        args.peer = phys_[S.dev] != phys_[D.dev] ? 1 : 0;
         const int64_t sn1 = S.box.extent(1), sn2 = S.box.extent(2);
         const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
         uint64_t bytes = 0;

@@ -143,6 +143,7 @@ private:
     void checkd(CUresult e, const char* what);
     void signal_deps(const Instr& ins, int owner_dev);
     Token local_part(const std::vector<uint64_t>& deps) const;
+    Token multi_local_part(const std::vector<uint64_t>& deps) const;
     char* alloc_ptr(int64_t aid);
     void exec_copy(const Instr& ins);
     void exec_kernel(const Instr& ins);
@@ -159,6 +160,7 @@ private:
     std::vector<std::vector<cudaEvent_t>> pool_;
     std::vector<Arena> arenas_;
     std::unordered_map<uint64_t, Token> tok_;
+    std::unordered_map<uint64_t, Token> ltok_;     // local part of horizons / epochs
     std::unordered_map<uint64_t, int> kind_of_;    // iid -> owner device for event-only instrs (-1 all)
     std::unordered_map<int64_t, AllocRec> allocs_;
     std::unordered_map<uint32_t, std::pair<char*, size_t>> host_init_;
@@ -176,6 +178,7 @@ private:
     uint64_t prev_horizon_ = 0;
     std::unordered_set<uint64_t> live_alloc_iid_;
     std::vector<uint32_t> host_drop_;
+    bool trace_ = false;
     static constexpr uint64_t kRing = 1u << 16;
 };
 

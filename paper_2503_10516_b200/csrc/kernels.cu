@@ -103,6 +103,9 @@ __global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyA
         default: copy_span<uint8_t>(src, dst, nbytes); break;
         }
     }
+    // pushes into peer memory: make the stores visible system-wide before the
+    // kernel retires (a flag written after this kernel releases the data)
+    if (a.peer) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ helpers

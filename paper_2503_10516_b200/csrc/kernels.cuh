@@ -27,6 +27,7 @@ constexpr uint32_t kCopyUnit = 16384;     // bytes of one row chunk per CTA iter
 struct CopyArgs {
     CopySeg seg[kMaxSegs];
     int nseg;
+    int peer;                  // destination is another GPU's memory: fence before exit
     uint64_t total_units;
 };
 

@@ -29,6 +29,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--execute", type=int, default=1)
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--only", default=None)
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo")
@@ -36,6 +37,8 @@ def main():
     progs = [P.c1_chain(4096), P.wavesim(1024, 9, rows=700), P.nbody(3000, 2), P.nbody(500, 2, host_init=True),
              P.rsim(3000, 20), P.jacobi3d(40, 3)]
     modes = ["auto", "none"]
+    if args.only:
+        progs = [p for p in progs if p["name"] == args.only]
     if not args.quick:
         progs += [P.random_program(300 + s) for s in range(12)]
     nfail = 0
