@@ -172,6 +172,14 @@ int cel_ipc_import(cel_runtime* rt, int32_t rank, const void* blob);
 int cel_buffer_create(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
                       const void* host_init, cel_buffer* out);
 
+/* Same, with flags.  CEL_BUFFER_BORROW_HOST: host_init is NOT copied; the
+ * caller keeps it valid and unmodified until the buffer is destroyed (or the
+ * runtime is); page-locked memory is then uploaded by DMA at full speed with
+ * no staging copy and no pinning cost. */
+#define CEL_BUFFER_BORROW_HOST 1u
+int cel_buffer_create_ex(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
+                         const void* host_init, uint32_t flags, cel_buffer* out);
+
 /* Submit a task: returns after its instructions are generated and enqueued
  * (asynchronous).  >0: uninitialised-read warning; <0: rejected, no effect. */
 int cel_task_submit(cel_runtime* rt, const cel_task_desc* desc, cel_task* out);

@@ -83,6 +83,8 @@ lib.cel_ipc_blob_size.restype = C.c_size_t
 lib.cel_ipc_export.argtypes = [_P, C.c_void_p]
 lib.cel_ipc_import.argtypes = [_P, C.c_int32, C.c_void_p]
 lib.cel_buffer_create.argtypes = [_P, C.c_int32, C.POINTER(C.c_uint64), C.c_uint32, C.c_void_p, C.POINTER(C.c_uint32)]
+lib.cel_buffer_create_ex.argtypes = [_P, C.c_int32, C.POINTER(C.c_uint64), C.c_uint32, C.c_void_p, C.c_uint32,
+                                     C.POINTER(C.c_uint32)]
 lib.cel_task_submit.argtypes = [_P, C.POINTER(cel_task_desc), C.POINTER(C.c_uint64)]
 lib.cel_wait.argtypes = [_P]
 lib.cel_buffer_read.argtypes = [_P, C.c_uint32, C.POINTER(cel_box), C.c_void_p]
@@ -93,7 +95,9 @@ lib.cel_profile_read.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64
 lib.cel_runtime_destroy.argtypes = [_P]
 lib.cel_last_error.restype = C.c_char_p
 
+BORROW_HOST = 1
 SYMBOLS = ["cel_runtime_create", "cel_ipc_blob_size", "cel_ipc_export", "cel_ipc_import", "cel_buffer_create",
+           "cel_buffer_create_ex",
            "cel_task_submit", "cel_wait", "cel_buffer_read", "cel_buffer_destroy", "cel_stats_get",
            "cel_profile_enable", "cel_profile_read", "cel_runtime_destroy", "cel_last_error"]
 
@@ -192,7 +196,7 @@ class Runtime:
         _check(lib.cel_ipc_import(self.h, rank, C.c_char_p(blob)))
 
     # -- the paper's model
-    def buffer_create(self, dims, extent, elem_size, host_init=None):
+    def buffer_create(self, dims, extent, elem_size, host_init=None, borrow=False):
         ext = (C.c_uint64 * 3)(*(list(extent) + [1] * (3 - len(extent))))
         out = C.c_uint32()
         ptr = None
@@ -200,7 +204,11 @@ class Runtime:
             host_init = np.ascontiguousarray(host_init)
             assert host_init.nbytes == int(np.prod(extent)) * elem_size
             ptr = host_init.ctypes.data_as(C.c_void_p)
-        _check(lib.cel_buffer_create(self.h, dims, ext, elem_size, ptr, C.byref(out)))
+        if borrow:
+            self._keep.append(host_init)
+            _check(lib.cel_buffer_create_ex(self.h, dims, ext, elem_size, ptr, BORROW_HOST, C.byref(out)))
+        else:
+            _check(lib.cel_buffer_create(self.h, dims, ext, elem_size, ptr, C.byref(out)))
         self.meta[out.value] = (dims, list(extent), elem_size)
         return out.value
 

@@ -120,6 +120,11 @@ int cel_ipc_import(cel_runtime* rt, int32_t rank, const void* blob) {
 
 int cel_buffer_create(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
                       const void* host_init, cel_buffer* out) {
+    return cel_buffer_create_ex(rt, dims, extent, elem_size, host_init, 0, out);
+}
+
+int cel_buffer_create_ex(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
+                         const void* host_init, uint32_t flags, cel_buffer* out) {
     if (int rc = check_poison(rt)) return rc;
     if (!extent || !out) return fail(CEL_E_INVALID, "null argument");
     int64_t ext[3] = {1, 1, 1};
@@ -132,7 +137,8 @@ int cel_buffer_create(cel_runtime* rt, int32_t dims, const uint64_t extent[3], u
     const int rc = rt->sched->buffer_create(dims, ext, elem_size, host_init != nullptr, &bid);
     if (rc != 0) return fail(rc, "invalid buffer (dims 1..3, extents > 0, elem_size > 0)");
     if (host_init && rt->exec) {
-        const int r2 = rt->exec->set_host_init(bid, host_init, size_t(n) * elem_size);
+        const int r2 = rt->exec->set_host_init(bid, host_init, size_t(n) * elem_size,
+                                               (flags & CEL_BUFFER_BORROW_HOST) != 0);
         if (r2 != 0) return fail(r2, "cannot pin host memory for host_init");
     }
     *out = bid;

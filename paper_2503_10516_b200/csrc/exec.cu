@@ -113,7 +113,8 @@ Executor::~Executor() {
         // one cudaMalloc per physical device+virtual device
         if (arenas_[d].base) cudaFree(arenas_[d].base);
     }
-    for (auto& kv : host_init_) cudaFreeHost(kv.second.first);
+    for (auto& kv : host_init_)
+        if (kv.second.second) cudaFreeHost(kv.second.first);
 }
 
 void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
@@ -175,10 +176,16 @@ int Executor::init(std::string* err) {
         A.free_[data_off] = FreeRange{arena - data_off, Token{}};
         if (!owned(d)) continue;
         set_dev(d);
+        // copies, pushes and signals get the highest priority: their CTAs are
+        // scheduled ahead of queued stencil CTAs, so a halo push never waits
+        // for the next step's kernel to drain (P:L490 overlap of copies and kernels)
+        int prio_lo = 0, prio_hi = 0;
+        cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
         for (int k = 0; k < kStreamsPerDev; ++k) {
             Stream& s = streams_[d * kStreamsPerDev + k];
             s.dev = d;
-            if (cudaStreamCreateWithFlags(&s.s, cudaStreamNonBlocking) != cudaSuccess) {
+            const int prio = k == S_COMPUTE ? prio_lo : prio_hi;
+            if (cudaStreamCreateWithPriority(&s.s, cudaStreamNonBlocking, prio) != cudaSuccess) {
                 *err = "cudaStreamCreate failed";
                 return E_CUDA;
             }
@@ -236,7 +243,11 @@ int Executor::ipc_import(int rank, const void* blob) {
     return E_OK;
 }
 
-int Executor::set_host_init(uint32_t bid, const void* data, size_t bytes) {
+int Executor::set_host_init(uint32_t bid, const void* data, size_t bytes, bool borrow) {
+    if (borrow) {
+        host_init_[bid] = {const_cast<char*>(static_cast<const char*>(data)), 0};
+        return E_OK;
+    }
     void* p = nullptr;
     if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
         cudaGetLastError();
@@ -251,7 +262,7 @@ void Executor::drop_host_init(uint32_t bid) {
     auto it = host_init_.find(bid);
     if (it == host_init_.end()) return;
     sync_all();
-    cudaFreeHost(it->second.first);
+    if (it->second.second) cudaFreeHost(it->second.first);
     host_init_.erase(it);
 }
 
@@ -586,7 +597,7 @@ void Executor::exec_epoch(const Instr& ins) {
     for (uint32_t bid : host_drop_) {
         auto it = host_init_.find(bid);
         if (it != host_init_.end()) {
-            cudaFreeHost(it->second.first);
+            if (it->second.second) cudaFreeHost(it->second.first);
             host_init_.erase(it);
         }
     }

@@ -67,8 +67,9 @@ public:
     int init(std::string* err);
     void on_instr(const Instr& ins) override;
 
-    // host data of a host-initialised buffer (copied, pinned)
-    int set_host_init(uint32_t bid, const void* data, size_t bytes);
+    // host data of a host-initialised buffer: copied into pinned memory, or
+    // borrowed (size 0 marks a borrowed pointer; the caller keeps it valid)
+    int set_host_init(uint32_t bid, const void* data, size_t bytes, bool borrow);
     void drop_host_init(uint32_t bid);
     void drop_host_init_later(uint32_t bid) { host_drop_.push_back(bid); }
     void set_scheduler(Scheduler* s) { sched_ = s; }
