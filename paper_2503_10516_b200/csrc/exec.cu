@@ -35,8 +35,8 @@ struct Drv {
     }
 } g_drv;
 
-constexpr int kStreamsPerDev = 4;
-enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3 };
+constexpr int kStreamsPerDev = 5;
+enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3, S_HALO = 4 };
 constexpr uint64_t kAlign = 512;
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 }  // namespace
@@ -90,6 +90,8 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     G_ = int(cfg_.cuda_devices.size());
     const char* tr = getenv("CEL_TRACE");
     trace_ = tr && tr[0] == '1';
+    const char* ns = getenv("CEL_NO_SPLIT");
+    split_ = !(ns && ns[0] == '1');
 }
 
 Executor::~Executor() {
@@ -395,6 +397,18 @@ void Executor::prune_tokens(uint64_t below) {
         else
             ++it;
     }
+    for (auto it = copy_info_.begin(); it != copy_info_.end();) {
+        if (it->first < below)
+            it = copy_info_.erase(it);
+        else
+            ++it;
+    }
+    for (auto it = parts_.begin(); it != parts_.end();) {
+        if (it->first < below)
+            it = parts_.erase(it);
+        else
+            ++it;
+    }
 }
 
 // Local part of a horizon / epoch (executed by every process): the full tokens
@@ -541,6 +555,7 @@ void Executor::on_instr(const Instr& ins) {
         return;
     }
     case IKind::Copy:
+        copy_info_[ins.iid] = CopyInfo{ins.src_aid, ins.dst_aid, rbbox(ins.region), ins.region};
         if (!mine) {
             tok_[ins.iid] = Token{{}, {{owner_rank(od), ins.iid}}};
             return;
@@ -629,7 +644,23 @@ void Executor::exec_epoch(const Instr& ins) {
 void Executor::exec_copy(const Instr& ins) {
     const uint32_t es = sched_->elem_size(ins.buffer);
     Token deps;
-    for (uint64_t j : ins.deps) merge(deps, dep_token(j));
+    for (uint64_t j : ins.deps) {
+        // a copy that reads only rows a split kernel wrote in its shell launch
+        // waits for that launch, not for the interior (computation /
+        // communication overlap)
+        auto pit = parts_.find(j);
+        if (pit != parts_.end() && pit->second.write_aid == ins.src_aid && ins.src_mem >= 2 &&
+            std::find(pit->second.bound.begin(), pit->second.bound.end(), ins.dst_aid) == pit->second.bound.end()) {
+            bool touches = false;
+            for (const Box& b : ins.region)
+                if (!intersect(b, pit->second.interior).empty()) touches = true;
+            if (!touches) {
+                merge(deps, pit->second.shell);
+                continue;
+            }
+        }
+        merge(deps, dep_token(j));
+    }
     if (ins.src_mem >= 2 && ins.dst_mem >= 2) {
         const AllocRec& S = allocs_.at(ins.src_aid);
         const AllocRec& D = allocs_.at(ins.dst_aid);
@@ -863,22 +894,107 @@ void Executor::exec_kernel(const Instr& ins) {
             }
         }
     }
-    int n;
-    if (cfg_.profile) {
-        Prof p{d.kernel, nullptr, nullptr};
-        cudaEventCreate(&p.a);
-        cudaEventCreate(&p.b);
-        cudaEventRecord(p.a, streams_[sidx].s);
-        n = launch_workload(a, streams_[sidx].s);
-        cudaEventRecord(p.b, streams_[sidx].s);
-        prof_pending_.push_back(p);
-    } else {
-        n = launch_workload(a, streams_[sidx].s);
+    // Shell / interior split of stencil launches: the boundary bands that
+    // neighbouring devices read (halo rows) are computed first on a
+    // high-priority stream, so their coherence copies leave while the interior
+    // is still running.  Same instruction, same result; only the launch order
+    // and the per-part completion events change.
+    Box interior = ins.chunk;
+    bool split = false;
+    if (split_ && (d.kernel == K_WAVE5 || d.kernel == K_JACOBI7 || d.kernel == K_STENCIL3)) {
+        for (const Access& ac : d.acc) {
+            if (ac.map.kind != MapKind::Neighborhood || (ac.mode != MODE_READ && ac.mode != MODE_READ_WRITE)) continue;
+            const Box rb = map_access(ac.map, ins.chunk, sched_->extent(ac.buf));
+            for (int k = 0; k < 3; ++k) {
+                if (rb.lo[k] < ins.chunk.lo[k]) {
+                    interior.lo[k] = std::max(interior.lo[k], ins.chunk.lo[k] + ac.map.border[k]);
+                    split = true;
+                }
+                if (rb.hi[k] > ins.chunk.hi[k]) {
+                    interior.hi[k] = std::min(interior.hi[k], ins.chunk.hi[k] - ac.map.border[k]);
+                    split = true;
+                }
+            }
+        }
+        if (interior.empty()) split = false;
     }
-    check(cudaGetLastError(), "kernel launch");
-    st_.kernel_launches += n;
-    st_.workload_launches += n;
-    tok_[ins.iid] = record(sidx);
+    auto launch = [&](const Box& ch, int stream) {
+        KArgs b = a;
+        for (int k = 0; k < 3; ++k) {
+            b.chunk.lo[k] = ch.lo[k];
+            b.chunk.hi[k] = ch.hi[k];
+        }
+        for (int i = 0; i < b.n_acc; ++i) {
+            const Box mb = map_access(d.acc[i].map, ch, sched_->extent(d.acc[i].buf));
+            for (int k = 0; k < 3; ++k) {
+                b.acc[i].box.lo[k] = mb.lo[k];
+                b.acc[i].box.hi[k] = mb.hi[k];
+            }
+        }
+        int n;
+        if (cfg_.profile) {
+            Prof p{d.kernel, nullptr, nullptr};
+            cudaEventCreate(&p.a);
+            cudaEventCreate(&p.b);
+            cudaEventRecord(p.a, streams_[stream].s);
+            n = launch_workload(b, streams_[stream].s);
+            cudaEventRecord(p.b, streams_[stream].s);
+            prof_pending_.push_back(p);
+        } else {
+            n = launch_workload(b, streams_[stream].s);
+        }
+        check(cudaGetLastError(), "kernel launch");
+        st_.kernel_launches += n;
+        st_.workload_launches += n;
+    };
+    if (!split) {
+        launch(ins.chunk, sidx);
+        tok_[ins.iid] = record(sidx);
+        return;
+    }
+    // shell launches: every dependency (they read the incoming halos)
+    const int hidx = dev * kStreamsPerDev + S_HALO;
+    wait_token(hidx, deps);
+    std::vector<Box> shell;
+    subtract_into(ins.chunk, interior, shell);
+    for (const Box& b : shell) launch(b, hidx);
+    Token tshell = record(hidx);
+    // interior launch: only dependencies whose accesses conflict with the
+    // interior's (copies into halo rows it never reads are skipped)
+    Token ideps;
+    for (uint64_t j : ins.deps) {
+        auto ci = copy_info_.find(j);
+        bool conflict = true;
+        if (ci != copy_info_.end()) {
+            conflict = false;
+            for (size_t i = 0; i < d.acc.size() && !conflict; ++i) {
+                const Access& ac = d.acc[i];
+                const int64_t aid = ins.bindings[i];
+                const Box ib = map_access(ac.map, interior, sched_->extent(ac.buf));
+                auto hits = [&](const CopyInfo& c) {
+                    if (intersect(c.bb, ib).empty()) return false;
+                    for (const Box& b : c.region)
+                        if (!intersect(b, ib).empty()) return true;
+                    return false;
+                };
+                if (ci->second.dst_aid == aid && hits(ci->second)) conflict = true;             // RAW / WAW
+                if (ci->second.src_aid == aid && (ac.mode & MODE_WRITE) && hits(ci->second)) conflict = true;  // WAR
+            }
+        }
+        if (conflict) merge(ideps, dep_token(j));
+    }
+    wait_token(sidx, ideps);
+    // the interior must also follow the shell launches' own predecessors on
+    // the halo stream only through real conflicts, which `ideps` carries
+    launch(interior, sidx);
+    Token tint = record(sidx);
+    Token all = tint;
+    merge(all, tshell);
+    tok_[ins.iid] = all;
+    int64_t waid = 0;
+    for (size_t i = 0; i < d.acc.size(); ++i)
+        if (d.acc[i].mode & MODE_WRITE) waid = ins.bindings[i];
+    parts_[ins.iid] = Parts{tshell, interior, waid, ins.bindings};
 }
 
 int Executor::profile_read(double* ms, uint64_t* count, int n) {

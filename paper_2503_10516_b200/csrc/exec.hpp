@@ -124,6 +124,17 @@ private:
         int kind;
         cudaEvent_t a, b;
     };
+    struct CopyInfo {
+        int64_t src_aid, dst_aid;
+        Box bb;
+        Region region;
+    };
+    struct Parts {                                 // a kernel launched as shell + interior
+        Token shell;
+        Box interior;
+        int64_t write_aid;
+        std::vector<int64_t> bound;                // every allocation the kernel touches
+    };
     struct Readback {
         char* dst;
         Box box;
@@ -157,7 +168,7 @@ private:
     ExecConfig cfg_;
     Scheduler* sched_;
     int G_ = 0;
-    std::vector<Stream> streams_;                  // dev*4 + {0 compute, 1 copy, 2 push, 3 sync}
+    std::vector<Stream> streams_;                  // dev*5 + {0 compute, 1 copy, 2 push, 3 sync, 4 halo}
     std::vector<std::vector<cudaEvent_t>> pool_;
     std::vector<Arena> arenas_;
     std::unordered_map<uint64_t, Token> tok_;
@@ -180,6 +191,9 @@ private:
     std::unordered_set<uint64_t> live_alloc_iid_;
     std::vector<uint32_t> host_drop_;
     bool trace_ = false;
+    bool split_ = true;
+    std::unordered_map<uint64_t, CopyInfo> copy_info_;
+    std::unordered_map<uint64_t, Parts> parts_;
     static constexpr uint64_t kRing = 1u << 16;
 };
 

@@ -157,6 +157,27 @@ inline Region canon(std::vector<Box> boxes) {
         out.push_back(boxes[0]);
         return out;
     }
+    // fast path: every box has the same (dim1, dim2) cross-section (row slabs,
+    // plane slabs) -> the canonical form is the merged dim-0 intervals
+    const Box& f = boxes[0];
+    bool same = true;
+    for (const Box& b : boxes)
+        if (b.lo[1] != f.lo[1] || b.hi[1] != f.hi[1] || b.lo[2] != f.lo[2] || b.hi[2] != f.hi[2]) {
+            same = false;
+            break;
+        }
+    if (same) {
+        std::sort(boxes.begin(), boxes.end(), [](const Box& a, const Box& b) { return a.lo[0] < b.lo[0]; });
+        out.reserve(boxes.size());
+        for (const Box& b : boxes) {
+            if (!out.empty() && b.lo[0] <= out.back().hi[0]) {
+                if (b.hi[0] > out.back().hi[0]) out.back().hi[0] = b.hi[0];
+            } else {
+                out.push_back(b);
+            }
+        }
+        return out;
+    }
     detail::canon_dim(boxes, 0, out);
     return out;
 }
@@ -172,6 +193,11 @@ inline Region runion(const Region& a, const Region& b) {
 }
 
 inline Region rinter(const Region& a, const Region& b) {
+    if (a.empty() || b.empty()) return {};
+    if (a.size() == 1 && b.size() == 1) {
+        Box i = intersect(a[0], b[0]);
+        return i.empty() ? Region{} : Region{i};
+    }
     std::vector<Box> out;
     for (const Box& x : a)
         for (const Box& y : b) {
@@ -182,10 +208,32 @@ inline Region rinter(const Region& a, const Region& b) {
     return canon(std::move(out));
 }
 
-inline Region rinter(const Region& a, const Box& b) { return rinter(a, region_of(b)); }
+inline Region rinter(const Region& a, const Box& b) {
+    if (b.empty() || a.empty()) return {};
+    std::vector<Box> out;
+    bool whole = true;
+    for (const Box& x : a) {
+        Box i = intersect(x, b);
+        if (i.empty()) {
+            whole = false;
+            continue;
+        }
+        if (i != x) whole = false;
+        out.push_back(i);
+    }
+    if (whole) return a;              // a ⊆ b: already canonical
+    if (out.size() <= 1) return out;
+    return canon(std::move(out));
+}
 
+inline Box rbbox(const Region& r);
+inline Region rdiff_nobb(const Region& a, const Region& b);
 inline Region rdiff(const Region& a, const Region& b) {
     if (a.empty() || b.empty()) return a;
+    if (intersect(rbbox(a), rbbox(b)).empty()) return a;
+    return rdiff_nobb(a, b);
+}
+inline Region rdiff_nobb(const Region& a, const Region& b) {
     std::vector<Box> cur(a), nxt;
     bool changed = false;
     for (const Box& y : b) {
@@ -228,32 +276,46 @@ inline bool rintersects(const Region& a, const Box& b) {
 // pairwise disjoint; their union is the extent.
 template <class V>
 struct RegionMap {
+    struct Entry {
+        V first;
+        Region second;
+        Box bb;                        // bounding box of `second` (cheap rejects)
+    };
     Box extent;
-    std::vector<std::pair<V, Region>> e;
+    std::vector<Entry> e;             // sorted by value
 
     RegionMap() = default;
     RegionMap(const Box& ext, const V& dflt) : extent(ext) {
-        if (!ext.empty()) e.push_back({dflt, Region{ext}});
+        if (!ext.empty()) e.push_back({dflt, Region{ext}, ext});
     }
 
     void put(const V& v, const Region& r) {
         if (r.empty()) return;
-        auto it = std::lower_bound(e.begin(), e.end(), v,
-                                   [](const std::pair<V, Region>& p, const V& x) { return p.first < x; });
-        if (it != e.end() && it->first == v)
+        auto it = std::lower_bound(e.begin(), e.end(), v, [](const Entry& p, const V& x) { return p.first < x; });
+        if (it != e.end() && it->first == v) {
             it->second = runion(it->second, r);
-        else
-            e.insert(it, {v, r});
+            it->bb = bbox(it->bb, rbbox(r));
+        } else {
+            e.insert(it, Entry{v, r, rbbox(r)});
+        }
     }
 
     void update(const Region& reg0, const V& v) {
         Region reg = rinter(reg0, extent);
         if (reg.empty()) return;
-        std::vector<std::pair<V, Region>> ne;
+        const Box rb = rbbox(reg);
+        std::vector<Entry> ne;
         ne.reserve(e.size() + 1);
         for (auto& p : e) {
-            Region rr = rdiff(p.second, reg);
-            if (!rr.empty()) ne.push_back({p.first, std::move(rr)});
+            if (intersect(p.bb, rb).empty()) {
+                ne.push_back(std::move(p));
+                continue;
+            }
+            Region rr = rdiff_nobb(p.second, reg);
+            if (!rr.empty()) {
+                Box bb = rbbox(rr);
+                ne.push_back(Entry{p.first, std::move(rr), bb});
+            }
         }
         e.swap(ne);
         put(v, reg);
@@ -263,25 +325,32 @@ struct RegionMap {
     void apply(const Region& reg0, F fn) {
         Region reg = rinter(reg0, extent);
         if (reg.empty()) return;
-        std::vector<std::pair<V, Region>> old;
-        old.swap(e);
+        const Box rb = rbbox(reg);
+        // entries not touching reg stay in place; touched ones are split
         std::vector<std::pair<V, Region>> inside;
-        for (auto& p : old) {
-            Region in = rinter(p.second, reg);
-            if (in.empty()) {
-                put(p.first, p.second);
-                continue;
+        size_t w = 0;
+        for (size_t i = 0; i < e.size(); ++i) {
+            Entry& p = e[i];
+            if (!intersect(p.bb, rb).empty()) {
+                Region in = rinter(p.second, reg);
+                if (!in.empty()) {
+                    Region out = rdiff_nobb(p.second, reg);
+                    inside.push_back({fn(p.first), std::move(in)});
+                    if (out.empty()) continue;
+                    p.bb = rbbox(out);
+                    p.second = std::move(out);
+                }
             }
-            Region out = rdiff(p.second, reg);
-            if (!out.empty()) put(p.first, out);
-            inside.push_back({fn(p.first), std::move(in)});
+            if (w != i) e[w] = std::move(p);
+            ++w;
         }
+        e.resize(w);
         for (auto& p : inside) put(p.first, p.second);
     }
 
     template <class F>
     void map_values(F fn) {
-        std::vector<std::pair<V, Region>> old;
+        std::vector<Entry> old;
         old.swap(e);
         for (auto& p : old) put(fn(p.first), p.second);
     }
@@ -290,19 +359,43 @@ struct RegionMap {
     std::vector<std::pair<Region, V>> query(const Region& reg) const {
         std::vector<std::pair<Region, V>> out;
         if (reg.empty()) return out;
+        const Box rb = rbbox(reg);
         for (auto& p : e) {
+            if (intersect(p.bb, rb).empty()) continue;
             Region i = rinter(p.second, reg);
             if (!i.empty()) out.push_back({std::move(i), p.first});
         }
         return out;
     }
 
+    // Values present on reg (no regions computed).
+    template <class F>
+    void for_values_in(const Region& reg, F fn) const {
+        if (reg.empty()) return;
+        const Box rb = rbbox(reg);
+        for (auto& p : e) {
+            if (intersect(p.bb, rb).empty()) continue;
+            bool hit = false;
+            for (const Box& x : p.second) {
+                if (intersect(x, rb).empty()) continue;
+                for (const Box& y : reg)
+                    if (!intersect(x, y).empty()) {
+                        hit = true;
+                        break;
+                    }
+                if (hit) break;
+            }
+            if (hit) fn(p.first);
+        }
+    }
+
     template <class P>
     Region where(P pred) const {
-        Region out;
+        std::vector<Box> all;
         for (auto& p : e)
-            if (pred(p.first)) out = runion(out, p.second);
-        return out;
+            if (pred(p.first)) all.insert(all.end(), p.second.begin(), p.second.end());
+        if (all.size() <= 1) return all;
+        return canon(std::move(all));
     }
 };
 

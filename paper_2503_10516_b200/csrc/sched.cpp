@@ -197,13 +197,15 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
     // RAW / WAR / WAW at element granularity
     std::vector<int64_t> deps;
     for (auto& kv : reads)
-        for (auto& q : tbufs_[kv.first].last_writer.query(kv.second))
-            if (q.second >= 0) deps.push_back(q.second);
+        tbufs_[kv.first].last_writer.for_values_in(kv.second, [&](int64_t v) {
+            if (v >= 0) deps.push_back(v);
+        });
     for (auto& kv : writes) {
         TBuf& t = tbufs_[kv.first];
-        for (auto& q : t.readers.query(kv.second)) deps.insert(deps.end(), q.second.begin(), q.second.end());
-        for (auto& q : t.last_writer.query(kv.second))
-            if (q.second >= 0) deps.push_back(q.second);
+        t.readers.for_values_in(kv.second, [&](const std::vector<int64_t>& s) { deps.insert(deps.end(), s.begin(), s.end()); });
+        t.last_writer.for_values_in(kv.second, [&](int64_t v) {
+            if (v >= 0) deps.push_back(v);
+        });
     }
     if (deps.empty()) deps.push_back(t_fallback_);
     const int64_t tid = next_tid_++;
@@ -601,15 +603,18 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
                          int64_t rb) {
     // Table 1 `copy` with R12 dependencies
     std::vector<uint64_t> deps;
+    auto add = [&](int64_t v) {
+        if (v >= 0) deps.push_back(uint64_t(v));
+    };
+    auto adds = [&](const std::vector<int64_t>& s) {
+        for (int64_t r : s) deps.push_back(uint64_t(r));
+    };
     if (src->iid >= 0) deps.push_back(uint64_t(src->iid));
-    for (auto& q : src->last_writer.query(reg))
-        if (q.second >= 0) deps.push_back(uint64_t(q.second));
+    src->last_writer.for_values_in(reg, add);
     if (dst) {
         deps.push_back(uint64_t(dst->iid));
-        for (auto& q : dst->readers.query(reg))
-            for (int64_t r : q.second) deps.push_back(uint64_t(r));
-        for (auto& q : dst->last_writer.query(reg))
-            if (q.second >= 0) deps.push_back(uint64_t(q.second));
+        dst->readers.for_values_in(reg, adds);
+        dst->last_writer.for_values_in(reg, add);
     }
     Instr ins;
     ins.kind = IKind::Copy;
@@ -640,9 +645,14 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
 }
 
 std::map<std::tuple<int64_t, int, int64_t>, Region> Scheduler::source_parts(Buf& buf, const Region& need, int m_dst) {
+    return source_parts_q(buf, buf.uptodate.query(need), m_dst);
+}
+
+std::map<std::tuple<int64_t, int, int64_t>, Region> Scheduler::source_parts_q(
+    Buf& buf, const std::vector<std::pair<Region, uint32_t>>& need_by_mask, int m_dst) {
     // producer split x source memory (R10) x source allocation
     std::map<std::tuple<int64_t, int, int64_t>, Region> parts;
-    for (auto& q : buf.uptodate.query(need)) {
+    for (auto& q : need_by_mask) {
         const uint32_t mask = q.second;
         int s = -1;
         for (int m = 2; m < 32; ++m)
@@ -749,11 +759,12 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         const int m = 2 + kv.first.first;
         const uint32_t bid = kv.first.second;
         Buf& buf = *bufs_[bid];
-        Region need = rdiff(rit->second, buf.uptodate.where([m](uint32_t mask) { return ((mask >> m) & 1u) != 0; }));
+        // need = reads - uptodate(M_d) - uninitialised, partitioned by mask in one query
+        std::vector<std::pair<Region, uint32_t>> need;
+        for (auto& q : buf.uptodate.query(rit->second))
+            if (q.second != 0 && ((q.second >> m) & 1u) == 0) need.push_back(std::move(q));
         if (need.empty()) continue;
-        need = rinter(need, buf.uptodate.where([](uint32_t mask) { return mask != 0; }));
-        if (need.empty()) continue;
-        auto parts = source_parts(buf, need, m);
+        auto parts = source_parts_q(buf, need, m);
         for (auto& p : parts) {
             const int64_t aid = std::get<2>(p.first);
             Alloc* src = aid == HOST_AID ? buf.host.get() : allocs_.at(aid).get();
@@ -774,16 +785,17 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         for (auto it = c.req.lower_bound({d, 0}); it != c.req.end() && it->first.first == d; ++it) {
             Alloc* a = binding[it->first];
             deps.push_back(uint64_t(a->iid));
+            auto add = [&](int64_t v) {
+                if (v >= 0) deps.push_back(uint64_t(v));
+            };
             auto rit = c.reads.find(it->first);
-            if (rit != c.reads.end())
-                for (auto& q : a->last_writer.query(rit->second))
-                    if (q.second >= 0) deps.push_back(uint64_t(q.second));
+            if (rit != c.reads.end()) a->last_writer.for_values_in(rit->second, add);
             auto wit = c.writes.find(it->first);
             if (wit != c.writes.end()) {
-                for (auto& q : a->readers.query(wit->second))
-                    for (int64_t r : q.second) deps.push_back(uint64_t(r));
-                for (auto& q : a->last_writer.query(wit->second))
-                    if (q.second >= 0) deps.push_back(uint64_t(q.second));
+                a->readers.for_values_in(wit->second, [&](const std::vector<int64_t>& s) {
+                    for (int64_t r : s) deps.push_back(uint64_t(r));
+                });
+                a->last_writer.for_values_in(wit->second, add);
             }
         }
         Instr ins;

@@ -192,6 +192,8 @@ private:
     void free_alloc(Alloc* a, int64_t tid);
     uint64_t copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Alloc* dst, const Region& reg, int64_t rb);
     std::map<std::tuple<int64_t, int, int64_t>, Region> source_parts(Buf& buf, const Region& need, int m_dst);
+    std::map<std::tuple<int64_t, int, int64_t>, Region> source_parts_q(
+        Buf& buf, const std::vector<std::pair<Region, uint32_t>>& need_by_mask, int m_dst);
     void subsume(int64_t h);
     void log_instr(const Instr& ins);
     int prepare(const TaskDesc& d, Cmd& c, std::string* err) const;
