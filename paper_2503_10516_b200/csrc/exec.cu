@@ -920,7 +920,6 @@ void Executor::exec_kernel(const Instr& ins) {
     }
     auto launch = [&](const Box& ch, int stream) {
         KArgs b = a;
-        b.reserve_slot = split ? 1 : 0;
         for (int k = 0; k < 3; ++k) {
             b.chunk.lo[k] = ch.lo[k];
             b.chunk.hi[k] = ch.hi[k];

@@ -214,9 +214,10 @@ __global__ void wave5_scalar(const __grid_constant__ KArgs a) {
     }
 }
 
+constexpr int kWaveRows = 16;
 
-// vector path: 128 threads x float4 = 512 columns per CTA, a balanced range of
-// rows (one wave of CTAs) marched top to bottom with a 3-row register window; west/east
+// vector path: 128 threads x float4 = 512 columns per CTA, a strip of kWaveRows
+// rows marched top to bottom with a 3-row register window; west/east
 // neighbours come from warp shuffles (scalar loads only at warp edges).
 __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a) {
     const DAcc& U = a.acc[0];
@@ -227,12 +228,8 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
     const int lane = threadIdx.x & 31;
     const int64_t c = c0 + (int64_t(blockIdx.x) * 128 + threadIdx.x) * 4;
     const bool valid = c < c1;
-    // one wave: CTA row y of gridDim.y marches a contiguous, balanced row range
-    const int64_t nrows = r1 - r0;
-    const int64_t q = nrows / gridDim.y, rem = nrows % gridDim.y;
-    const int64_t rs = r0 + int64_t(blockIdx.y) * q + (int64_t(blockIdx.y) < rem ? int64_t(blockIdx.y) : rem);
-    const int64_t re = rs + q + (int64_t(blockIdx.y) < rem ? 1 : 0);
-    if (rs >= re) return;
+    const int64_t rs = r0 + int64_t(blockIdx.y) * kWaveRows;
+    const int64_t re = rs + kWaveRows < r1 ? rs + kWaveRows : r1;
     const float* ub = reinterpret_cast<const float*>(U.base);
     float* pb = reinterpret_cast<float*>(P.base);
     const int64_t uoff = c - U.lo[1];
@@ -248,7 +245,7 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
     const bool need_w = valid && lane == 0;
     const int64_t cw = c > 0 ? c - 1 : 0;
     const int64_t ce = c + 4 < E1 ? c + 4 : E1 - 1;
-#pragma unroll 4
+#pragma unroll 2
     for (int64_t r = rs; r < re; ++r) {
         const int64_t rn = r + 1 < E0 ? r + 1 : E0 - 1;
         float4 nxt = z4, up = z4;
@@ -528,20 +525,7 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
                          P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
                          aligned16(U.base) && aligned16(P.base);
         if (vec) {
-            // a single wave of resident CTAs; one slot per SM is left free when
-            // the launch shares the GPU with halo / copy launches
-            static int occ = 0;
-            if (occ == 0) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
-                if (occ < 2) occ = 2;
-            }
-            const int64_t cols = (w / 4 + 127) / 128;
-            const int64_t rows = a.chunk.hi[0] - a.chunk.lo[0];
-            const int64_t slots = int64_t(num_sms()) * (a.reserve_slot ? occ - 1 : occ);
-            int64_t ny = slots / cols;
-            if (ny < 1) ny = 1;
-            if (ny > rows) ny = rows;
-            dim3 grid{unsigned(cols), unsigned(ny), 1u};
+            dim3 grid(unsigned((w / 4 + 127) / 128), unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kWaveRows - 1) / kWaveRows));
             wave5_vec<<<grid, 128, 0, s>>>(a);
         } else {
             wave5_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);

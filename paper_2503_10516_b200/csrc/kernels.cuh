@@ -59,7 +59,6 @@ struct KArgs {
     float value;
     uint32_t t;
     uint32_t salt;
-    int reserve_slot;          // leave one CTA slot per SM for concurrent halo / copy launches
     DAcc acc[kMaxAcc];
 };
 
