@@ -9,6 +9,7 @@
 #pragma once
 
 #include <algorithm>
+#include <initializer_list>
 #include <cstdint>
 #include <utility>
 #include <vector>
@@ -79,10 +80,142 @@ inline Box bbox(const Box& a, const Box& b) {
     return r;
 }
 
-using Region = std::vector<Box>;  // canonical (R2) unless stated otherwise
+// Small vector with inline storage: most regions on the hot path hold 1-3
+// boxes, so region algebra should not touch the heap.
+template <class T, unsigned N>
+class SmallVec {
+public:
+    using value_type = T;
+    using iterator = T*;
+    using const_iterator = const T*;
+    SmallVec() = default;
+    SmallVec(std::initializer_list<T> il) {
+        reserve(il.size());
+        for (const T& x : il) push_back(x);
+    }
+    template <class It, class = decltype(*std::declval<It>())>
+    SmallVec(It b, It e) {
+        for (; b != e; ++b) push_back(*b);
+    }
+    SmallVec(const SmallVec& o) {
+        reserve(o.n_);
+        for (unsigned i = 0; i < o.n_; ++i) data()[i] = o.data()[i];
+        n_ = o.n_;
+    }
+    SmallVec(SmallVec&& o) noexcept { steal(o); }
+    SmallVec& operator=(const SmallVec& o) {
+        if (this != &o) {
+            n_ = 0;
+            reserve(o.n_);
+            for (unsigned i = 0; i < o.n_; ++i) data()[i] = o.data()[i];
+            n_ = o.n_;
+        }
+        return *this;
+    }
+    SmallVec& operator=(SmallVec&& o) noexcept {
+        if (this != &o) {
+            release();
+            steal(o);
+        }
+        return *this;
+    }
+    ~SmallVec() { release(); }
+    T* data() { return heap_ ? heap_ : reinterpret_cast<T*>(buf_); }
+    const T* data() const { return heap_ ? heap_ : reinterpret_cast<const T*>(buf_); }
+    T* begin() { return data(); }
+    T* end() { return data() + n_; }
+    const T* begin() const { return data(); }
+    const T* end() const { return data() + n_; }
+    size_t size() const { return n_; }
+    bool empty() const { return n_ == 0; }
+    T& operator[](size_t i) { return data()[i]; }
+    const T& operator[](size_t i) const { return data()[i]; }
+    T& back() { return data()[n_ - 1]; }
+    const T& back() const { return data()[n_ - 1]; }
+    void clear() { n_ = 0; }
+    void reserve(size_t c) {
+        if (c <= cap_) return;
+        unsigned nc = cap_ * 2;
+        if (nc < c) nc = unsigned(c);
+        T* h = static_cast<T*>(::operator new(sizeof(T) * nc));
+        for (unsigned i = 0; i < n_; ++i) h[i] = data()[i];
+        if (heap_) ::operator delete(heap_);
+        heap_ = h;
+        cap_ = nc;
+    }
+    void push_back(const T& x) {
+        if (n_ == cap_) reserve(n_ + 1);
+        data()[n_++] = x;
+    }
+    template <class It>
+    void insert(T* pos, It b, It e) {  // append only (pos == end())
+        (void)pos;
+        for (; b != e; ++b) push_back(*b);
+    }
+    T* insert_at(T* pos, const T& x) {
+        const size_t i = size_t(pos - data());
+        push_back(x);
+        T* d = data();
+        for (size_t k = n_ - 1; k > i; --k) d[k] = d[k - 1];
+        d[i] = x;
+        return d + i;
+    }
+    bool operator<(const SmallVec& o) const {
+        return std::lexicographical_compare(begin(), end(), o.begin(), o.end());
+    }
+    T* erase(T* first, T* last) {
+        T* d = data();
+        const size_t f = size_t(first - d), l = size_t(last - d);
+        for (size_t i = l; i < n_; ++i) d[f + i - l] = d[i];
+        n_ -= unsigned(l - f);
+        return d + f;
+    }
+    void swap(SmallVec& o) {
+        SmallVec t(std::move(o));
+        o = std::move(*this);
+        *this = std::move(t);
+    }
+    bool operator==(const SmallVec& o) const {
+        if (n_ != o.n_) return false;
+        for (unsigned i = 0; i < n_; ++i)
+            if (!(data()[i] == o.data()[i])) return false;
+        return true;
+    }
+    bool operator!=(const SmallVec& o) const { return !(*this == o); }
+
+private:
+    void release() {
+        if (heap_) ::operator delete(heap_);
+        heap_ = nullptr;
+        cap_ = N;
+        n_ = 0;
+    }
+    void steal(SmallVec& o) {
+        if (o.heap_) {
+            heap_ = o.heap_;
+            cap_ = o.cap_;
+            n_ = o.n_;
+            o.heap_ = nullptr;
+            o.cap_ = N;
+            o.n_ = 0;
+        } else {
+            heap_ = nullptr;
+            cap_ = N;
+            n_ = o.n_;
+            for (unsigned i = 0; i < n_; ++i) reinterpret_cast<T*>(buf_)[i] = reinterpret_cast<const T*>(o.buf_)[i];
+            o.n_ = 0;
+        }
+    }
+    alignas(T) unsigned char buf_[sizeof(T) * N];
+    T* heap_ = nullptr;
+    unsigned n_ = 0, cap_ = N;
+};
+
+using Region = SmallVec<Box, 3>;  // canonical (R2) unless stated otherwise
 
 // a \ b as disjoint boxes appended to out (peel slabs off dim 0, 1, 2).
-inline void subtract_into(const Box& a, const Box& b, std::vector<Box>& out) {
+template <class Vec>
+inline void subtract_into(const Box& a, const Box& b, Vec& out) {
     Box i = intersect(a, b);
     if (i.empty()) {
         if (!a.empty()) out.push_back(a);
@@ -98,7 +231,7 @@ inline void subtract_into(const Box& a, const Box& b, std::vector<Box>& out) {
 
 namespace detail {
 // Canonical boxes for the union of `bs` over dims d..2 (dims < d identical).
-inline void canon_dim(std::vector<Box>& bs, int d, std::vector<Box>& out) {
+inline void canon_dim(Region& bs, int d, Region& out) {
     if (d == 2) {
         std::sort(bs.begin(), bs.end(), [](const Box& a, const Box& b) {
             return a.lo[2] != b.lo[2] ? a.lo[2] < b.lo[2] : a.hi[2] < b.hi[2];
@@ -128,8 +261,8 @@ inline void canon_dim(std::vector<Box>& bs, int d, std::vector<Box>& out) {
     std::sort(cuts.begin(), cuts.end());
     cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     // slabs: [lo, hi) with their canonical cross-section
-    std::vector<std::pair<std::pair<int64_t, int64_t>, std::vector<Box>>> slabs;
-    std::vector<Box> cover, sub;
+    std::vector<std::pair<std::pair<int64_t, int64_t>, Region>> slabs;
+    Region cover, sub;
     for (size_t k = 0; k + 1 < cuts.size(); ++k) {
         const int64_t lo = cuts[k], hi = cuts[k + 1];
         cover.clear();
@@ -149,7 +282,7 @@ inline void canon_dim(std::vector<Box>& bs, int d, std::vector<Box>& out) {
 }
 }  // namespace detail
 
-inline Region canon(std::vector<Box> boxes) {
+inline Region canon(Region boxes) {
     boxes.erase(std::remove_if(boxes.begin(), boxes.end(), [](const Box& b) { return b.empty(); }), boxes.end());
     Region out;
     if (boxes.empty()) return out;
@@ -187,7 +320,7 @@ inline Region region_of(const Box& b) { return b.empty() ? Region{} : Region{b};
 inline Region runion(const Region& a, const Region& b) {
     if (a.empty()) return b;
     if (b.empty()) return a;
-    std::vector<Box> all(a);
+    Region all(a);
     all.insert(all.end(), b.begin(), b.end());
     return canon(std::move(all));
 }
@@ -198,7 +331,7 @@ inline Region rinter(const Region& a, const Region& b) {
         Box i = intersect(a[0], b[0]);
         return i.empty() ? Region{} : Region{i};
     }
-    std::vector<Box> out;
+    Region out;
     for (const Box& x : a)
         for (const Box& y : b) {
             Box i = intersect(x, y);
@@ -210,7 +343,7 @@ inline Region rinter(const Region& a, const Region& b) {
 
 inline Region rinter(const Region& a, const Box& b) {
     if (b.empty() || a.empty()) return {};
-    std::vector<Box> out;
+    Region out;
     bool whole = true;
     for (const Box& x : a) {
         Box i = intersect(x, b);
@@ -234,7 +367,7 @@ inline Region rdiff(const Region& a, const Region& b) {
     return rdiff_nobb(a, b);
 }
 inline Region rdiff_nobb(const Region& a, const Region& b) {
-    std::vector<Box> cur(a), nxt;
+    Region cur(a), nxt;
     bool changed = false;
     for (const Box& y : b) {
         nxt.clear();
@@ -304,20 +437,22 @@ struct RegionMap {
         Region reg = rinter(reg0, extent);
         if (reg.empty()) return;
         const Box rb = rbbox(reg);
-        std::vector<Entry> ne;
-        ne.reserve(e.size() + 1);
-        for (auto& p : e) {
-            if (intersect(p.bb, rb).empty()) {
-                ne.push_back(std::move(p));
-                continue;
+        // only entries touching reg change; the rest stay in place
+        size_t w = 0;
+        for (size_t i = 0; i < e.size(); ++i) {
+            Entry& p = e[i];
+            if (!intersect(p.bb, rb).empty()) {
+                Region rr = rdiff_nobb(p.second, reg);
+                if (rr.empty()) continue;
+                if (rr.size() != p.second.size() || !(rr == p.second)) {
+                    p.bb = rbbox(rr);
+                    p.second = std::move(rr);
+                }
             }
-            Region rr = rdiff_nobb(p.second, reg);
-            if (!rr.empty()) {
-                Box bb = rbbox(rr);
-                ne.push_back(Entry{p.first, std::move(rr), bb});
-            }
+            if (w != i) e[w] = std::move(p);
+            ++w;
         }
-        e.swap(ne);
+        e.resize(w);
         put(v, reg);
     }
 
@@ -391,7 +526,7 @@ struct RegionMap {
 
     template <class P>
     Region where(P pred) const {
-        std::vector<Box> all;
+        Region all;
         for (auto& p : e)
             if (pred(p.first)) all.insert(all.end(), p.second.begin(), p.second.end());
         if (all.size() <= 1) return all;

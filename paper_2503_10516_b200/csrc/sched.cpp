@@ -111,13 +111,13 @@ int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out) {
     return E_INVALID;
 }
 
-void sorted_insert(std::vector<int64_t>& v, int64_t x) {
+void sorted_insert(IdSet& v, int64_t x) {
     auto it = std::lower_bound(v.begin(), v.end(), x);
-    if (it == v.end() || *it != x) v.insert(it, x);
+    if (it == v.end() || *it != x) v.insert_at(it, x);
 }
 
-std::vector<int64_t> subsume_set(const std::vector<int64_t>& s, int64_t h) {
-    std::vector<int64_t> out;
+IdSet subsume_set(const IdSet& s, int64_t h) {
+    IdSet out;
     out.reserve(s.size());
     bool hit = false;
     for (int64_t x : s) {
@@ -181,11 +181,11 @@ int Scheduler::buffer_create(int dims, const int64_t extent[3], uint32_t elem_si
     b->uptodate = RegionMap<uint32_t>(b->extent, host_init ? 1u : 0u);
     if (host_init) {
         b->host.reset(new Alloc{HOST_AID, bid, 0, b->extent, -1, RegionMap<int64_t>(b->extent, fallback_),
-                                RegionMap<std::vector<int64_t>>(b->extent, {})});
+                                RegionMap<IdSet>(b->extent, {})});
     }
     TBuf& t = tbufs_[bid];
     t.last_writer = RegionMap<int64_t>(b->extent, host_init ? t_fallback_ : NONE);
-    t.readers = RegionMap<std::vector<int64_t>>(b->extent, {});
+    t.readers = RegionMap<IdSet>(b->extent, {});
     t.initialized = host_init ? Region{b->extent} : Region{};
     bufs_[bid] = std::move(b);
     *out = bid;
@@ -202,7 +202,7 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
         });
     for (auto& kv : writes) {
         TBuf& t = tbufs_[kv.first];
-        t.readers.for_values_in(kv.second, [&](const std::vector<int64_t>& s) { deps.insert(deps.end(), s.begin(), s.end()); });
+        t.readers.for_values_in(kv.second, [&](const IdSet& s) { deps.insert(deps.end(), s.begin(), s.end()); });
         t.last_writer.for_values_in(kv.second, [&](int64_t v) {
             if (v >= 0) deps.push_back(v);
         });
@@ -212,7 +212,7 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
     int64_t cp = 0;
     for (int64_t d : deps) cp = std::max(cp, cp_[d]);
     cp_[tid] = cp + 1;
-    for (auto& kv : reads) tbufs_[kv.first].readers.apply(kv.second, [tid](std::vector<int64_t> s) {
+    for (auto& kv : reads) tbufs_[kv.first].readers.apply(kv.second, [tid](IdSet s) {
         sorted_insert(s, tid);
         return s;
     });
@@ -229,7 +229,7 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
 void Scheduler::tdag_subsume(int64_t h) {
     for (auto& kv : tbufs_) {
         kv.second.last_writer.map_values([h](int64_t v) { return (v >= 0 && v < h) ? h : v; });
-        kv.second.readers.map_values([h](const std::vector<int64_t>& s) { return subsume_set(s, h); });
+        kv.second.readers.map_values([h](const IdSet& s) { return subsume_set(s, h); });
     }
 }
 
@@ -569,7 +569,7 @@ Scheduler::Alloc* Scheduler::new_alloc(uint32_t bid, int mem, const Box& box, in
     std::vector<uint64_t> deps;
     const uint64_t iid = emit(ins, deps);
     auto a = std::unique_ptr<Alloc>(new Alloc{ins.aid, bid, mem, box, int64_t(iid), RegionMap<int64_t>(box, NONE),
-                                              RegionMap<std::vector<int64_t>>(box, {})});
+                                              RegionMap<IdSet>(box, {})});
     Alloc* p = a.get();
     allocs_[ins.aid] = std::move(a);
     bufs_[bid]->live[mem].push_back(p);
@@ -606,7 +606,7 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
     auto add = [&](int64_t v) {
         if (v >= 0) deps.push_back(uint64_t(v));
     };
-    auto adds = [&](const std::vector<int64_t>& s) {
+    auto adds = [&](const IdSet& s) {
         for (int64_t r : s) deps.push_back(uint64_t(r));
     };
     if (src->iid >= 0) deps.push_back(uint64_t(src->iid));
@@ -629,7 +629,7 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
     ins.readback = rb;
     const uint64_t iid = emit(ins, deps);
     const int64_t me = int64_t(iid);
-    src->readers.apply(reg, [me](std::vector<int64_t> s) {
+    src->readers.apply(reg, [me](IdSet s) {
         sorted_insert(s, me);
         return s;
     });
@@ -792,7 +792,7 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
             if (rit != c.reads.end()) a->last_writer.for_values_in(rit->second, add);
             auto wit = c.writes.find(it->first);
             if (wit != c.writes.end()) {
-                a->readers.for_values_in(wit->second, [&](const std::vector<int64_t>& s) {
+                a->readers.for_values_in(wit->second, [&](const IdSet& s) {
                     for (int64_t r : s) deps.push_back(uint64_t(r));
                 });
                 a->last_writer.for_values_in(wit->second, add);
@@ -813,7 +813,7 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         for (auto it = c.req.lower_bound({d, 0}); it != c.req.end() && it->first.first == d; ++it) {
             Alloc* a = binding[it->first];
             auto rit = c.reads.find(it->first);
-            if (rit != c.reads.end()) a->readers.apply(rit->second, [me](std::vector<int64_t> s) {
+            if (rit != c.reads.end()) a->readers.apply(rit->second, [me](IdSet s) {
                 sorted_insert(s, me);
                 return s;
             });
@@ -835,7 +835,7 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
 void Scheduler::subsume(int64_t h) {
     // horizon / epoch application (R7)
     auto f = [h](int64_t v) { return (v >= 0 && v < h) ? h : v; };
-    auto fs = [h](const std::vector<int64_t>& s) { return subsume_set(s, h); };
+    auto fs = [h](const IdSet& s) { return subsume_set(s, h); };
     for (auto& kv : bufs_) {
         Buf& b = *kv.second;
         b.orig_writer.map_values(f);
@@ -888,4 +888,26 @@ void Scheduler::compile_epoch(Cmd& c) {
     pending_h_ = -1;
 }
 
+}  // namespace cel
+
+namespace cel {
+void Scheduler::debug_dump(FILE* f) const {
+    for (auto& kv : bufs_) {
+        const Buf& b = *kv.second;
+        size_t ob = 0, ub = 0;
+        for (auto& e : b.orig_writer.e) ob += e.second.size();
+        for (auto& e : b.uptodate.e) ub += e.second.size();
+        fprintf(f, "buffer %u: orig_writer %zu entries / %zu boxes, uptodate %zu entries / %zu boxes\n", kv.first,
+                b.orig_writer.e.size(), ob, b.uptodate.e.size(), ub);
+        for (auto& lv : b.live)
+            for (const Alloc* a : lv.second) {
+                size_t lb = 0, rb = 0;
+                for (auto& e : a->last_writer.e) lb += e.second.size();
+                for (auto& e : a->readers.e) rb += e.second.size();
+                fprintf(f, "  alloc %lld mem %d: last_writer %zu/%zu readers %zu/%zu\n", (long long)a->aid, a->mem,
+                        a->last_writer.e.size(), lb, a->readers.e.size(), rb);
+            }
+    }
+    fprintf(f, "tdag cp entries %zu, front %zu\n", cp_.size(), front_.size());
+}
 }  // namespace cel

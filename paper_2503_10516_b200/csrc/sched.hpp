@@ -67,6 +67,8 @@ struct TaskDesc {
     std::vector<Access> acc;
 };
 
+using IdSet = SmallVec<int64_t, 6>;      // a set of instruction / task ids, sorted
+
 enum class IKind : uint8_t { Alloc, Free, Copy, Kernel, Horizon, Epoch };
 enum CopyReason : int { REASON_RESIZE = 0, REASON_COHERENCE = 1, REASON_READBACK = 2 };
 
@@ -130,6 +132,7 @@ public:
     const SchedStats& stats() const { return st_; }
     int64_t next_readback_id() const { return next_rb_; }
     uint64_t next_iid() const { return next_iid_; }
+    void debug_dump(FILE* f) const;
 
 private:
     struct Alloc {
@@ -139,7 +142,7 @@ private:
         Box box;
         int64_t iid;                                  // alloc instruction, -1 for HOST_AID
         RegionMap<int64_t> last_writer;
-        RegionMap<std::vector<int64_t>> readers;
+        RegionMap<IdSet> readers;
     };
     struct Buf {
         uint32_t bid;
@@ -154,7 +157,7 @@ private:
     };
     struct TBuf {                                     // task-graph tracking
         RegionMap<int64_t> last_writer;
-        RegionMap<std::vector<int64_t>> readers;
+        RegionMap<IdSet> readers;
         Region initialized;
     };
     using Key = std::pair<int, uint32_t>;             // (device, buffer)
