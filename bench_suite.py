@@ -70,10 +70,10 @@ def c1():
     return out
 
 
-def c3(steps=2):
+def c3(steps=2, fast=False):
     N = 1 << 20
     G = 1
-    rt = cel.Runtime(G, arena_bytes=1 << 30)
+    rt = cel.Runtime(G, arena_bytes=1 << 30, fast_math=fast)
     prog = P.nbody(N, steps=1)
     Pb = rt.buffer_create(1, [N], 16)
     Vb = rt.buffer_create(1, [N], 16)
@@ -95,7 +95,13 @@ def c3(steps=2):
                          "(the kernel is built with -fmad=false and IEEE div/sqrt for bit-exact parity: no FMA)",
                          "frac": (flops / km / 1e12 / FP32_NOMINAL_TFLOPS) if km else None,
                          "flop_per_interaction": 20},
-            "profile_ms": {k: v[0] for k, v in prof.items()}, "n": N, "devices": G}
+            "profile_ms": {k: v[0] for k, v in prof.items()}, "n": N, "devices": G, "fast_math": fast}
+
+
+def c3fast():
+    r = c3(steps=4, fast=True)
+    r["roofline"]["peak_source"] = "nominal 148 SM x 128 FP32 lanes x 2 x 1.965 GHz (fast_math: FMA + MUFU rsqrt)"
+    return r
 
 
 def c4(T=1024, W=84000):
@@ -193,7 +199,7 @@ def copy_sweep():
                                               "accesses": [(0, "read", ("all",)), (1, "write", ("one_to_one",))]}))
             prof = rt.profile_read()
             rt.shutdown()
-            ms, cnt = prof["copy"]
+            ms, cnt = prof["copy_peer"]
             half = N * 16 // 2
             out["peer_push_%dMiB" % mib] = {"payload_bytes_per_copy": half, "copies": cnt, "ms_total": ms,
                                             "GBps_per_direction": half / (ms / cnt / 1e3) / 1e9,
@@ -204,12 +210,12 @@ def copy_sweep():
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c3,c4,c5,copy")
+    ap.add_argument("--only", default="c1,c3,c3fast,c4,c5,copy")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     res = {"gpu": torch.cuda.get_device_name(0), "gpus": torch.cuda.device_count(), "hbm_peak_gbs": HBM,
            "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())}
-    fns = {"c1": c1, "c3": c3, "c4": c4, "c5": c5, "copy": copy_sweep}
+    fns = {"c1": c1, "c3": c3, "c3fast": c3fast, "c4": c4, "c5": c5, "copy": copy_sweep}
     for k in args.only.split(","):
         t0 = time.time()
         res[k] = fns[k]()

@@ -140,6 +140,8 @@ typedef struct {
     uint64_t arena_bytes;      /* device memory reserved per device; 0 = 16 GiB */
     int32_t rank;              /* multi-process: this process's rank; device `rank` is its own */
     int32_t world;             /* multi-process: number of processes (= n_devices), 1 = single process */
+    int32_t fast_math;         /* 1: ALU-bound kernels (N-body) use FMA + rsqrt; results then match the
+                                  oracle within a tolerance instead of bit for bit (R16) */
 } cel_config;
 
 typedef struct {
@@ -200,7 +202,9 @@ int cel_stats_get(cel_runtime* rt, cel_stats* out);
 
 /* Device-time profile of the kernels this process launched, measured with
  * CUDA events on the launching streams: ms[k], count[k] for k = cel_kernel
- * kinds 0..9 and k = 10 for the copy kernel.  n = array length (11). */
+ * kinds 0..9, k = 10 for copy kernels within one GPU (resize, copies between
+ * virtual devices of one GPU) and k = 11 for peer pushes to another GPU.
+ * n = array length (12). */
 int cel_profile_enable(cel_runtime* rt, int32_t on);
 int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n);
 

@@ -26,8 +26,9 @@ SPLITS = {"1d": 0, "2d": 1}
 KERNELS = {"fill_hash": 0, "fill_const": 1, "stencil3": 2, "wave5": 3, "jacobi7": 4, "nbody_step": 5,
            "nbody_update": 6, "rsim_row": 7, "probe": 8, "callback": 9}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
-PROFILE_SLOTS = 11       # kernel kinds 0..9 + copy kernel (10)
+PROFILE_SLOTS = 12       # kernel kinds 0..9, copy within a GPU (10), peer push (11)
 COPY_SLOT = 10
+PEER_SLOT = 11
 
 
 class cel_box(C.Structure):
@@ -65,7 +66,7 @@ class cel_config(C.Structure):
     _fields_ = [("cuda_devices", C.POINTER(C.c_int)), ("n_devices", C.c_int32), ("execute", C.c_int32),
                 ("lookahead", C.c_int32), ("horizon_step", C.c_int32), ("checks", C.c_int32),
                 ("instr_log_path", C.c_char_p), ("arena_bytes", C.c_uint64), ("rank", C.c_int32),
-                ("world", C.c_int32)]
+                ("world", C.c_int32), ("fast_math", C.c_int32)]
 
 
 class cel_stats(C.Structure):
@@ -165,7 +166,7 @@ class Runtime:
     """The C-ABI runtime.  Method names follow include/cel.h (cel_ prefix dropped)."""
 
     def __init__(self, n_devices, cuda_devices=None, execute=True, lookahead="auto", horizon_step=4, checks=True,
-                 instr_log_path=None, arena_bytes=0, rank=0, world=1):
+                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False):
         cfg = cel_config()
         devs = list(cuda_devices) if cuda_devices is not None else list(range(n_devices))
         self._devs = (C.c_int * len(devs))(*devs)
@@ -179,6 +180,7 @@ class Runtime:
         cfg.arena_bytes = int(arena_bytes)
         cfg.rank = rank
         cfg.world = world
+        cfg.fast_math = 1 if fast_math else 0
         h = _P()
         _check(lib.cel_runtime_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -258,7 +260,8 @@ class Runtime:
         out = {}
         for k in range(PROFILE_SLOTS):
             if cnt[k]:
-                out["copy" if k == COPY_SLOT else KERNEL_NAMES[k]] = (ms[k], cnt[k])
+                name = "copy" if k == COPY_SLOT else ("copy_peer" if k == PEER_SLOT else KERNEL_NAMES[k])
+                out[name] = (ms[k], cnt[k])
         return out
 
     def shutdown(self):

@@ -90,6 +90,7 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
         ec.rank = world > 1 ? cfg->rank : 0;
         ec.world = world;
         ec.arena_bytes = cfg->arena_bytes;
+        ec.fast_math = cfg->fast_math != 0;
         rt->exec = std::make_unique<Executor>(ec, nullptr);
         std::string err;
         const int rc = rt->exec->init(&err);

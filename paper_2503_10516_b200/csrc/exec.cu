@@ -681,7 +681,7 @@ void Executor::exec_copy(const Instr& ins) {
         auto flush = [&]() {
             if (args.nseg == 0) return;
             if (cfg_.profile) {
-                Prof p{K_NUM, nullptr, nullptr};
+                Prof p{args.peer ? K_NUM + 1 : K_NUM, nullptr, nullptr};
                 cudaEventCreate(&p.a);
                 cudaEventCreate(&p.b);
                 cudaEventRecord(p.a, streams_[sidx].s);
@@ -867,6 +867,7 @@ void Executor::exec_kernel(const Instr& ins) {
     a.value = d.params.value;
     a.t = d.params.t;
     a.salt = d.params.salt;
+    a.fast = cfg_.fast_math ? 1 : 0;
     for (int i = 0; i < a.n_acc; ++i) {
         const Access& ac = d.acc[i];
         DAcc& A = a.acc[i];
@@ -1008,7 +1009,7 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
         cudaEventDestroy(p.b);
     }
     prof_pending_.clear();
-    for (int i = 0; i < n && i <= K_NUM; ++i) {
+    for (int i = 0; i < n && i <= K_NUM + 1; ++i) {
         ms[i] = prof_ms_[i];
         count[i] = prof_n_[i];
     }
@@ -1016,10 +1017,10 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
 }
 
 void Executor::profile_reset() {
-    double ms[K_NUM + 1];
-    uint64_t c[K_NUM + 1];
-    profile_read(ms, c, K_NUM + 1);
-    for (int i = 0; i <= K_NUM; ++i) {
+    double ms[K_NUM + 2];
+    uint64_t c[K_NUM + 2];
+    profile_read(ms, c, K_NUM + 2);
+    for (int i = 0; i <= K_NUM + 1; ++i) {
         prof_ms_[i] = 0;
         prof_n_[i] = 0;
     }

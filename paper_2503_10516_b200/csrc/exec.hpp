@@ -47,6 +47,7 @@ struct ExecConfig {
     int rank = 0, world = 1;           // world > 1: device d is owned by rank d
     uint64_t arena_bytes = 0;          // per device; 0 = auto
     bool profile = false;
+    bool fast_math = false;
 };
 
 struct ExecStats {
@@ -179,8 +180,8 @@ private:
     std::unordered_map<int64_t, Readback> readbacks_;
     std::unordered_set<uint64_t> signalled_;       // (iid * world + target) already signalled
     std::vector<Prof> prof_pending_;
-    double prof_ms_[K_NUM + 1] = {};
-    uint64_t prof_n_[K_NUM + 1] = {};
+    double prof_ms_[K_NUM + 2] = {};     // kernel kinds, K_NUM = local copy, K_NUM+1 = peer copy
+    uint64_t prof_n_[K_NUM + 2] = {};
     std::vector<int> phys_;
     bool memops64_ = false;
     int err_ = 0;

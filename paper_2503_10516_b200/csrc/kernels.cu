@@ -389,6 +389,60 @@ __global__ void __launch_bounds__(kNbTile) nbody_step_kernel(const __grid_consta
     }
 }
 
+// fast-math timestep: FMA contraction and the MUFU reciprocal square root,
+// 4 bodies j per unrolled iteration; same summation order over j
+__global__ void __launch_bounds__(kNbTile) nbody_step_fast_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& P = a.acc[0];
+    const DAcc& V = a.acc[1];
+    __shared__ float4 sp[kNbTile];
+    const int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * kNbTile + threadIdx.x;
+    const bool valid = i < a.chunk.hi[0];
+    const int64_t N = P.ext[0];
+    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) pi = *ptr<const float4>(P, i, 0, 0);
+    float ax = 0.f, ay = 0.f, az = 0.f;
+    for (int64_t j0 = 0; j0 < N; j0 += kNbTile) {
+        const int64_t j = j0 + threadIdx.x;
+        sp[threadIdx.x] = j < N ? *ptr<const float4>(P, j, 0, 0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        __syncthreads();
+        const int jn = N - j0 < kNbTile ? int(N - j0) : kNbTile;
+        if (jn == kNbTile) {
+#pragma unroll 8
+            for (int k = 0; k < kNbTile; ++k) {
+                const float4 pj = sp[k];
+                const float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+                const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmaf_rn(dx, dx, NB_EPS2)));
+                const float inv = rsqrtf(r2);
+                const float s = inv * inv * inv;
+                ax = __fmaf_rn(dx, s, ax);
+                ay = __fmaf_rn(dy, s, ay);
+                az = __fmaf_rn(dz, s, az);
+            }
+        } else {
+            for (int k = 0; k < jn; ++k) {
+                const float4 pj = sp[k];
+                const float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
+                const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmaf_rn(dx, dx, NB_EPS2)));
+                const float inv = rsqrtf(r2);
+                const float s = inv * inv * inv;
+                ax = __fmaf_rn(dx, s, ax);
+                ay = __fmaf_rn(dy, s, ay);
+                az = __fmaf_rn(dz, s, az);
+            }
+        }
+        __syncthreads();
+    }
+    if (valid) {
+        float4* vp = ptr<float4>(V, i, 0, 0);
+        float4 v = *vp;
+        const float c = NB_DT * NB_MASS;
+        v.x = __fmaf_rn(c, ax, v.x);
+        v.y = __fmaf_rn(c, ay, v.y);
+        v.z = __fmaf_rn(c, az, v.z);
+        *vp = v;
+    }
+}
+
 __global__ void nbody_update_kernel(const __grid_constant__ KArgs a) {
     const DAcc& V = a.acc[0];
     const DAcc& P = a.acc[1];
@@ -412,11 +466,27 @@ __global__ void rsim_row_kernel(const __grid_constant__ KArgs a) {
     const int64_t W = R.ext[1];
     for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
          i += int64_t(gridDim.x) * blockDim.x) {
+        // sum over s ascending (sequential adds, R16); the loads of a group of
+        // 8 rows are independent and issued together for memory parallelism
         float acc = 0.f;
-        int64_t col = i;
-        for (int64_t s = 0; s < t; ++s) {
-            acc = acc + *ptr<const float>(R, s, col, 0);
-            col = col + 1 == W ? 0 : col + 1;
+        const float* base = ptr<const float>(R, 0, 0, 0);
+        const int64_t pitch = R.n[1];
+        int64_t s = 0;
+        for (; s + 8 <= t; s += 8) {
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                int64_t c = i + s + k;
+                c = c >= W ? c - W : c;
+                v[k] = __ldg(base + (s + k) * pitch + c);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc = acc + v[k];
+        }
+        for (; s < t; ++s) {
+            int64_t c = i + s;
+            c = c >= W ? c - W : c;
+            acc = acc + __ldg(base + s * pitch + c);
         }
         const float prev = *ptr<const float>(R, t - 1, i, 0);
         const float coef = 0.5f / float(t);
@@ -551,7 +621,10 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
     case K_NBODY_STEP: {
         if (cv == 0) return 0;
         const int64_t n = a.chunk.hi[0] - a.chunk.lo[0];
-        nbody_step_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
+        if (a.fast)
+            nbody_step_fast_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
+        else
+            nbody_step_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
         return 1;
     }
     case K_NBODY_UPDATE:

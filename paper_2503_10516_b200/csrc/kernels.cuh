@@ -59,6 +59,7 @@ struct KArgs {
     float value;
     uint32_t t;
     uint32_t salt;
+    int fast;                  // fast-math variant (FMA + rsqrt) of ALU-bound kernels
     DAcc acc[kMaxAcc];
 };
 
