@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -106,6 +107,89 @@ __global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyA
     // pushes into peer memory: make the stores visible system-wide before the
     // kernel retires (a flag written after this kernel releases the data)
     if (a.peer) __threadfence_system();
+}
+
+// ------------------------------------------------------------------ copy (TMA bulk engine)
+// One elected thread per CTA drives the Tensor Memory Accelerator's bulk
+// copies (cp.async.bulk, SASS UBLKCP): global -> shared (completion on an
+// mbarrier) -> global, 8 stages x 16 KiB in flight per SM.  Used for local
+// copies whose segments are all 16-byte aligned (see launch_copy).
+constexpr int kTmaStages = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            bar),
+        "r"(phase)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(32) copy_kernel_tma(const __grid_constant__ CopyArgs a) {
+    extern __shared__ __align__(128) unsigned char stage_buf[];
+    __shared__ __align__(8) uint64_t bar[kTmaStages];
+    if (threadIdx.x != 0) return;
+    for (int k = 0; k < kTmaStages; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[k])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    auto unit_addr = [&](uint64_t u, const char** src, char** dst, uint32_t* nbytes) {
+        int s = 0;
+        while (s + 1 < a.nseg && a.seg[s + 1].units_begin <= u) ++s;
+        const CopySeg& g = a.seg[s];
+        const uint64_t lu = u - g.units_begin;
+        const uint64_t row_lin = lu / g.units_per_row;
+        const uint32_t chunk = uint32_t(lu - row_lin * g.units_per_row);
+        const uint64_t plane = row_lin / g.rows;
+        const uint64_t row = row_lin - plane * g.rows;
+        const uint64_t off = uint64_t(chunk) * kCopyUnit;
+        *src = g.src + plane * g.src_plane_stride + row * g.src_row_stride + off;
+        *dst = g.dst + plane * g.dst_plane_stride + row * g.dst_row_stride + off;
+        const uint64_t rem = g.row_bytes - off;
+        *nbytes = rem < kCopyUnit ? uint32_t(rem) : kCopyUnit;
+    };
+    auto issue_load = [&](uint64_t u, int st) {
+        const char* src;
+        char* dst;
+        uint32_t nb;
+        unit_addr(u, &src, &dst, &nb);
+        const uint32_t b = smem_u32(&bar[st]);
+        const uint32_t d = smem_u32(stage_buf + size_t(st) * kCopyUnit);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nb) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+                     "l"(src), "r"(nb), "r"(b)
+                     : "memory");
+    };
+    // units of this CTA: u_k = blockIdx.x + k * gridDim.x
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    for (int k = 0; k < kTmaStages; ++k) {
+        const uint64_t u = first + uint64_t(k) * step;
+        if (u >= a.total_units) break;
+        issue_load(u, k);
+    }
+    for (uint64_t k = 0;; ++k) {
+        const uint64_t u = first + k * step;
+        if (u >= a.total_units) break;
+        const int st = int(k % kTmaStages);
+        mbar_wait(smem_u32(&bar[st]), uint32_t((k / kTmaStages) & 1));
+        const char* src;
+        char* dst;
+        uint32_t nb;
+        unit_addr(u, &src, &dst, &nb);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                     "r"(smem_u32(stage_buf + size_t(st) * kCopyUnit)), "r"(nb)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        const uint64_t un = first + (k + kTmaStages) * step;
+        if (un < a.total_units) {
+            // the stage may be refilled once the store has read it out of shared memory
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            issue_load(un, st);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ helpers
@@ -321,18 +405,29 @@ __global__ void __launch_bounds__(128) jacobi7_vec(const __grid_constant__ KArgs
     }
     const bool need_e = valid && (lane == 31 || x + 4 >= ch.hi[2]);
     const bool need_w = valid && lane == 0;
-    for (int64_t z = zs; z < ze; ++z) {
+    // software pipeline: the loads of plane z+1 are in flight while plane z
+    // is computed and stored (the kernel is latency-bound otherwise)
+    auto load = [&](int64_t z, float4& nxt, float4& fm, float4& fp, float& w0, float& e0) {
         const int64_t zn = z + 1 < E0 ? z + 1 : E0 - 1;
-        float4 nxt = z4, fm = z4, fp = z4;
         if (valid) {
             nxt = __ldg(reinterpret_cast<const float4*>(arow(zn, y) + x));
             fm = __ldg(reinterpret_cast<const float4*>(arow(z, ym) + x));
             fp = __ldg(reinterpret_cast<const float4*>(arow(z, yp) + x));
         }
+        if (need_w) w0 = __ldg(arow(z, y) + xw);
+        if (need_e) e0 = __ldg(arow(z, y) + xe);
+    };
+    float4 nxt = z4, fm = z4, fp = z4;
+    float wl = 0.f, el = 0.f;
+    if (zs < ze) load(zs, nxt, fm, fp, wl, el);
+    for (int64_t z = zs; z < ze; ++z) {
+        float4 nxt2 = z4, fm2 = z4, fp2 = z4;
+        float wl2 = 0.f, el2 = 0.f;
+        if (z + 1 < ze) load(z + 1, nxt2, fm2, fp2, wl2, el2);
         float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
         float e = __shfl_down_sync(0xffffffffu, cur.x, 1);
-        if (need_w) w = __ldg(arow(z, y) + xw);
-        if (need_e) e = __ldg(arow(z, y) + xe);
+        if (need_w) w = wl;
+        if (need_e) e = el;
         float4 o;
         o.x = jac1(cur.x, prev.x, nxt.x, fm.x, fp.x, w, cur.y);
         o.y = jac1(cur.y, prev.y, nxt.y, fm.y, fp.y, cur.x, cur.z);
@@ -342,6 +437,11 @@ __global__ void __launch_bounds__(128) jacobi7_vec(const __grid_constant__ KArgs
             *reinterpret_cast<float4*>(bb + ((z - B.lo[0]) * B.n[1] + (y - B.lo[1])) * B.n[2] + (x - B.lo[2])) = o;
         prev = cur;
         cur = nxt;
+        nxt = nxt2;
+        fm = fm2;
+        fp = fp2;
+        wl = wl2;
+        el = el2;
     }
 }
 
@@ -563,6 +663,22 @@ void set_copy_blocks_per_sm(int n) { g_copy_blocks_per_sm = n > 0 ? n : 8; }
 
 int launch_copy(const CopyArgs& a, cudaStream_t s) {
     if (a.total_units == 0 || a.nseg == 0) return 0;
+    static int use_tma = -1;
+    if (use_tma < 0) {
+        const char* e = getenv("CEL_COPY");
+        use_tma = (e && e[0] == 't') ? 1 : 0;
+        if (use_tma)
+            cudaFuncSetAttribute(copy_kernel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kTmaStages * kCopyUnit));
+    }
+    bool all16 = true;
+    for (int i = 0; i < a.nseg; ++i) all16 = all16 && a.seg[i].vec == 16;
+    if (use_tma && all16 && !a.peer) {
+        int64_t grid = num_sms();
+        if (int64_t(a.total_units) < grid) grid = int64_t(a.total_units);
+        copy_kernel_tma<<<unsigned(grid), 32, kTmaStages * kCopyUnit, s>>>(a);
+        return 1;
+    }
     int64_t grid = int64_t(num_sms()) * g_copy_blocks_per_sm;
     if (int64_t(a.total_units) < grid) grid = int64_t(a.total_units);
     copy_kernel<<<unsigned(grid), 256, 0, s>>>(a);
