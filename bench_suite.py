@@ -149,7 +149,7 @@ def c5(steps=20, n=1024):
 
 
 def copy_sweep():
-    out = {}
+    out = {"impl": os.environ.get("CEL_COPY", "lsu")}
     # (a) 1 GiB contiguous resize copy: write [0, 2^28), then a task needs [0, 2^28 + 1)
     n = 1 << 28
     for reps in range(1):

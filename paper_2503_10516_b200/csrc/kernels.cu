@@ -405,29 +405,18 @@ __global__ void __launch_bounds__(128) jacobi7_vec(const __grid_constant__ KArgs
     }
     const bool need_e = valid && (lane == 31 || x + 4 >= ch.hi[2]);
     const bool need_w = valid && lane == 0;
-    // software pipeline: the loads of plane z+1 are in flight while plane z
-    // is computed and stored (the kernel is latency-bound otherwise)
-    auto load = [&](int64_t z, float4& nxt, float4& fm, float4& fp, float& w0, float& e0) {
+    for (int64_t z = zs; z < ze; ++z) {
         const int64_t zn = z + 1 < E0 ? z + 1 : E0 - 1;
+        float4 nxt = z4, fm = z4, fp = z4;
         if (valid) {
             nxt = __ldg(reinterpret_cast<const float4*>(arow(zn, y) + x));
             fm = __ldg(reinterpret_cast<const float4*>(arow(z, ym) + x));
             fp = __ldg(reinterpret_cast<const float4*>(arow(z, yp) + x));
         }
-        if (need_w) w0 = __ldg(arow(z, y) + xw);
-        if (need_e) e0 = __ldg(arow(z, y) + xe);
-    };
-    float4 nxt = z4, fm = z4, fp = z4;
-    float wl = 0.f, el = 0.f;
-    if (zs < ze) load(zs, nxt, fm, fp, wl, el);
-    for (int64_t z = zs; z < ze; ++z) {
-        float4 nxt2 = z4, fm2 = z4, fp2 = z4;
-        float wl2 = 0.f, el2 = 0.f;
-        if (z + 1 < ze) load(z + 1, nxt2, fm2, fp2, wl2, el2);
         float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
         float e = __shfl_down_sync(0xffffffffu, cur.x, 1);
-        if (need_w) w = wl;
-        if (need_e) e = el;
+        if (need_w) w = __ldg(arow(z, y) + xw);
+        if (need_e) e = __ldg(arow(z, y) + xe);
         float4 o;
         o.x = jac1(cur.x, prev.x, nxt.x, fm.x, fp.x, w, cur.y);
         o.y = jac1(cur.y, prev.y, nxt.y, fm.y, fp.y, cur.x, cur.z);
@@ -437,11 +426,6 @@ __global__ void __launch_bounds__(128) jacobi7_vec(const __grid_constant__ KArgs
             *reinterpret_cast<float4*>(bb + ((z - B.lo[0]) * B.n[1] + (y - B.lo[1])) * B.n[2] + (x - B.lo[2])) = o;
         prev = cur;
         cur = nxt;
-        nxt = nxt2;
-        fm = fm2;
-        fp = fp2;
-        wl = wl2;
-        el = el2;
     }
 }
 
@@ -664,16 +648,21 @@ void set_copy_blocks_per_sm(int n) { g_copy_blocks_per_sm = n > 0 ? n : 8; }
 int launch_copy(const CopyArgs& a, cudaStream_t s) {
     if (a.total_units == 0 || a.nseg == 0) return 0;
     static int use_tma = -1;
+    static bool attr_set[64] = {};
     if (use_tma < 0) {
         const char* e = getenv("CEL_COPY");
         use_tma = (e && e[0] == 't') ? 1 : 0;
-        if (use_tma)
-            cudaFuncSetAttribute(copy_kernel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kTmaStages * kCopyUnit));
     }
     bool all16 = true;
     for (int i = 0; i < a.nseg; ++i) all16 = all16 && a.seg[i].vec == 16;
     if (use_tma && all16 && !a.peer) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 0 && dev < 64 && !attr_set[dev]) {   // function attributes are per device
+            cudaFuncSetAttribute(copy_kernel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 int(kTmaStages * kCopyUnit));
+            attr_set[dev] = true;
+        }
         int64_t grid = num_sms();
         if (int64_t(a.total_units) < grid) grid = int64_t(a.total_units);
         copy_kernel_tma<<<unsigned(grid), 32, kTmaStages * kCopyUnit, s>>>(a);
