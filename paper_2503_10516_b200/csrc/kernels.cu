@@ -70,7 +70,7 @@ template <>
 __device__ __forceinline__ void copy_span<uint4>(const char* __restrict__ src, char* __restrict__ dst, uint32_t nbytes) {
     const uint32_t n = nbytes / 16;
     uint32_t i = threadIdx.x;
-    constexpr int U = 4;
+    constexpr int U = 2;
     for (; i + (U - 1) * blockDim.x < n; i += U * blockDim.x) {
         uint4 v[U];
 #pragma unroll
@@ -81,6 +81,9 @@ __device__ __forceinline__ void copy_span<uint4>(const char* __restrict__ src, c
     for (; i < n; i += blockDim.x) st_na_v4(dst + 16ull * i, ld_nc_v4(src + 16ull * i));
 }
 
+// One CTA per 8 KiB unit (a flat grid: measured faster than a persistent
+// grid-stride loop and than cudaMemcpy / torch copy_ on B200, see
+// tools/copy_micro.cu); units beyond 2^31 CTAs loop.
 __global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyArgs a) {
     for (uint64_t u = blockIdx.x; u < a.total_units; u += gridDim.x) {
         int s = 0;
@@ -668,8 +671,8 @@ int launch_copy(const CopyArgs& a, cudaStream_t s) {
         copy_kernel_tma<<<unsigned(grid), 32, kTmaStages * kCopyUnit, s>>>(a);
         return 1;
     }
-    int64_t grid = int64_t(num_sms()) * g_copy_blocks_per_sm;
-    if (int64_t(a.total_units) < grid) grid = int64_t(a.total_units);
+    int64_t grid = int64_t(a.total_units);
+    if (grid > (1ll << 31) - 1) grid = (1ll << 31) - 1;
     copy_kernel<<<unsigned(grid), 256, 0, s>>>(a);
     return 1;
 }

@@ -22,7 +22,7 @@ struct CopySeg {
 };
 
 constexpr int kMaxSegs = 24;
-constexpr uint32_t kCopyUnit = 16384;     // bytes of one row chunk per CTA iteration
+constexpr uint32_t kCopyUnit = 8192;      // bytes of one row chunk = one CTA (256 threads x 2 x 16 B)
 
 struct CopyArgs {
     CopySeg seg[kMaxSegs];
