@@ -671,7 +671,10 @@ int launch_copy(const CopyArgs& a, cudaStream_t s) {
         copy_kernel_tma<<<unsigned(grid), 32, kTmaStages * kCopyUnit, s>>>(a);
         return 1;
     }
+    // local copies: flat grid (one CTA per unit); peer pushes over NVLink: a
+    // persistent grid of 8 CTAs per SM (fewer outstanding remote CTAs measured faster)
     int64_t grid = int64_t(a.total_units);
+    if (a.peer && grid > int64_t(num_sms()) * g_copy_blocks_per_sm) grid = int64_t(num_sms()) * g_copy_blocks_per_sm;
     if (grid > (1ll << 31) - 1) grid = (1ll << 31) - 1;
     copy_kernel<<<unsigned(grid), 256, 0, s>>>(a);
     return 1;
