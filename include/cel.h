@@ -203,8 +203,10 @@ int cel_stats_get(cel_runtime* rt, cel_stats* out);
 /* Device-time profile of the kernels this process launched, measured with
  * CUDA events on the launching streams: ms[k], count[k] for k = cel_kernel
  * kinds 0..9, k = 10 for copy kernels within one GPU (resize, copies between
- * virtual devices of one GPU) and k = 11 for peer pushes to another GPU.
- * n = array length (12). */
+ * virtual devices of one GPU), k = 11 for peer pushes to another GPU and
+ * k = 12 for the boundary (shell) launches of stencil kernels that are split
+ * for halo overlap (their interiors count under the kernel's kind).
+ * n = array length (13). */
 int cel_profile_enable(cel_runtime* rt, int32_t on);
 int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n);
 

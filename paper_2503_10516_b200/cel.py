@@ -26,9 +26,10 @@ SPLITS = {"1d": 0, "2d": 1}
 KERNELS = {"fill_hash": 0, "fill_const": 1, "stencil3": 2, "wave5": 3, "jacobi7": 4, "nbody_step": 5,
            "nbody_update": 6, "rsim_row": 7, "probe": 8, "callback": 9}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
-PROFILE_SLOTS = 12       # kernel kinds 0..9, copy within a GPU (10), peer push (11)
+PROFILE_SLOTS = 13       # kernel kinds 0..9, copy within a GPU (10), peer push (11), stencil shell launches (12)
 COPY_SLOT = 10
 PEER_SLOT = 11
+SHELL_SLOT = 12
 
 
 class cel_box(C.Structure):
@@ -260,7 +261,7 @@ class Runtime:
         out = {}
         for k in range(PROFILE_SLOTS):
             if cnt[k]:
-                name = "copy" if k == COPY_SLOT else ("copy_peer" if k == PEER_SLOT else KERNEL_NAMES[k])
+                name = {COPY_SLOT: "copy", PEER_SLOT: "copy_peer", SHELL_SLOT: "shell"}.get(k) or KERNEL_NAMES[k]
                 out[name] = (ms[k], cnt[k])
         return out
 

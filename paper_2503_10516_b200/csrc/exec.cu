@@ -919,7 +919,7 @@ void Executor::exec_kernel(const Instr& ins) {
         }
         if (interior.empty()) split = false;
     }
-    auto launch = [&](const Box& ch, int stream) {
+    auto launch = [&](const Box& ch, int stream, bool shell_part) {
         KArgs b = a;
         for (int k = 0; k < 3; ++k) {
             b.chunk.lo[k] = ch.lo[k];
@@ -934,7 +934,7 @@ void Executor::exec_kernel(const Instr& ins) {
         }
         int n;
         if (cfg_.profile) {
-            Prof p{d.kernel, nullptr, nullptr};
+            Prof p{shell_part ? K_NUM + 2 : d.kernel, nullptr, nullptr};
             cudaEventCreate(&p.a);
             cudaEventCreate(&p.b);
             cudaEventRecord(p.a, streams_[stream].s);
@@ -949,7 +949,7 @@ void Executor::exec_kernel(const Instr& ins) {
         st_.workload_launches += n;
     };
     if (!split) {
-        launch(ins.chunk, sidx);
+        launch(ins.chunk, sidx, false);
         tok_[ins.iid] = record(sidx);
         return;
     }
@@ -958,7 +958,7 @@ void Executor::exec_kernel(const Instr& ins) {
     wait_token(hidx, deps);
     std::vector<Box> shell;
     subtract_into(ins.chunk, interior, shell);
-    for (const Box& b : shell) launch(b, hidx);
+    for (const Box& b : shell) launch(b, hidx, true);
     Token tshell = record(hidx);
     // interior launch: only dependencies whose accesses conflict with the
     // interior's (copies into halo rows it never reads are skipped)
@@ -987,7 +987,7 @@ void Executor::exec_kernel(const Instr& ins) {
     wait_token(sidx, ideps);
     // the interior must also follow the shell launches' own predecessors on
     // the halo stream only through real conflicts, which `ideps` carries
-    launch(interior, sidx);
+    launch(interior, sidx, false);
     Token tint = record(sidx);
     Token all = tint;
     merge(all, tshell);
@@ -1009,7 +1009,7 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
         cudaEventDestroy(p.b);
     }
     prof_pending_.clear();
-    for (int i = 0; i < n && i <= K_NUM + 1; ++i) {
+    for (int i = 0; i < n && i <= K_NUM + 2; ++i) {
         ms[i] = prof_ms_[i];
         count[i] = prof_n_[i];
     }
@@ -1017,10 +1017,10 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
 }
 
 void Executor::profile_reset() {
-    double ms[K_NUM + 2];
-    uint64_t c[K_NUM + 2];
-    profile_read(ms, c, K_NUM + 2);
-    for (int i = 0; i <= K_NUM + 1; ++i) {
+    double ms[K_NUM + 3];
+    uint64_t c[K_NUM + 3];
+    profile_read(ms, c, K_NUM + 3);
+    for (int i = 0; i <= K_NUM + 2; ++i) {
         prof_ms_[i] = 0;
         prof_n_[i] = 0;
     }

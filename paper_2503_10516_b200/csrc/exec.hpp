@@ -180,8 +180,8 @@ private:
     std::unordered_map<int64_t, Readback> readbacks_;
     std::unordered_set<uint64_t> signalled_;       // (iid * world + target) already signalled
     std::vector<Prof> prof_pending_;
-    double prof_ms_[K_NUM + 2] = {};     // kernel kinds, K_NUM = local copy, K_NUM+1 = peer copy
-    uint64_t prof_n_[K_NUM + 2] = {};
+    double prof_ms_[K_NUM + 3] = {};     // kernel kinds, K_NUM = local copy, +1 peer copy, +2 shell launches
+    uint64_t prof_n_[K_NUM + 3] = {};
     std::vector<int> phys_;
     bool memops64_ = false;
     int err_ = 0;

@@ -315,8 +315,9 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
     const int lane = threadIdx.x & 31;
     const int64_t c = c0 + (int64_t(blockIdx.x) * 128 + threadIdx.x) * 4;
     const bool valid = c < c1;
-    const int64_t rs = r0 + int64_t(blockIdx.y) * kWaveRows;
-    const int64_t re = rs + kWaveRows < r1 ? rs + kWaveRows : r1;
+    const int64_t h = a.strip > 0 ? a.strip : kWaveRows;
+    const int64_t rs = r0 + int64_t(blockIdx.y) * h;
+    const int64_t re = rs + h < r1 ? rs + h : r1;
     const float* ub = reinterpret_cast<const float*>(U.base);
     float* pb = reinterpret_cast<float*>(P.base);
     const int64_t uoff = c - U.lo[1];
@@ -706,8 +707,23 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
                          P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
                          aligned16(U.base) && aligned16(P.base);
         if (vec) {
-            dim3 grid(unsigned((w / 4 + 127) / 128), unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kWaveRows - 1) / kWaveRows));
-            wave5_vec<<<grid, 128, 0, s>>>(a);
+            // strip height: 16 rows, lowered (>= 4) until the grid has about 8
+            // waves of resident CTAs, so the last-wave tail stays small on the
+            // thin chunks of many-GPU runs
+            static int occ = 0;
+            if (occ == 0) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
+                if (occ < 1) occ = 1;
+            }
+            const int64_t cols = (w / 4 + 127) / 128;
+            const int64_t rows = a.chunk.hi[0] - a.chunk.lo[0];
+            const int64_t resident = int64_t(num_sms()) * occ;
+            int64_t h = (rows * cols) / (resident * 8);
+            h = h < 4 ? 4 : (h > kWaveRows ? kWaveRows : h);
+            KArgs b = a;
+            b.strip = int(h);
+            dim3 grid(unsigned(cols), unsigned((rows + h - 1) / h));
+            wave5_vec<<<grid, 128, 0, s>>>(b);
         } else {
             wave5_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);
         }

@@ -60,6 +60,7 @@ struct KArgs {
     uint32_t t;
     uint32_t salt;
     int fast;                  // fast-math variant (FMA + rsqrt) of ALU-bound kernels
+    int strip;                 // rows per CTA of the stencil kernels (0 = default)
     DAcc acc[kMaxAcc];
 };
 
