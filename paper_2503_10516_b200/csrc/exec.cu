@@ -793,12 +793,42 @@ void Executor::exec_copy(const Instr& ins) {
         dbox = S.box;
     }
     for (const Box& b : ins.region) {
+        // DMA: collapse to one linear copy when the box is contiguous in both
+        // layouts (full rows / planes), else a 2-D copy per plane, else 3-D
+        const size_t hrow = size_t(hbox.extent(2)) * es, drow = size_t(dbox.extent(2)) * es;
+        const size_t width = size_t(b.extent(2)) * es;
+        auto hoff = [&](int64_t z, int64_t y) {
+            return ((size_t(z - hbox.lo[0]) * size_t(hbox.extent(1)) + size_t(y - hbox.lo[1])) * hrow) +
+                   size_t(b.lo[2] - hbox.lo[2]) * es;
+        };
+        auto doff = [&](int64_t z, int64_t y) {
+            return ((size_t(z - dbox.lo[0]) * size_t(dbox.extent(1)) + size_t(y - dbox.lo[1])) * drow) +
+                   size_t(b.lo[2] - dbox.lo[2]) * es;
+        };
+        char* hp0 = hbase + hoff(b.lo[0], b.lo[1]);
+        char* dp0 = dbase + doff(b.lo[0], b.lo[1]);
+        const bool rows_contig = width == hrow && width == drow;
+        const bool planes_contig = rows_contig && b.extent(1) == hbox.extent(1) && b.extent(1) == dbox.extent(1);
+        const cudaStream_t st = streams_[sidx].s;
+        if (planes_contig || (rows_contig && b.extent(0) == 1)) {
+            const size_t bytes = width * size_t(b.extent(1)) * size_t(b.extent(0));
+            check(h2d ? cudaMemcpyAsync(dp0, hp0, bytes, cudaMemcpyHostToDevice, st)
+                      : cudaMemcpyAsync(hp0, dp0, bytes, cudaMemcpyDeviceToHost, st),
+                  "cudaMemcpyAsync");
+            st_.memcpy_calls++;
+            continue;
+        }
+        if (b.extent(0) == 1) {
+            check(h2d ? cudaMemcpy2DAsync(dp0, drow, hp0, hrow, width, size_t(b.extent(1)), cudaMemcpyHostToDevice, st)
+                      : cudaMemcpy2DAsync(hp0, hrow, dp0, drow, width, size_t(b.extent(1)), cudaMemcpyDeviceToHost, st),
+                  "cudaMemcpy2DAsync");
+            st_.memcpy_calls++;
+            continue;
+        }
         cudaMemcpy3DParms p;
         memset(&p, 0, sizeof p);
-        cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, size_t(hbox.extent(2)) * es, size_t(hbox.extent(2)) * es,
-                                                size_t(hbox.extent(1)));
-        cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, size_t(dbox.extent(2)) * es, size_t(dbox.extent(2)) * es,
-                                                size_t(dbox.extent(1)));
+        cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, hrow, hrow, size_t(hbox.extent(1)));
+        cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, drow, drow, size_t(dbox.extent(1)));
         cudaPos hpos = make_cudaPos(size_t(b.lo[2] - hbox.lo[2]) * es, size_t(b.lo[1] - hbox.lo[1]),
                                     size_t(b.lo[0] - hbox.lo[0]));
         cudaPos dpos = make_cudaPos(size_t(b.lo[2] - dbox.lo[2]) * es, size_t(b.lo[1] - dbox.lo[1]),
@@ -816,8 +846,8 @@ void Executor::exec_copy(const Instr& ins) {
             p.dstPos = hpos;
             p.kind = cudaMemcpyDeviceToHost;
         }
-        p.extent = make_cudaExtent(size_t(b.extent(2)) * es, size_t(b.extent(1)), size_t(b.extent(0)));
-        check(cudaMemcpy3DAsync(&p, streams_[sidx].s), "cudaMemcpy3DAsync");
+        p.extent = make_cudaExtent(width, size_t(b.extent(1)), size_t(b.extent(0)));
+        check(cudaMemcpy3DAsync(&p, st), "cudaMemcpy3DAsync");
         st_.memcpy_calls++;
     }
     st_.bytes_copy[h2d ? 3 : 4] += rvolume(ins.region) * es;
