@@ -1,0 +1,169 @@
+"""Multi-GPU measurement of the other BASELINE configs with bench.py's protocol
+(one process per GPU under torchrun, barrier + synchronize around the timed
+region, CUDA events, max over ranks).  Prints one JSON line on rank 0.
+
+  python bench_config.py --workload jacobi3d|nbody|rsim --gpus N [--steps K] [--warmup W]
+                         [--fast-math] [--lookahead auto|none]
+
+  jacobi3d  C5: 1024^3 fp32 7-point, 2-D split (z, y), strided y-face halos
+  nbody     C3: 2^20 float4 bodies, 'all' read of P -> G(G-1) peer pushes per step
+  rsim      C4: W = 84,000, T rows (default 1024): whole program timed (value = rows/s)
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2503_10516_b200 import cel  # noqa: E402
+from workloads import programs as P  # noqa: E402
+
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", required=True, choices=["jacobi3d", "nbody", "rsim"])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=0)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--fast-math", action="store_true")
+    ap.add_argument("--lookahead", default="auto")
+    ap.add_argument("--rows", type=int, default=1024)
+    args = ap.parse_args()
+    rank, world, local = bench.env_rank()
+    G = args.gpus
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+    torch.cuda.set_device(local if world > 1 else 0)
+    peak, peak_kind = bench.measured_peaks()
+
+    if args.workload == "jacobi3d":
+        n = 1024
+        steps = args.steps or 200
+        arena = int(2 * n ** 3 * 4 / G * 1.2) + (1 << 30)
+        rt = bench.make_runtime(cel, G, rank, world, dist, arena)
+        rt.buffer_create(3, [n, n, n], 4)
+        rt.buffer_create(3, [n, n, n], 4)
+        rt.task_submit(P.jacobi3d(n, 1)["ops"][0][1])
+        descs = [cel.task_desc(P.jacobi_step(n, k)[1]) for k in (0, 1)]
+        submit = lambda s: rt.submit_desc(descs[s % 2][0])  # noqa: E731
+        kernel = "jacobi7"
+    elif args.workload == "nbody":
+        N = 1 << 20
+        steps = args.steps or 3
+        rt = bench.make_runtime(cel, G, rank, world, dist, 1 << 30) if not args.fast_math else None
+        if rt is None:
+            if world > 1:
+                rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=1 << 30, rank=rank, world=world,
+                                 fast_math=True)
+                blobs = [None] * world
+                dist.all_gather_object(blobs, rt.ipc_export())
+                for r, b in enumerate(blobs):
+                    if r != rank:
+                        rt.ipc_import(r, b)
+                dist.barrier()
+            else:
+                rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=1 << 30, fast_math=True)
+        prog = P.nbody(N, 1)
+        rt.buffer_create(1, [N], 16)
+        rt.buffer_create(1, [N], 16)
+        for op in prog["ops"][:2]:
+            rt.task_submit(op[1])
+        descs = [cel.task_desc(op[1]) for op in prog["ops"][2:4]]
+
+        def submit(s):
+            rt.submit_desc(descs[0][0])
+            rt.submit_desc(descs[1][0])
+        kernel = "nbody_step"
+    else:
+        W, T = 84000, args.rows
+        steps = T
+        rt = bench.make_runtime(cel, G, rank, world, dist, 4 << 30) if args.lookahead == "auto" else None
+        if rt is None:
+            rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=4 << 30, rank=rank, world=world,
+                             lookahead=args.lookahead)
+            if world > 1:
+                blobs = [None] * world
+                dist.all_gather_object(blobs, rt.ipc_export())
+                for r, b in enumerate(blobs):
+                    if r != rank:
+                        rt.ipc_import(r, b)
+                dist.barrier()
+        prog = P.rsim(W, T)
+        rt.buffer_create(2, [T, W], 4)
+        descs = [cel.task_desc(op[1]) for op in prog["ops"] if op[0] == "task"]
+        submit = lambda s: rt.submit_desc(descs[s][0])  # noqa: E731
+        kernel = "rsim_row"
+
+    if args.workload != "rsim":
+        for s in range(args.warmup):
+            submit(s)
+    rt.wait()
+    st0 = rt.stats()
+    rt.profile_enable(True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    t0 = time.perf_counter()
+    for s in range(steps):
+        submit(s if args.workload == "rsim" else args.warmup + s)
+    rt.wait()
+    e1.record()
+    torch.cuda.synchronize()
+    host_s = time.perf_counter() - t0
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = rt.profile_read()
+    st1 = rt.stats()
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    rt.wait()
+    if dist:
+        dist.barrier()
+    rt.shutdown()
+    km = prof.get(kernel, (0.0, 0))[0] + prof.get("shell", (0.0, 0))[0]
+    line = {"workload": args.workload, "n_gpus": G, "processes": world, "steps": steps,
+            "value": steps / (ms / 1e3), "unit": "rows/s" if args.workload == "rsim" else "steps/s",
+            "ms_per_step": ms / steps, "host_ms_per_step": host_s * 1e3 / steps,
+            "gen_us_per_step": (st1["gen_ns"] - st0["gen_ns"]) / 1e3 / steps,
+            "gpu_launches": st1["kernel_launches"] - st0["kernel_launches"],
+            "profile_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()}}
+    if args.workload == "jacobi3d":
+        cells = 1024 ** 3 / G
+        line["roofline"] = {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_kind,
+                            "achieved": 8 * cells / (km / 1e3 / steps) / 1e9,
+                            "note": "rank-0 chunk; kernel time = interior + shell launch durations (they overlap, so this is a lower bound)"}
+        line["roofline"]["frac"] = line["roofline"]["achieved"] / peak
+    elif args.workload == "nbody":
+        inter = (1 << 20) * (1 << 20) / G * steps
+        line["roofline"] = {"bound": "alu", "unit": "TFLOP/s", "peak": FP32_NOMINAL_TFLOPS,
+                            "achieved": 20 * inter / (km / 1e3) / 1e12, "fast_math": args.fast_math}
+        line["roofline"]["frac"] = line["roofline"]["achieved"] / FP32_NOMINAL_TFLOPS
+        line["interactions_per_s"] = (1 << 40) * steps / (ms / 1e3)
+    else:
+        line["lookahead"] = args.lookahead
+        line["alloc"] = st1["n_alloc"] - st0["n_alloc"]
+        line["resize_copies"] = st1["copies_resize"] - st0["copies_resize"]
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
