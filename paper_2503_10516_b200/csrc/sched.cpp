@@ -111,25 +111,6 @@ int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out) {
     return E_INVALID;
 }
 
-void sorted_insert(IdSet& v, int64_t x) {
-    auto it = std::lower_bound(v.begin(), v.end(), x);
-    if (it == v.end() || *it != x) v.insert_at(it, x);
-}
-
-IdSet subsume_set(const IdSet& s, int64_t h) {
-    IdSet out;
-    out.reserve(s.size());
-    bool hit = false;
-    for (int64_t x : s) {
-        if (x < h)
-            hit = true;
-        else
-            out.push_back(x);
-    }
-    if (hit) sorted_insert(out, h);
-    return out;
-}
-
 bool is_read(int mode) { return mode == MODE_READ || mode == MODE_READ_WRITE; }
 bool is_write(int mode) { return mode == MODE_WRITE || mode == MODE_READ_WRITE; }
 
@@ -180,12 +161,11 @@ int Scheduler::buffer_create(int dims, const int64_t extent[3], uint32_t elem_si
     b->orig_writer = RegionMap<int64_t>(b->extent, host_init ? fallback_ : NONE);
     b->uptodate = RegionMap<uint32_t>(b->extent, host_init ? 1u : 0u);
     if (host_init) {
-        b->host.reset(new Alloc{HOST_AID, bid, 0, b->extent, -1, RegionMap<int64_t>(b->extent, fallback_),
-                                RegionMap<IdSet>(b->extent, {})});
+        b->host.reset(new Alloc{HOST_AID, bid, 0, b->extent, -1, RegionMap<int64_t>(b->extent, fallback_), ReaderList{}});
     }
     TBuf& t = tbufs_[bid];
     t.last_writer = RegionMap<int64_t>(b->extent, host_init ? t_fallback_ : NONE);
-    t.readers = RegionMap<IdSet>(b->extent, {});
+    t.readers = ReaderList{};
     t.initialized = host_init ? Region{b->extent} : Region{};
     bufs_[bid] = std::move(b);
     *out = bid;
@@ -202,7 +182,7 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
         });
     for (auto& kv : writes) {
         TBuf& t = tbufs_[kv.first];
-        t.readers.for_values_in(kv.second, [&](const IdSet& s) { deps.insert(deps.end(), s.begin(), s.end()); });
+        t.readers.ids_in(kv.second, [&](int64_t r) { deps.push_back(r); });
         t.last_writer.for_values_in(kv.second, [&](int64_t v) {
             if (v >= 0) deps.push_back(v);
         });
@@ -212,14 +192,11 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
     int64_t cp = 0;
     for (int64_t d : deps) cp = std::max(cp, cp_[d]);
     cp_[tid] = cp + 1;
-    for (auto& kv : reads) tbufs_[kv.first].readers.apply(kv.second, [tid](IdSet s) {
-        sorted_insert(s, tid);
-        return s;
-    });
+    for (auto& kv : reads) tbufs_[kv.first].readers.add(tid, kv.second);
     for (auto& kv : writes) {
         TBuf& t = tbufs_[kv.first];
         t.last_writer.update(kv.second, tid);
-        t.readers.update(kv.second, {});
+        t.readers.remove(kv.second);
         t.initialized = runion(t.initialized, kv.second);
     }
     max_cp_ = std::max(max_cp_, cp_[tid]);
@@ -229,7 +206,7 @@ int64_t Scheduler::tdag_submit(const std::map<uint32_t, Region>& reads, const st
 void Scheduler::tdag_subsume(int64_t h) {
     for (auto& kv : tbufs_) {
         kv.second.last_writer.map_values([h](int64_t v) { return (v >= 0 && v < h) ? h : v; });
-        kv.second.readers.map_values([h](const IdSet& s) { return subsume_set(s, h); });
+        kv.second.readers.subsume(h);
     }
 }
 
@@ -569,7 +546,7 @@ Scheduler::Alloc* Scheduler::new_alloc(uint32_t bid, int mem, const Box& box, in
     std::vector<uint64_t> deps;
     const uint64_t iid = emit(ins, deps);
     auto a = std::unique_ptr<Alloc>(new Alloc{ins.aid, bid, mem, box, int64_t(iid), RegionMap<int64_t>(box, NONE),
-                                              RegionMap<IdSet>(box, {})});
+                                              ReaderList{}});
     Alloc* p = a.get();
     allocs_[ins.aid] = std::move(a);
     bufs_[bid]->live[mem].push_back(p);
@@ -582,8 +559,7 @@ void Scheduler::free_alloc(Alloc* a, int64_t tid) {
     std::vector<uint64_t> deps{uint64_t(a->iid)};
     for (auto& p : a->last_writer.e)
         if (p.first >= 0) deps.push_back(uint64_t(p.first));
-    for (auto& p : a->readers.e)
-        for (int64_t r : p.first) deps.push_back(uint64_t(r));
+    a->readers.all_ids([&](int64_t r) { deps.push_back(uint64_t(r)); });
     Instr ins;
     ins.kind = IKind::Free;
     ins.task = tid;
@@ -606,14 +582,11 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
     auto add = [&](int64_t v) {
         if (v >= 0) deps.push_back(uint64_t(v));
     };
-    auto adds = [&](const IdSet& s) {
-        for (int64_t r : s) deps.push_back(uint64_t(r));
-    };
     if (src->iid >= 0) deps.push_back(uint64_t(src->iid));
     src->last_writer.for_values_in(reg, add);
     if (dst) {
         deps.push_back(uint64_t(dst->iid));
-        dst->readers.for_values_in(reg, adds);
+        dst->readers.ids_in(reg, [&](int64_t r) { deps.push_back(uint64_t(r)); });
         dst->last_writer.for_values_in(reg, add);
     }
     Instr ins;
@@ -629,13 +602,10 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
     ins.readback = rb;
     const uint64_t iid = emit(ins, deps);
     const int64_t me = int64_t(iid);
-    src->readers.apply(reg, [me](IdSet s) {
-        sorted_insert(s, me);
-        return s;
-    });
+    src->readers.add(me, reg);
     if (dst) {
         dst->last_writer.update(reg, me);
-        dst->readers.update(reg, {});
+        dst->readers.remove(reg);
     }
     const uint64_t bytes = rvolume(reg) * bufs_[bid]->elem_size;
     st_.copies_by_reason[reason]++;
@@ -792,9 +762,7 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
             if (rit != c.reads.end()) a->last_writer.for_values_in(rit->second, add);
             auto wit = c.writes.find(it->first);
             if (wit != c.writes.end()) {
-                a->readers.for_values_in(wit->second, [&](const IdSet& s) {
-                    for (int64_t r : s) deps.push_back(uint64_t(r));
-                });
+                a->readers.ids_in(wit->second, [&](int64_t r) { deps.push_back(uint64_t(r)); });
                 a->last_writer.for_values_in(wit->second, add);
             }
         }
@@ -813,14 +781,11 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         for (auto it = c.req.lower_bound({d, 0}); it != c.req.end() && it->first.first == d; ++it) {
             Alloc* a = binding[it->first];
             auto rit = c.reads.find(it->first);
-            if (rit != c.reads.end()) a->readers.apply(rit->second, [me](IdSet s) {
-                sorted_insert(s, me);
-                return s;
-            });
+            if (rit != c.reads.end()) a->readers.add(me, rit->second);
             auto wit = c.writes.find(it->first);
             if (wit != c.writes.end()) {
                 a->last_writer.update(wit->second, me);
-                a->readers.update(wit->second, {});
+                a->readers.remove(wit->second);
             }
         }
         kernels[d] = k;
@@ -835,18 +800,17 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
 void Scheduler::subsume(int64_t h) {
     // horizon / epoch application (R7)
     auto f = [h](int64_t v) { return (v >= 0 && v < h) ? h : v; };
-    auto fs = [h](const IdSet& s) { return subsume_set(s, h); };
     for (auto& kv : bufs_) {
         Buf& b = *kv.second;
         b.orig_writer.map_values(f);
         for (auto& lv : b.live)
             for (Alloc* a : lv.second) {
                 a->last_writer.map_values(f);
-                a->readers.map_values(fs);
+                a->readers.subsume(h);
             }
         if (b.host) {
             b.host->last_writer.map_values(f);
-            b.host->readers.map_values(fs);
+            b.host->readers.subsume(h);
         }
     }
 }
@@ -903,9 +867,9 @@ void Scheduler::debug_dump(FILE* f) const {
             for (const Alloc* a : lv.second) {
                 size_t lb = 0, rb = 0;
                 for (auto& e : a->last_writer.e) lb += e.second.size();
-                for (auto& e : a->readers.e) rb += e.second.size();
+                for (auto& e : a->readers.recs) rb += e.r.size();
                 fprintf(f, "  alloc %lld mem %d: last_writer %zu/%zu readers %zu/%zu\n", (long long)a->aid, a->mem,
-                        a->last_writer.e.size(), lb, a->readers.e.size(), rb);
+                        a->last_writer.e.size(), lb, a->readers.recs.size(), rb);
             }
     }
     fprintf(f, "tdag cp entries %zu, front %zu\n", cp_.size(), front_.size());

@@ -69,6 +69,94 @@ struct TaskDesc {
 
 using IdSet = SmallVec<int64_t, 6>;      // a set of instruction / task ids, sorted
 
+// Readers since the last write, as append-only records (id, region): a read
+// appends, a write removes its region from every record it overlaps, a
+// horizon renames ids older than it and merges equal ids.  The set of ids
+// overlapping any region equals that of a region map of id sets (R12), at
+// O(1) cost per read.
+struct ReaderList {
+    struct Rec {
+        int64_t id;
+        Region r;
+        Box bb;
+    };
+    std::vector<Rec> recs;
+
+    void add(int64_t id, const Region& r) {
+        if (r.empty()) return;
+        if (!recs.empty() && recs.back().id == id) {
+            recs.back().r = runion(recs.back().r, r);
+            recs.back().bb = bbox(recs.back().bb, rbbox(r));
+            return;
+        }
+        recs.push_back(Rec{id, r, rbbox(r)});
+    }
+    template <class F>
+    void ids_in(const Region& w, F fn) const {
+        if (w.empty()) return;
+        const Box wb = rbbox(w);
+        for (const Rec& x : recs) {
+            if (intersect(x.bb, wb).empty()) continue;
+            bool hit = false;
+            for (const Box& a : x.r) {
+                for (const Box& b : w)
+                    if (!intersect(a, b).empty()) {
+                        hit = true;
+                        break;
+                    }
+                if (hit) break;
+            }
+            if (hit) fn(x.id);
+        }
+    }
+    void remove(const Region& w) {
+        if (w.empty()) return;
+        const Box wb = rbbox(w);
+        size_t k = 0;
+        for (size_t i = 0; i < recs.size(); ++i) {
+            Rec& x = recs[i];
+            if (!intersect(x.bb, wb).empty()) {
+                Region rest = rdiff_nobb(x.r, w);
+                if (rest.empty()) continue;
+                if (!(rest == x.r)) {
+                    x.bb = rbbox(rest);
+                    x.r = std::move(rest);
+                }
+            }
+            if (k != i) recs[k] = std::move(x);
+            ++k;
+        }
+        recs.resize(k);
+    }
+    void subsume(int64_t h) {
+        bool any = false;
+        for (Rec& x : recs)
+            if (x.id < h) {
+                x.id = h;
+                any = true;
+            }
+        if (!any) return;
+        // merge records of equal id (keeps the list bounded across horizons)
+        std::vector<Rec> out;
+        for (Rec& x : recs) {
+            bool merged = false;
+            for (Rec& y : out)
+                if (y.id == x.id) {
+                    y.r = runion(y.r, x.r);
+                    y.bb = bbox(y.bb, x.bb);
+                    merged = true;
+                    break;
+                }
+            if (!merged) out.push_back(std::move(x));
+        }
+        recs.swap(out);
+    }
+    template <class F>
+    void all_ids(F fn) const {
+        for (const Rec& x : recs) fn(x.id);
+    }
+};
+
 enum class IKind : uint8_t { Alloc, Free, Copy, Kernel, Horizon, Epoch };
 enum CopyReason : int { REASON_RESIZE = 0, REASON_COHERENCE = 1, REASON_READBACK = 2 };
 
@@ -142,7 +230,7 @@ private:
         Box box;
         int64_t iid;                                  // alloc instruction, -1 for HOST_AID
         RegionMap<int64_t> last_writer;
-        RegionMap<IdSet> readers;
+        ReaderList readers;
     };
     struct Buf {
         uint32_t bid;
@@ -157,7 +245,7 @@ private:
     };
     struct TBuf {                                     // task-graph tracking
         RegionMap<int64_t> last_writer;
-        RegionMap<IdSet> readers;
+        ReaderList readers;
         Region initialized;
     };
     using Key = std::pair<int, uint32_t>;             // (device, buffer)
