@@ -412,8 +412,7 @@ std::map<std::pair<uint32_t, int>, Box> Scheduler::anticipated(const std::vector
 
 bool Scheduler::is_allocating(const Cmd& c) const {
     // "whether compiling it right away would emit any alloc instructions"
-    std::map<std::pair<uint32_t, int>, Box> ant;
-    if (!queue_.empty()) ant = anticipated(queue_);
+    const auto& ant = queue_ant_;     // bbox of the queued commands' requirements (incremental)
     for (auto& kv : c.req) {
         const int m = 2 + kv.first.first;
         const Buf& b = *bufs_.at(kv.first.second);
@@ -444,7 +443,7 @@ void Scheduler::push(Cmd&& c) {
             compile(c, {});
             return;
         }
-        queue_.push_back(std::move(c));
+        queue_.push_back(std::move(c));   // horizons carry no requirements
         ++counter_;
         if (mode_ == 1 && counter_ >= 2) flush();  // P:L584 "two horizons after the last allocating command"
         return;
@@ -454,6 +453,10 @@ void Scheduler::push(Cmd&& c) {
         compile(c, {});
         return;
     }
+    for (auto& kv : c.req) {
+        Box& b = queue_ant_[{kv.first.second, 2 + kv.first.first}];
+        b = bbox(b, kv.second);
+    }
     queue_.push_back(std::move(c));
     if (alloc) counter_ = 0;
 }
@@ -462,7 +465,8 @@ void Scheduler::flush() {
     if (queue_.empty()) return;
     std::vector<Cmd> q;
     q.swap(queue_);
-    auto ant = anticipated(q);
+    std::map<std::pair<uint32_t, int>, Box> ant;
+    ant.swap(queue_ant_);
     counter_ = 0;
     st_.flushes++;
     for (Cmd& c : q) compile(c, ant);

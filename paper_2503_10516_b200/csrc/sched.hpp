@@ -305,6 +305,7 @@ private:
 
     // lookahead
     std::vector<Cmd> queue_;
+    std::map<std::pair<uint32_t, int>, Box> queue_ant_;   // P:L589 requirements observed while queued
     int counter_ = 0;
 
     // IDAG
