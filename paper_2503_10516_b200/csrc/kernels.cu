@@ -11,10 +11,13 @@
 //    3-D 7-point, N-body timestep/update (Listing 1), RSim row
 //    (P:L632), integer probe.  Arithmetic order is exactly the oracle's
 //    (oracle/kernels.py); the library is built with -fmad=false (R16).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <tuple>
 
 #include "kernels.cuh"
 
@@ -433,6 +436,123 @@ __global__ void __launch_bounds__(128) jacobi7_vec(const __grid_constant__ KArgs
     }
 }
 
+// TMA tensor-map version: one elected thread streams z-plane tiles of the
+// input allocation, (BY+2) rows x (BX+8) columns (y halo + 16-byte aligned x
+// halo), into a 4-stage shared-memory ring with cp.async.bulk.tensor.3d
+// (SASS UTMALDG) completing on mbarriers; 512 consumer threads compute a
+// BY x BX output tile per plane from shared memory (z-1, z, z+1 are all in
+// the ring) and store float4 rows.  Out-of-bounds tile parts are zero-filled
+// by TMA and never read: the consumers clamp at the buffer edges (R16 order
+// of operations unchanged).
+constexpr int kJBX = 128, kJBY = 16, kJZS = 64, kJStages = 4;
+constexpr int kJPW = kJBX + 8, kJPH = kJBY + 2, kJPlane = kJPW * kJPH;   // floats per staged plane
+constexpr int kJStride = (kJPlane + 31) / 32 * 32;                          // stage stride: 128-byte aligned
+
+__global__ void __launch_bounds__(512) jacobi7_tma(const __grid_constant__ CUtensorMap tm, const __grid_constant__ KArgs a) {
+    extern __shared__ __align__(128) float jsm[];
+    __shared__ __align__(8) uint64_t jbar[kJStages];
+    const DAcc& A = a.acc[0];
+    const DAcc& B = a.acc[1];
+    const DBox& ch = a.chunk;
+    const int64_t E0 = A.ext[0], E1 = A.ext[1], E2 = A.ext[2];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int64_t x0 = ch.lo[2] + int64_t(blockIdx.x) * kJBX;
+    const int64_t y0 = ch.lo[1] + int64_t(blockIdx.y) * kJBY;
+    const int64_t zs = ch.lo[0] + int64_t(blockIdx.z) * kJZS;
+    const int64_t ze = zs + kJZS < ch.hi[0] ? zs + kJZS : ch.hi[0];
+    const int nplanes = int(ze - zs) + 2;                       // planes zs-1 .. ze (clamped)
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+        for (int k = 0; k < kJStages; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&jbar[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int i) {       // plane i (0 -> zs-1), clamped to the buffer extent
+        int64_t z = zs - 1 + i;
+        z = z < 0 ? 0 : (z > E0 - 1 ? E0 - 1 : z);
+        const int st = i % kJStages;
+        const uint32_t b = smem_u32(&jbar[st]);
+        const int c0 = int(x0 - 4 - A.lo[2]), c1 = int(y0 - 1 - A.lo[1]), c2 = int(z - A.lo[0]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(uint32_t(kJPlane * 4))
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                smem_u32(jsm + size_t(st) * kJStride)),
+            "l"(reinterpret_cast<uint64_t>(&tm)), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+            : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (int i = 0; i < 3 && i < nplanes; ++i) issue(i);
+    const int64_t gx = x0 + 4 * tx, gy = y0 + ty;
+    const bool valid = gx < ch.hi[2] && gy < ch.hi[1];
+    const int cx = 4 * tx + 4, ry = ty + 1;
+    const int rym = gy == 0 ? ry : ry - 1;
+    const int ryp = gy == E1 - 1 ? ry : ry + 1;
+    float* bb = reinterpret_cast<float*>(B.base);
+    for (int j = 0; j + 2 < nplanes; ++j) {
+        if (threadIdx.x == 0 && j + 3 < nplanes) issue(j + 3);   // stage of plane j-1, freed by the last barrier
+        for (int i = j; i <= j + 2; ++i) mbar_wait(smem_u32(&jbar[i % kJStages]), uint32_t((i / kJStages) & 1));
+        const float* P0 = jsm + size_t(j % kJStages) * kJStride;
+        const float* P1 = jsm + size_t((j + 1) % kJStages) * kJStride;
+        const float* P2 = jsm + size_t((j + 2) % kJStages) * kJStride;
+        if (valid) {
+            const float4 c = *reinterpret_cast<const float4*>(P1 + ry * kJPW + cx);
+            const float4 zm = *reinterpret_cast<const float4*>(P0 + ry * kJPW + cx);
+            const float4 zp = *reinterpret_cast<const float4*>(P2 + ry * kJPW + cx);
+            const float4 fm = *reinterpret_cast<const float4*>(P1 + rym * kJPW + cx);
+            const float4 fp = *reinterpret_cast<const float4*>(P1 + ryp * kJPW + cx);
+            const float w = gx == 0 ? c.x : P1[ry * kJPW + cx - 1];
+            const float e = gx + 4 >= E2 ? c.w : P1[ry * kJPW + cx + 4];
+            float4 o;
+            o.x = jac1(c.x, zm.x, zp.x, fm.x, fp.x, w, c.y);
+            o.y = jac1(c.y, zm.y, zp.y, fm.y, fp.y, c.x, c.z);
+            o.z = jac1(c.z, zm.z, zp.z, fm.z, fp.z, c.y, c.w);
+            o.w = jac1(c.w, zm.w, zp.w, fm.w, fp.w, c.z, e);
+            const int64_t z = zs + j;
+            *reinterpret_cast<float4*>(bb + ((z - B.lo[0]) * B.n[1] + (gy - B.lo[1])) * B.n[2] + (gx - B.lo[2])) = o;
+        }
+        __syncthreads();
+    }
+}
+
+// Tensor maps of input allocations, cached by (base, extents).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                              const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool jacobi_tensor_map(const DAcc& A, CUtensorMap* out) {
+    static EncodeFn enc = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
+    }
+    if (!enc) return false;
+    static std::map<std::tuple<const char*, int64_t, int64_t, int64_t>, CUtensorMap> cache;
+    auto key = std::make_tuple(static_cast<const char*>(A.base), A.n[0], A.n[1], A.n[2]);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {cuuint64_t(A.n[2]), cuuint64_t(A.n[1]), cuuint64_t(A.n[0])};
+    const cuuint64_t strides[2] = {cuuint64_t(A.n[2]) * 4, cuuint64_t(A.n[1] * A.n[2]) * 4};
+    const cuuint32_t box[3] = {kJPW, kJPH, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, A.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (cache.size() > 256) cache.clear();
+    cache[key] = m;
+    *out = m;
+    return true;
+}
+
 // ------------------------------------------------------------------ C3 N-body
 constexpr float NB_DT = 0x1p-7f;
 constexpr float NB_MASS = 0x1p-20f;
@@ -736,7 +856,25 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         const int64_t x0 = a.chunk.lo[2], w = a.chunk.hi[2] - x0;
         const bool vec = A.es == 4 && B.es == 4 && A.n[2] % 4 == 0 && B.n[2] % 4 == 0 && (x0 - A.lo[2]) % 4 == 0 &&
                          (x0 - B.lo[2]) % 4 == 0 && w % 4 == 0 && aligned16(A.base) && aligned16(B.base);
-        if (vec) {
+        static int use_tma = -1;
+        static bool attr_set[64] = {};
+        if (use_tma < 0) {
+            const char* e = getenv("CEL_JACOBI");
+            use_tma = (e && e[0] == 'l') ? 0 : 1;
+        }
+        CUtensorMap tm;
+        if (vec && use_tma && A.n[2] % 4 == 0 && jacobi_tensor_map(A, &tm)) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+                cudaFuncSetAttribute(jacobi7_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(kJStages * kJStride * sizeof(float)));
+                attr_set[dev] = true;
+            }
+            dim3 grid{unsigned((w + kJBX - 1) / kJBX), unsigned((a.chunk.hi[1] - a.chunk.lo[1] + kJBY - 1) / kJBY),
+                      unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kJZS - 1) / kJZS)};
+            jacobi7_tma<<<grid, 32 * kJBY, kJStages * kJStride * sizeof(float), s>>>(tm, a);
+        } else if (vec) {
             dim3 grid(unsigned((w / 4 + 127) / 128), unsigned(a.chunk.hi[1] - a.chunk.lo[1]),
                       unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kJacZ - 1) / kJacZ));
             jacobi7_vec<<<grid, 128, 0, s>>>(a);
