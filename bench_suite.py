@@ -127,7 +127,9 @@ def c4(T=1024, W=84000):
     return res
 
 
-def c5(steps=20, n=1024):
+def c5(steps=40, n=1024):
+    """C5 at G=1: wall-clock steps/s between two epochs (no profiling in the
+    timed window; per-launch profile events add ~4% to a 1.4 ms kernel)."""
     G = 1
     rt = cel.Runtime(G, arena_bytes=int(2 * n ** 3 * 4 * 1.05) + (512 << 20))
     prog = P.jacobi3d(n, 2)
@@ -137,15 +139,14 @@ def c5(steps=20, n=1024):
     d = [cel.task_desc(P.jacobi_step(n, k)[1]) for k in (0, 1)]
     for k in range(4):
         rt.submit_desc(d[k % 2][0])
-    rt.profile_enable(True)
     dt = timed(rt, lambda: [rt.submit_desc(d[k % 2][0]) for k in range(steps)])
-    prof = rt.profile_read()
     rt.shutdown()
-    km = prof.get("jacobi7", (0, 0))[0] / 1e3 / steps
     alg = 8.0 * n ** 3
-    return {"steps_per_s": steps / dt, "roofline": {"bound": "hbm", "achieved": alg / km / 1e9, "peak": HBM,
-                                                    "unit": "GB/s", "frac": alg / km / 1e9 / HBM,
-                                                    "alg_bytes_per_launch": alg}, "devices": G}
+    ach = alg * steps / dt / 1e9
+    return {"steps_per_s": steps / dt, "kernel": "jacobi7_tma (TMA tensor-map plane tiles)",
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": HBM, "unit": "GB/s", "frac": ach / HBM,
+                         "alg_bytes_per_launch": alg, "basis": "wall-clock per step (one launch per step)"},
+            "devices": G}
 
 
 def copy_sweep():

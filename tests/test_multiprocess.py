@@ -20,10 +20,11 @@ def torchrun(n, *args, port=29533, timeout=600):
     return subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, timeout=timeout, env=env, cwd=ROOT)
 
 
-def test_replicated_scheduler_gloo_world2():
+@pytest.mark.parametrize("world", [2, 4])
+def test_replicated_scheduler_gloo(world):
     import __graft_entry__
     __graft_entry__.build()
-    r = torchrun(2, "--execute", "0", "--quick")
+    r = torchrun(world, "--execute", "0", "--quick", port=29533 + world)
     out = r.stdout.decode()
     assert r.returncode == 0 and "MP_CHECK PASS" in out, out[-3000:]
 
