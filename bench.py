@@ -214,7 +214,9 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
+    th0 = time.perf_counter()
     steps(args.warmup, args.steps)
+    th1 = time.perf_counter()
     rt.wait()
     ev1.record()
     torch.cuda.synchronize()
@@ -315,6 +317,7 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
+        "host_submit_us_per_step": (th1 - th0) / args.steps * 1e6,
         "clocks": clocks,
         "profile_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()},
     }
