@@ -214,12 +214,14 @@ def main():
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
+    sh0 = rt.stats()
     th0 = time.perf_counter()
     # host cost per step: measured over the first steps, before the executor's
     # in-flight cap (2048 events per stream) starts pacing the host to the GPU
     kh = min(args.steps, 300)
     steps(args.warmup, kh)
     th1 = time.perf_counter()
+    sh1 = rt.stats()
     steps(args.warmup + kh, args.steps - kh)
     rt.wait()
     ev1.record()
@@ -322,6 +324,9 @@ def main():
         "e2e": e2e,
         "gpu_launches": launches,
         "host_submit_us_per_step": (th1 - th0) / kh * 1e6,
+        "host_us_per_step_by_part": {k[8:] if k.startswith("exec_ns_") else k: (sh1[k] - sh0[k]) / kh / 1e3
+                                     for k in ("exec_ns_copy", "exec_ns_kernel", "exec_ns_alloc", "exec_ns_free",
+                                               "exec_ns_horizon", "signal_ns", "remote_wait_ns")},
         "clocks": clocks,
         "profile_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()},
     }

@@ -152,7 +152,10 @@ typedef struct {
     uint64_t flushes;          /* lookahead queue flushes */
     uint64_t kernel_launches;  /* CUDA kernels launched by this process (workload + copy) */
     uint64_t copy_launches, memcpy_calls, event_waits, remote_waits, signals, host_syncs;
-    uint64_t gen_ns;           /* host time spent in scheduling + issue */
+    uint64_t gen_ns;           /* host time spent in scheduling + issue (incl. epoch waits) */
+    uint64_t exec_ns_alloc, exec_ns_free, exec_ns_copy, exec_ns_kernel, exec_ns_horizon, exec_ns_epoch;
+                               /* host time of the executor per instruction kind (part of gen_ns) */
+    uint64_t signal_ns, remote_wait_ns; /* host time in cross-process flag writes / waits */
 } cel_stats;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

@@ -76,7 +76,9 @@ class cel_stats(C.Structure):
         "copies_resize", "copies_coherence", "copies_readback",
         "bytes_resize", "bytes_coherence", "bytes_readback", "bytes_d2d_peer",
         "alloc_bytes_peak", "flushes", "kernel_launches", "copy_launches", "memcpy_calls",
-        "event_waits", "remote_waits", "signals", "host_syncs", "gen_ns")]
+        "event_waits", "remote_waits", "signals", "host_syncs", "gen_ns",
+        "exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon", "exec_ns_epoch",
+        "signal_ns", "remote_wait_ns")]
 
 
 _P = C.c_void_p

@@ -246,6 +246,14 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
         o->remote_waits = e.remote_waits;
         o->signals = e.signals;
         o->host_syncs = e.host_syncs;
+        o->exec_ns_alloc = e.exec_ns[0];
+        o->exec_ns_free = e.exec_ns[1];
+        o->exec_ns_copy = e.exec_ns[2];
+        o->exec_ns_kernel = e.exec_ns[3];
+        o->exec_ns_horizon = e.exec_ns[4];
+        o->exec_ns_epoch = e.exec_ns[5];
+        o->signal_ns = e.signal_ns;
+        o->remote_wait_ns = e.remote_wait_ns;
     }
     return CEL_OK;
 }

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 
@@ -341,10 +342,12 @@ void Executor::wait_token(int sidx, const Token& t) {
             fprintf(stderr, "[cel r%d] stream %d waits for iid %llu from rank %d\n", cfg_.rank, sidx,
                     (unsigned long long)r.second, r.first);
         // the producer's process writes iid into this GPU's slot when done
+        const uint64_t tw = now_ns();
         checkd(g_drv.wait64(reinterpret_cast<CUstream>(s.s),
                                    reinterpret_cast<CUdeviceptr>(sig_slot(s.dev, r.first, r.second)), r.second,
                                    CU_STREAM_WAIT_VALUE_GEQ),
                "cuStreamWaitValue64");
+        st_.remote_wait_ns += now_ns() - tw;
         st_.remote_waits++;
     }
 }
@@ -476,10 +479,12 @@ void Executor::signal_deps(const Instr& ins, int owner_dev) {
         }
         if (trace_)
             fprintf(stderr, "[cel r%d] signal iid %llu -> rank %d\n", cfg_.rank, (unsigned long long)j, o);
+        const uint64_t ts = now_ns();
         checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
                                     reinterpret_cast<CUdeviceptr>(sig_slot(o, cfg_.rank, j)), j,
                                     CU_STREAM_WRITE_VALUE_DEFAULT),
                "cuStreamWriteValue64");
+        st_.signal_ns += now_ns() - ts;
         st_.signals++;
     }
 }
@@ -492,7 +497,21 @@ char* Executor::alloc_ptr(int64_t aid) {
 }
 
 // ------------------------------------------------------------ dispatch
+namespace {
+inline uint64_t now_ns() {
+    return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now().time_since_epoch())
+                        .count());
+}
+}  // namespace
+
 void Executor::on_instr(const Instr& ins) {
+    const uint64_t t0 = now_ns();
+    on_instr_impl(ins);
+    st_.exec_ns[int(ins.kind)] += now_ns() - t0;
+}
+
+void Executor::on_instr_impl(const Instr& ins) {
     if (err_) return;
     const int od = instr_owner(ins);
     const bool mine = od < 0 || owner_rank(od) == cfg_.rank;

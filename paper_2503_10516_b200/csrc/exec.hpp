@@ -58,6 +58,8 @@ struct ExecStats {
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
     uint64_t event_waits = 0, remote_waits = 0, signals = 0;
     uint64_t host_syncs = 0;
+    uint64_t exec_ns[6] = {};          // host time in on_instr per instruction kind (IKind order)
+    uint64_t signal_ns = 0, remote_wait_ns = 0;
 };
 
 class Executor : public InstrSink {
@@ -67,6 +69,7 @@ public:
 
     int init(std::string* err);
     void on_instr(const Instr& ins) override;
+    void on_instr_impl(const Instr& ins);
 
     // host data of a host-initialised buffer: copied into pinned memory, or
     // borrowed (size 0 marks a borrowed pointer; the caller keeps it valid)
