@@ -36,6 +36,12 @@ struct Drv {
     }
 } g_drv;
 
+inline uint64_t now_ns() {
+    return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                        std::chrono::steady_clock::now().time_since_epoch())
+                        .count());
+}
+
 constexpr int kStreamsPerDev = 5;
 enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3, S_HALO = 4 };
 constexpr uint64_t kAlign = 512;
@@ -497,14 +503,6 @@ char* Executor::alloc_ptr(int64_t aid) {
 }
 
 // ------------------------------------------------------------ dispatch
-namespace {
-inline uint64_t now_ns() {
-    return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
-                        std::chrono::steady_clock::now().time_since_epoch())
-                        .count());
-}
-}  // namespace
-
 void Executor::on_instr(const Instr& ins) {
     const uint64_t t0 = now_ns();
     on_instr_impl(ins);
