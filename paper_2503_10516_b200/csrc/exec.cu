@@ -107,6 +107,8 @@ Executor::~Executor() {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
     }
+    for (auto& pool : prof_pool_)
+        for (cudaEvent_t e : pool) cudaEventDestroy(e);
     for (int d = 0; d < int(arenas_.size()); ++d) {
         if (!owned(d)) {
             if (cfg_.world > 1 && arenas_[d].base) cudaIpcCloseMemHandle(arenas_[d].base);
@@ -160,6 +162,7 @@ int Executor::init(std::string* err) {
     }
     streams_.resize(size_t(G_) * kStreamsPerDev);
     pool_.resize(G_);
+    prof_pool_.resize(G_);
     arenas_.resize(G_);
     uint64_t arena = cfg_.arena_bytes ? cfg_.arena_bytes : (16ull << 30);
     const uint64_t sig_bytes = cfg_.world > 1 ? uint64_t(cfg_.world) * kRing * 8 : 0;
@@ -344,6 +347,12 @@ void Executor::wait_token(int sidx, const Token& t) {
         st_.event_waits++;
     }
     for (auto& r : t.remote) {
+        // a flag this stream already waited for is satisfied for everything
+        // queued after it on the stream (FIFO): skip the repeat (e.g. the
+        // lifetime dependency of every halo push on the peer's allocation)
+        const uint64_t key = (uint64_t(r.first) << 56) ^ r.second;
+        if (s.waited_remote.size() > (1u << 16)) s.waited_remote.clear();   // redundant waits are harmless
+        if (!s.waited_remote.insert(key).second) continue;
         if (trace_)
             fprintf(stderr, "[cel r%d] stream %d waits for iid %llu from rank %d\n", cfg_.rank, sidx,
                     (unsigned long long)r.second, r.first);
@@ -640,6 +649,7 @@ void Executor::exec_epoch(const Instr& ins) {
     // everything before the epoch is complete locally: drop old tokens
     prune_tokens(ins.iid);
     prev_horizon_ = 0;
+    for (auto& st : streams_) st.waited_remote.clear();
     for (auto it = signalled_.begin(); it != signalled_.end();) {
         const uint64_t j = *it / uint64_t(cfg_.world);
         if (j < ins.iid && !live_alloc_iid_.count(j))
@@ -698,9 +708,7 @@ void Executor::exec_copy(const Instr& ins) {
         auto flush = [&]() {
             if (args.nseg == 0) return;
             if (cfg_.profile) {
-                Prof p{args.peer ? K_NUM + 1 : K_NUM, nullptr, nullptr};
-                cudaEventCreate(&p.a);
-                cudaEventCreate(&p.b);
+                Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev};
                 cudaEventRecord(p.a, streams_[sidx].s);
                 st_.kernel_launches += launch_copy(args, streams_[sidx].s);
                 cudaEventRecord(p.b, streams_[sidx].s);
@@ -981,9 +989,7 @@ void Executor::exec_kernel(const Instr& ins) {
         }
         int n;
         if (cfg_.profile) {
-            Prof p{shell_part ? K_NUM + 2 : d.kernel, nullptr, nullptr};
-            cudaEventCreate(&p.a);
-            cudaEventCreate(&p.b);
+            Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev};
             cudaEventRecord(p.a, streams_[stream].s);
             n = launch_workload(b, streams_[stream].s);
             cudaEventRecord(p.b, streams_[stream].s);
@@ -1045,6 +1051,18 @@ void Executor::exec_kernel(const Instr& ins) {
     parts_[ins.iid] = Parts{tshell, interior, waid, ins.bindings};
 }
 
+cudaEvent_t Executor::prof_event(int dev) {
+    auto& p = prof_pool_[dev];
+    if (!p.empty()) {
+        cudaEvent_t e = p.back();
+        p.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    check(cudaEventCreate(&e), "cudaEventCreate");   // timing-enabled
+    return e;
+}
+
 int Executor::profile_read(double* ms, uint64_t* count, int n) {
     for (auto& p : prof_pending_) {
         float t = 0.f;
@@ -1052,8 +1070,8 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
         cudaEventElapsedTime(&t, p.a, p.b);
         prof_ms_[p.kind] += t;
         prof_n_[p.kind]++;
-        cudaEventDestroy(p.a);
-        cudaEventDestroy(p.b);
+        prof_pool_[p.dev].push_back(p.a);
+        prof_pool_[p.dev].push_back(p.b);
     }
     prof_pending_.clear();
     for (int i = 0; i < n && i <= K_NUM + 2; ++i) {

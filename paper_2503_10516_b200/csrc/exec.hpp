@@ -103,6 +103,7 @@ private:
         uint64_t seq = 0;
         uint64_t done = 0;
         std::deque<std::pair<uint64_t, cudaEvent_t>> inflight;
+        std::unordered_set<uint64_t> waited_remote;   // (rank, iid) flags already waited on this stream
     };
     struct FreeRange {
         uint64_t len;
@@ -127,6 +128,7 @@ private:
     struct Prof {
         int kind;
         cudaEvent_t a, b;
+        int dev;
     };
     struct CopyInfo {
         int64_t src_aid, dst_aid;
@@ -167,6 +169,7 @@ private:
     void throttle();
     void prune_tokens(uint64_t below);
     Token materialize(int dev, const Token& t);
+    cudaEvent_t prof_event(int dev);
     uint64_t* sig_slot(int dev, int from_rank, uint64_t iid);
 
     ExecConfig cfg_;
@@ -174,6 +177,7 @@ private:
     int G_ = 0;
     std::vector<Stream> streams_;                  // dev*5 + {0 compute, 1 copy, 2 push, 3 sync, 4 halo}
     std::vector<std::vector<cudaEvent_t>> pool_;
+    std::vector<std::vector<cudaEvent_t>> prof_pool_;  // timing-enabled events for the profile
     std::vector<Arena> arenas_;
     std::unordered_map<uint64_t, Token> tok_;
     std::unordered_map<uint64_t, Token> ltok_;     // local part of horizons / epochs
