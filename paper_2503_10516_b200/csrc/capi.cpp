@@ -137,6 +137,7 @@ int cel_buffer_create_ex(cel_runtime* rt, int32_t dims, const uint64_t extent[3]
     uint32_t bid = 0;
     const int rc = rt->sched->buffer_create(dims, ext, elem_size, host_init != nullptr, &bid);
     if (rc != 0) return fail(rc, "invalid buffer (dims 1..3, extents > 0, elem_size > 0)");
+    if (rt->exec) rt->exec->add_buffer(bid, rt->sched->extent(bid), elem_size);
     if (host_init && rt->exec) {
         const int r2 = rt->exec->set_host_init(bid, host_init, size_t(n) * elem_size,
                                                (flags & CEL_BUFFER_BORROW_HOST) != 0);
@@ -191,6 +192,7 @@ int cel_wait(cel_runtime* rt) {
     if (int rc = check_poison(rt)) return rc;
     const uint64_t t0 = now_ns();
     rt->sched->wait();
+    if (rt->exec) rt->exec->drain();       // the epoch has been executed
     rt->gen_ns += now_ns() - t0;
     return after(rt, CEL_OK);
 }
@@ -205,6 +207,7 @@ int cel_buffer_read(cel_runtime* rt, cel_buffer buf, const cel_box* box, void* h
     int64_t rb = 0;
     const int rc = rt->sched->readback(buf, b, &rb, &err);
     if (rc < 0) return fail(rc, err);
+    if (rt->exec) rt->exec->drain();
     return after(rt, CEL_OK);
 }
 
@@ -263,7 +266,7 @@ int cel_profile_enable(cel_runtime* rt, int32_t on) {
     if (!rt->exec) return fail(CEL_E_STATE, "runtime does not execute");
     rt->exec->set_profile(on != 0);
     if (on) rt->exec->profile_reset();
-    return CEL_OK;
+    return after(rt, CEL_OK);
 }
 
 int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n) {
@@ -278,6 +281,7 @@ int cel_runtime_destroy(cel_runtime* rt) {
     int rc = CEL_OK;
     if (!rt->poisoned && !(rt->exec && rt->exec->error())) {
         rt->sched->shutdown();
+        if (rt->exec) rt->exec->drain();
         if (rt->exec && rt->exec->error()) rc = fail(rt->exec->error(), rt->exec->error_msg());
     } else {
         rc = rt->poisoned ? rt->poisoned : rt->exec->error();

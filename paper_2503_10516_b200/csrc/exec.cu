@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <immintrin.h>
 
 #include "../../include/cel.h"
 
@@ -102,6 +103,16 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
 }
 
 Executor::~Executor() {
+    if (threaded_) {
+        drain();
+        {
+            std::lock_guard<std::mutex> l(qm_);
+            stop_ = true;
+        }
+        qcv_.notify_one();
+        thr_.join();
+        threaded_ = false;
+    }
     if (err_ == 0) sync_all();
     for (auto& p : prof_pending_) {
         cudaEventDestroy(p.a);
@@ -132,16 +143,16 @@ void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
 
 void Executor::check(cudaError_t e, const char* what) {
     if (e == cudaSuccess || err_) return;
-    err_ = E_CUDA;
     errmsg_ = std::string(what) + ": " + cudaGetErrorString(e);
+    err_ = E_CUDA;
 }
 
 void Executor::checkd(CUresult e, const char* what) {
     if (e == CUDA_SUCCESS || err_) return;
     const char* s = nullptr;
     if (g_drv.errstr) g_drv.errstr(e, &s);
-    err_ = E_CUDA;
     errmsg_ = std::string(what) + ": " + (s ? s : "driver error");
+    err_ = E_CUDA;
 }
 
 int Executor::init(std::string* err) {
@@ -225,7 +236,12 @@ int Executor::init(std::string* err) {
         }
     }
     cudaDeviceSynchronize();
-    return err_;
+    const char* et = getenv("CEL_EXEC_THREAD");
+    if (!(et && et[0] == '0')) {
+        threaded_ = true;
+        thr_ = std::thread([this] { thread_main(); });
+    }
+    return err_.load();
 }
 
 size_t Executor::ipc_blob_size() const { return sizeof(cudaIpcMemHandle_t); }
@@ -241,6 +257,7 @@ int Executor::ipc_export(void* blob) const {
 
 int Executor::ipc_import(int rank, const void* blob) {
     if (cfg_.world <= 1 || rank < 0 || rank >= G_) return E_INVALID;
+    drain();
     if (rank == cfg_.rank) return E_OK;
     cudaIpcMemHandle_t h;
     memcpy(&h, blob, sizeof h);
@@ -256,21 +273,24 @@ int Executor::ipc_import(int rank, const void* blob) {
 }
 
 int Executor::set_host_init(uint32_t bid, const void* data, size_t bytes, bool borrow) {
-    if (borrow) {
-        host_init_[bid] = {const_cast<char*>(static_cast<const char*>(data)), 0};
-        return E_OK;
+    char* p = const_cast<char*>(static_cast<const char*>(data));
+    size_t owned_bytes = 0;
+    if (!borrow) {
+        void* q = nullptr;
+        if (cudaHostAlloc(&q, bytes, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            return E_OOM;
+        }
+        memcpy(q, data, bytes);
+        p = static_cast<char*>(q);
+        owned_bytes = bytes;
     }
-    void* p = nullptr;
-    if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
-        cudaGetLastError();
-        return E_OOM;
-    }
-    memcpy(p, data, bytes);
-    host_init_[bid] = {static_cast<char*>(p), bytes};
+    post([this, bid, p, owned_bytes] { host_init_[bid] = {p, owned_bytes}; });
     return E_OK;
 }
 
 void Executor::drop_host_init(uint32_t bid) {
+    drain();
     auto it = host_init_.find(bid);
     if (it == host_init_.end()) return;
     sync_all();
@@ -279,7 +299,7 @@ void Executor::drop_host_init(uint32_t bid) {
 }
 
 void Executor::set_readback(int64_t rb, void* dst, const Box& box, uint32_t es) {
-    readbacks_[rb] = Readback{static_cast<char*>(dst), box, es};
+    post([this, rb, dst, box, es] { readbacks_[rb] = Readback{static_cast<char*>(dst), box, es}; });
 }
 
 // ------------------------------------------------------------ events / tokens
@@ -397,6 +417,7 @@ void Executor::throttle() {
 }
 
 void Executor::sync_all() {
+    drain();
     for (auto& s : streams_)
         if (s.s) cudaStreamSynchronize(s.s);
     poll(true);
@@ -513,9 +534,100 @@ char* Executor::alloc_ptr(int64_t aid) {
 
 // ------------------------------------------------------------ dispatch
 void Executor::on_instr(const Instr& ins) {
+    if (threaded_) {
+        Item it;
+        it.kind = 0;
+        it.ins = ins;
+        push(std::move(it));
+        return;
+    }
     const uint64_t t0 = now_ns();
     on_instr_impl(ins);
     st_.exec_ns[int(ins.kind)] += now_ns() - t0;
+}
+
+// ------------------------------------------------------------ executor thread
+void Executor::push(Item&& it) {
+    bool wake;
+    {
+        std::unique_lock<std::mutex> l(qm_);
+        while (q_.size() >= 16384) qfull_cv_.wait(l);   // bounded run-ahead of the scheduler
+        q_.push_back(std::move(it));
+        qsize_.store(q_.size(), std::memory_order_release);
+        wake = sleeping_;
+    }
+    if (wake) qcv_.notify_one();
+}
+
+void Executor::post(std::function<void()> fn) {
+    if (!threaded_) {
+        fn();
+        return;
+    }
+    Item it;
+    it.kind = 1;
+    it.fn = std::move(fn);
+    push(std::move(it));
+}
+
+void Executor::drain() {
+    if (!threaded_) return;
+    Item it;
+    it.kind = 2;
+    it.mark = ++marks_posted_;
+    const uint64_t m = it.mark;
+    push(std::move(it));
+    std::unique_lock<std::mutex> l(dm_);
+    done_cv_.wait(l, [&] { return marks_done_ >= m; });
+}
+
+void Executor::thread_main() {
+    for (;;) {
+        Item it;
+        {
+            std::unique_lock<std::mutex> l(qm_);
+            if (q_.empty()) {
+                l.unlock();
+                // spin briefly: the scheduler usually posts the next
+                // instruction within microseconds (latency of
+                // instruction selection matters for strong scaling)
+                for (int i = 0; i < 20000 && qsize_.load(std::memory_order_acquire) == 0; ++i) _mm_pause();
+                l.lock();
+                while (q_.empty() && !stop_) {
+                    sleeping_ = true;
+                    qcv_.wait(l);
+                    sleeping_ = false;
+                }
+                if (q_.empty() && stop_) return;
+            }
+            it = std::move(q_.front());
+            q_.pop_front();
+            qsize_.store(q_.size(), std::memory_order_release);
+            if (q_.size() == 8192) qfull_cv_.notify_all();
+        }
+        if (it.kind == 0) {
+            const uint64_t t0 = now_ns();
+            on_instr_impl(it.ins);
+            st_.exec_ns[int(it.ins.kind)] += now_ns() - t0;
+        } else if (it.kind == 1) {
+            it.fn();
+        } else {
+            {
+                std::lock_guard<std::mutex> l(dm_);
+                marks_done_ = it.mark;
+            }
+            done_cv_.notify_all();
+        }
+    }
+}
+
+void Executor::add_buffer(uint32_t bid, const Box& extent, uint32_t es) {
+    post([this, bid, extent, es] { bufinfo_[bid] = BufInfo{extent, es}; });
+}
+
+void Executor::set_profile(bool on) {
+    drain();
+    cfg_.profile = on;
 }
 
 void Executor::on_instr_impl(const Instr& ins) {
@@ -533,15 +645,15 @@ void Executor::on_instr_impl(const Instr& ins) {
     switch (ins.kind) {
     case IKind::Alloc: {
         const int dev = ins.mem - 2;
-        const uint32_t es = sched_->elem_size(ins.buffer);
+        const uint32_t es = bufinfo_.at(ins.buffer).es;
         const uint64_t bytes = ins.box.volume() * es;
         uint64_t off = 0;
         Token t;
         if (!arenas_[dev].alloc(bytes, &off, &t)) {
-            err_ = E_OOM;
             char buf[200];
             snprintf(buf, sizeof buf, "device %d arena exhausted allocating %.3f GiB", dev, double(bytes) / (1ull << 30));
             errmsg_ = buf;
+            err_ = E_OOM;
             return;
         }
         allocs_[ins.aid] = AllocRec{dev, off, bytes, ins.box, es, ins.iid};
@@ -556,8 +668,8 @@ void Executor::on_instr_impl(const Instr& ins) {
     case IKind::Free: {
         auto it = allocs_.find(ins.aid);
         if (it == allocs_.end()) {
-            err_ = E_STATE;
             errmsg_ = "free of an unknown allocation";
+            err_ = E_STATE;
             return;
         }
         const AllocRec r = it->second;
@@ -669,7 +781,7 @@ void Executor::exec_epoch(const Instr& ins) {
 }
 
 void Executor::exec_copy(const Instr& ins) {
-    const uint32_t es = sched_->elem_size(ins.buffer);
+    const uint32_t es = bufinfo_.at(ins.buffer).es;
     Token deps;
     for (uint64_t j : ins.deps) {
         // a copy that reads only rows a split kernel wrote in its shell launch
@@ -767,11 +879,11 @@ void Executor::exec_copy(const Instr& ins) {
         auto hi = host_init_.find(ins.buffer);
         auto rb = readbacks_.find(ins.readback);
         if (hi == host_init_.end() || rb == readbacks_.end()) {
-            err_ = E_STATE;
             errmsg_ = "host copy without source or destination";
+            err_ = E_STATE;
             return;
         }
-        const Box E = sched_->extent(ins.buffer);
+        const Box E = bufinfo_.at(ins.buffer).extent;
         const Box& R = rb->second.box;
         for (const Box& b : ins.region)
             for (int64_t z = b.lo[0]; z < b.hi[0]; ++z)
@@ -795,20 +907,20 @@ void Executor::exec_copy(const Instr& ins) {
     if (h2d) {
         auto hi = host_init_.find(ins.buffer);
         if (hi == host_init_.end()) {
-            err_ = E_STATE;
             errmsg_ = "H2D copy of a buffer without host data";
+            err_ = E_STATE;
             return;
         }
         hbase = hi->second.first;
-        hbox = sched_->extent(ins.buffer);
+        hbox = bufinfo_.at(ins.buffer).extent;
         const AllocRec& D = allocs_.at(ins.dst_aid);
         dbase = arenas_[D.dev].base + D.off;
         dbox = D.box;
     } else {
         auto rb = readbacks_.find(ins.readback);
         if (rb == readbacks_.end()) {
-            err_ = E_STATE;
             errmsg_ = "readback copy without a destination";
+            err_ = E_STATE;
             return;
         }
         hbase = rb->second.dst;
@@ -926,9 +1038,9 @@ void Executor::exec_kernel(const Instr& ins) {
     for (int i = 0; i < a.n_acc; ++i) {
         const Access& ac = d.acc[i];
         DAcc& A = a.acc[i];
-        const Box ext = sched_->extent(ac.buf);
+        const Box ext = bufinfo_.at(ac.buf).extent;
         for (int k = 0; k < 3; ++k) A.ext[k] = ext.hi[k];
-        A.es = sched_->elem_size(ac.buf);
+        A.es = bufinfo_.at(ac.buf).es;
         A.mode = ac.mode;
         A.map = int(ac.map.kind);
         for (int k = 0; k < 3; ++k) {
@@ -960,7 +1072,7 @@ void Executor::exec_kernel(const Instr& ins) {
     if (split_ && (d.kernel == K_WAVE5 || d.kernel == K_JACOBI7 || d.kernel == K_STENCIL3)) {
         for (const Access& ac : d.acc) {
             if (ac.map.kind != MapKind::Neighborhood || (ac.mode != MODE_READ && ac.mode != MODE_READ_WRITE)) continue;
-            const Box rb = map_access(ac.map, ins.chunk, sched_->extent(ac.buf));
+            const Box rb = map_access(ac.map, ins.chunk, bufinfo_.at(ac.buf).extent);
             for (int k = 0; k < 3; ++k) {
                 if (rb.lo[k] < ins.chunk.lo[k]) {
                     interior.lo[k] = std::max(interior.lo[k], ins.chunk.lo[k] + ac.map.border[k]);
@@ -981,7 +1093,7 @@ void Executor::exec_kernel(const Instr& ins) {
             b.chunk.hi[k] = ch.hi[k];
         }
         for (int i = 0; i < b.n_acc; ++i) {
-            const Box mb = map_access(d.acc[i].map, ch, sched_->extent(d.acc[i].buf));
+            const Box mb = map_access(d.acc[i].map, ch, bufinfo_.at(d.acc[i].buf).extent);
             for (int k = 0; k < 3; ++k) {
                 b.acc[i].box.lo[k] = mb.lo[k];
                 b.acc[i].box.hi[k] = mb.hi[k];
@@ -1024,7 +1136,7 @@ void Executor::exec_kernel(const Instr& ins) {
             for (size_t i = 0; i < d.acc.size() && !conflict; ++i) {
                 const Access& ac = d.acc[i];
                 const int64_t aid = ins.bindings[i];
-                const Box ib = map_access(ac.map, interior, sched_->extent(ac.buf));
+                const Box ib = map_access(ac.map, interior, bufinfo_.at(ac.buf).extent);
                 auto hits = [&](const CopyInfo& c) {
                     if (intersect(c.bb, ib).empty()) return false;
                     for (const Box& b : c.region)
@@ -1064,6 +1176,7 @@ cudaEvent_t Executor::prof_event(int dev) {
 }
 
 int Executor::profile_read(double* ms, uint64_t* count, int n) {
+    drain();
     for (auto& p : prof_pending_) {
         float t = 0.f;
         cudaEventSynchronize(p.b);

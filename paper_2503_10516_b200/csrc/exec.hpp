@@ -15,8 +15,13 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <map>
 #include <string>
 #include <unordered_map>
@@ -68,14 +73,25 @@ public:
     ~Executor() override;
 
     int init(std::string* err);
+    // Called by the scheduler (API thread) in iid order.  With the executor
+    // thread running (default), the instruction is queued and issued by that
+    // thread (scheduler and executor decoupled over a queue).
     void on_instr(const Instr& ins) override;
     void on_instr_impl(const Instr& ins);
+    // Wait until the executor thread has processed everything queued so far
+    // (after an epoch instruction: until the epoch's GPU work is complete).
+    void drain();
+    // Run fn on the executor thread, in queue order.
+    void post(std::function<void()> fn);
+    void add_buffer(uint32_t bid, const Box& extent, uint32_t es);
 
     // host data of a host-initialised buffer: copied into pinned memory, or
     // borrowed (size 0 marks a borrowed pointer; the caller keeps it valid)
     int set_host_init(uint32_t bid, const void* data, size_t bytes, bool borrow);
     void drop_host_init(uint32_t bid);
-    void drop_host_init_later(uint32_t bid) { host_drop_.push_back(bid); }
+    void drop_host_init_later(uint32_t bid) {
+        post([this, bid] { host_drop_.push_back(bid); });
+    }
     void set_scheduler(Scheduler* s) { sched_ = s; }
     void set_readback(int64_t rb, void* dst, const Box& box, uint32_t elem_size);
 
@@ -84,12 +100,12 @@ public:
     int ipc_export(void* blob) const;
     int ipc_import(int rank, const void* blob);
 
-    int error() const { return err_; }
+    int error() const { return err_.load(); }
     const std::string& error_msg() const { return errmsg_; }
     const ExecStats& stats() const { return st_; }
 
     // profiling: per kernel kind, accumulated device ms and launch count
-    void set_profile(bool on) { cfg_.profile = on; }
+    void set_profile(bool on);
     int profile_read(double* ms, uint64_t* count, int n);
     void profile_reset();
     int device_count() const { return G_; }
@@ -191,7 +207,31 @@ private:
     uint64_t prof_n_[K_NUM + 3] = {};
     std::vector<int> phys_;
     bool memops64_ = false;
-    int err_ = 0;
+    std::atomic<int> err_{0};
+    // executor thread and its queue
+    struct Item {
+        int kind = 0;                              // 0 instruction, 1 function, 2 drain mark
+        Instr ins;
+        std::function<void()> fn;
+        uint64_t mark = 0;
+    };
+    void push(Item&& it);
+    void thread_main();
+    std::thread thr_;
+    bool threaded_ = false;
+    std::deque<Item> q_;
+    std::mutex qm_;
+    std::condition_variable qcv_, qfull_cv_, done_cv_;
+    std::atomic<size_t> qsize_{0};
+    bool sleeping_ = false, stop_ = false;
+    uint64_t marks_posted_ = 0;
+    uint64_t marks_done_ = 0;
+    std::mutex dm_;
+    struct BufInfo {
+        Box extent;
+        uint32_t es;
+    };
+    std::unordered_map<uint32_t, BufInfo> bufinfo_;   // executor-side copy of buffer shapes
     std::string errmsg_;
     ExecStats st_;
     uint64_t since_poll_ = 0;
