@@ -213,6 +213,12 @@ int cel_stats_get(cel_runtime* rt, cel_stats* out);
 int cel_profile_enable(cel_runtime* rt, int32_t on);
 int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n);
 
+/* Write the launches profiled since cel_profile_enable(rt, 1) as JSONL, one
+ * record per launch: {"iid", "rank", "device", "stream", "kind", "start_us",
+ * "end_us"} with times from CUDA events relative to the enable call, per
+ * device (the instruction trace of SURVEY §5 / S:L528). */
+int cel_trace_dump(cel_runtime* rt, const char* path);
+
 /* Shutdown epoch, free everything. */
 int cel_runtime_destroy(cel_runtime* rt);
 

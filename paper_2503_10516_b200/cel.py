@@ -97,13 +97,14 @@ lib.cel_stats_get.argtypes = [_P, C.POINTER(cel_stats)]
 lib.cel_profile_enable.argtypes = [_P, C.c_int32]
 lib.cel_profile_read.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]
 lib.cel_runtime_destroy.argtypes = [_P]
+lib.cel_trace_dump.argtypes = [_P, C.c_char_p]
 lib.cel_last_error.restype = C.c_char_p
 
 BORROW_HOST = 1
 SYMBOLS = ["cel_runtime_create", "cel_ipc_blob_size", "cel_ipc_export", "cel_ipc_import", "cel_buffer_create",
            "cel_buffer_create_ex",
            "cel_task_submit", "cel_wait", "cel_buffer_read", "cel_buffer_destroy", "cel_stats_get",
-           "cel_profile_enable", "cel_profile_read", "cel_runtime_destroy", "cel_last_error"]
+           "cel_profile_enable", "cel_profile_read", "cel_trace_dump", "cel_runtime_destroy", "cel_last_error"]
 
 
 class CelError(Exception):
@@ -266,6 +267,9 @@ class Runtime:
                 name = {COPY_SLOT: "copy", PEER_SLOT: "copy_peer", SHELL_SLOT: "shell"}.get(k) or KERNEL_NAMES[k]
                 out[name] = (ms[k], cnt[k])
         return out
+
+    def trace_dump(self, path):
+        _check(lib.cel_trace_dump(self.h, path.encode()))
 
     def shutdown(self):
         if self.h is not None:

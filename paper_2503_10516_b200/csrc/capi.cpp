@@ -276,6 +276,13 @@ int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n) {
     return after(rt, rt->exec->profile_read(ms, count, n));
 }
 
+int cel_trace_dump(cel_runtime* rt, const char* path) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!rt->exec) return fail(CEL_E_STATE, "runtime does not execute");
+    if (!path) return fail(CEL_E_INVALID, "null path");
+    return after(rt, rt->exec->trace_dump(path));
+}
+
 int cel_runtime_destroy(cel_runtime* rt) {
     if (!rt) return fail(CEL_E_INVALID, "null runtime");
     int rc = CEL_OK;

@@ -628,6 +628,35 @@ void Executor::add_buffer(uint32_t bid, const Box& extent, uint32_t es) {
 void Executor::set_profile(bool on) {
     drain();
     cfg_.profile = on;
+    if (!on) return;
+    // time origin of the trace on every owned device
+    trace_ref_.assign(G_, nullptr);
+    trace_.clear();
+    for (int d = 0; d < G_; ++d) {
+        if (!owned(d)) continue;
+        set_dev(d);
+        cudaEvent_t e = nullptr;
+        check(cudaEventCreate(&e), "cudaEventCreate");
+        check(cudaEventRecord(e, streams_[d * kStreamsPerDev + S_SYNC].s), "cudaEventRecord");
+        trace_ref_[d] = e;
+    }
+}
+
+int Executor::trace_dump(const char* path) {
+    double ms[K_NUM + 3];
+    uint64_t c[K_NUM + 3];
+    profile_read(ms, c, K_NUM + 3);          // resolves pending launches into trace_
+    FILE* f = fopen(path, "w");
+    if (!f) return E_INVALID;
+    static const char* names[] = {"fill_hash", "fill_const", "stencil3", "wave5",  "jacobi7", "nbody_step",
+                                  "nbody_update", "rsim_row", "probe", "callback", "copy", "copy_peer", "shell"};
+    static const char* snames[] = {"compute", "copy", "push", "sync", "halo"};
+    for (const TraceRec& t : trace_)
+        fprintf(f, "{\"iid\":%llu,\"rank\":%d,\"device\":%d,\"stream\":\"%s\",\"kind\":\"%s\",\"start_us\":%.3f,\"end_us\":%.3f}\n",
+                (unsigned long long)t.iid, cfg_.rank, t.dev, snames[t.stream % kStreamsPerDev], names[t.kind],
+                t.start_us, t.end_us);
+    fclose(f);
+    return E_OK;
 }
 
 void Executor::on_instr_impl(const Instr& ins) {
@@ -820,7 +849,7 @@ void Executor::exec_copy(const Instr& ins) {
         auto flush = [&]() {
             if (args.nseg == 0) return;
             if (cfg_.profile) {
-                Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev};
+                Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev, ins.iid, sidx};
                 cudaEventRecord(p.a, streams_[sidx].s);
                 st_.kernel_launches += launch_copy(args, streams_[sidx].s);
                 cudaEventRecord(p.b, streams_[sidx].s);
@@ -1101,7 +1130,7 @@ void Executor::exec_kernel(const Instr& ins) {
         }
         int n;
         if (cfg_.profile) {
-            Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev};
+            Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev, ins.iid, stream};
             cudaEventRecord(p.a, streams_[stream].s);
             n = launch_workload(b, streams_[stream].s);
             cudaEventRecord(p.b, streams_[stream].s);
@@ -1183,6 +1212,12 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
         cudaEventElapsedTime(&t, p.a, p.b);
         prof_ms_[p.kind] += t;
         prof_n_[p.kind]++;
+        if (p.dev < int(trace_ref_.size()) && trace_ref_[p.dev] && trace_.size() < 200000) {
+            float s0 = 0.f, s1 = 0.f;
+            cudaEventElapsedTime(&s0, trace_ref_[p.dev], p.a);
+            cudaEventElapsedTime(&s1, trace_ref_[p.dev], p.b);
+            trace_.push_back(TraceRec{p.iid, p.dev, p.stream, p.kind, s0 * 1e3, s1 * 1e3});
+        }
         prof_pool_[p.dev].push_back(p.a);
         prof_pool_[p.dev].push_back(p.b);
     }

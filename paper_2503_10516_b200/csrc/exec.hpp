@@ -107,6 +107,9 @@ public:
     // profiling: per kernel kind, accumulated device ms and launch count
     void set_profile(bool on);
     int profile_read(double* ms, uint64_t* count, int n);
+    // JSONL trace of the profiled launches (S:L528 format): iid, device,
+    // stream, kind, start_us, end_us relative to profile_enable, per device
+    int trace_dump(const char* path);
     void profile_reset();
     int device_count() const { return G_; }
     int owned(int d) const { return owner_rank(d) == cfg_.rank; }
@@ -145,6 +148,13 @@ private:
         int kind;
         cudaEvent_t a, b;
         int dev;
+        uint64_t iid = 0;
+        int stream = 0;
+    };
+    struct TraceRec {
+        uint64_t iid;
+        int dev, stream, kind;
+        double start_us, end_us;
     };
     struct CopyInfo {
         int64_t src_aid, dst_aid;
@@ -194,6 +204,8 @@ private:
     std::vector<Stream> streams_;                  // dev*5 + {0 compute, 1 copy, 2 push, 3 sync, 4 halo}
     std::vector<std::vector<cudaEvent_t>> pool_;
     std::vector<std::vector<cudaEvent_t>> prof_pool_;  // timing-enabled events for the profile
+    std::vector<cudaEvent_t> trace_ref_;              // per device: time origin of the trace
+    std::vector<TraceRec> trace_;
     std::vector<Arena> arenas_;
     std::unordered_map<uint64_t, Token> tok_;
     std::unordered_map<uint64_t, Token> ltok_;     // local part of horizons / epochs
