@@ -631,7 +631,7 @@ void Executor::set_profile(bool on) {
     if (!on) return;
     // time origin of the trace on every owned device
     trace_ref_.assign(G_, nullptr);
-    trace_.clear();
+    trace_recs_.clear();
     for (int d = 0; d < G_; ++d) {
         if (!owned(d)) continue;
         set_dev(d);
@@ -645,13 +645,13 @@ void Executor::set_profile(bool on) {
 int Executor::trace_dump(const char* path) {
     double ms[K_NUM + 3];
     uint64_t c[K_NUM + 3];
-    profile_read(ms, c, K_NUM + 3);          // resolves pending launches into trace_
+    profile_read(ms, c, K_NUM + 3);          // resolves pending launches into trace_recs_
     FILE* f = fopen(path, "w");
     if (!f) return E_INVALID;
     static const char* names[] = {"fill_hash", "fill_const", "stencil3", "wave5",  "jacobi7", "nbody_step",
                                   "nbody_update", "rsim_row", "probe", "callback", "copy", "copy_peer", "shell"};
     static const char* snames[] = {"compute", "copy", "push", "sync", "halo"};
-    for (const TraceRec& t : trace_)
+    for (const TraceRec& t : trace_recs_)
         fprintf(f, "{\"iid\":%llu,\"rank\":%d,\"device\":%d,\"stream\":\"%s\",\"kind\":\"%s\",\"start_us\":%.3f,\"end_us\":%.3f}\n",
                 (unsigned long long)t.iid, cfg_.rank, t.dev, snames[t.stream % kStreamsPerDev], names[t.kind],
                 t.start_us, t.end_us);
@@ -1212,11 +1212,11 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
         cudaEventElapsedTime(&t, p.a, p.b);
         prof_ms_[p.kind] += t;
         prof_n_[p.kind]++;
-        if (p.dev < int(trace_ref_.size()) && trace_ref_[p.dev] && trace_.size() < 200000) {
+        if (p.dev < int(trace_ref_.size()) && trace_ref_[p.dev] && trace_recs_.size() < 200000) {
             float s0 = 0.f, s1 = 0.f;
             cudaEventElapsedTime(&s0, trace_ref_[p.dev], p.a);
             cudaEventElapsedTime(&s1, trace_ref_[p.dev], p.b);
-            trace_.push_back(TraceRec{p.iid, p.dev, p.stream, p.kind, s0 * 1e3, s1 * 1e3});
+            trace_recs_.push_back(TraceRec{p.iid, p.dev, p.stream, p.kind, s0 * 1e3, s1 * 1e3});
         }
         prof_pool_[p.dev].push_back(p.a);
         prof_pool_[p.dev].push_back(p.b);

@@ -205,7 +205,7 @@ private:
     std::vector<std::vector<cudaEvent_t>> pool_;
     std::vector<std::vector<cudaEvent_t>> prof_pool_;  // timing-enabled events for the profile
     std::vector<cudaEvent_t> trace_ref_;              // per device: time origin of the trace
-    std::vector<TraceRec> trace_;
+    std::vector<TraceRec> trace_recs_;
     std::vector<Arena> arenas_;
     std::unordered_map<uint64_t, Token> tok_;
     std::unordered_map<uint64_t, Token> ltok_;     // local part of horizons / epochs
