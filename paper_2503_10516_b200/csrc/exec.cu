@@ -640,6 +640,10 @@ void Executor::set_profile(bool on) {
         check(cudaEventRecord(e, streams_[d * kStreamsPerDev + S_SYNC].s), "cudaEventRecord");
         trace_ref_[d] = e;
     }
+    // the device is idle here (drained), so the reference event fires now
+    for (int d = 0; d < G_; ++d)
+        if (trace_ref_[d]) cudaEventSynchronize(trace_ref_[d]);
+    trace_ref_ns_ = now_ns();
 }
 
 int Executor::trace_dump(const char* path) {
@@ -652,9 +656,11 @@ int Executor::trace_dump(const char* path) {
                                   "nbody_update", "rsim_row", "probe", "callback", "copy", "copy_peer", "shell"};
     static const char* snames[] = {"compute", "copy", "push", "sync", "halo"};
     for (const TraceRec& t : trace_recs_)
-        fprintf(f, "{\"iid\":%llu,\"rank\":%d,\"device\":%d,\"stream\":\"%s\",\"kind\":\"%s\",\"start_us\":%.3f,\"end_us\":%.3f}\n",
+        fprintf(f,
+                "{\"iid\":%llu,\"rank\":%d,\"device\":%d,\"stream\":\"%s\",\"kind\":\"%s\",\"start_us\":%.3f,"
+                "\"end_us\":%.3f,\"host_issue_us\":%.3f}\n",
                 (unsigned long long)t.iid, cfg_.rank, t.dev, snames[t.stream % kStreamsPerDev], names[t.kind],
-                t.start_us, t.end_us);
+                t.start_us, t.end_us, t.issue_us);
     fclose(f);
     return E_OK;
 }
@@ -849,7 +855,7 @@ void Executor::exec_copy(const Instr& ins) {
         auto flush = [&]() {
             if (args.nseg == 0) return;
             if (cfg_.profile) {
-                Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev, ins.iid, sidx};
+                Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev, ins.iid, sidx, now_ns()};
                 cudaEventRecord(p.a, streams_[sidx].s);
                 st_.kernel_launches += launch_copy(args, streams_[sidx].s);
                 cudaEventRecord(p.b, streams_[sidx].s);
@@ -1130,7 +1136,7 @@ void Executor::exec_kernel(const Instr& ins) {
         }
         int n;
         if (cfg_.profile) {
-            Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev, ins.iid, stream};
+            Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev, ins.iid, stream, now_ns()};
             cudaEventRecord(p.a, streams_[stream].s);
             n = launch_workload(b, streams_[stream].s);
             cudaEventRecord(p.b, streams_[stream].s);
@@ -1216,7 +1222,8 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
             float s0 = 0.f, s1 = 0.f;
             cudaEventElapsedTime(&s0, trace_ref_[p.dev], p.a);
             cudaEventElapsedTime(&s1, trace_ref_[p.dev], p.b);
-            trace_recs_.push_back(TraceRec{p.iid, p.dev, p.stream, p.kind, s0 * 1e3, s1 * 1e3});
+            trace_recs_.push_back(TraceRec{p.iid, p.dev, p.stream, p.kind, s0 * 1e3, s1 * 1e3,
+                                           (double(p.issue_ns) - double(trace_ref_ns_)) / 1e3});
         }
         prof_pool_[p.dev].push_back(p.a);
         prof_pool_[p.dev].push_back(p.b);

@@ -150,11 +150,12 @@ private:
         int dev;
         uint64_t iid = 0;
         int stream = 0;
+        uint64_t issue_ns = 0;
     };
     struct TraceRec {
         uint64_t iid;
         int dev, stream, kind;
-        double start_us, end_us;
+        double start_us, end_us, issue_us;
     };
     struct CopyInfo {
         int64_t src_aid, dst_aid;
@@ -205,6 +206,7 @@ private:
     std::vector<std::vector<cudaEvent_t>> pool_;
     std::vector<std::vector<cudaEvent_t>> prof_pool_;  // timing-enabled events for the profile
     std::vector<cudaEvent_t> trace_ref_;              // per device: time origin of the trace
+    uint64_t trace_ref_ns_ = 0;                       // host clock at the same point
     std::vector<TraceRec> trace_recs_;
     std::vector<Arena> arenas_;
     std::unordered_map<uint64_t, Token> tok_;

@@ -34,5 +34,5 @@ if rank == 0:
     recs.sort(key=lambda r: r["start_us"])
     t0 = recs[0]["start_us"]
     for r in recs[-24:]:
-        print("%-6s %-8s %-7s iid %6d  %9.1f -> %9.1f  (%6.1f us)" % (r["kind"], r["stream"], "", r["iid"], r["start_us"] - t0, r["end_us"] - t0, r["end_us"] - r["start_us"]))
+        print("%-6s %-8s iid %6d  issued %9.1f  gpu %9.1f -> %9.1f  (%6.1f us)" % (r["kind"], r["stream"], r["iid"], r["host_issue_us"] - t0, r["start_us"] - t0, r["end_us"] - t0, r["end_us"] - r["start_us"]))
 if dist: dist.destroy_process_group()
