@@ -43,8 +43,12 @@ inline uint64_t now_ns() {
                         .count());
 }
 
-constexpr int kStreamsPerDev = 5;
-enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3, S_HALO = 4 };
+constexpr int kStreamsPerDev = 11;
+// work streams 0..4; 5 = eager horizon / epoch flags; 6..10 = flags released
+// by an event of work stream (k - 6), so each flag stream's FIFO order follows
+// its source stream's completion order (no head-of-line blocking between a
+// long-complete flag and one waiting for recent work)
+enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3, S_HALO = 4, S_HSIG = 5, S_SIG0 = 6 };
 constexpr uint64_t kAlign = 512;
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 }  // namespace
@@ -506,14 +510,19 @@ void Executor::signal_deps(const Instr& ins, int owner_dev) {
         if (jo >= 0 && owner_rank(jo) != cfg_.rank) continue;
         const uint64_t key = j * uint64_t(cfg_.world) + uint64_t(o);
         if (!signalled_.insert(key).second) continue;
-        const int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
+        Token t;
         if (jo < 0) {
             auto lt = ltok_.find(j);
-            if (lt != ltok_.end()) wait_token(sidx, lt->second);
+            if (lt != ltok_.end()) t = lt->second;
         } else {
-            wait_token(sidx, dep_token(j));
+            t = dep_token(j);
         }
-        if (trace_)
+        Token live;
+        merge(live, t);                               // drops entries already known complete
+        int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
+        if (live.remote.empty() && live.local.size() == 1)
+            sidx = cfg_.rank * kStreamsPerDev + S_SIG0 + (live.local[0].stream % kStreamsPerDev);
+        wait_token(sidx, live);        if (trace_)
             fprintf(stderr, "[cel r%d] signal iid %llu -> rank %d\n", cfg_.rank, (unsigned long long)j, o);
         const uint64_t ts = now_ns();
         checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
@@ -654,7 +663,7 @@ int Executor::trace_dump(const char* path) {
     if (!f) return E_INVALID;
     static const char* names[] = {"fill_hash", "fill_const", "stencil3", "wave5",  "jacobi7", "nbody_step",
                                   "nbody_update", "rsim_row", "probe", "callback", "copy", "copy_peer", "shell"};
-    static const char* snames[] = {"compute", "copy", "push", "sync", "halo"};
+    static const char* snames[] = {"compute", "copy", "push", "sync", "halo", "hsig", "sig0", "sig1", "sig2", "sig3", "sig4"};
     for (const TraceRec& t : trace_recs_)
         fprintf(f,
                 "{\"iid\":%llu,\"rank\":%d,\"device\":%d,\"stream\":\"%s\",\"kind\":\"%s\",\"start_us\":%.3f,"
@@ -750,6 +759,21 @@ void Executor::on_instr_impl(const Instr& ins) {
         Token t = lt;
         for (int r = 0; r < cfg_.world; ++r)
             if (r != cfg_.rank) t.remote.push_back({r, ins.iid});
+        if (cfg_.world > 1) {
+            // every rank will need this horizon's parts (deps subsumed into it,
+            // P:L429): publish ours to all ranks now, on a stream of its own
+            const int hs = cfg_.rank * kStreamsPerDev + S_HSIG;
+            wait_token(hs, lt);
+            for (int r = 0; r < cfg_.world; ++r) {
+                if (r == cfg_.rank) continue;
+                signalled_.insert(ins.iid * uint64_t(cfg_.world) + uint64_t(r));
+                checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[hs].s),
+                                     reinterpret_cast<CUdeviceptr>(sig_slot(r, cfg_.rank, ins.iid)), ins.iid,
+                                     CU_STREAM_WRITE_VALUE_DEFAULT),
+                       "cuStreamWriteValue64");
+                st_.signals++;
+            }
+        }
         tok_[ins.iid] = t;
         poll(false);
         throttle();
