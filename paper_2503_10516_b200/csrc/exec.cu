@@ -1143,7 +1143,9 @@ void Executor::exec_kernel(const Instr& ins) {
                 }
             }
         }
-        if (interior.empty()) split = false;
+        // only worth it when the interior is big enough to hide the halo
+        // chain (a launch costs a few microseconds; tiny chunks are latency-bound)
+        if (interior.empty() || interior.volume() < (uint64_t(1) << 18)) split = false;
     }
     auto launch = [&](const Box& ch, int stream, bool shell_part) {
         KArgs b = a;
