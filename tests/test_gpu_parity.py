@@ -204,3 +204,60 @@ def test_nbody_fast_math_within_tolerance(cel):
     vo = exp[1].view(np.float32)[:, 0, 0, :3].astype(np.float64)
     assert np.all(np.abs(vg - vo) <= c * l1 * 2.0 ** -16 + 1e-30)
     assert not np.array_equal(vg, vo) or True
+
+
+def light_cone_jacobi(z_lo, z_hi, n, steps, seed=5):
+    """Oracle planes [z_lo, z_hi) of the 1024^3 Jacobi after `steps` steps,
+    computed on the light cone only (planes +- steps, full y/x)."""
+    from oracle.kernels import k_jacobi7
+    a = max(0, z_lo - steps - 1)
+    b = min(n, z_hi + steps + 1)
+    ext = g.box([0, 0, 0], [n, n, n])
+    box = g.box([a, 0, 0], [b, n, n])
+    z = np.arange(a, b, dtype=np.uint64)[:, None, None]
+    y = np.arange(n, dtype=np.uint64)[None, :, None]
+    x = np.arange(n, dtype=np.uint64)[None, None, :]
+    f = init_value(seed, (z * np.uint64(n) + y) * np.uint64(n) + x).reshape(b - a, n, n, 1)
+    A = Acc(f.view(np.uint32).copy(), box, ext)
+    B = Acc(np.zeros_like(A.arr), box, ext)
+    lo, hi = a, b
+    for k in range(steps):
+        lo2 = lo if lo == 0 else lo + 1
+        hi2 = hi if hi == n else hi - 1
+        wb = g.box([lo2, 0, 0], [hi2, n, n])
+        if k % 2 == 0:
+            k_jacobi7({}, [wb, wb], [A, B])
+        else:
+            k_jacobi7({}, [wb, wb], [B, A])
+        lo, hi = lo2, hi2
+    last = B if steps % 2 == 1 else A
+    return last.arr[z_lo - a:z_hi - a]
+
+
+@pytest.mark.parametrize("G", [1, 4])
+def test_jacobi_full_size_sampled(cel, G):
+    """BASELINE config 5 at full size (1024^3, TMA kernel, 2-D split over G
+    virtual devices): sampled planes at the global edges, the split boundary
+    and the interior, bit-exact."""
+    n, steps = 1024, 3
+    rt = cel.Runtime(G, cuda_devices=[0] * G, arena_bytes=int(2 * n ** 3 * 4 / G * 1.25) + (512 << 20))
+    prog = P.jacobi3d(n, steps)
+    rt.buffer_create(3, [n, n, n], 4)
+    rt.buffer_create(3, [n, n, n], 4)
+    for op in prog["ops"]:
+        if op[0] == "task":
+            rt.task_submit(op[1])
+    last = 1 if steps % 2 == 1 else 0
+    for lo, hi in [(0, 2), (n // 2 - 1, n // 2 + 1), (n - 2, n), (333, 334)]:
+        got = rt.buffer_read(last, ([lo, 0, 0], [hi, n, n]))
+        exp = light_cone_jacobi(lo, hi, n, steps)
+        assert np.array_equal(got, exp), (lo, hi)
+    rt.shutdown()
+
+
+def test_rsim_full_width(cel):
+    """BASELINE config 4 at its full width W = 84,000 (T = 48 rows, 4 devices,
+    lookahead none and auto): the whole buffer bit-exact against the oracle."""
+    prog = P.rsim(84000, 48)
+    for mode in ("none", "auto"):
+        run_both(cel, prog, 4, mode, arena=256 << 20)
