@@ -713,6 +713,68 @@ __global__ void __launch_bounds__(128) nbody_step_fast2_kernel(const __grid_cons
     }
 }
 
+// fast-math timestep on Blackwell packed FP32x2 (FFMA2 / FADD2 / FMUL2):
+// bodies i and i + 128 ride in the two lanes of every float2 operation, so
+// one instruction does the arithmetic of two interactions (rsqrt stays scalar)
+__global__ void __launch_bounds__(128) nbody_step_fast_x2_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& P = a.acc[0];
+    const DAcc& V = a.acc[1];
+    __shared__ float4 sp[kNbTile];
+    const int64_t i0 = a.chunk.lo[0] + int64_t(blockIdx.x) * kNbTile + threadIdx.x;
+    const int64_t i1 = i0 + 128;
+    const bool v0 = i0 < a.chunk.hi[0], v1 = i1 < a.chunk.hi[0];
+    const int64_t N = P.ext[0];
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 p0 = v0 ? *ptr<const float4>(P, i0, 0, 0) : z4;
+    const float4 p1 = v1 ? *ptr<const float4>(P, i1, 0, 0) : z4;
+    const float2 npx = make_float2(-p0.x, -p1.x), npy = make_float2(-p0.y, -p1.y), npz = make_float2(-p0.z, -p1.z);
+    const float2 eps = make_float2(NB_EPS2, NB_EPS2);
+    float2 ax = make_float2(0.f, 0.f), ay = ax, az = ax;
+    for (int64_t j0 = 0; j0 < N; j0 += kNbTile) {
+        for (int t = threadIdx.x; t < kNbTile; t += 128) {
+            const int64_t j = j0 + t;
+            sp[t] = j < N ? *ptr<const float4>(P, j, 0, 0) : z4;
+        }
+        __syncthreads();
+        const int jn = N - j0 < kNbTile ? int(N - j0) : kNbTile;
+        auto body = [&](const float4 pj) {
+            const float2 dx = __fadd2_rn(make_float2(pj.x, pj.x), npx);
+            const float2 dy = __fadd2_rn(make_float2(pj.y, pj.y), npy);
+            const float2 dz = __fadd2_rn(make_float2(pj.z, pj.z), npz);
+            const float2 r2 = __ffma2_rn(dz, dz, __ffma2_rn(dy, dy, __ffma2_rn(dx, dx, eps)));
+            const float2 q = make_float2(rsqrtf(r2.x), rsqrtf(r2.y));
+            const float2 sq = __fmul2_rn(__fmul2_rn(q, q), q);
+            ax = __ffma2_rn(dx, sq, ax);
+            ay = __ffma2_rn(dy, sq, ay);
+            az = __ffma2_rn(dz, sq, az);
+        };
+        if (jn == kNbTile) {
+#pragma unroll 8
+            for (int k = 0; k < kNbTile; ++k) body(sp[k]);
+        } else {
+            for (int k = 0; k < jn; ++k) body(sp[k]);
+        }
+        __syncthreads();
+    }
+    const float c = NB_DT * NB_MASS;
+    if (v0) {
+        float4* vp = ptr<float4>(V, i0, 0, 0);
+        float4 v = *vp;
+        v.x = __fmaf_rn(c, ax.x, v.x);
+        v.y = __fmaf_rn(c, ay.x, v.y);
+        v.z = __fmaf_rn(c, az.x, v.z);
+        *vp = v;
+    }
+    if (v1) {
+        float4* vp = ptr<float4>(V, i1, 0, 0);
+        float4 v = *vp;
+        v.x = __fmaf_rn(c, ax.y, v.x);
+        v.y = __fmaf_rn(c, ay.y, v.y);
+        v.z = __fmaf_rn(c, az.y, v.z);
+        *vp = v;
+    }
+}
+
 __global__ void nbody_update_kernel(const __grid_constant__ KArgs a) {
     const DAcc& V = a.acc[0];
     const DAcc& P = a.acc[1];
@@ -951,9 +1013,11 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         static int variant = -1;
         if (variant < 0) {
             const char* e = getenv("CEL_NBODY");
-            variant = (e && e[0] == '1') ? 1 : 2;
+            variant = (e && e[0] == '1') ? 1 : ((e && e[0] == '2') ? 2 : 3);
         }
-        if (a.fast && variant == 2)
+        if (a.fast && variant == 3)
+            nbody_step_fast_x2_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), 128, 0, s>>>(a);
+        else if (a.fast && variant == 2)
             nbody_step_fast2_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), 128, 0, s>>>(a);
         else if (a.fast)
             nbody_step_fast_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
