@@ -159,6 +159,7 @@ def main():
         line["lookahead"] = args.lookahead
         line["alloc"] = st1["n_alloc"] - st0["n_alloc"]
         line["resize_copies"] = st1["copies_resize"] - st0["copies_resize"]
+        line["resize_copies_elided"] = st1["copies_elided"] - st0["copies_elided"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:

@@ -156,6 +156,7 @@ typedef struct {
     uint64_t exec_ns_alloc, exec_ns_free, exec_ns_copy, exec_ns_kernel, exec_ns_horizon, exec_ns_epoch;
                                /* host time of the executor per instruction kind (part of gen_ns) */
     uint64_t signal_ns, remote_wait_ns; /* host time in cross-process flag writes / waits */
+    uint64_t copies_elided, bytes_elided; /* resize copies made no-ops by in-place allocation growth */
 } cel_stats;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

@@ -78,7 +78,7 @@ class cel_stats(C.Structure):
         "alloc_bytes_peak", "flushes", "kernel_launches", "copy_launches", "memcpy_calls",
         "event_waits", "remote_waits", "signals", "host_syncs", "gen_ns",
         "exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon", "exec_ns_epoch",
-        "signal_ns", "remote_wait_ns")]
+        "signal_ns", "remote_wait_ns", "copies_elided", "bytes_elided")]
 
 
 _P = C.c_void_p

@@ -257,6 +257,8 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
         o->exec_ns_epoch = e.exec_ns[5];
         o->signal_ns = e.signal_ns;
         o->remote_wait_ns = e.remote_wait_ns;
+        o->copies_elided = e.copies_elided;
+        o->bytes_elided = e.bytes_elided;
     }
     return CEL_OK;
 }

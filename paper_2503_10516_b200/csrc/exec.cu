@@ -74,6 +74,19 @@ bool Executor::Arena::alloc(uint64_t bytes, uint64_t* off, Token* tok) {
     return false;
 }
 
+bool Executor::Arena::extend(uint64_t off, uint64_t old_bytes, uint64_t new_bytes, Token* tok) {
+    const uint64_t a = off + round_up(std::max<uint64_t>(old_bytes, 1), kAlign);
+    const uint64_t b = off + round_up(std::max<uint64_t>(new_bytes, 1), kAlign);
+    if (b <= a) return true;
+    auto it = free_.find(a);
+    if (it == free_.end() || it->second.len < b - a) return false;
+    *tok = it->second.tok;
+    FreeRange rest{it->second.len - (b - a), it->second.tok};
+    free_.erase(it);
+    if (rest.len) free_[b] = rest;
+    return true;
+}
+
 void Executor::Arena::release(uint64_t off, uint64_t bytes, Token tok) {
     bytes = round_up(std::max<uint64_t>(bytes, 1), kAlign);
     auto nx = free_.lower_bound(off);
@@ -104,6 +117,9 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     trace_ = tr && tr[0] == '1';
     const char* ns = getenv("CEL_NO_SPLIT");
     split_ = !(ns && ns[0] == '1');
+    const char* ng = getenv("CEL_NO_GROW");
+    no_grow_ = ng && ng[0] == '1';
+    grown_ = !no_grow_;
 }
 
 Executor::~Executor() {
@@ -427,6 +443,24 @@ void Executor::sync_all() {
     poll(true);
 }
 
+// record which local work touched each allocation (in-place growth must
+// order the grown allocation's users after it)
+void Executor::note_use(const Instr& ins) {
+    auto tit = tok_.find(ins.iid);
+    if (tit == tok_.end() || tit->second.local.empty()) return;
+    const Token loc{tit->second.local, {}};
+    auto add = [&](int64_t aid) {
+        auto a = allocs_.find(aid);
+        if (a != allocs_.end()) merge(a->second.use, loc);
+    };
+    if (ins.kind == IKind::Copy) {
+        add(ins.src_aid);
+        add(ins.dst_aid);
+    } else if (ins.kind == IKind::Kernel) {
+        for (int64_t aid : ins.bindings) add(aid);
+    }
+}
+
 void Executor::prune_tokens(uint64_t below) {
     for (auto it = tok_.begin(); it != tok_.end();) {
         if (it->first < below && !live_alloc_iid_.count(it->first))
@@ -693,14 +727,40 @@ void Executor::on_instr_impl(const Instr& ins) {
         const uint64_t bytes = ins.box.volume() * es;
         uint64_t off = 0;
         Token t;
-        if (!arenas_[dev].alloc(bytes, &off, &t)) {
+        // In-place growth: a resize that keeps a live
+        // allocation's rows as the prefix of the new box (same lo, same row
+        // pitch, growth at the end of dim 0) takes the old allocation's
+        // address when the arena range right after it is free.  Its resize
+        // copies then move nothing and its free releases nothing.  Every rank
+        // replays this decision identically (it depends only on the
+        // instruction stream and the arena state).
+        AllocRec* grow = nullptr;
+        for (auto& kv : allocs_) {
+            AllocRec& o = kv.second;
+            if (no_grow_ || o.dev != dev || o.buffer != ins.buffer || o.absorbed_into) continue;
+            const Box& ob = o.box;
+            if (ob.lo[0] == ins.box.lo[0] && ob.lo[1] == ins.box.lo[1] && ob.lo[2] == ins.box.lo[2] &&
+                ob.hi[1] == ins.box.hi[1] && ob.hi[2] == ins.box.hi[2] && ob.hi[0] <= ins.box.hi[0]) {
+                grow = &o;
+                break;
+            }
+        }
+        if (grow && arenas_[dev].extend(grow->off, grow->bytes, bytes, &t)) {
+            // the grown allocation's users write memory the old one's readers
+            // may still read: follow every local use of the old allocation
+            // (remote ranks only write it, and those writes reach the new
+            // allocation's users through the resize copies' dependencies)
+            off = grow->off;
+            grow->absorbed_into = ins.aid;
+            if (mine) merge(t, grow->use);
+        } else if (!arenas_[dev].alloc(bytes, &off, &t)) {
             char buf[200];
             snprintf(buf, sizeof buf, "device %d arena exhausted allocating %.3f GiB", dev, double(bytes) / (1ull << 30));
             errmsg_ = buf;
             err_ = E_OOM;
             return;
         }
-        allocs_[ins.aid] = AllocRec{dev, off, bytes, ins.box, es, ins.iid};
+        allocs_[ins.aid] = AllocRec{dev, off, bytes, ins.box, es, ins.iid, ins.buffer};
         live_alloc_iid_.insert(ins.iid);
         Token mt;
         if (mine) merge(mt, t);
@@ -730,7 +790,7 @@ void Executor::on_instr_impl(const Instr& ins) {
         } else {
             t.remote.push_back({owner_rank(r.dev), ins.iid});
         }
-        arenas_[r.dev].release(r.off, r.bytes, t);
+        if (!r.absorbed_into) arenas_[r.dev].release(r.off, r.bytes, t);   // else: lives on in the grown one
         tok_[ins.iid] = t;
         live_alloc_iid_.erase(r.iid);
         allocs_.erase(it);
@@ -786,6 +846,7 @@ void Executor::on_instr_impl(const Instr& ins) {
         exec_epoch(ins);
         return;
     }
+    if (grown_) note_use(ins);
     if (++since_poll_ >= 64) {
         since_poll_ = 0;
         poll(false);
@@ -862,6 +923,14 @@ void Executor::exec_copy(const Instr& ins) {
     if (ins.src_mem >= 2 && ins.dst_mem >= 2) {
         const AllocRec& S = allocs_.at(ins.src_aid);
         const AllocRec& D = allocs_.at(ins.dst_aid);
+        if (S.dev == D.dev && S.off == D.off && S.box.lo[0] == D.box.lo[0] && S.box.lo[1] == D.box.lo[1] &&
+            S.box.lo[2] == D.box.lo[2] && S.box.extent(1) == D.box.extent(1) && S.box.extent(2) == D.box.extent(2)) {
+            // in-place growth: source and destination bytes coincide
+            st_.copies_elided++;
+            st_.bytes_elided += rvolume(ins.region) * es;
+            tok_[ins.iid] = deps;
+            return;
+        }
         const int dev = S.dev;
         const bool peer = S.dev != D.dev;
         const int sidx = dev * kStreamsPerDev + (peer ? S_PUSH : S_COPY);

@@ -62,6 +62,7 @@ struct ExecStats {
     uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
     uint64_t event_waits = 0, remote_waits = 0, signals = 0;
+    uint64_t copies_elided = 0, bytes_elided = 0;   // resize copies made no-ops by in-place growth
     uint64_t host_syncs = 0;
     uint64_t exec_ns[6] = {};          // host time in on_instr per instruction kind (IKind order)
     uint64_t signal_ns = 0, remote_wait_ns = 0;
@@ -134,6 +135,9 @@ private:
         uint64_t data_off = 0;         // after the signal area
         std::map<uint64_t, FreeRange> free_;
         bool alloc(uint64_t bytes, uint64_t* off, Token* tok);
+        // grow [off, off + old_bytes) in place to new_bytes if the range right
+        // after it is free; tok receives that range's completion token
+        bool extend(uint64_t off, uint64_t old_bytes, uint64_t new_bytes, Token* tok);
         void release(uint64_t off, uint64_t bytes, Token tok);
     };
     struct AllocRec {
@@ -143,6 +147,9 @@ private:
         Box box;
         uint32_t es;
         uint64_t iid;
+        uint32_t buffer = 0;
+        int64_t absorbed_into = 0;                // in-place growth: memory now owned by this aid
+        Token use;                                // local work that read / wrote it (in-place growth)
     };
     struct Prof {
         int kind;
@@ -195,6 +202,7 @@ private:
     void exec_epoch(const Instr& ins);
     void throttle();
     void prune_tokens(uint64_t below);
+    void note_use(const Instr& ins);
     Token materialize(int dev, const Token& t);
     cudaEvent_t prof_event(int dev);
     uint64_t* sig_slot(int dev, int from_rank, uint64_t iid);
@@ -254,6 +262,8 @@ private:
     std::vector<uint32_t> host_drop_;
     bool trace_ = false;
     bool split_ = true;
+    bool no_grow_ = false;                      // CEL_NO_GROW=1: disable in-place growth (A/B)
+    bool grown_ = true;                           // track allocation uses for in-place growth
     std::unordered_map<uint64_t, CopyInfo> copy_info_;
     std::unordered_map<uint64_t, Parts> parts_;
     static constexpr uint64_t kRing = 1u << 16;

@@ -40,6 +40,13 @@ def run_both(cel, prog, G, mode="auto", devices=None, arena=256 << 20, step=4):
     devices = devices if devices is not None else [0] * G
     rt = cel.Runtime(G, cuda_devices=devices, lookahead=mode, arena_bytes=arena, instr_log_path=LOG,
                      horizon_step=step)
+    close = rt.shutdown
+
+    def shutdown():                  # keep the final executor statistics for the caller
+        if rt.h is not None:
+            rt.final_stats = rt.stats()
+        close()
+    rt.shutdown = shutdown
     got = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
     o = OracleRuntime(G, lookahead=mode, horizon_step=step)
     run_program(o, prog)
@@ -99,6 +106,20 @@ def test_nbody(cel, G):
 @pytest.mark.parametrize("G,mode", [(1, "auto"), (2, "auto"), (2, "none"), (4, "none"), (3, "infinite")])
 def test_rsim(cel, G, mode):
     run_both(cel, P.rsim(1000, 24), G, mode)
+
+
+@pytest.mark.parametrize("grow", [True, False])
+def test_rsim_in_place_growth(cel, grow, monkeypatch):
+    """Without lookahead every RSim row resizes the allocation (alloc -> copy ->
+    free).  In-place growth takes the old allocation's address, so the
+    resize copies move nothing; results and the instruction log are unchanged."""
+    if not grow:
+        monkeypatch.setenv("CEL_NO_GROW", "1")
+    for G in (1, 2):
+        st = run_both(cel, P.rsim(1000, 24), G, "none").final_stats
+        assert st["copies_resize"] > 0
+        assert (st["copies_elided"] > 0) == grow
+        assert st["copies_elided"] <= st["copies_resize"]
 
 
 def test_physical_multi_gpu(cel):
