@@ -146,9 +146,9 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def make_runtime(cel, G, rank, world, dist, arena):
+def make_runtime(cel, G, rank, world, dist, arena, **kw):
     if world > 1:
-        rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=arena, rank=rank, world=world)
+        rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=arena, rank=rank, world=world, **kw)
         blob = rt.ipc_export()
         blobs = [None] * world
         dist.all_gather_object(blobs, blob)
@@ -157,7 +157,7 @@ def make_runtime(cel, G, rank, world, dist, arena):
                 rt.ipc_import(r, b)
         dist.barrier()
         return rt
-    return cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=arena)
+    return cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=arena, **kw)
 
 
 def main():

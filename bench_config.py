@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--fast-math", action="store_true")
     ap.add_argument("--lookahead", default="auto")
     ap.add_argument("--rows", type=int, default=1024)
+    ap.add_argument("--collective", type=int, default=1, help="1: all-gather copy sets as NCCL broadcasts")
     args = ap.parse_args()
     rank, world, local = bench.env_rank()
     G = args.gpus
@@ -61,19 +62,8 @@ def main():
     elif args.workload == "nbody":
         N = 1 << 20
         steps = args.steps or 3
-        rt = bench.make_runtime(cel, G, rank, world, dist, 1 << 30) if not args.fast_math else None
-        if rt is None:
-            if world > 1:
-                rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=1 << 30, rank=rank, world=world,
-                                 fast_math=True)
-                blobs = [None] * world
-                dist.all_gather_object(blobs, rt.ipc_export())
-                for r, b in enumerate(blobs):
-                    if r != rank:
-                        rt.ipc_import(r, b)
-                dist.barrier()
-            else:
-                rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=1 << 30, fast_math=True)
+        rt = bench.make_runtime(cel, G, rank, world, dist, 1 << 30, fast_math=args.fast_math,
+                                collective=bool(args.collective))
         prog = P.nbody(N, 1)
         rt.buffer_create(1, [N], 16)
         rt.buffer_create(1, [N], 16)
@@ -88,17 +78,8 @@ def main():
     else:
         W, T = 84000, args.rows
         steps = T
-        rt = bench.make_runtime(cel, G, rank, world, dist, 4 << 30) if args.lookahead == "auto" else None
-        if rt is None:
-            rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=4 << 30, rank=rank, world=world,
-                             lookahead=args.lookahead)
-            if world > 1:
-                blobs = [None] * world
-                dist.all_gather_object(blobs, rt.ipc_export())
-                for r, b in enumerate(blobs):
-                    if r != rank:
-                        rt.ipc_import(r, b)
-                dist.barrier()
+        rt = bench.make_runtime(cel, G, rank, world, dist, 4 << 30, lookahead=args.lookahead,
+                                collective=bool(args.collective))
         prog = P.rsim(W, T)
         rt.buffer_create(2, [T, W], 4)
         descs = [cel.task_desc(op[1]) for op in prog["ops"] if op[0] == "task"]
@@ -142,6 +123,8 @@ def main():
             "ms_per_step": ms / steps, "host_ms_per_step": host_s * 1e3 / steps,
             "gen_us_per_step": (st1["gen_ns"] - st0["gen_ns"]) / 1e3 / steps,
             "gpu_launches": st1["kernel_launches"] - st0["kernel_launches"],
+            "collective": bool(args.collective),
+            "coll_groups": st1["coll_groups"] - st0["coll_groups"],
             "profile_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()}}
     if args.workload == "jacobi3d":
         cells = 1024 ** 3 / G

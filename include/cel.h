@@ -142,6 +142,12 @@ typedef struct {
     int32_t world;             /* multi-process: number of processes (= n_devices), 1 = single process */
     int32_t fast_math;         /* 1: ALU-bound kernels (N-body) use FMA + rsqrt; results then match the
                                   oracle within a tolerance instead of bit for bit (R16) */
+    int32_t collective;        /* 1: a task's all-gather copy set (buffer read through `all` / `fixed`,
+                                  every device receiving every other device's contiguous chunk; SURVEY
+                                  §8 a7) runs as one group of NCCL broadcasts when the
+                                  devices are distinct GPUs; 0: as peer pushes.  The instruction graph
+                                  is the same either way.  NCCL (libnccl.so.2) is opened at run time;
+                                  a failed communicator setup is CEL_E_NCCL (sticky). */
 } cel_config;
 
 typedef struct {
@@ -157,6 +163,8 @@ typedef struct {
                                /* host time of the executor per instruction kind (part of gen_ns) */
     uint64_t signal_ns, remote_wait_ns; /* host time in cross-process flag writes / waits */
     uint64_t copies_elided, bytes_elided; /* resize copies made no-ops by in-place allocation growth */
+    uint64_t coll_groups, coll_copies;    /* all-gather copy sets run as NCCL collectives, and their copies */
+    uint64_t gather_sets;                 /* coherence copy sets the scheduler found to be all-gathers */
 } cel_stats;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of
@@ -164,10 +172,12 @@ typedef struct {
  * distinct GPUs.  Fails with CEL_E_CUDA if no GPU is visible. */
 int cel_runtime_create(const cel_config* cfg, cel_runtime** out);
 
-/* Multi-process (world > 1, one process per GPU): export this rank's arena
- * handle (cel_ipc_blob_size() bytes into blob), import every other rank's,
- * then cel_ipc_connect.  Copies into another rank's memory are pushed by SM
- * stores over NVLink; cross-process dependencies are flags in GPU memory. */
+/* Multi-process (world > 1, one process per GPU): export this rank's blob
+ * (cel_ipc_blob_size() bytes into blob: the arena's CUDA IPC handle and, from
+ * rank 0, the NCCL unique id of the all-gather communicator), then import every
+ * other rank's before submitting work.  Copies into another rank's memory are
+ * pushed by SM stores over NVLink; cross-process dependencies are flags in GPU
+ * memory; the communicator is built when the first all-gather set executes. */
 size_t cel_ipc_blob_size(void);
 int cel_ipc_export(cel_runtime* rt, void* blob);
 int cel_ipc_import(cel_runtime* rt, int32_t rank, const void* blob);
@@ -209,8 +219,9 @@ int cel_stats_get(cel_runtime* rt, cel_stats* out);
  * kinds 0..9, k = 10 for copy kernels within one GPU (resize, copies between
  * virtual devices of one GPU), k = 11 for peer pushes to another GPU and
  * k = 12 for the boundary (shell) launches of stencil kernels that are split
- * for halo overlap (their interiors count under the kernel's kind).
- * n = array length (13). */
+ * for halo overlap (their interiors count under the kernel's kind) and k = 13
+ * for NCCL all-gather groups (per device, broadcast group start to end).
+ * n = array length (14). */
 int cel_profile_enable(cel_runtime* rt, int32_t on);
 int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n);
 

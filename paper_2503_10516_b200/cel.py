@@ -26,10 +26,12 @@ SPLITS = {"1d": 0, "2d": 1}
 KERNELS = {"fill_hash": 0, "fill_const": 1, "stencil3": 2, "wave5": 3, "jacobi7": 4, "nbody_step": 5,
            "nbody_update": 6, "rsim_row": 7, "probe": 8, "callback": 9}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
-PROFILE_SLOTS = 13       # kernel kinds 0..9, copy within a GPU (10), peer push (11), stencil shell launches (12)
+PROFILE_SLOTS = 14       # kernel kinds 0..9, copy within a GPU (10), peer push (11), stencil shell launches (12),
+                         # NCCL all-gather groups (13)
 COPY_SLOT = 10
 PEER_SLOT = 11
 SHELL_SLOT = 12
+COLL_SLOT = 13
 
 
 class cel_box(C.Structure):
@@ -67,7 +69,7 @@ class cel_config(C.Structure):
     _fields_ = [("cuda_devices", C.POINTER(C.c_int)), ("n_devices", C.c_int32), ("execute", C.c_int32),
                 ("lookahead", C.c_int32), ("horizon_step", C.c_int32), ("checks", C.c_int32),
                 ("instr_log_path", C.c_char_p), ("arena_bytes", C.c_uint64), ("rank", C.c_int32),
-                ("world", C.c_int32), ("fast_math", C.c_int32)]
+                ("world", C.c_int32), ("fast_math", C.c_int32), ("collective", C.c_int32)]
 
 
 class cel_stats(C.Structure):
@@ -78,7 +80,8 @@ class cel_stats(C.Structure):
         "alloc_bytes_peak", "flushes", "kernel_launches", "copy_launches", "memcpy_calls",
         "event_waits", "remote_waits", "signals", "host_syncs", "gen_ns",
         "exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon", "exec_ns_epoch",
-        "signal_ns", "remote_wait_ns", "copies_elided", "bytes_elided")]
+        "signal_ns", "remote_wait_ns", "copies_elided", "bytes_elided", "coll_groups", "coll_copies",
+        "gather_sets")]
 
 
 _P = C.c_void_p
@@ -170,7 +173,7 @@ class Runtime:
     """The C-ABI runtime.  Method names follow include/cel.h (cel_ prefix dropped)."""
 
     def __init__(self, n_devices, cuda_devices=None, execute=True, lookahead="auto", horizon_step=4, checks=True,
-                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False):
+                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False, collective=True):
         cfg = cel_config()
         devs = list(cuda_devices) if cuda_devices is not None else list(range(n_devices))
         self._devs = (C.c_int * len(devs))(*devs)
@@ -185,6 +188,7 @@ class Runtime:
         cfg.rank = rank
         cfg.world = world
         cfg.fast_math = 1 if fast_math else 0
+        cfg.collective = 1 if collective else 0
         h = _P()
         _check(lib.cel_runtime_create(C.byref(cfg), C.byref(h)))
         self.h = h
@@ -264,7 +268,7 @@ class Runtime:
         out = {}
         for k in range(PROFILE_SLOTS):
             if cnt[k]:
-                name = {COPY_SLOT: "copy", PEER_SLOT: "copy_peer", SHELL_SLOT: "shell"}.get(k) or KERNEL_NAMES[k]
+                name = {COPY_SLOT: "copy", PEER_SLOT: "copy_peer", SHELL_SLOT: "shell", COLL_SLOT: "coll"}.get(k) or KERNEL_NAMES[k]
                 out[name] = (ms[k], cnt[k])
         return out
 

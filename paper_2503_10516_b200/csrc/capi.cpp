@@ -68,7 +68,7 @@ extern "C" {
 
 const char* cel_last_error(void) { return g_err.c_str(); }
 
-size_t cel_ipc_blob_size(void) { return 64; }
+size_t cel_ipc_blob_size(void) { return Executor::kBlobBytes; }
 
 int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
     if (!cfg || !out) return fail(CEL_E_INVALID, "null argument");
@@ -91,6 +91,7 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
         ec.world = world;
         ec.arena_bytes = cfg->arena_bytes;
         ec.fast_math = cfg->fast_math != 0;
+        ec.collective = cfg->collective != 0;
         rt->exec = std::make_unique<Executor>(ec, nullptr);
         std::string err;
         const int rc = rt->exec->init(&err);
@@ -239,6 +240,7 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
     o->bytes_d2d_peer = s.bytes_d2d_peer;
     o->alloc_bytes_peak = s.alloc_bytes_peak;
     o->flushes = s.flushes;
+    o->gather_sets = s.gather_sets;
     o->gen_ns = rt->gen_ns;
     if (rt->exec) {
         const ExecStats& e = rt->exec->stats();
@@ -259,6 +261,8 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
         o->remote_wait_ns = e.remote_wait_ns;
         o->copies_elided = e.copies_elided;
         o->bytes_elided = e.bytes_elided;
+        o->coll_groups = e.coll_groups;
+        o->coll_copies = e.coll_copies;
     }
     return CEL_OK;
 }

@@ -8,7 +8,9 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
 #include <immintrin.h>
+#include <nccl.h>
 
 #include "../../include/cel.h"
 
@@ -36,6 +38,36 @@ struct Drv {
         cudaGetDriverEntryPoint("cuDeviceGetAttribute", reinterpret_cast<void**>(&devattr), cudaEnableDefault, &q);
     }
 } g_drv;
+
+// NCCL, opened at run time (the process may already hold torch's copy of
+// libnccl.so.2; the C API is stable across the 2.2x releases in this image).
+struct Nccl {
+    ncclResult_t (*get_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*group_start)() = nullptr;
+    ncclResult_t (*group_end)() = nullptr;
+    ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*errstr)(ncclResult_t) = nullptr;
+    int state = 0;   // 0 not tried, 1 loaded, -1 unavailable
+    bool load() {
+        if (state) return state > 0;
+        state = -1;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        get_id = reinterpret_cast<decltype(get_id)>(dlsym(h, "ncclGetUniqueId"));
+        init_rank = reinterpret_cast<decltype(init_rank)>(dlsym(h, "ncclCommInitRank"));
+        init_all = reinterpret_cast<decltype(init_all)>(dlsym(h, "ncclCommInitAll"));
+        destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "ncclCommDestroy"));
+        group_start = reinterpret_cast<decltype(group_start)>(dlsym(h, "ncclGroupStart"));
+        group_end = reinterpret_cast<decltype(group_end)>(dlsym(h, "ncclGroupEnd"));
+        bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
+        errstr = reinterpret_cast<decltype(errstr)>(dlsym(h, "ncclGetErrorString"));
+        if (get_id && init_rank && init_all && destroy && group_start && group_end && bcast && errstr) state = 1;
+        return state > 0;
+    }
+} g_nccl;
 
 inline uint64_t now_ns() {
     return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -140,6 +172,9 @@ Executor::~Executor() {
     }
     for (auto& pool : prof_pool_)
         for (cudaEvent_t e : pool) cudaEventDestroy(e);
+    for (void* c : comms_)
+        if (c) g_nccl.destroy(static_cast<ncclComm_t>(c));
+    comms_.clear();
     for (int d = 0; d < int(arenas_.size()); ++d) {
         if (!owned(d)) {
             if (cfg_.world > 1 && arenas_[d].base) cudaIpcCloseMemHandle(arenas_[d].base);
@@ -255,6 +290,25 @@ int Executor::init(std::string* err) {
             return E_CUDA;
         }
     }
+    if (cfg_.collective && G_ >= 2) {
+        // one NCCL rank per GPU: the virtual devices must be distinct GPUs
+        bool distinct = true;
+        for (int a = 0; a < G_; ++a)
+            for (int b = a + 1; b < G_; ++b)
+                if (phys_[a] == phys_[b]) distinct = false;
+        const char* cv = getenv("CEL_COLL");
+        if (cv && cv[0] == '0') distinct = false;
+        coll_ = distinct && g_nccl.load();
+        if (coll_ && cfg_.world > 1 && cfg_.rank == 0) {
+            ncclUniqueId id;
+            if (g_nccl.get_id(&id) != ncclSuccess) {
+                coll_ = false;
+            } else {
+                memcpy(nccl_id_, &id, sizeof id);
+                nccl_id_set_ = true;
+            }
+        }
+    }
     cudaDeviceSynchronize();
     const char* et = getenv("CEL_EXEC_THREAD");
     if (!(et && et[0] == '0')) {
@@ -264,14 +318,19 @@ int Executor::init(std::string* err) {
     return err_.load();
 }
 
-size_t Executor::ipc_blob_size() const { return sizeof(cudaIpcMemHandle_t); }
+// blob = arena IPC handle | flag byte | NCCL unique id (rank 0's is used)
+static_assert(sizeof(cudaIpcMemHandle_t) == 64 && sizeof(ncclUniqueId) == 128, "IPC blob layout");
+size_t Executor::ipc_blob_size() const { return kBlobBytes; }
 
 int Executor::ipc_export(void* blob) const {
     if (cfg_.world <= 1) return E_STATE;
     cudaIpcMemHandle_t h;
     cudaSetDevice(phys_[cfg_.rank]);
     if (cudaIpcGetMemHandle(&h, arenas_[cfg_.rank].base) != cudaSuccess) return E_CUDA;
-    memcpy(blob, &h, sizeof h);
+    char* b = static_cast<char*>(blob);
+    memcpy(b, &h, sizeof h);
+    b[sizeof h] = nccl_id_set_ ? 1 : 0;
+    memcpy(b + sizeof h + 1, nccl_id_, sizeof(nccl_id_));
     return E_OK;
 }
 
@@ -281,6 +340,15 @@ int Executor::ipc_import(int rank, const void* blob) {
     if (rank == cfg_.rank) return E_OK;
     cudaIpcMemHandle_t h;
     memcpy(&h, blob, sizeof h);
+    if (rank == 0) {
+        const char* b = static_cast<const char*>(blob);
+        if (b[sizeof h]) {
+            memcpy(nccl_id_, b + sizeof h + 1, sizeof(nccl_id_));
+            nccl_id_set_ = true;
+        } else {
+            coll_ = false;          // rank 0 runs without the collective: so must everyone
+        }
+    }
     void* p = nullptr;
     set_dev(cfg_.rank);
     cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
@@ -690,13 +758,13 @@ void Executor::set_profile(bool on) {
 }
 
 int Executor::trace_dump(const char* path) {
-    double ms[K_NUM + 3];
-    uint64_t c[K_NUM + 3];
-    profile_read(ms, c, K_NUM + 3);          // resolves pending launches into trace_recs_
+    double ms[kProfSlots];
+    uint64_t c[kProfSlots];
+    profile_read(ms, c, kProfSlots);          // resolves pending launches into trace_recs_
     FILE* f = fopen(path, "w");
     if (!f) return E_INVALID;
     static const char* names[] = {"fill_hash", "fill_const", "stencil3", "wave5",  "jacobi7", "nbody_step",
-                                  "nbody_update", "rsim_row", "probe", "callback", "copy", "copy_peer", "shell"};
+                                  "nbody_update", "rsim_row", "probe", "callback", "copy", "copy_peer", "shell", "coll"};
     static const char* snames[] = {"compute", "copy", "push", "sync", "halo", "hsig", "sig0", "sig1", "sig2", "sig3", "sig4"};
     for (const TraceRec& t : trace_recs_)
         fprintf(f,
@@ -715,6 +783,25 @@ void Executor::on_instr_impl(const Instr& ins) {
     if (trace_)
         fprintf(stderr, "[cel r%d] iid %llu kind %d owner %d %s\n", cfg_.rank, (unsigned long long)ins.iid,
                 int(ins.kind), od, mine ? "exec" : "skip");
+    if (coll_ && ins.kind == IKind::Copy && ins.coll_n) {
+        // §8 a7: a member of an all-gather copy set.  Every rank takes part;
+        // the source's and the destination's ranks each wait for the member's
+        // dependencies, so the other ranks signal theirs to both.
+        const int sd = ins.src_mem - 2, dd = ins.dst_mem - 2;
+        if (cfg_.world > 1) {
+            kind_of_[ins.iid] = -1;
+            if (owner_rank(sd) != cfg_.rank) signal_deps(ins, sd);
+            if (owner_rank(dd) != cfg_.rank) signal_deps(ins, dd);
+        }
+        copy_info_[ins.iid] = CopyInfo{ins.src_aid, ins.dst_aid, rbbox(ins.region), ins.region};
+        auto& g = coll_pending_[ins.coll];
+        g.push_back(ins);
+        if (g.size() == ins.coll_n) {
+            exec_coll(g);
+            coll_pending_.erase(ins.coll);
+        }
+        return;
+    }
     if (cfg_.world > 1) {
         if (od >= 0) kind_of_[ins.iid] = od;
         else kind_of_[ins.iid] = -1;
@@ -898,6 +985,133 @@ void Executor::exec_epoch(const Instr& ins) {
             else ++it;
         }
     }
+}
+
+bool Executor::coll_init() {
+    if (coll_state_) return coll_state_ > 0;
+    coll_state_ = -1;
+    if (cfg_.world > 1) {
+        if (!nccl_id_set_) return false;
+        ncclUniqueId id;
+        memcpy(&id, nccl_id_, sizeof id);
+        ncclComm_t c = nullptr;
+        set_dev(cfg_.rank);
+        // collective over all ranks; every rank reaches the same first group
+        if (trace_) fprintf(stderr, "[cel r%d] ncclCommInitRank ...\n", cfg_.rank);
+        if (g_nccl.init_rank(&c, cfg_.world, id, cfg_.rank) != ncclSuccess) return false;
+        if (trace_) fprintf(stderr, "[cel r%d] ncclCommInitRank done\n", cfg_.rank);
+        comms_.assign(1, c);
+    } else {
+        std::vector<ncclComm_t> cs(G_, nullptr);
+        if (g_nccl.init_all(cs.data(), G_, phys_.data()) != ncclSuccess) return false;
+        comms_.assign(cs.begin(), cs.end());
+    }
+    coll_state_ = 1;
+    return true;
+}
+
+// §8 a7: an all-gather copy set (Scheduler::all_gathers) executed as
+// one group of NCCL broadcasts, one per source device, in place in every
+// device's allocation (the `all` mapper; NVLink / NVSwitch
+// collectives instead of G(G-1) separate pushes).
+void Executor::exec_coll(const std::vector<Instr>& m) {
+    const uint32_t es = bufinfo_.at(m[0].buffer).es;
+    if (!coll_init()) {
+        errmsg_ = "NCCL communicator setup failed (set collective = 0 to use peer pushes)";
+        err_ = E_NCCL;
+        return;
+    }
+    // local devices taking part: all G (one process) or this rank's device
+    std::vector<int> locals;
+    if (cfg_.world > 1) locals.push_back(cfg_.rank);
+    else
+        for (int v = 0; v < G_; ++v) locals.push_back(v);
+    auto lin = [](const Box& b, const Box& a) {          // element offset of b.lo in a row-major over a
+        return uint64_t(((b.lo[0] - a.lo[0]) * a.extent(1) + (b.lo[1] - a.lo[1])) * a.extent(2) + (b.lo[2] - a.lo[2]));
+    };
+    std::vector<Token> tv(G_);
+    for (int v : locals) {
+        Token t;
+        for (const Instr& x : m)
+            if (x.src_mem - 2 == v || x.dst_mem - 2 == v) merge(t, local_part(x.deps));
+        const int sidx = v * kStreamsPerDev + S_PUSH;
+        set_dev(v);
+        wait_token(sidx, t);
+    }
+    // roots in ascending device order; a root's region is the same box for all receivers
+    std::map<int, std::vector<const Instr*>> roots;
+    for (const Instr& x : m) roots[x.src_mem - 2].push_back(&x);
+    std::vector<Prof> profs;
+    if (cfg_.profile)
+        for (int v : locals) {
+            const int sidx = v * kStreamsPerDev + S_PUSH;
+            Prof p{K_NUM + 3, prof_event(v), prof_event(v), v, m[0].iid, sidx, now_ns()};
+            cudaEventRecord(p.a, streams_[sidx].s);
+            profs.push_back(p);
+        }
+    uint64_t bytes_total = 0;
+    ncclResult_t r = g_nccl.group_start();
+    for (auto& rt : roots) {
+        const int s = rt.first;
+        const Instr& x0 = *rt.second[0];
+        const Box& b = x0.region[0];
+        const AllocRec& S = allocs_.at(x0.src_aid);
+        const size_t bytes = size_t(b.volume()) * es;
+        bytes_total += bytes * rt.second.size();
+        for (size_t k = 0; k < locals.size() && r == ncclSuccess; ++k) {
+            const int v = locals[k];
+            char* buf = nullptr;
+            if (v == s) {
+                buf = arenas_[S.dev].base + S.off + lin(b, S.box) * es;
+            } else {
+                for (const Instr* x : rt.second)
+                    if (x->dst_mem - 2 == v) {
+                        const AllocRec& D = allocs_.at(x->dst_aid);
+                        buf = arenas_[D.dev].base + D.off + lin(b, D.box) * es;
+                    }
+            }
+            if (!buf) {
+                errmsg_ = "all-gather set without a receiver on a device";
+                err_ = E_STATE;
+                g_nccl.group_end();
+                return;
+            }
+            const int sidx = v * kStreamsPerDev + S_PUSH;
+            r = g_nccl.bcast(buf, buf, bytes, ncclUint8, s, static_cast<ncclComm_t>(comms_[k]), streams_[sidx].s);
+        }
+    }
+    const ncclResult_t r2 = g_nccl.group_end();
+    if (trace_) fprintf(stderr, "[cel r%d] broadcast group of %zu copies issued\n", cfg_.rank, m.size());
+    if (r != ncclSuccess || r2 != ncclSuccess) {
+        errmsg_ = std::string("ncclBroadcast: ") + g_nccl.errstr(r != ncclSuccess ? r : r2);
+        err_ = E_NCCL;
+        return;
+    }
+    for (auto& p : profs) {
+        cudaEventRecord(p.b, streams_[p.stream].s);
+        prof_pending_.push_back(p);
+    }
+    for (int v : locals) {
+        set_dev(v);                  // events come from the device's pool
+        tv[v] = record(v * kStreamsPerDev + S_PUSH);
+    }
+    for (const Instr& x : m) {
+        const int sd = x.src_mem - 2, dd = x.dst_mem - 2;
+        Token lt;
+        for (int v : locals)
+            if (v == sd || v == dd) merge(lt, tv[v]);
+        if (cfg_.world > 1) {
+            // the source's rank (sendbuff reusable) and the destination's rank
+            // (data arrived) each hold part of the completion
+            ltok_[x.iid] = lt;
+            for (int rk : {owner_rank(sd), owner_rank(dd)})
+                if (rk != cfg_.rank) lt.remote.push_back({rk, x.iid});
+        }
+        tok_[x.iid] = lt;
+    }
+    st_.coll_groups++;
+    st_.coll_copies += m.size();
+    st_.bytes_copy[2] += bytes_total;   // NCCL's kernels are library launches: not in kernel_launches
 }
 
 void Executor::exec_copy(const Instr& ins) {
@@ -1324,7 +1538,7 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
         prof_pool_[p.dev].push_back(p.b);
     }
     prof_pending_.clear();
-    for (int i = 0; i < n && i <= K_NUM + 2; ++i) {
+    for (int i = 0; i < n && i < kProfSlots; ++i) {
         ms[i] = prof_ms_[i];
         count[i] = prof_n_[i];
     }
@@ -1332,10 +1546,10 @@ int Executor::profile_read(double* ms, uint64_t* count, int n) {
 }
 
 void Executor::profile_reset() {
-    double ms[K_NUM + 3];
-    uint64_t c[K_NUM + 3];
-    profile_read(ms, c, K_NUM + 3);
-    for (int i = 0; i <= K_NUM + 2; ++i) {
+    double ms[kProfSlots];
+    uint64_t c[kProfSlots];
+    profile_read(ms, c, kProfSlots);
+    for (int i = 0; i < kProfSlots; ++i) {
         prof_ms_[i] = 0;
         prof_n_[i] = 0;
     }

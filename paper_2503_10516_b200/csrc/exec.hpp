@@ -53,6 +53,7 @@ struct ExecConfig {
     uint64_t arena_bytes = 0;          // per device; 0 = auto
     bool profile = false;
     bool fast_math = false;
+    bool collective = true;            // run all-gather copy sets as grouped NCCL broadcasts (§8 a7)
 };
 
 struct ExecStats {
@@ -63,10 +64,13 @@ struct ExecStats {
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
     uint64_t event_waits = 0, remote_waits = 0, signals = 0;
     uint64_t copies_elided = 0, bytes_elided = 0;   // resize copies made no-ops by in-place growth
+    uint64_t coll_groups = 0, coll_copies = 0;      // all-gather copy sets run as NCCL collectives
     uint64_t host_syncs = 0;
     uint64_t exec_ns[6] = {};          // host time in on_instr per instruction kind (IKind order)
     uint64_t signal_ns = 0, remote_wait_ns = 0;
 };
+
+constexpr int kProfSlots = K_NUM + 4;
 
 class Executor : public InstrSink {
 public:
@@ -96,7 +100,8 @@ public:
     void set_scheduler(Scheduler* s) { sched_ = s; }
     void set_readback(int64_t rb, void* dst, const Box& box, uint32_t elem_size);
 
-    // multi-process plumbing
+    // multi-process plumbing: blob = arena IPC handle | flag | NCCL unique id
+    static constexpr size_t kBlobBytes = 64 + 1 + 128;
     size_t ipc_blob_size() const;
     int ipc_export(void* blob) const;
     int ipc_import(int rank, const void* blob);
@@ -203,6 +208,8 @@ private:
     void throttle();
     void prune_tokens(uint64_t below);
     void note_use(const Instr& ins);
+    void exec_coll(const std::vector<Instr>& members);
+    bool coll_init();
     Token materialize(int dev, const Token& t);
     cudaEvent_t prof_event(int dev);
     uint64_t* sig_slot(int dev, int from_rank, uint64_t iid);
@@ -225,8 +232,8 @@ private:
     std::unordered_map<int64_t, Readback> readbacks_;
     std::unordered_set<uint64_t> signalled_;       // (iid * world + target) already signalled
     std::vector<Prof> prof_pending_;
-    double prof_ms_[K_NUM + 3] = {};     // kernel kinds, K_NUM = local copy, +1 peer copy, +2 shell launches
-    uint64_t prof_n_[K_NUM + 3] = {};
+    double prof_ms_[kProfSlots] = {};    // kernel kinds, K_NUM = local copy, +1 peer copy, +2 shell, +3 collective
+    uint64_t prof_n_[kProfSlots] = {};
     std::vector<int> phys_;
     bool memops64_ = false;
     std::atomic<int> err_{0};
@@ -265,6 +272,14 @@ private:
     bool no_grow_ = false;                      // CEL_NO_GROW=1: disable in-place growth (A/B)
     bool grown_ = true;                           // track allocation uses for in-place growth
     std::unordered_map<uint64_t, CopyInfo> copy_info_;
+    // §8 a7 all-gather as a collective: members are held until the whole set
+    // has arrived (they are consecutive within one task's coherence copies)
+    bool coll_ = false;                           // NCCL loaded and the devices qualify
+    int coll_state_ = 0;                          // 0 communicators not built, 1 ready, -1 failed
+    std::vector<void*> comms_;                    // ncclComm_t per local device
+    unsigned char nccl_id_[128] = {};
+    bool nccl_id_set_ = false;
+    std::unordered_map<uint64_t, std::vector<Instr>> coll_pending_;
     std::unordered_map<uint64_t, Parts> parts_;
     static constexpr uint64_t kRing = 1u << 16;
 };

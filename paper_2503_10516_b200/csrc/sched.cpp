@@ -4,6 +4,8 @@
 // instruction logs are compared record for record by the tests.
 #include "sched.hpp"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cinttypes>
 #include <cstring>
@@ -124,6 +126,8 @@ Box map_access(const Mapper& m, const Box& chunk, const Box& ext) {
 
 Scheduler::Scheduler(int n_devices, int lookahead, int horizon_step, bool checks, InstrSink* sink, FILE* log)
     : G_(n_devices), mode_(lookahead), checks_(checks), sink_(sink), log_(log), horizon_step_(horizon_step) {
+    const char* cm = getenv("CEL_COLL_MIN_BYTES");
+    if (cm && cm[0]) coll_min_bytes_ = strtoull(cm, nullptr, 10);
     cp_[0] = 0;
     // init epoch: tid 0 / iid 0
     Instr e;
@@ -580,7 +584,7 @@ void Scheduler::free_alloc(Alloc* a, int64_t tid) {
 }
 
 uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Alloc* dst, const Region& reg,
-                         int64_t rb) {
+                         int64_t rb, uint64_t coll, uint32_t coll_n) {
     // Table 1 `copy` with R12 dependencies
     std::vector<uint64_t> deps;
     auto add = [&](int64_t v) {
@@ -604,6 +608,8 @@ uint64_t Scheduler::copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Allo
     ins.dst_mem = dst ? dst->mem : 0;
     ins.region = reg;
     ins.readback = rb;
+    ins.coll = coll;
+    ins.coll_n = coll_n;
     const uint64_t iid = emit(ins, deps);
     const int64_t me = int64_t(iid);
     src->readers.add(me, reg);
@@ -654,6 +660,89 @@ std::map<std::tuple<int64_t, int, int64_t>, Region> Scheduler::source_parts_q(
         }
     }
     return parts;
+}
+
+namespace {
+// a box is one contiguous byte run of a row-major allocation over `a`
+bool contiguous_in(const Box& b, const Box& a) {
+    int d = 2;
+    while (d > 0 && b.lo[d] == a.lo[d] && b.hi[d] == a.hi[d]) --d;
+    for (int o = 0; o < d; ++o)
+        if (b.extent(o) != 1) return false;
+    return true;
+}
+}  // namespace
+
+// §8 a7: a buffer read through chunk-independent mappers (`all`,
+// `fixed`) whose coherence copies are, for every source device s, one
+// contiguous box copied to each of the other G-1 devices is an all-gather
+// (P:L161-163).  Returns buffer -> number of copies for each such
+// buffer.  The copies stay as they are in the instruction graph; the executor
+// may run the set as one collective.
+std::map<uint32_t, uint32_t> Scheduler::all_gathers(
+    const Cmd& c, const std::vector<std::pair<Key, std::vector<std::pair<std::tuple<int64_t, int, int64_t>, Region>>>>& pend,
+    const std::map<Key, Alloc*>& binding) const {
+    std::map<uint32_t, uint32_t> out;
+    if (G_ < 2) return out;
+    std::map<uint32_t, bool> eligible;
+    for (const Access& a : c.desc->acc) {
+        if (!is_read(a.mode)) continue;
+        const bool ci = a.map.kind == MapKind::All || a.map.kind == MapKind::Fixed;
+        auto it = eligible.find(a.buf);
+        eligible[a.buf] = (it == eligible.end() ? true : it->second) && ci;
+    }
+    for (auto& e : eligible) {
+        if (!e.second) continue;
+        const uint32_t bid = e.first;
+        // per source device: region and the set of receivers
+        std::map<int, std::pair<Box, std::vector<int>>> roots;
+        bool ok = true;
+        uint32_t n = 0;
+        for (auto& pk : pend) {
+            if (pk.first.second != bid) continue;
+            const int d = pk.first.first;
+            auto bit = binding.find(pk.first);
+            for (auto& p : pk.second) {
+                const int ms = std::get<1>(p.first);
+                if (ms < 2 || p.second.size() != 1 || bit == binding.end()) {
+                    ok = false;
+                    break;
+                }
+                const int s = ms - 2;
+                const Box& b = p.second[0];
+                const Alloc* src = allocs_.at(std::get<2>(p.first)).get();
+                if (!contiguous_in(b, src->box) || !contiguous_in(b, bit->second->box)) {
+                    ok = false;
+                    break;
+                }
+                auto rit = roots.find(s);
+                if (rit == roots.end()) {
+                    roots[s] = {b, {d}};
+                } else {
+                    if (!(rit->second.first == b) ||
+                        std::find(rit->second.second.begin(), rit->second.second.end(), d) != rit->second.second.end()) {
+                        ok = false;
+                        break;
+                    }
+                    rit->second.second.push_back(d);
+                }
+                ++n;
+            }
+            if (!ok) break;
+        }
+        if (!ok || roots.empty()) continue;
+        uint64_t min_bytes = ~0ull;
+        for (auto& r : roots) {
+            if (int(r.second.second.size()) != G_ - 1) ok = false;
+            min_bytes = std::min<uint64_t>(min_bytes, r.second.first.volume() * bufs_.at(bid)->elem_size);
+        }
+        // small gathers (RSim's row, 84 KB per source at G = 4) are latency
+        // bound: NCCL's group launch and rendezvous cost ~1 ms per set there,
+        // against ~30 us for the peer pushes, so only sets whose
+        // every source sends >= coll_min_bytes_ qualify
+        if (ok && min_bytes >= coll_min_bytes_) out[bid] = n;
+    }
+    return out;
 }
 
 void Scheduler::compile(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant) {
@@ -727,6 +816,8 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
     }
     // R10 coherence copies; masks as they stood before this task
     std::vector<std::tuple<uint32_t, Region, int>> updates;
+    using Part = std::pair<std::tuple<int64_t, int, int64_t>, Region>;
+    std::vector<std::pair<Key, std::vector<Part>>> pend;
     for (auto& kv : c.req) {
         auto rit = c.reads.find(kv.first);
         if (rit == c.reads.end() || rit->second.empty()) continue;
@@ -739,11 +830,24 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
             if (q.second != 0 && ((q.second >> m) & 1u) == 0) need.push_back(std::move(q));
         if (need.empty()) continue;
         auto parts = source_parts_q(buf, need, m);
-        for (auto& p : parts) {
+        pend.emplace_back(kv.first, std::vector<Part>(parts.begin(), parts.end()));
+    }
+    const std::map<uint32_t, uint32_t> gathers = all_gathers(c, pend, binding);
+    std::map<uint32_t, uint64_t> group;
+    for (auto& g : gathers) group[g.first] = next_coll_++;
+    st_.gather_sets += gathers.size();
+    for (auto& pk : pend) {
+        const uint32_t bid = pk.first.second;
+        Buf& buf = *bufs_[bid];
+        auto git = group.find(bid);
+        for (auto& p : pk.second) {
             const int64_t aid = std::get<2>(p.first);
             Alloc* src = aid == HOST_AID ? buf.host.get() : allocs_.at(aid).get();
-            copy(tid, bid, REASON_COHERENCE, src, binding[kv.first], p.second, -1);
-            updates.emplace_back(bid, p.second, m);
+            if (git != group.end())
+                copy(tid, bid, REASON_COHERENCE, src, binding[pk.first], p.second, -1, git->second, gathers.at(bid));
+            else
+                copy(tid, bid, REASON_COHERENCE, src, binding[pk.first], p.second, -1);
+            updates.emplace_back(bid, p.second, 2 + pk.first.first);
         }
     }
     for (auto& u : updates) {

@@ -179,6 +179,10 @@ struct Instr {
     int src_mem = 0, dst_mem = 0;
     Region region;
     int64_t readback = -1;
+    // §8 a7: member of an all-gather copy set (not part of the instruction log):
+    // group id (0 = none) and the number of copies in the group
+    uint64_t coll = 0;
+    uint32_t coll_n = 0;
     // kernel
     int device = -1;
     Box chunk;
@@ -200,6 +204,7 @@ struct SchedStats {
     uint64_t bytes_d2d_peer = 0;
     uint64_t alloc_bytes_live = 0, alloc_bytes_peak = 0;
     uint64_t flushes = 0;
+    uint64_t gather_sets = 0;                          // coherence copy sets that are all-gathers (§8 a7)
 };
 
 class Scheduler {
@@ -281,10 +286,15 @@ private:
     uint64_t emit(Instr& ins, std::vector<uint64_t>& deps);
     Alloc* new_alloc(uint32_t bid, int mem, const Box& box, int64_t tid);
     void free_alloc(Alloc* a, int64_t tid);
-    uint64_t copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Alloc* dst, const Region& reg, int64_t rb);
+    uint64_t copy(int64_t tid, uint32_t bid, int reason, Alloc* src, Alloc* dst, const Region& reg, int64_t rb,
+                  uint64_t coll = 0, uint32_t coll_n = 0);
     std::map<std::tuple<int64_t, int, int64_t>, Region> source_parts(Buf& buf, const Region& need, int m_dst);
     std::map<std::tuple<int64_t, int, int64_t>, Region> source_parts_q(
         Buf& buf, const std::vector<std::pair<Region, uint32_t>>& need_by_mask, int m_dst);
+    std::map<uint32_t, uint32_t> all_gathers(
+        const Cmd& c,
+        const std::vector<std::pair<Key, std::vector<std::pair<std::tuple<int64_t, int, int64_t>, Region>>>>& pend,
+        const std::map<Key, Alloc*>& binding) const;
     void subsume(int64_t h);
     void log_instr(const Instr& ins);
     int prepare(const TaskDesc& d, Cmd& c, std::string* err) const;
@@ -316,6 +326,8 @@ private:
     int64_t fallback_ = 0, pending_h_ = -1;
     int64_t next_aid_ = 1;
     int64_t next_rb_ = 0;
+    uint64_t next_coll_ = 1;
+    uint64_t coll_min_bytes_ = 1ull << 20;            // CEL_COLL_MIN_BYTES: smallest per-source gather run as NCCL
     uint32_t next_bid_ = 0;
     bool shut_ = false;
 };

@@ -66,7 +66,17 @@ def main():
                     shape = tuple(mx[d] - mn[d] for d in range(3)) + (es // 4,)
                     return orig(bid, box, out=np.full(shape, GARBAGE, dtype=np.uint32))
                 rt.buffer_read = read_garbage
+                stats = {}
+
+                def keep_stats(rt=rt, close=rt.shutdown, stats=stats):
+                    if rt.h is not None:
+                        stats.update(rt.stats())
+                    close()
+                rt.shutdown = keep_stats
                 res = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
+                if rank == 0 and stats.get("gather_sets"):
+                    print("  all-gather sets %d, run as NCCL groups %d" % (stats["gather_sets"], stats["coll_groups"]),
+                          flush=True)
             else:
                 rt = cel.Runtime(world, execute=False, lookahead=mode, instr_log_path=log)
                 res = []

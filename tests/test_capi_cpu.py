@@ -101,6 +101,38 @@ def test_rsim_full_size_lookahead(cel):
     assert sum(1 for r in c if r["kind"] == "alloc") == 4 * 256
 
 
+def _gather_sets(cel, prog, G):
+    rt = cel.Runtime(G, execute=False)
+    st = {}
+
+    def keep(rt=rt, close=rt.shutdown):
+        if rt.h is not None:
+            st.update(rt.stats())
+        close()
+    rt.shutdown = keep
+    run_program(rt, prog)
+    return st["gather_sets"], st["copies_coherence"]
+
+
+def test_all_gather_detection(cel, monkeypatch):
+    """§8 a7: coherence copy sets of a buffer read through `all` / `fixed`
+    mappers, where every device receives each other device's one contiguous
+    chunk, are flagged as all-gathers; neighbourhood halos never are."""
+    monkeypatch.setenv("CEL_COLL_MIN_BYTES", "0")
+    for G in (2, 3, 4):
+        assert _gather_sets(cel, P.nbody(1000, 2), G) == (2, 2 * G * (G - 1))
+        assert _gather_sets(cel, P.rsim(1000, 8), G) == (7, 7 * G * (G - 1))
+        assert _gather_sets(cel, P.wavesim(256, 4, rows=64), G)[0] == 0
+        assert _gather_sets(cel, P.jacobi3d(16, 2), G)[0] == 0
+        assert _gather_sets(cel, P.c1_chain(64), G)[0] == 0
+    assert _gather_sets(cel, P.nbody(1000, 2), 1) == (0, 0)
+    # the default threshold (1 MiB per source) keeps small gathers on peer pushes
+    monkeypatch.delenv("CEL_COLL_MIN_BYTES")
+    assert _gather_sets(cel, P.nbody(1000, 2), 4)[0] == 0
+    assert _gather_sets(cel, P.rsim(84000, 8), 4)[0] == 0
+    assert _gather_sets(cel, P.nbody(1 << 20, 2), 4)[0] == 2
+
+
 def test_errors_and_warnings(cel):
     r = cel.Runtime(2, execute=False)
     a = r.buffer_create(1, [16], 4)

@@ -108,6 +108,26 @@ def test_rsim(cel, G, mode):
     run_both(cel, P.rsim(1000, 24), G, mode)
 
 
+def test_all_gather_collective_vs_pushes(cel, monkeypatch):
+    """§8 a7: the same programs with the all-gather copy sets run as NCCL
+    broadcasts and as peer pushes give identical bytes."""
+    monkeypatch.setenv("CEL_COLL_MIN_BYTES", "0")
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    devs = list(range(n))
+    for prog in (P.nbody(3000, 3), P.rsim(3001, 12), P.nbody(777, 2, host_init=True)):
+        for coll in (True, False):
+            rt = cel.Runtime(n, cuda_devices=devs, arena_bytes=256 << 20, collective=coll)
+            got = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
+            o = OracleRuntime(n)
+            run_program(o, prog)
+            exp = simulate(o)
+            for k, arr in enumerate(got):
+                defined = exp[k] != np.uint32(0x7FC00BAD)
+                assert np.array_equal(arr[defined], exp[k][defined]), (prog["name"], coll, k)
+
+
 @pytest.mark.parametrize("grow", [True, False])
 def test_rsim_in_place_growth(cel, grow, monkeypatch):
     """Without lookahead every RSim row resizes the allocation (alloc -> copy ->
@@ -122,15 +142,19 @@ def test_rsim_in_place_growth(cel, grow, monkeypatch):
         assert st["copies_elided"] <= st["copies_resize"]
 
 
-def test_physical_multi_gpu(cel):
+def test_physical_multi_gpu(cel, monkeypatch):
+    monkeypatch.setenv("CEL_COLL_MIN_BYTES", "0")     # small test gathers take the NCCL path too
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     devs = list(range(n))
     run_both(cel, P.wavesim(1024, 7, rows=600), n, devices=devs)
-    run_both(cel, P.nbody(2048, 2), n, devices=devs)
+    st = run_both(cel, P.nbody(2048, 2), n, devices=devs).final_stats
+    # the `all` gather of P runs as grouped NCCL broadcasts (§8 a7)
+    assert st["gather_sets"] == 2 and st["coll_groups"] == 2 and st["coll_copies"] == st["copies_coherence"]
     run_both(cel, P.jacobi3d(40, 3), n, devices=devs)
-    run_both(cel, P.rsim(2000, 16), n, "none", devices=devs)
+    st = run_both(cel, P.rsim(2000, 16), n, "none", devices=devs).final_stats
+    assert st["coll_groups"] == st["gather_sets"] > 0
     for s in range(6):
         run_both(cel, P.random_program(500 + s), n, devices=devs, arena=32 << 20)
 
