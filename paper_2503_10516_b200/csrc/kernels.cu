@@ -791,34 +791,218 @@ __global__ void nbody_update_kernel(const __grid_constant__ KArgs a) {
 }
 
 // ------------------------------------------------------------------ C4 RSim row
-__global__ void rsim_row_kernel(const __grid_constant__ KArgs a) {
+// Row t = 0.5 * row[t-1] + 0.5/t * sum_{s<t} row[s][(i+s) mod W], the sum taken
+// in ascending s with sequential adds (R16).  HBM bound: t*W*4 B per launch.
+// Each thread keeps U independent loads in flight (memory-level parallelism:
+// ~18 warps per SM at W = 84,000, so U = 16 puts ~36 KB per SM in flight).
+// Rows below `keep` are loaded with an L2 evict_last policy and the rest with
+// evict_first: every launch re-reads all earlier rows, a cyclic sweep larger
+// than L2 that plain LRU never hits; pinning a fixed prefix of rows makes that
+// prefix hit in every later launch.
+__device__ __forceinline__ float ld_policy(const float* p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Software-pipelined variant: the next group of U loads is issued before the
+// current group is summed, so 2U loads per thread stay in flight.
+template <int U>
+__global__ void rsim_row_pipe_kernel(const __grid_constant__ KArgs a) {
     const DAcc& R = a.acc[0];
     const DAcc& Wr = a.acc[1];
     const int64_t t = a.t;
     const int64_t W = R.ext[1];
+    const float* base = ptr<const float>(R, 0, 0, 0);
+    const int64_t pitch = R.n[1];
     for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
          i += int64_t(gridDim.x) * blockDim.x) {
-        // sum over s ascending (sequential adds, R16); the loads of a group of
-        // 8 rows are independent and issued together for memory parallelism
         float acc = 0.f;
-        const float* base = ptr<const float>(R, 0, 0, 0);
-        const int64_t pitch = R.n[1];
-        int64_t s = 0;
-        for (; s + 8 <= t; s += 8) {
-            float v[8];
+        const int64_t full = t / U * U;
+        float cur[U], nxt[U];
+        auto load = [&](float* v, int64_t s0) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
+            for (int k = 0; k < U; ++k) {
+                int64_t c = i + s0 + k;
+                c = c >= W ? c - W : c;
+                v[k] = __ldg(base + (s0 + k) * pitch + c);
+            }
+        };
+        if (full > 0) load(cur, 0);
+        for (int64_t s = 0; s < full; s += U) {
+            if (s + U < full) load(nxt, s + U);
+#pragma unroll
+            for (int k = 0; k < U; ++k) acc = acc + cur[k];
+#pragma unroll
+            for (int k = 0; k < U; ++k) cur[k] = nxt[k];
+        }
+        for (int64_t s = full; s < t; ++s) {
+            int64_t c = i + s;
+            c = c >= W ? c - W : c;
+            acc = acc + __ldg(base + s * pitch + c);
+        }
+        const float prev = *ptr<const float>(R, t - 1, i, 0);
+        const float coef = 0.5f / float(t);
+        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
+    }
+}
+
+// TMA-staged variant (default): a CTA owns kRC consecutive columns.  For a
+// stage of kRR rows starting at s0 it needs, from row s0+k, the kRC columns
+// starting at (i0 + s0 + k) mod W: all inside one kRR x kRB rectangle whose
+// first column is (i0 + s0) mod W rounded down to 16 bytes.  One elected
+// thread loads that rectangle with one cp.async.bulk.tensor.2d (SASS UTMALDG)
+// into a kRS-stage ring completing on mbarriers; where the rectangle would
+// cross column W it loads each row as two cp.async.bulk pieces (wrap) instead.
+// The kRC consumer threads add from shared memory in ascending s (R16).
+// ~3 stages x 9.5 KB in flight per CTA, 4-5 CTAs per SM.
+// Preconditions (host): the read allocation spans whole rows (pitch == W),
+// W % 4 == 0, W >= 2 kRB, base 16-byte aligned.
+constexpr int kRC = 128, kRR = 16, kRS = 4, kRB = kRC + kRR + 4;
+
+__global__ void __launch_bounds__(kRC) rsim_row_tma(const __grid_constant__ CUtensorMap tm,
+                                                    const __grid_constant__ KArgs a) {
+    extern __shared__ __align__(128) float rsm[];
+    __shared__ __align__(8) uint64_t rbar[kRS];
+    const DAcc& R = a.acc[0];
+    const DAcc& Wr = a.acc[1];
+    const int64_t t = a.t;
+    const int64_t W = R.ext[1];
+    const int64_t i0 = a.chunk.lo[0] + int64_t(blockIdx.x) * kRC;
+    const char* base = R.base;                       // row R.lo[0], column 0
+    const int nst = int((t + kRR - 1) / kRR);
+    if (threadIdx.x == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm)) : "memory");
+        for (int k = 0; k < kRS; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&rbar[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int g) {
+        const int st = g % kRS;
+        const int64_t s0 = int64_t(g) * kRR;
+        const int nr = int(t - s0 < kRR ? t - s0 : kRR);
+        const int64_t c0 = ((i0 + s0) % W) & ~int64_t(3);
+        const uint32_t b = smem_u32(&rbar[st]);
+        float* dst = rsm + size_t(st) * kRR * kRB;
+        if (c0 + kRB <= W) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(uint32_t(kRR * kRB * 4))
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                    smem_u32(dst)),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(int(c0)), "r"(int(s0 - R.lo[0])), "r"(b)
+                : "memory");
+        } else {
+            const uint32_t n1 = uint32_t(W - c0), n2 = uint32_t(kRB) - n1;   // floats, both multiples of 4
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(uint32_t(nr * kRB * 4))
+                         : "memory");
+            for (int k = 0; k < nr; ++k) {
+                const char* row = base + (s0 + k - R.lo[0]) * W * 4;
+                float* d = dst + k * kRB;
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_u32(d)),
+                             "l"(row + c0 * 4), "r"(n1 * 4), "r"(b)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                 smem_u32(d + n1)),
+                             "l"(row), "r"(n2 * 4), "r"(b)
+                             : "memory");
+            }
+        }
+    };
+    if (threadIdx.x == 0)
+        for (int g = 0; g < kRS - 1 && g < nst; ++g) issue(g);
+    const int j = threadIdx.x;
+    float acc = 0.f;
+    for (int g = 0; g < nst; ++g) {
+        if (threadIdx.x == 0 && g + kRS - 1 < nst) issue(g + kRS - 1);   // its stage was freed by the last barrier
+        const int st = g % kRS;
+        mbar_wait(smem_u32(&rbar[st]), uint32_t((g / kRS) & 1));
+        const int64_t s0 = int64_t(g) * kRR;
+        const int nr = int(t - s0 < kRR ? t - s0 : kRR);
+        // row k's columns start at offset r0 + k of the staged rectangle row
+        // ((i0 + s0) mod W mod 4 == (i0 + s0) mod 4 because 4 divides W)
+        const int r0 = int((i0 + s0) & 3);
+        const float* P = rsm + size_t(st) * kRR * kRB + r0 + j;
+        if (nr == kRR) {
+#pragma unroll
+            for (int k = 0; k < kRR; ++k) acc = acc + P[k * kRB + k];
+        } else {
+            for (int k = 0; k < nr; ++k) acc = acc + P[k * kRB + k];
+        }
+        __syncthreads();
+    }
+    const int64_t i = i0 + j;
+    if (i < a.chunk.hi[0]) {
+        const float prev = *ptr<const float>(R, t - 1, i, 0);
+        const float coef = 0.5f / float(t);
+        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
+    }
+}
+
+bool rsim_tensor_map(const DAcc& A, CUtensorMap* out) {
+    static EncodeFn enc = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
+    }
+    if (!enc) return false;
+    static std::map<std::tuple<const char*, int64_t, int64_t>, CUtensorMap> cache;
+    auto key = std::make_tuple(static_cast<const char*>(A.base), A.n[0], A.n[1]);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {cuuint64_t(A.n[1]), cuuint64_t(A.n[0])};
+    const cuuint64_t strides[1] = {cuuint64_t(A.n[1]) * 4};
+    const cuuint32_t box[2] = {kRB, kRR};
+    const cuuint32_t estr[2] = {1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, A.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (cache.size() > 256) cache.clear();
+    cache[key] = m;
+    *out = m;
+    return true;
+}
+
+template <int U>
+__global__ void __launch_bounds__(128) rsim_row_kernel(const __grid_constant__ KArgs a, int64_t keep) {
+    const DAcc& R = a.acc[0];
+    const DAcc& Wr = a.acc[1];
+    const int64_t t = a.t;
+    const int64_t W = R.ext[1];
+    uint64_t pol_keep, pol_stream;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const float* base = ptr<const float>(R, 0, 0, 0);
+    const int64_t pitch = R.n[1];
+    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
+         i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        int64_t s = 0;
+        for (; s + U <= t; s += U) {
+            float v[U];
+            const uint64_t pol = s + U <= keep ? pol_keep : pol_stream;
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
                 int64_t c = i + s + k;
                 c = c >= W ? c - W : c;
-                v[k] = __ldg(base + (s + k) * pitch + c);
+                v[k] = ld_policy(base + (s + k) * pitch + c, pol);
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) acc = acc + v[k];
+            for (int k = 0; k < U; ++k) acc = acc + v[k];
         }
         for (; s < t; ++s) {
             int64_t c = i + s;
             c = c >= W ? c - W : c;
-            acc = acc + __ldg(base + s * pitch + c);
+            acc = acc + ld_policy(base + s * pitch + c, s < keep ? pol_keep : pol_stream);
         }
         const float prev = *ptr<const float>(R, t - 1, i, 0);
         const float coef = 0.5f / float(t);
@@ -1031,8 +1215,55 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         return 1;
     case K_RSIM_ROW:
         if (cv == 0) return 0;
-        rsim_row_kernel<<<grid_for(cv, 128), 128, 0, s>>>(a);
+    {
+        static int unroll = 0;
+        static int64_t keep_bytes = -1;
+        if (!unroll) {
+            const char* e = getenv("CEL_RSIM_UNROLL");
+            unroll = e ? atoi(e) : 16;
+            const char* k = getenv("CEL_RSIM_KEEP_MB");
+            keep_bytes = (k ? atoll(k) : 48) << 20;
+        }
+        const int64_t row_bytes = a.acc[0].n[1] * 4;
+        const int64_t keep = row_bytes > 0 ? keep_bytes / row_bytes : 0;
+        static int variant = -1;
+        if (variant < 0) {
+            const char* e = getenv("CEL_RSIM");
+            variant = e ? atoi(e) : 5;
+        }
+        const DAcc& R0 = a.acc[0];
+        CUtensorMap tm;
+        if (variant == 5 && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
+            R0.lo[2] == 0 && R0.es == 4 && R0.ext[1] >= 2 * kRB && R0.lo[0] == 0 &&
+            (reinterpret_cast<uintptr_t>(R0.base) & 15) == 0 && a.t > 0 && rsim_tensor_map(R0, &tm)) {
+            const unsigned grid = unsigned((cv + kRC - 1) / kRC);
+            rsim_row_tma<<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a);
+            return 1;
+        }
+        if (variant == 1) {         // pipelined, 64-thread CTAs
+            rsim_row_pipe_kernel<16><<<grid_for(cv, 64), 64, 0, s>>>(a);
+            return 1;
+        }
+        if (variant == 2) {         // pipelined, 128-thread CTAs
+            rsim_row_pipe_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a);
+            return 1;
+        }
+        if (variant == 3) {         // pipelined U=8, 64-thread CTAs
+            rsim_row_pipe_kernel<8><<<grid_for(cv, 64), 64, 0, s>>>(a);
+            return 1;
+        }
+        if (variant == 4) {         // burst U=16, 64-thread CTAs
+            rsim_row_kernel<16><<<grid_for(cv, 64), 64, 0, s>>>(a, keep);
+            return 1;
+        }
+        if (unroll == 8)
+            rsim_row_kernel<8><<<grid_for(cv, 128), 128, 0, s>>>(a, keep);
+        else if (unroll == 32)
+            rsim_row_kernel<32><<<grid_for(cv, 128), 128, 0, s>>>(a, keep);
+        else
+            rsim_row_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a, keep);
         return 1;
+    }
     case K_PROBE: {
         int n = 0;
         for (int w = 0; w < a.n_acc; ++w) {
