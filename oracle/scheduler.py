@@ -17,6 +17,13 @@ Instruction log record (one dict per instruction, iid order):
   kernel  {iid, kind, task, device, chunk, bindings, deps}
   horizon {iid, kind, task, deps}
   epoch   {iid, kind, task, deps}
+Virtual-node mode (oracle/cluster.py) adds, per node:
+  send          {iid, kind, task, buffer, target, msg, src_aid, src_mem, box, deps}
+  receive       {iid, kind, task, buffer, transfer, dst_aid, dst_mem, region, deps}
+  split_receive {iid, kind, task, buffer, transfer, dst_aid, dst_mem, region, deps}
+  await_receive {iid, kind, task, buffer, transfer, region, deps}
+  transfer = [tid, buffer] (S:L261 convention); src/dst of sends and receives
+  is the node's M1 staging allocation ("coherence copy to host memory").
 Boxes are [[min0,min1,min2],[max0,max1,max2]]; regions are lists of boxes in
 R2 canonical order.
 """
@@ -165,6 +172,10 @@ class _Cmd:
         self.readback = None  # (rb_id, bid, box)
         self.destroy = []     # bids
         self.shutdown = False
+        # virtual-node mode (oracle/cluster.py): this node's transfers for the task
+        self.pushes = []      # [(target node, bid, Region)] sorted by (target, bid)
+        self.awaits = {}      # bid -> Region awaited from other nodes
+        self.remote_writes = {}   # bid -> Region written by other nodes in this task
 
 
 class Runtime:
@@ -195,6 +206,9 @@ class Runtime:
         self.counter = 0
         self.flushes = 0
         self.shut = False
+        self.node = 0                        # node id in virtual-node mode
+        self.next_msg = 0                    # P:L400 "locally unique message id"
+        self.pilots = []                     # P:L401 pilot messages of this node's sends
         # init epoch, iid 0 / tid 0 (P:L238 epochs; "the first task is an epoch")
         self.log.append({"iid": 0, "kind": "epoch", "task": 0, "deps": []})
         self.front = {0}
@@ -219,19 +233,36 @@ class Runtime:
         if self.shut:
             raise CelError(CelError.STATE, "runtime shut down")
         cmd = self._prepare(spec)          # validation + split + mappers + checks
-        status = 0
-        if self.checks:
-            for bid in sorted({b for (_, b) in cmd.reads}):
-                r = g.region_union(*[cmd.reads[k] for k in cmd.reads if k[1] == bid])
-                un = g.region_difference(r, self.tdag.initialized[bid])
-                if un:
-                    status = 1
-                    self.warnings.append(("uninitialized_read", bid, un))
         reads, writes = {}, {}
         for (d, b), r in cmd.reads.items():
             reads[b] = g.region_union(reads.get(b, ()), r)
         for (d, b), w in cmd.writes.items():
             writes[b] = g.region_union(writes.get(b, ()), w)
+        return self._submit(cmd, reads, writes)
+
+    def task_submit_node(self, spec, node_range, reads, writes, pushes, awaits, remote_writes):
+        """Virtual-node mode: this node's share of a
+        task -- its command chunk `node_range` split "a second time" over the
+        local devices -- plus the push / await-push transfers the replicated
+        command-graph generation derived for it (oracle/cluster.py).  The task
+        graph sees the whole task (`reads` / `writes` over all nodes)."""
+        if self.shut:
+            raise CelError(CelError.STATE, "runtime shut down")
+        cmd = self._prepare(spec, node_range)
+        cmd.pushes = list(pushes)
+        cmd.awaits = dict(awaits)
+        cmd.remote_writes = dict(remote_writes)
+        self._transfer_req(cmd)
+        return self._submit(cmd, reads, writes)
+
+    def _submit(self, cmd, reads, writes):
+        status = 0
+        if self.checks:
+            for bid in sorted(reads):
+                un = g.region_difference(reads[bid], self.tdag.initialized[bid])
+                if un:
+                    status = 1
+                    self.warnings.append(("uninitialized_read", bid, un))
         tid = self.tdag.submit(reads, writes)
         cmd.tid = tid
         self.tasks[tid] = cmd.spec
@@ -240,6 +271,18 @@ class Runtime:
             h = _Cmd("horizon", self.tdag.horizon())
             self._push(h)
         return tid, status
+
+    def _transfer_req(self, cmd):
+        """P:L398 / P:L417: pushed data is staged in, and awaited data received
+        into, one contiguous M1 allocation per buffer (requirement key d = -1,
+        memory 2 + d = M1), covering every transferred region of the command."""
+        boxes = {}
+        for (_, b, reg) in cmd.pushes:
+            boxes.setdefault(b, []).extend(reg)
+        for b, reg in cmd.awaits.items():
+            boxes.setdefault(b, []).extend(reg)
+        for b, bs in boxes.items():
+            cmd.req[(-1, b)] = g.bounding_box(bs)
 
     def wait(self):
         self._epoch(_Cmd("epoch"))
@@ -281,11 +324,11 @@ class Runtime:
         self.shut = True
 
     # ------------------------------------------------------------ prepare
-    def _prepare(self, spec):
+    def _prepare(self, spec, node_range=None):
         dims = spec["dims"]
         if not 1 <= dims <= 3:
             raise CelError(CelError.INVALID, "bad dims")
-        rng = g.box(spec["range"][0], spec["range"][1])
+        rng = g.box(spec["range"][0], spec["range"][1]) if node_range is None else node_range
         spec = dict(spec)
         spec["accesses"] = [(bid, mode, _norm_mapper(mp)) for (bid, mode, mp) in spec["accesses"]]
         for (bid, mode, mapper) in spec["accesses"]:
@@ -490,12 +533,13 @@ class Runtime:
                     self._free(a, None)
                 del self.bufs[bid]
 
-    def _compile_task(self, cmd, ant):
+    def _allocate(self, cmd, ant):
+        """R9 allocation (Fig. 3; resize chain alloc -> copy -> free)
+        for every requirement of the command, M1 (d = -1) first.  Returns the
+        binding (d, bid) -> allocation."""
         tid = cmd.tid
-        G = self.G
         keys = sorted(cmd.req, key=lambda k: (k[0], k[1]))     # device asc, buffer asc
         binding = {}
-        # R9 allocation (Fig. 3; resize chain alloc -> copy -> free)
         for (d, b) in keys:
             req = cmd.req[(d, b)]
             m = 2 + d
@@ -520,6 +564,94 @@ class Runtime:
                     self._copy(tid, b, "resize", a, new, reg)
                 self._free(a, tid)
             binding[(d, b)] = new
+        return binding
+
+    def _transfers(self, cmd, binding, readback_consumer=False):
+        """Virtual-node mode, §3.4 Peer-to-Peer Communication.
+        Outbound: the pushed region is made coherent in M1 ("a
+        coherence copy to host memory"), then one send per rectangle of each
+        original-producer fragment ("again subject to producer split"), each
+        with a locally unique message id and a pilot for the receiver.
+        Inbound: if every consumer reads the same part of the
+        awaited region (or there is one consumer) one receive into M1;
+        otherwise a split receive followed by one await receive per
+        consumer-split fragment (R17 [reading]: the fragments are the atoms of
+        the consumers' regions, refined device by device in ascending order)."""
+        tid = cmd.tid
+        for (target, b, reg) in cmd.pushes:
+            buf = self.bufs[b]
+            m1 = binding[(-1, b)]
+            need = g.region_difference(reg, buf.uptodate.region_where(lambda mask: (mask >> 1) & 1))
+            need = g.region_intersect(need, buf.uptodate.region_where(lambda mask: mask != 0))
+            if need:
+                parts = self._source_parts(buf, need, 1)
+                for (p, s_, aid) in sorted(parts):
+                    src = buf.host if aid == HOST_AID else self.allocs[aid]
+                    self._copy(tid, b, "coherence", src, m1, parts[(p, s_, aid)])
+                for k in sorted(parts):
+                    buf.uptodate.apply(parts[k], lambda mask: mask | 2)
+            for reg2, p in buf.orig_writer.query(reg):
+                for bx in reg2:
+                    deps = {m1.iid}
+                    deps |= {v for _, v in m1.last_writer.query((bx,)) if v >= 0}
+                    msg = self.next_msg
+                    self.next_msg += 1
+                    iid = self._emit({"kind": "send", "task": tid, "buffer": b, "target": target, "msg": msg,
+                                      "src_aid": m1.aid, "src_mem": 1, "box": _jbox(bx)}, deps)
+                    m1.readers.apply((bx,), lambda s, iid=iid: s | {iid})
+                    self.pilots.append({"sender": self.node, "msg": msg, "receiver": target,
+                                        "transfer": (tid, b), "box": bx})
+        for b in sorted(cmd.awaits):
+            reg = cmd.awaits[b]
+            buf = self.bufs[b]
+            m1 = binding[(-1, b)]
+            if readback_consumer:
+                consumers = [reg]
+            else:
+                consumers = []
+                for d in range(self.G):
+                    c = g.region_intersect(cmd.reads.get((d, b), ()), reg)
+                    if c:
+                        consumers.append(c)
+            deps = {m1.iid}
+            for _, s_ in m1.readers.query(reg):
+                deps |= s_
+            deps |= {v for _, v in m1.last_writer.query(reg) if v >= 0}
+            rec = {"task": tid, "buffer": b, "transfer": [tid, b], "dst_aid": m1.aid, "dst_mem": 1,
+                   "region": _jregion(reg)}
+            if len(set(consumers)) <= 1:
+                iid = self._emit(dict(rec, kind="receive"), deps)
+                frags = [(reg, iid)]
+            else:
+                sr = self._emit(dict(rec, kind="split_receive"), deps)
+                atoms = [reg]
+                for c in consumers:
+                    nxt = []
+                    for a in atoms:
+                        i = g.region_intersect(a, c)
+                        o = g.region_difference(a, c)
+                        if i:
+                            nxt.append(i)
+                        if o:
+                            nxt.append(o)
+                    atoms = nxt
+                frags = []
+                for a in atoms:
+                    frags.append((a, self._emit({"kind": "await_receive", "task": tid, "buffer": b,
+                                                 "transfer": [tid, b], "region": _jregion(a)}, {sr})))
+            for r, iid in frags:
+                m1.last_writer.update(r, iid)
+                m1.readers.update(r, frozenset())
+                buf.orig_writer.update(r, iid)
+            buf.uptodate.update(reg, 2)
+
+    def _compile_task(self, cmd, ant):
+        tid = cmd.tid
+        G = self.G
+        binding = self._allocate(cmd, ant)
+        keys = sorted(k for k in cmd.req if k[0] >= 0)          # device asc, buffer asc
+        if cmd.pushes or cmd.awaits:
+            self._transfers(cmd, binding)
         # R10 coherence copies (P:L371-378), masks as they stood before this task
         updates = []
         for (d, b) in keys:
@@ -580,6 +712,11 @@ class Runtime:
             if w:
                 self.bufs[b].orig_writer.update(w, kernels[d])
                 self.bufs[b].uptodate.update(w, 1 << (2 + d))
+        # virtual-node mode: what other nodes wrote in this task is stale here
+        for b in sorted(cmd.remote_writes):
+            r = cmd.remote_writes[b]
+            self.bufs[b].uptodate.update(r, 0)
+            self.bufs[b].orig_writer.update(r, NONE)
 
     def _subsume(self, h):
         """Horizon/epoch application ("limiting the set of ...
@@ -604,6 +741,9 @@ class Runtime:
         self.pending_h = h
 
     def _compile_epoch(self, cmd):
+        if cmd.pushes or cmd.awaits:          # virtual-node readback gather (oracle/cluster.py)
+            binding = self._allocate(cmd, {})
+            self._transfers(cmd, binding, readback_consumer=True)
         if cmd.readback is not None:
             rb, bid, rbox = cmd.readback
             buf = self.bufs[bid]

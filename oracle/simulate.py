@@ -44,19 +44,77 @@ def _view(arr, abox, bx):
                bx[0][2] - b[2]:bx[1][2] - b[2]]
 
 
+class _NodeState:
+    def __init__(self, rt, with_results):
+        self.rt = rt
+        self.meta = rt.buf_meta
+        self.arrays = {}
+        self.boxes = {}
+        self.host = {}
+        for bid, m in self.meta.items():
+            if m["host_init"] is not None:
+                self.host[bid] = host_array(m["host_init"], m["extent"], m["elem_size"])
+        self.results = {}
+        if with_results:
+            for rb, (bid, rbox) in rt.readbacks.items():
+                self.results[rb] = np.full(g.shape(rbox) + (_words(self.meta[bid]["elem_size"]),), GARBAGE,
+                                           dtype=np.uint32)
+        self.split = {}          # transfer -> dst aid of its split receive
+
+
 def simulate(rt):
     """Run rt.log over arrays.  Returns {readback id: uint32 array}."""
-    meta = rt.buf_meta
-    arrays = {}
-    boxes = {}
-    host = {}
-    for bid, m in meta.items():
-        if m["host_init"] is not None:
-            host[bid] = host_array(m["host_init"], m["extent"], m["elem_size"])
-    results = {}
-    for rb, (bid, rbox) in rt.readbacks.items():
-        results[rb] = np.full(g.shape(rbox) + (_words(meta[bid]["elem_size"]),), GARBAGE, dtype=np.uint32)
+    st = _NodeState(rt, True)
     for rec in rt.log:
+        _step(st, rec)
+    return st.results
+
+
+def simulate_cluster(cl):
+    """Virtual-node mode (oracle/cluster.py): run every node's log; a send
+    publishes its box's bytes under (sender, message id); a receive / await
+    receive takes the bytes of every pilot addressed to it (P:L534-544 receive
+    arbitration: placement by the pilot's box) once they have been sent.  The
+    nodes advance round-robin, each until it reaches a receive whose data is
+    not yet sent.  Returns node 0's readbacks."""
+    states = [_NodeState(rt, n == 0) for n, rt in enumerate(cl.nodes)]
+    pilots = cl.pilots()
+    sent = {}
+    pcs = [0] * len(states)
+    while True:
+        progress = False
+        for n, st in enumerate(states):
+            log = st.rt.log
+            while pcs[n] < len(log):
+                rec = log[pcs[n]]
+                if rec["kind"] in ("receive", "await_receive"):
+                    tr = tuple(rec["transfer"])
+                    reg = [_tobox(jb) for jb in rec["region"]]
+                    mine = [p for p in pilots if p["receiver"] == n and tuple(p["transfer"]) == tr and
+                            g.region_intersect((p["box"],), tuple(reg))]
+                    if any((p["sender"], p["msg"]) not in sent for p in mine):
+                        break
+                    aid = rec["dst_aid"] if rec["kind"] == "receive" else st.split[tr]
+                    for p in mine:
+                        _view(st.arrays[aid], st.boxes[aid], p["box"])[...] = sent[(p["sender"], p["msg"])]
+                elif rec["kind"] == "send":
+                    bx = _tobox(rec["box"])
+                    sent[(n, rec["msg"])] = _view(st.arrays[rec["src_aid"]], st.boxes[rec["src_aid"]], bx).copy()
+                elif rec["kind"] == "split_receive":
+                    st.split[tuple(rec["transfer"])] = rec["dst_aid"]
+                else:
+                    _step(st, rec)
+                pcs[n] += 1
+                progress = True
+        if all(pcs[n] == len(st.rt.log) for n, st in enumerate(states)):
+            return states[0].results
+        if not progress:
+            raise AssertionError("virtual-node simulation deadlocked at %s" % pcs)
+
+
+def _step(st, rec):
+    rt, meta, arrays, boxes, host, results = st.rt, st.meta, st.arrays, st.boxes, st.host, st.results
+    if True:
         k = rec["kind"]
         if k == "alloc":
             bx = _tobox(rec["box"])
@@ -87,7 +145,6 @@ def simulate(rt):
                 bxs.append(apply_mapper(mapper, chunk, ext))
                 accs.append(Acc(arrays[aid], boxes[aid], ext) if aid > 0 else None)
             run_kernel(spec, bxs, accs)
-    return results
 
 
 def sequential(program):
