@@ -148,6 +148,15 @@ typedef struct {
                                   devices are distinct GPUs; 0: as peer pushes.  The instruction graph
                                   is the same either way.  NCCL (libnccl.so.2) is opened at run time;
                                   a failed communicator setup is CEL_E_NCCL (sticky). */
+    int32_t n_nodes;           /* virtual-node mode (§3.4, §4.2): > 1 runs
+                                  n_nodes node schedulers of n_devices devices each in this process;
+                                  cuda_devices then lists n_nodes * n_devices entries (node-major).
+                                  Nodes exchange data only through push / await-push commands lowered
+                                  to send, receive, split receive and await receive instructions
+                                  staged in pinned host memory (M1), with pilot messages and receive
+                                  arbitration.  Node k's instruction log goes to
+                                  "<instr_log_path>.<k>"; readbacks gather on node 0.
+                                  0 or 1 = one node (the default). */
 } cel_config;
 
 typedef struct {
@@ -165,6 +174,8 @@ typedef struct {
     uint64_t copies_elided, bytes_elided; /* resize copies made no-ops by in-place allocation growth */
     uint64_t coll_groups, coll_copies;    /* all-gather copy sets run as NCCL collectives, and their copies */
     uint64_t gather_sets;                 /* coherence copy sets the scheduler found to be all-gathers */
+    uint64_t n_send, n_receive, n_split_receive, n_await_receive;   /* virtual-node mode (n_nodes > 1) */
+    uint64_t pulls, pull_bytes;           /* virtual-node mode: pilot-matched transfers executed, bytes */
 } cel_stats;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

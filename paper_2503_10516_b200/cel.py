@@ -69,7 +69,8 @@ class cel_config(C.Structure):
     _fields_ = [("cuda_devices", C.POINTER(C.c_int)), ("n_devices", C.c_int32), ("execute", C.c_int32),
                 ("lookahead", C.c_int32), ("horizon_step", C.c_int32), ("checks", C.c_int32),
                 ("instr_log_path", C.c_char_p), ("arena_bytes", C.c_uint64), ("rank", C.c_int32),
-                ("world", C.c_int32), ("fast_math", C.c_int32), ("collective", C.c_int32)]
+                ("world", C.c_int32), ("fast_math", C.c_int32), ("collective", C.c_int32),
+                ("n_nodes", C.c_int32)]
 
 
 class cel_stats(C.Structure):
@@ -81,7 +82,7 @@ class cel_stats(C.Structure):
         "event_waits", "remote_waits", "signals", "host_syncs", "gen_ns",
         "exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon", "exec_ns_epoch",
         "signal_ns", "remote_wait_ns", "copies_elided", "bytes_elided", "coll_groups", "coll_copies",
-        "gather_sets")]
+        "gather_sets", "n_send", "n_receive", "n_split_receive", "n_await_receive", "pulls", "pull_bytes")]
 
 
 _P = C.c_void_p
@@ -173,9 +174,12 @@ class Runtime:
     """The C-ABI runtime.  Method names follow include/cel.h (cel_ prefix dropped)."""
 
     def __init__(self, n_devices, cuda_devices=None, execute=True, lookahead="auto", horizon_step=4, checks=True,
-                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False, collective=True):
+                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False, collective=True, n_nodes=1):
+        """n_nodes > 1: virtual-node mode, n_nodes nodes of n_devices devices each
+        (cuda_devices lists n_nodes * n_devices entries, node-major); node k's
+        instruction log is written to instr_log_path + ".k"."""
         cfg = cel_config()
-        devs = list(cuda_devices) if cuda_devices is not None else list(range(n_devices))
+        devs = list(cuda_devices) if cuda_devices is not None else list(range(n_devices * max(1, n_nodes)))
         self._devs = (C.c_int * len(devs))(*devs)
         cfg.cuda_devices = self._devs
         cfg.n_devices = n_devices
@@ -189,6 +193,7 @@ class Runtime:
         cfg.world = world
         cfg.fast_math = 1 if fast_math else 0
         cfg.collective = 1 if collective else 0
+        cfg.n_nodes = int(n_nodes)
         h = _P()
         _check(lib.cel_runtime_create(C.byref(cfg), C.byref(h)))
         self.h = h

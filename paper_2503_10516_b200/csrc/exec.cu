@@ -192,6 +192,8 @@ Executor::~Executor() {
     }
     for (auto& kv : host_init_)
         if (kv.second.second) cudaFreeHost(kv.second.first);
+    if (host_arena_.base) cudaFreeHost(host_arena_.base);
+    if (vflags_) cudaFree(vflags_);
 }
 
 void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
@@ -309,9 +311,36 @@ int Executor::init(std::string* err) {
             }
         }
     }
+    if (cfg_.comm) {
+        // virtual-node mode: M1 staging arena (pinned, mapped: copy kernels and
+        // the communicator's pulls address it directly) and the flags sends and
+        // receives wait on (device memory of the node's first GPU)
+        g_drv.load();
+        if (!g_drv.wait64 || !g_drv.write64) {
+            *err = "virtual-node mode needs stream memory operations";
+            return E_CUDA;
+        }
+        void* h = nullptr;
+        if (cudaHostAlloc(&h, cfg_.host_arena_bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            *err = "cannot allocate the M1 staging arena";
+            return E_OOM;
+        }
+        host_arena_.base = static_cast<char*>(h);
+        host_arena_.size = cfg_.host_arena_bytes;
+        host_arena_.free_[0] = FreeRange{cfg_.host_arena_bytes, Token{}};
+        set_dev(0);
+        if (cudaMalloc(&vflags_, 2 * kRing * sizeof(uint64_t)) != cudaSuccess) {
+            cudaGetLastError();
+            *err = "cannot allocate transfer flags";
+            return E_OOM;
+        }
+        cudaMemset(vflags_, 0, 2 * kRing * sizeof(uint64_t));
+        cfg_.comm->attach(cfg_.node, phys_[0]);
+    }
     cudaDeviceSynchronize();
     const char* et = getenv("CEL_EXEC_THREAD");
-    if (!(et && et[0] == '0')) {
+    if (cfg_.comm || !(et && et[0] == '0')) {   // nodes must progress independently
         threaded_ = true;
         thr_ = std::thread([this] { thread_main(); });
     }
@@ -582,11 +611,11 @@ int Executor::instr_owner(const Instr& ins) const {
     switch (ins.kind) {
     case IKind::Alloc:
     case IKind::Free:
-        return ins.mem - 2;
+        return ins.mem >= 2 ? ins.mem - 2 : -1;
     case IKind::Kernel:
         return ins.device;
     case IKind::Copy:
-        return ins.src_mem >= 2 ? ins.src_mem - 2 : ins.dst_mem - 2;   // push model: the producer's GPU
+        return ins.src_mem >= 2 ? ins.src_mem - 2 : (ins.dst_mem >= 2 ? ins.dst_mem - 2 : -1);   // push model: the producer's GPU
     default:
         return -1;
     }
@@ -640,7 +669,7 @@ char* Executor::alloc_ptr(int64_t aid) {
     auto it = allocs_.find(aid);
     if (it == allocs_.end()) return nullptr;
     const AllocRec& r = it->second;
-    return arenas_[r.dev].base + r.off;
+    return base_of(r);
 }
 
 // ------------------------------------------------------------ dispatch
@@ -832,7 +861,7 @@ void Executor::on_instr_impl(const Instr& ins) {
                 break;
             }
         }
-        if (grow && arenas_[dev].extend(grow->off, grow->bytes, bytes, &t)) {
+        if (grow && arena(dev).extend(grow->off, grow->bytes, bytes, &t)) {
             // the grown allocation's users write memory the old one's readers
             // may still read: follow every local use of the old allocation
             // (remote ranks only write it, and those writes reach the new
@@ -840,7 +869,7 @@ void Executor::on_instr_impl(const Instr& ins) {
             off = grow->off;
             grow->absorbed_into = ins.aid;
             if (mine) merge(t, grow->use);
-        } else if (!arenas_[dev].alloc(bytes, &off, &t)) {
+        } else if (!arena(dev).alloc(bytes, &off, &t)) {
             char buf[200];
             snprintf(buf, sizeof buf, "device %d arena exhausted allocating %.3f GiB", dev, double(bytes) / (1ull << 30));
             errmsg_ = buf;
@@ -877,7 +906,7 @@ void Executor::on_instr_impl(const Instr& ins) {
         } else {
             t.remote.push_back({owner_rank(r.dev), ins.iid});
         }
-        if (!r.absorbed_into) arenas_[r.dev].release(r.off, r.bytes, t);   // else: lives on in the grown one
+        if (!r.absorbed_into) arena(r.dev).release(r.off, r.bytes, t);   // else: lives on in the grown one
         tok_[ins.iid] = t;
         live_alloc_iid_.erase(r.iid);
         allocs_.erase(it);
@@ -932,6 +961,12 @@ void Executor::on_instr_impl(const Instr& ins) {
     case IKind::Epoch:
         exec_epoch(ins);
         return;
+    case IKind::Send:
+    case IKind::Receive:
+    case IKind::SplitReceive:
+    case IKind::AwaitReceive:
+        exec_transfer(ins);
+        break;
     }
     if (grown_) note_use(ins);
     if (++since_poll_ >= 64) {
@@ -1114,6 +1149,288 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
     st_.bytes_copy[2] += bytes_total;   // NCCL's kernels are library launches: not in kernel_launches
 }
 
+
+// ------------------------------------------------------------ virtual-node communicator
+namespace {
+// one box of a row-major allocation copied into another: a copy-kernel segment
+void box_seg(CopyArgs& args, const char* sb, const Box& S, char* db, const Box& D, const Box& b, uint32_t es) {
+    const int64_t sn1 = S.extent(1), sn2 = S.extent(2), dn1 = D.extent(1), dn2 = D.extent(2);
+    CopySeg g;
+    const int64_t so = ((b.lo[0] - S.lo[0]) * sn1 + (b.lo[1] - S.lo[1])) * sn2 + (b.lo[2] - S.lo[2]);
+    const int64_t dof = ((b.lo[0] - D.lo[0]) * dn1 + (b.lo[1] - D.lo[1])) * dn2 + (b.lo[2] - D.lo[2]);
+    g.src = sb + so * es;
+    g.dst = db + dof * es;
+    g.row_bytes = uint64_t(b.extent(2)) * es;
+    g.rows = uint32_t(b.extent(1));
+    g.planes = uint32_t(b.extent(0));
+    g.src_row_stride = uint64_t(sn2) * es;
+    g.dst_row_stride = uint64_t(dn2) * es;
+    g.src_plane_stride = uint64_t(sn1 * sn2) * es;
+    g.dst_plane_stride = uint64_t(dn1 * dn2) * es;
+    if (g.row_bytes == g.src_row_stride && g.row_bytes == g.dst_row_stride) {
+        g.row_bytes *= g.rows;
+        g.rows = 1;
+        if (g.row_bytes == g.src_plane_stride && g.row_bytes == g.dst_plane_stride) {
+            g.row_bytes *= g.planes;
+            g.planes = 1;
+        }
+    }
+    uint64_t a = uintptr_t(g.src) | uintptr_t(g.dst) | g.row_bytes;
+    if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
+    if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
+    g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
+    g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
+    g.units_begin = args.total_units;
+    args.seg[args.nseg++] = g;
+    args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
+}
+}  // namespace
+
+Communicator::Communicator(int nodes) : nodes_(nodes), phys_(nodes, -1), stream_(nodes, nullptr) {}
+
+Communicator::~Communicator() {
+    for (int n = 0; n < nodes_; ++n)
+        if (stream_[n]) {
+            cudaSetDevice(phys_[n]);
+            cudaStreamSynchronize(stream_[n]);
+            cudaStreamDestroy(stream_[n]);
+        }
+}
+
+void Communicator::attach(int node, int phys_dev) {
+    std::lock_guard<std::mutex> l(m_);
+    phys_[node] = phys_dev;
+    cudaSetDevice(phys_dev);
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&stream_[node], cudaStreamNonBlocking, hi);
+    // pulls write the peer's completion flags: peer access between the nodes' GPUs
+    for (int k = 0; k < nodes_; ++k) {
+        if (k == node || phys_[k] < 0 || phys_[k] == phys_dev) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, phys_dev, phys_[k]);
+        if (can && cudaDeviceEnablePeerAccess(phys_[k], 0) == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        cudaSetDevice(phys_[k]);
+        cudaDeviceCanAccessPeer(&can, phys_[k], phys_dev);
+        if (can && cudaDeviceEnablePeerAccess(phys_dev, 0) == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        cudaSetDevice(phys_dev);
+    }
+}
+
+void Communicator::add_pilots(const std::vector<Pilot>& ps) {
+    std::lock_guard<std::mutex> l(m_);
+    std::vector<Key> touched;
+    for (const Pilot& p : ps) {
+        const Key k{p.receiver, p.transfer, p.buffer};
+        recv_[k].pilots.push_back(PilotRec{p.sender, p.msg, p.box});
+        pilot_key_[{p.sender, p.msg}] = k;
+        touched.push_back(k);
+    }
+    for (const Key& k : touched) try_pulls(k);
+}
+
+void Communicator::post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready, uint64_t* done,
+                             uint64_t done_val) {
+    std::lock_guard<std::mutex> l(m_);
+    sends_[{node, msg}] = Send{src, ready, done, done_val};
+    auto it = pilot_key_.find({node, msg});
+    if (it != pilot_key_.end()) try_pulls(it->second);
+}
+
+void Communicator::post_dest(int node, int64_t tid, uint32_t buf, const Mem& dst, cudaEvent_t dst_ready) {
+    std::lock_guard<std::mutex> l(m_);
+    const Key k{node, tid, buf};
+    Recv& r = recv_[k];
+    r.has_dest = true;
+    r.dst = dst;
+    r.dst_ready = dst_ready;
+    try_pulls(k);
+}
+
+void Communicator::post_frag(int node, int64_t tid, uint32_t buf, const Region& reg, uint64_t* counter,
+                             uint64_t base, uint64_t* target, cudaEvent_t* after) {
+    std::lock_guard<std::mutex> l(m_);
+    const Key k{node, tid, buf};
+    Recv& r = recv_[k];
+    // pulls already issued: covered by an event on the communication stream;
+    // later pulls raise the counter
+    uint64_t done = 0;
+    for (const Box& b : r.issued) done += rvolume(rinter(Region{b}, reg));
+    *after = nullptr;
+    if (done) {
+        cudaSetDevice(phys_[node]);
+        cudaEventCreateWithFlags(after, cudaEventDisableTiming);
+        cudaEventRecord(*after, stream_[node]);
+    }
+    *target = base + (rvolume(reg) - done);
+    r.frags.push_back(Frag{reg, counter, base, 0});
+}
+
+void Communicator::try_pulls(const Key& k) {
+    auto rit = recv_.find(k);
+    if (rit == recv_.end() || !rit->second.has_dest) return;
+    Recv& r = rit->second;
+    for (PilotRec& p : r.pilots) {
+        if (p.issued) continue;
+        auto sit = sends_.find({p.sender, p.msg});
+        if (sit == sends_.end()) continue;
+        pull(k, r, p, sit->second);
+        if (sit->second.ready) cudaEventDestroy(sit->second.ready);
+        sends_.erase(sit);
+    }
+}
+
+void Communicator::pull(const Key& k, Recv& r, PilotRec& p, Send& snd) {
+    const int node = std::get<0>(k);
+    cudaSetDevice(phys_[node]);
+    cudaStream_t st = stream_[node];
+    cudaStreamWaitEvent(st, snd.ready, 0);                    // the sender's staged data
+    if (r.dst_ready) cudaStreamWaitEvent(st, r.dst_ready, 0); // the receive's own dependencies
+    CopyArgs args;
+    args.nseg = 0;
+    args.total_units = 0;
+    args.peer = 0;
+    box_seg(args, snd.src.base, snd.src.box, r.dst.base, r.dst.box, p.box, r.dst.es);
+    launch_copy(args, st);
+    for (Frag& f : r.frags) {
+        const uint64_t v = rvolume(rinter(Region{p.box}, f.reg));
+        if (!v) continue;
+        f.cum += v;
+        g_drv.write64(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(f.counter), f.base + f.cum,
+                      CU_STREAM_WRITE_VALUE_DEFAULT);
+    }
+    g_drv.write64(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(snd.done), snd.done_val,
+                  CU_STREAM_WRITE_VALUE_DEFAULT);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess && !err_) {
+        err_ = E_CUDA;
+        errmsg_ = std::string("receive arbitration: ") + cudaGetErrorString(e);
+    }
+    p.issued = true;
+    r.issued.push_back(p.box);
+    pulls_++;
+    pull_bytes_ += uint64_t(p.box.volume()) * r.dst.es;
+}
+
+// Send / receive / split receive / await receive (virtual-node mode, Table 1).
+void Executor::exec_transfer(const Instr& ins) {
+    Communicator& comm = *cfg_.comm;
+    const Token deps = local_part(ins.deps);
+    const uint32_t es = bufinfo_.at(ins.buffer).es;
+    set_dev(0);
+    const int s_sync = S_SYNC, s_send = S_HSIG, s_recv = S_SIG0;   // device 0 of the node
+    auto mem = [&](int64_t aid) {
+        const AllocRec& a = allocs_.at(aid);
+        return Communicator::Mem{base_of(a), a.box, es};
+    };
+    auto ready_event = [&]() {          // an event after the instruction's dependencies
+        wait_token(s_sync, deps);
+        cudaEvent_t e = nullptr;
+        check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventRecord(e, streams_[s_sync].s), "cudaEventRecord");
+        return e;
+    };
+    auto wait_frag = [&](const Region& reg) {
+        const uint64_t slot = kRing + (frag_seq_ % kRing);
+        const uint64_t base = (++frag_seq_) << 32;
+        uint64_t target = 0;
+        cudaEvent_t after = nullptr;
+        comm.post_frag(cfg_.node, ins.transfer, ins.buffer, reg, vflags_ + slot, base, &target, &after);
+        if (after) {
+            check(cudaStreamWaitEvent(streams_[s_recv].s, after, 0), "cudaStreamWaitEvent");
+            cudaEventDestroy(after);
+        }
+        if (target > base)
+            checkd(g_drv.wait64(reinterpret_cast<CUstream>(streams_[s_recv].s),
+                                reinterpret_cast<CUdeviceptr>(vflags_ + slot), target, CU_STREAM_WAIT_VALUE_GEQ),
+                   "cuStreamWaitValue64");
+        return record(s_recv);
+    };
+    switch (ins.kind) {
+    case IKind::Send: {
+        const cudaEvent_t ready = ready_event();
+        const uint64_t slot = send_seq_ % kRing;
+        const uint64_t val = ++send_seq_;
+        comm.post_send(cfg_.node, ins.msg, mem(ins.src_aid), ready, vflags_ + slot, val);
+        // complete once the receiver has pulled the box (the staging copy may then be reused)
+        checkd(g_drv.wait64(reinterpret_cast<CUstream>(streams_[s_send].s),
+                            reinterpret_cast<CUdeviceptr>(vflags_ + slot), val, CU_STREAM_WAIT_VALUE_GEQ),
+               "cuStreamWaitValue64");
+        tok_[ins.iid] = record(s_send);
+        st_.bytes_copy[5] += uint64_t(ins.box.volume()) * es;
+        break;
+    }
+    case IKind::Receive:
+        comm.post_dest(cfg_.node, ins.transfer, ins.buffer, mem(ins.dst_aid), ready_event());
+        tok_[ins.iid] = wait_frag(ins.region);
+        break;
+    case IKind::SplitReceive:
+        comm.post_dest(cfg_.node, ins.transfer, ins.buffer, mem(ins.dst_aid), ready_event());
+        tok_[ins.iid] = deps;
+        break;
+    case IKind::AwaitReceive:
+        tok_[ins.iid] = wait_frag(ins.region);
+        break;
+    default:
+        break;
+    }
+    if (comm.error() && !err_) {
+        errmsg_ = comm.error_msg();
+        err_ = comm.error();
+    }
+}
+
+// Copies between host-side memories (M0 host data / user pointer and the M1
+// staging arena): plain host copies once the dependencies have completed.
+void Executor::exec_host_copy(const Instr& ins, const Token& deps) {
+    const uint32_t es = bufinfo_.at(ins.buffer).es;
+    for (const TokEntry& e : deps.local)
+        if (e.seq > streams_[e.stream].done) check(cudaEventSynchronize(e.ev), "host copy wait");
+    const char* sb;
+    Box sbox;
+    if (ins.src_mem == 1) {
+        const AllocRec& S = allocs_.at(ins.src_aid);
+        sb = base_of(S);
+        sbox = S.box;
+    } else {
+        auto hi = host_init_.find(ins.buffer);
+        if (hi == host_init_.end()) {
+            errmsg_ = "host copy of a buffer without host data";
+            err_ = E_STATE;
+            return;
+        }
+        sb = hi->second.first;
+        sbox = bufinfo_.at(ins.buffer).extent;
+    }
+    char* db;
+    Box dbox;
+    if (ins.dst_aid == USER_AID) {
+        auto rb = readbacks_.find(ins.readback);
+        if (rb == readbacks_.end()) {
+            errmsg_ = "readback copy without a destination";
+            err_ = E_STATE;
+            return;
+        }
+        db = rb->second.dst;
+        dbox = rb->second.box;
+    } else {
+        const AllocRec& D = allocs_.at(ins.dst_aid);
+        db = base_of(D);
+        dbox = D.box;
+    }
+    for (const Box& b : ins.region)
+        for (int64_t z = b.lo[0]; z < b.hi[0]; ++z)
+            for (int64_t y = b.lo[1]; y < b.hi[1]; ++y) {
+                const int64_t so = ((z - sbox.lo[0]) * sbox.extent(1) + (y - sbox.lo[1])) * sbox.extent(2) +
+                                   (b.lo[2] - sbox.lo[2]);
+                const int64_t dof = ((z - dbox.lo[0]) * dbox.extent(1) + (y - dbox.lo[1])) * dbox.extent(2) +
+                                    (b.lo[2] - dbox.lo[2]);
+                memcpy(db + dof * es, sb + so * es, size_t(b.extent(2)) * es);
+            }
+    st_.bytes_copy[5] += rvolume(ins.region) * es;
+    tok_[ins.iid] = Token{};
+}
+
 void Executor::exec_copy(const Instr& ins) {
     const uint32_t es = bufinfo_.at(ins.buffer).es;
     Token deps;
@@ -1134,7 +1451,9 @@ void Executor::exec_copy(const Instr& ins) {
         }
         merge(deps, dep_token(j));
     }
-    if (ins.src_mem >= 2 && ins.dst_mem >= 2) {
+    if (ins.src_mem >= 1 && ins.dst_mem >= 1) {
+        // allocation to allocation: device memories, or the pinned + mapped M1
+        // staging arena of virtual-node mode on either side (copy kernel)
         const AllocRec& S = allocs_.at(ins.src_aid);
         const AllocRec& D = allocs_.at(ins.dst_aid);
         if (S.dev == D.dev && S.off == D.off && S.box.lo[0] == D.box.lo[0] && S.box.lo[1] == D.box.lo[1] &&
@@ -1145,17 +1464,17 @@ void Executor::exec_copy(const Instr& ins) {
             tok_[ins.iid] = deps;
             return;
         }
-        const int dev = S.dev;
-        const bool peer = S.dev != D.dev;
+        const int dev = S.dev >= 0 ? S.dev : (D.dev >= 0 ? D.dev : 0);
+        const bool peer = S.dev >= 0 && D.dev >= 0 && S.dev != D.dev;
         const int sidx = dev * kStreamsPerDev + (peer ? S_PUSH : S_COPY);
         set_dev(dev);
         wait_token(sidx, deps);
-        const char* sb = arenas_[S.dev].base + S.off;
-        char* db = arenas_[D.dev].base + D.off;
+        const char* sb = base_of(S);
+        char* db = base_of(D);
         CopyArgs args;
         args.nseg = 0;
         args.total_units = 0;
-        args.peer = phys_[S.dev] != phys_[D.dev] ? 1 : 0;
+        args.peer = peer && phys_[S.dev] != phys_[D.dev] ? 1 : 0;
         const int64_t sn1 = S.box.extent(1), sn2 = S.box.extent(2);
         const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
         uint64_t bytes = 0;
@@ -1216,6 +1535,10 @@ void Executor::exec_copy(const Instr& ins) {
     // host <-> device: DMA (cudaMemcpy3DAsync per box)
     const bool h2d = ins.src_mem == 0 && ins.dst_mem >= 2;
     const bool d2h = ins.src_mem >= 2 && ins.dst_aid == USER_AID;
+    if (!h2d && !d2h && (ins.src_mem == 1 || ins.dst_mem == 1)) {
+        exec_host_copy(ins, deps);           // M1 <-> M0 / user pointer (virtual-node mode)
+        return;
+    }
     if (!h2d && !d2h) {
         // host implicit allocation -> user pointer: plain host copy
         auto hi = host_init_.find(ins.buffer);

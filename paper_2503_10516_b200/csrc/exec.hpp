@@ -21,8 +21,10 @@
 #include <deque>
 #include <functional>
 #include <mutex>
+#include <tuple>
 #include <thread>
 #include <map>
+#include <memory>
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
@@ -47,6 +49,81 @@ struct Token {
     bool empty() const { return local.empty() && remote.empty(); }
 };
 
+// Virtual-node mode: the "communicator" between the node
+// executors of one process.  Sends publish their staged M1 box;
+// receives and await receives register their destination and fragments;
+// pilots arrive from the schedulers at compile time.  Receive
+// arbitration: as soon as a pilot's send has been issued and its transfer's
+// destination is known, the box is pulled into the receiver's M1 allocation by
+// a copy kernel on the receiver's communication stream; the pull then raises
+// the fragment counters the receiver's await-receive waits on (GPU stream
+// memory operations: completion is "as soon as its subregion or a superset
+// thereof has been received") and the sender's completion flag (its
+// staging buffer may be reused).
+class Communicator {
+public:
+    struct Mem {
+        char* base = nullptr;   // device-accessible (pinned + mapped host) allocation base
+        Box box;                // allocation box, row-major
+        uint32_t es = 0;
+    };
+    explicit Communicator(int nodes);
+    ~Communicator();
+    void attach(int node, int phys_dev);
+    void add_pilots(const std::vector<Pilot>& p);
+    void post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready, uint64_t* done, uint64_t done_val);
+    // destination of transfer (tid, buf) on `node`; writes start after `dst_ready`
+    void post_dest(int node, int64_t tid, uint32_t buf, const Mem& dst, cudaEvent_t dst_ready);
+    // a fragment the receiver waits on: counter >= *target, after *after (null if none)
+    void post_frag(int node, int64_t tid, uint32_t buf, const Region& reg, uint64_t* counter, uint64_t base,
+                   uint64_t* target, cudaEvent_t* after);
+    int error() const { return err_; }
+    const std::string& error_msg() const { return errmsg_; }
+    uint64_t pulls() const { return pulls_; }
+    uint64_t pull_bytes() const { return pull_bytes_; }
+
+private:
+    using Key = std::tuple<int, int64_t, uint32_t>;     // (receiver, tid, buffer)
+    struct PilotRec {
+        int sender;
+        uint64_t msg;
+        Box box;
+        bool issued = false;
+    };
+    struct Frag {
+        Region reg;
+        uint64_t* counter;
+        uint64_t base;
+        uint64_t cum = 0;
+    };
+    struct Recv {
+        bool has_dest = false;
+        Mem dst;
+        cudaEvent_t dst_ready = nullptr;
+        std::vector<PilotRec> pilots;
+        std::vector<Frag> frags;
+        std::vector<Box> issued;
+    };
+    struct Send {
+        Mem src;
+        cudaEvent_t ready = nullptr;
+        uint64_t* done = nullptr;
+        uint64_t done_val = 0;
+    };
+    void try_pulls(const Key& k);
+    void pull(const Key& k, Recv& r, PilotRec& p, Send& snd);
+    std::mutex m_;
+    int nodes_;
+    std::vector<int> phys_;
+    std::vector<cudaStream_t> stream_;                     // per receiving node
+    std::map<Key, Recv> recv_;
+    std::map<std::pair<int, uint64_t>, Send> sends_;       // (sender, msg)
+    std::map<std::pair<int, uint64_t>, Key> pilot_key_;    // (sender, msg) -> transfer
+    int err_ = 0;
+    std::string errmsg_;
+    uint64_t pulls_ = 0, pull_bytes_ = 0;
+};
+
 struct ExecConfig {
     std::vector<int> cuda_devices;     // physical device of each virtual device
     int rank = 0, world = 1;           // world > 1: device d is owned by rank d
@@ -54,6 +131,9 @@ struct ExecConfig {
     bool profile = false;
     bool fast_math = false;
     bool collective = true;            // run all-gather copy sets as grouped NCCL broadcasts (§8 a7)
+    int node = 0;                      // virtual-node mode: this executor's node
+    std::shared_ptr<Communicator> comm;
+    uint64_t host_arena_bytes = 256ull << 20;   // M1 (pinned, mapped) staging arena, virtual-node mode
 };
 
 struct ExecStats {
@@ -66,7 +146,7 @@ struct ExecStats {
     uint64_t copies_elided = 0, bytes_elided = 0;   // resize copies made no-ops by in-place growth
     uint64_t coll_groups = 0, coll_copies = 0;      // all-gather copy sets run as NCCL collectives
     uint64_t host_syncs = 0;
-    uint64_t exec_ns[6] = {};          // host time in on_instr per instruction kind (IKind order)
+    uint64_t exec_ns[kNumIKinds] = {}; // host time in on_instr per instruction kind (IKind order)
     uint64_t signal_ns = 0, remote_wait_ns = 0;
 };
 
@@ -208,6 +288,10 @@ private:
     void throttle();
     void prune_tokens(uint64_t below);
     void note_use(const Instr& ins);
+    void exec_transfer(const Instr& ins);
+    void exec_host_copy(const Instr& ins, const Token& deps);
+    Arena& arena(int dev) { return dev < 0 ? host_arena_ : arenas_[dev]; }
+    char* base_of(const AllocRec& r) { return (r.dev < 0 ? host_arena_.base : arenas_[r.dev].base) + r.off; }
     void exec_coll(const std::vector<Instr>& members);
     bool coll_init();
     Token materialize(int dev, const Token& t);
@@ -280,6 +364,10 @@ private:
     unsigned char nccl_id_[128] = {};
     bool nccl_id_set_ = false;
     std::unordered_map<uint64_t, std::vector<Instr>> coll_pending_;
+    // virtual-node mode: M1 staging arena and the flags sends / receives wait on
+    Arena host_arena_;
+    uint64_t* vflags_ = nullptr;                  // [0, kRing) send done flags, [kRing, 2 kRing) fragment counters
+    uint64_t send_seq_ = 0, frag_seq_ = 0;
     std::unordered_map<uint64_t, Parts> parts_;
     static constexpr uint64_t kRing = 1u << 16;
 };

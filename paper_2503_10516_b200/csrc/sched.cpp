@@ -253,7 +253,7 @@ int64_t Scheduler::tdag_epoch() {
 }
 
 // ------------------------------------------------------------ submit
-int Scheduler::prepare(const TaskDesc& d, Cmd& c, std::string* err) const {
+int Scheduler::prepare(const TaskDesc& d, Cmd& c, std::string* err, const Box* node_range) const {
     if (d.dims < 1 || d.dims > 3) {
         if (err) *err = "task dims must be 1..3";
         return E_INVALID;
@@ -272,7 +272,7 @@ int Scheduler::prepare(const TaskDesc& d, Cmd& c, std::string* err) const {
             return E_INVALID;
         }
     }
-    c.chunks = split(d.range, G_, d.split);
+    c.chunks = split(node_range ? *node_range : d.range, G_, d.split);
     for (int dev = 0; dev < G_; ++dev) {
         const Box& ch = c.chunks[dev];
         if (ch.empty()) continue;
@@ -317,16 +317,68 @@ int Scheduler::task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string*
     c.kind = 0;
     const int rc = prepare(desc, c, err);
     if (rc != E_OK) return rc;
-    int status = E_OK;
     std::map<uint32_t, Region> reads, writes;
     for (auto& kv : c.reads) reads[kv.first.second] = runion(reads[kv.first.second], kv.second);
     for (auto& kv : c.writes) writes[kv.first.second] = runion(writes[kv.first.second], kv.second);
+    c.desc = std::make_shared<const TaskDesc>(desc);
+    return submit_cmd(std::move(c), reads, writes, tid_out);
+}
+
+int Scheduler::task_submit_node(const TaskDesc& desc, const Box& node_range, const std::map<uint32_t, Region>& reads,
+                                const std::map<uint32_t, Region>& writes, const std::vector<Push>& pushes,
+                                const std::map<uint32_t, Region>& awaits,
+                                const std::map<uint32_t, Region>& remote_writes, uint64_t* tid_out,
+                                std::string* err) {
+    if (shut_) return E_STATE;
+    Cmd c;
+    c.kind = 0;
+    const int rc = prepare(desc, c, err, &node_range);
+    if (rc != E_OK) return rc;
+    c.pushes = pushes;
+    c.awaits = awaits;
+    c.remote_writes = remote_writes;
+    transfer_req(c);
+    c.desc = std::make_shared<const TaskDesc>(desc);
+    return submit_cmd(std::move(c), reads, writes, tid_out);
+}
+
+void Scheduler::transfer_req(Cmd& c) const {
+    // P:L398 / P:L417: pushed data is staged in, and awaited data received into,
+    // one contiguous M1 allocation per buffer (requirement key device -1 -> M1)
+    std::map<uint32_t, Box> boxes;
+    for (auto& p : c.pushes) {
+        Box& b = boxes[std::get<1>(p)];
+        b = bbox(b, rbbox(std::get<2>(p)));
+    }
+    for (auto& kv : c.awaits) {
+        Box& b = boxes[kv.first];
+        b = bbox(b, rbbox(kv.second));
+    }
+    for (auto& kv : boxes) c.req[{-1, kv.first}] = kv.second;
+}
+
+void Scheduler::epoch_node(int64_t rb, uint32_t rb_buf, const Box& rb_box, const std::vector<Push>& pushes,
+                           const std::map<uint32_t, Region>& awaits) {
+    if (shut_) return;
+    Cmd e;
+    e.kind = 2;
+    e.rb = rb;
+    e.rb_buf = rb_buf;
+    e.rb_box = rb_box.normalized();
+    e.pushes = pushes;
+    e.awaits = awaits;
+    transfer_req(e);
+    epoch_cmd(std::move(e));
+}
+
+int Scheduler::submit_cmd(Cmd&& c, const std::map<uint32_t, Region>& reads, const std::map<uint32_t, Region>& writes,
+                          uint64_t* tid_out) {
+    int status = E_OK;
     if (checks_) {  // §4.4 uninitialised-read detection: warning
         for (auto& kv : reads)
             if (!rdiff(kv.second, tbufs_[kv.first].initialized).empty()) status = W_UNINIT_READ;
     }
     c.tid = tdag_submit(reads, writes);
-    c.desc = std::make_shared<const TaskDesc>(desc);
     if (tid_out) *tid_out = uint64_t(c.tid);
     push(std::move(c));
     if (max_cp_ - cp_ref_ >= horizon_step_) {
@@ -483,7 +535,8 @@ void Scheduler::log_instr(const Instr& ins) {
         fprintf(log_, "[[%" PRId64 ",%" PRId64 ",%" PRId64 "],[%" PRId64 ",%" PRId64 ",%" PRId64 "]]", b.lo[0],
                 b.lo[1], b.lo[2], b.hi[0], b.hi[1], b.hi[2]);
     };
-    static const char* kinds[] = {"alloc", "free", "copy", "kernel", "horizon", "epoch"};
+    static const char* kinds[] = {"alloc", "free",  "copy",    "kernel",        "horizon",
+                                  "epoch", "send", "receive", "split_receive", "await_receive"};
     static const char* reasons[] = {"resize", "coherence", "readback"};
     fprintf(log_, "{\"iid\":%" PRIu64 ",\"kind\":\"%s\",\"task\":", ins.iid, kinds[int(ins.kind)]);
     if (ins.task < 0)
@@ -515,6 +568,24 @@ void Scheduler::log_instr(const Instr& ins) {
         pbox(ins.chunk);
         fprintf(log_, ",\"bindings\":[");
         for (size_t i = 0; i < ins.bindings.size(); ++i) fprintf(log_, i ? ",%" PRId64 : "%" PRId64, ins.bindings[i]);
+        fputc(']', log_);
+        break;
+    case IKind::Send:
+        fprintf(log_, ",\"buffer\":%u,\"target\":%d,\"msg\":%" PRIu64 ",\"src_aid\":%" PRId64 ",\"src_mem\":%d,\"box\":",
+                ins.buffer, ins.target, ins.msg, ins.src_aid, ins.src_mem);
+        pbox(ins.box);
+        break;
+    case IKind::Receive:
+    case IKind::SplitReceive:
+    case IKind::AwaitReceive:
+        fprintf(log_, ",\"buffer\":%u,\"transfer\":[%" PRId64 ",%u]", ins.buffer, ins.transfer, ins.buffer);
+        if (ins.kind != IKind::AwaitReceive)
+            fprintf(log_, ",\"dst_aid\":%" PRId64 ",\"dst_mem\":%d", ins.dst_aid, ins.dst_mem);
+        fprintf(log_, ",\"region\":[");
+        for (size_t i = 0; i < ins.region.size(); ++i) {
+            if (i) fputc(',', log_);
+            pbox(ins.region[i]);
+        }
         fputc(']', log_);
         break;
     default:
@@ -769,10 +840,12 @@ void Scheduler::compile(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& a
     }
 }
 
-void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant) {
+std::map<Scheduler::Key, Scheduler::Alloc*> Scheduler::allocate(Cmd& c,
+                                                                 const std::map<std::pair<uint32_t, int>, Box>& ant) {
     const int64_t tid = c.tid;
     std::map<Key, Alloc*> binding;
-    // R9 allocation (Fig. 3): resize chain alloc -> copy -> free
+    // R9 allocation (Fig. 3): resize chain alloc -> copy -> free;
+    // M1 requirements (device -1, virtual-node transfers) come first
     for (auto& kv : c.req) {
         const int m = 2 + kv.first.first;
         const uint32_t bid = kv.first.second;
@@ -814,6 +887,129 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         }
         binding[kv.first] = na;
     }
+    return binding;
+}
+
+// Virtual-node mode, §3.4 Peer-to-Peer Communication (mirrors
+// oracle/scheduler.py Runtime._transfers).  Outbound: the pushed
+// region is made coherent in M1, then one send per rectangle of each
+// original-producer fragment, each with a locally unique message id and a
+// pilot.  Inbound: one receive into M1 when every consumer reads
+// the same part of the awaited region, else a split receive plus one await
+// receive per consumer-split fragment (R17).
+void Scheduler::transfers(Cmd& c, std::map<Key, Alloc*>& binding, bool readback_consumer) {
+    const int64_t tid = c.tid;
+    for (auto& p : c.pushes) {
+        const int target = std::get<0>(p);
+        const uint32_t bid = std::get<1>(p);
+        const Region& reg = std::get<2>(p);
+        Buf& buf = *bufs_.at(bid);
+        Alloc* m1 = binding.at({-1, bid});
+        std::vector<std::pair<Region, uint32_t>> need;
+        for (auto& q : buf.uptodate.query(reg))
+            if (q.second != 0 && ((q.second >> 1) & 1u) == 0) need.push_back(std::move(q));
+        if (!need.empty()) {
+            auto parts = source_parts_q(buf, need, 1);
+            for (auto& pp : parts) {
+                const int64_t aid = std::get<2>(pp.first);
+                Alloc* src = aid == HOST_AID ? buf.host.get() : allocs_.at(aid).get();
+                copy(tid, bid, REASON_COHERENCE, src, m1, pp.second, -1);
+            }
+            for (auto& pp : parts) buf.uptodate.apply(pp.second, [](uint32_t mask) { return mask | 2u; });
+        }
+        for (auto& q : buf.orig_writer.query(reg)) {
+            for (const Box& bx : q.first) {
+                std::vector<uint64_t> deps{uint64_t(m1->iid)};
+                m1->last_writer.for_values_in(Region{bx}, [&](int64_t v) {
+                    if (v >= 0) deps.push_back(uint64_t(v));
+                });
+                Instr ins;
+                ins.kind = IKind::Send;
+                ins.task = tid;
+                ins.buffer = bid;
+                ins.target = target;
+                ins.msg = next_msg_++;
+                ins.src_aid = m1->aid;
+                ins.src_mem = 1;
+                ins.box = bx;
+                const uint64_t iid = emit(ins, deps);
+                m1->readers.add(int64_t(iid), Region{bx});
+                pilots_.push_back(Pilot{node_, ins.msg, target, tid, bid, bx});
+            }
+        }
+    }
+    for (auto& kv : c.awaits) {
+        const uint32_t bid = kv.first;
+        const Region& reg = kv.second;
+        Buf& buf = *bufs_.at(bid);
+        Alloc* m1 = binding.at({-1, bid});
+        std::vector<Region> consumers;
+        if (readback_consumer) {
+            consumers.push_back(reg);
+        } else {
+            for (int d = 0; d < G_; ++d) {
+                auto rit = c.reads.find({d, bid});
+                if (rit == c.reads.end()) continue;
+                Region x = rinter(rit->second, reg);
+                if (!x.empty()) consumers.push_back(std::move(x));
+            }
+        }
+        bool same = true;
+        for (size_t i = 1; i < consumers.size(); ++i)
+            if (!(consumers[i] == consumers[0])) same = false;
+        std::vector<uint64_t> deps{uint64_t(m1->iid)};
+        m1->readers.ids_in(reg, [&](int64_t r) { deps.push_back(uint64_t(r)); });
+        m1->last_writer.for_values_in(reg, [&](int64_t v) {
+            if (v >= 0) deps.push_back(uint64_t(v));
+        });
+        Instr ins;
+        ins.kind = same ? IKind::Receive : IKind::SplitReceive;
+        ins.task = tid;
+        ins.buffer = bid;
+        ins.transfer = tid;
+        ins.dst_aid = m1->aid;
+        ins.dst_mem = 1;
+        ins.region = reg;
+        const uint64_t r_iid = emit(ins, deps);
+        std::vector<std::pair<Region, uint64_t>> frags;
+        if (same) {
+            frags.push_back({reg, r_iid});
+        } else {
+            std::vector<Region> atoms{reg};
+            for (const Region& cr : consumers) {
+                std::vector<Region> nxt;
+                for (const Region& a : atoms) {
+                    Region i = rinter(a, cr);
+                    Region o = rdiff(a, cr);
+                    if (!i.empty()) nxt.push_back(std::move(i));
+                    if (!o.empty()) nxt.push_back(std::move(o));
+                }
+                atoms.swap(nxt);
+            }
+            for (const Region& a : atoms) {
+                Instr aw;
+                aw.kind = IKind::AwaitReceive;
+                aw.task = tid;
+                aw.buffer = bid;
+                aw.transfer = tid;
+                aw.region = a;
+                std::vector<uint64_t> ad{r_iid};
+                frags.push_back({a, emit(aw, ad)});
+            }
+        }
+        for (auto& f : frags) {
+            m1->last_writer.update(f.first, int64_t(f.second));
+            m1->readers.remove(f.first);
+            buf.orig_writer.update(f.first, int64_t(f.second));
+        }
+        buf.uptodate.update(reg, 2u);
+    }
+}
+
+void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant) {
+    const int64_t tid = c.tid;
+    std::map<Key, Alloc*> binding = allocate(c, ant);
+    if (!c.pushes.empty() || !c.awaits.empty()) transfers(c, binding, false);
     // R10 coherence copies; masks as they stood before this task
     std::vector<std::tuple<uint32_t, Region, int>> updates;
     using Part = std::pair<std::tuple<int64_t, int, int64_t>, Region>;
@@ -903,6 +1099,12 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         buf.orig_writer.update(kv.second, int64_t(kernels[kv.first.first]));
         buf.uptodate.update(kv.second, 1u << (2 + kv.first.first));
     }
+    // virtual-node mode: what other nodes wrote in this task is stale here
+    for (auto& kv : c.remote_writes) {
+        Buf& buf = *bufs_.at(kv.first);
+        buf.uptodate.update(kv.second, 0u);
+        buf.orig_writer.update(kv.second, NONE);
+    }
 }
 
 void Scheduler::subsume(int64_t h) {
@@ -938,6 +1140,10 @@ void Scheduler::compile_horizon(Cmd& c) {
 }
 
 void Scheduler::compile_epoch(Cmd& c) {
+    if (!c.pushes.empty() || !c.awaits.empty()) {   // virtual-node readback gather
+        std::map<Key, Alloc*> binding = allocate(c, {});
+        transfers(c, binding, true);
+    }
     if (c.rb >= 0) {  // R13 readback into the user pointer
         Buf& buf = *bufs_[c.rb_buf];
         Region need = rinter(buf.uptodate.where([](uint32_t mask) { return mask != 0; }), c.rb_box);
@@ -982,4 +1188,175 @@ void Scheduler::debug_dump(FILE* f) const {
     }
     fprintf(f, "tdag cp entries %zu, front %zu\n", cp_.size(), front_.size());
 }
+}  // namespace cel
+
+// ------------------------------------------------------------ virtual-node mode
+namespace cel {
+
+Cluster::Cluster(int n_nodes, int devices_per_node, int lookahead, int horizon_step, bool checks,
+                 const std::vector<InstrSink*>& sinks, const std::vector<FILE*>& logs)
+    : N_(n_nodes), D_(devices_per_node) {
+    for (int k = 0; k < N_; ++k) {
+        s_.emplace_back(new Scheduler(D_, lookahead, horizon_step, checks, sinks[k], logs[k]));
+        s_.back()->set_node(k);
+    }
+}
+
+int Cluster::buffer_create(int dims, const int64_t extent[3], uint32_t elem_size, bool host_init, uint32_t* out) {
+    uint32_t bid = 0;
+    for (int k = 0; k < N_; ++k) {
+        const int rc = s_[k]->buffer_create(dims, extent, elem_size, host_init, &bid);
+        if (rc != E_OK) return rc;
+    }
+    const Box ext = s_[0]->extent(bid);
+    t_.emplace(bid, Track{RegionMap<int64_t>(ext, host_init ? -2 : -1),
+                          RegionMap<uint32_t>(ext, host_init ? uint32_t((1ull << N_) - 1) : 0u)});
+    *out = bid;
+    return E_OK;
+}
+
+// For each receiving node m and buffer b: the elements of need[m][b] that m
+// does not hold come from their owner (never-written elements: nothing).
+// Pushes are coalesced per (owner, receiver, buffer); the await
+// region of m is the union.
+void Cluster::transfers(const std::vector<std::map<uint32_t, Region>>& need, std::vector<std::vector<Push>>& pushes,
+                        std::vector<std::map<uint32_t, Region>>& awaits) const {
+    std::vector<std::map<std::pair<int, uint32_t>, Region>> pm(N_);
+    awaits.assign(N_, {});
+    for (int m = 0; m < N_; ++m) {
+        for (auto& kv : need[m]) {
+            const Track& tr = t_.at(kv.first);
+            const Region held = tr.holders.where([m](uint32_t mask) { return ((mask >> m) & 1u) != 0; });
+            const Region miss = rdiff(kv.second, held);
+            for (auto& q : tr.owner.query(miss)) {
+                const int64_t n = q.second;
+                if (n < 0 || n == m) continue;
+                Region& r = pm[n][{m, kv.first}];
+                r = runion(r, q.first);
+                Region& a = awaits[m][kv.first];
+                a = runion(a, q.first);
+            }
+        }
+    }
+    pushes.assign(N_, {});
+    for (int n = 0; n < N_; ++n)
+        for (auto& kv : pm[n]) pushes[n].push_back(Push{kv.first.first, kv.first.second, kv.second});
+}
+
+int Cluster::task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string* err) {
+    for (const Access& a : desc.acc)
+        if (!s_[0]->has_buffer(a.buf)) {
+            if (err) *err = "access to an unknown or destroyed buffer";
+            return E_INVALID;
+        }
+    if (desc.dims < 1 || desc.dims > 3) {
+        if (err) *err = "task dims must be 1..3";
+        return E_INVALID;
+    }
+    // R17: command chunks, 1-D over the nodes; the task's split applies inside a node
+    const std::vector<Box> chunks = split(desc.range, N_, 0);
+    std::vector<std::map<uint32_t, Region>> rd(N_), wr(N_);
+    for (int n = 0; n < N_; ++n) {
+        if (chunks[n].empty()) continue;
+        for (const Access& a : desc.acc) {
+            Box bx;
+            const int rc = apply_mapper(a.map, chunks[n], s_[0]->extent(a.buf), &bx);
+            if (rc != E_OK) {
+                if (err) *err = "range mapper result outside the buffer extent";
+                return rc;
+            }
+            if (bx.empty()) continue;
+            if (is_read(a.mode)) rd[n][a.buf] = runion(rd[n][a.buf], Region{bx});
+            if (is_write(a.mode)) wr[n][a.buf] = runion(wr[n][a.buf], Region{bx});
+        }
+    }
+    // §4.4 overlapping writes across nodes
+    for (int i = 0; i < N_; ++i)
+        for (int j = i + 1; j < N_; ++j)
+            for (auto& kv : wr[i]) {
+                auto it = wr[j].find(kv.first);
+                if (it != wr[j].end() && !rinter(kv.second, it->second).empty()) {
+                    if (err) {
+                        char buf[160];
+                        snprintf(buf, sizeof buf, "nodes %d and %d write overlapping regions of buffer %u", i, j,
+                                 kv.first);
+                        *err = buf;
+                    }
+                    return E_OVERLAPPING_WRITE;
+                }
+            }
+    std::map<uint32_t, Region> reads, writes;
+    for (int n = 0; n < N_; ++n) {
+        for (auto& kv : rd[n]) reads[kv.first] = runion(reads[kv.first], kv.second);
+        for (auto& kv : wr[n]) writes[kv.first] = runion(writes[kv.first], kv.second);
+    }
+    std::vector<std::vector<Push>> pushes;
+    std::vector<std::map<uint32_t, Region>> awaits;
+    transfers(rd, pushes, awaits);
+    int status = E_OK;
+    for (int n = 0; n < N_; ++n) {
+        std::map<uint32_t, Region> remote;
+        for (int k = 0; k < N_; ++k) {
+            if (k == n) continue;
+            for (auto& kv : wr[k]) remote[kv.first] = runion(remote[kv.first], kv.second);
+        }
+        uint64_t tid = 0;
+        const int rc = s_[n]->task_submit_node(desc, chunks[n], reads, writes, pushes[n], awaits[n], remote, &tid,
+                                               err);
+        if (rc < 0) return rc;   // a node rejected a chunk: only node-local validation can fail here
+        if (n == 0) {
+            status = rc;
+            if (tid_out) *tid_out = tid;
+        }
+    }
+    for (int m = 0; m < N_; ++m)
+        for (auto& kv : awaits[m])
+            t_.at(kv.first).holders.apply(kv.second, [m](uint32_t mask) { return mask | (1u << m); });
+    for (int n = 0; n < N_; ++n)
+        for (auto& kv : wr[n]) {
+            Track& tr = t_.at(kv.first);
+            tr.owner.update(kv.second, int64_t(n));
+            tr.holders.update(kv.second, 1u << n);
+        }
+    return status;
+}
+
+void Cluster::wait() {
+    for (auto& s : s_) s->wait();
+}
+
+int Cluster::readback(uint32_t bid, const Box& box, int64_t* rb_out, std::string* err) {
+    if (!s_[0]->has_buffer(bid)) {
+        if (err) *err = "unknown buffer";
+        return E_INVALID;
+    }
+    if (!s_[0]->extent(bid).contains(box)) {
+        if (err) *err = "readback box outside the buffer extent";
+        return E_OUT_OF_BOUNDS;
+    }
+    std::vector<std::map<uint32_t, Region>> need(N_);
+    need[0][bid] = Region{box.normalized()};
+    std::vector<std::vector<Push>> pushes;
+    std::vector<std::map<uint32_t, Region>> awaits;
+    transfers(need, pushes, awaits);
+    const int64_t rb = s_[0]->alloc_readback_id();
+    for (int n = 0; n < N_; ++n) s_[n]->epoch_node(n == 0 ? rb : -1, bid, box, pushes[n], awaits[n]);
+    for (auto& kv : awaits[0]) t_.at(kv.first).holders.apply(kv.second, [](uint32_t mask) { return mask | 1u; });
+    if (rb_out) *rb_out = rb;
+    return E_OK;
+}
+
+int Cluster::destroy(uint32_t bid, std::string* err) {
+    for (auto& s : s_) {
+        const int rc = s->destroy(bid, err);
+        if (rc != E_OK) return rc;
+    }
+    t_.erase(bid);
+    return E_OK;
+}
+
+void Cluster::shutdown() {
+    for (auto& s : s_) s->shutdown();
+}
+
 }  // namespace cel

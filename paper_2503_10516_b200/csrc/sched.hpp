@@ -157,7 +157,10 @@ struct ReaderList {
     }
 };
 
-enum class IKind : uint8_t { Alloc, Free, Copy, Kernel, Horizon, Epoch };
+// Table 1.  Send .. AwaitReceive occur only in virtual-node mode
+// (cluster.hpp).
+enum class IKind : uint8_t { Alloc, Free, Copy, Kernel, Horizon, Epoch, Send, Receive, SplitReceive, AwaitReceive };
+constexpr int kNumIKinds = 10;
 enum CopyReason : int { REASON_RESIZE = 0, REASON_COHERENCE = 1, REASON_READBACK = 2 };
 
 constexpr int64_t NONE = -1;          // no writer (uninitialised)
@@ -179,6 +182,12 @@ struct Instr {
     int src_mem = 0, dst_mem = 0;
     Region region;
     int64_t readback = -1;
+    // send (box, src_aid/src_mem = the node's M1 staging allocation) / receive /
+    // split receive (region, dst_aid/dst_mem) / await receive (region):
+    // transfer id = (transfer, buffer)
+    int target = -1;
+    uint64_t msg = 0;
+    int64_t transfer = -1;
     // §8 a7: member of an all-gather copy set (not part of the instruction log):
     // group id (0 = none) and the number of copies in the group
     uint64_t coll = 0;
@@ -197,8 +206,21 @@ struct InstrSink {
     virtual void on_instr(const Instr& ins) = 0;   // called in iid (topological) order
 };
 
+// a send's pilot message, "transmitted to the receiver ahead of
+// execution time"
+struct Pilot {
+    int sender = 0;
+    uint64_t msg = 0;
+    int receiver = 0;
+    int64_t transfer = 0;      // transfer id (transfer, buffer)
+    uint32_t buffer = 0;
+    Box box;
+};
+
+using Push = std::tuple<int, uint32_t, Region>;   // (target node, buffer, region)
+
 struct SchedStats {
-    uint64_t n_by_kind[8] = {};
+    uint64_t n_by_kind[16] = {};
     uint64_t copies_by_reason[3] = {};
     uint64_t bytes_by_reason[3] = {};
     uint64_t bytes_d2d_peer = 0;
@@ -214,6 +236,25 @@ public:
 
     int buffer_create(int dims, const int64_t extent[3], uint32_t elem_size, bool host_init, uint32_t* out);
     int task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string* err);
+    // Virtual-node mode (cluster.cpp): this node's share of a task -- the
+    // command chunk `node_range` split over the local devices -- with the
+    // transfers the replicated command-graph generation derived for it; the
+    // task graph sees the whole task (`reads` / `writes` over all nodes).
+    int task_submit_node(const TaskDesc& desc, const Box& node_range, const std::map<uint32_t, Region>& reads,
+                         const std::map<uint32_t, Region>& writes, const std::vector<Push>& pushes,
+                         const std::map<uint32_t, Region>& awaits, const std::map<uint32_t, Region>& remote_writes,
+                         uint64_t* tid_out, std::string* err);
+    // Virtual-node mode readback epoch: node 0 (rb >= 0) gathers, the others push.
+    void epoch_node(int64_t rb, uint32_t rb_buf, const Box& rb_box, const std::vector<Push>& pushes,
+                    const std::map<uint32_t, Region>& awaits);
+    void set_node(int n) { node_ = n; }
+    int node() const { return node_; }
+    std::vector<Pilot> take_pilots() {
+        std::vector<Pilot> p;
+        p.swap(pilots_);
+        return p;
+    }
+    int64_t alloc_readback_id() { return next_rb_++; }
     void wait();
     int readback(uint32_t bid, const Box& box, int64_t* rb_out, std::string* err);
     int destroy(uint32_t bid, std::string* err);
@@ -265,6 +306,9 @@ private:
         uint32_t rb_buf = 0;
         Box rb_box;
         std::vector<uint32_t> destroy;
+        // virtual-node mode
+        std::vector<Push> pushes;                     // sorted by (target, buffer)
+        std::map<uint32_t, Region> awaits, remote_writes;
     };
 
     // task graph (R7)
@@ -281,6 +325,11 @@ private:
     // IDAG (R9-R14)
     void compile(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant);
     void compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant);
+    std::map<Key, Alloc*> allocate(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant);
+    void transfers(Cmd& c, std::map<Key, Alloc*>& binding, bool readback_consumer);
+    void transfer_req(Cmd& c) const;
+    int submit_cmd(Cmd&& c, const std::map<uint32_t, Region>& reads, const std::map<uint32_t, Region>& writes,
+                   uint64_t* tid_out);
     void compile_horizon(Cmd& c);
     void compile_epoch(Cmd& c);
     uint64_t emit(Instr& ins, std::vector<uint64_t>& deps);
@@ -297,7 +346,7 @@ private:
         const std::map<Key, Alloc*>& binding) const;
     void subsume(int64_t h);
     void log_instr(const Instr& ins);
-    int prepare(const TaskDesc& d, Cmd& c, std::string* err) const;
+    int prepare(const TaskDesc& d, Cmd& c, std::string* err, const Box* node_range = nullptr) const;
 
     int G_;
     int mode_;
@@ -327,9 +376,45 @@ private:
     int64_t next_aid_ = 1;
     int64_t next_rb_ = 0;
     uint64_t next_coll_ = 1;
+    int node_ = 0;                                    // virtual-node mode: this node's id
+    uint64_t next_msg_ = 0;                           // P:L400 "locally unique message id"
+    std::vector<Pilot> pilots_;
     uint64_t coll_min_bytes_ = 1ull << 20;            // CEL_COLL_MIN_BYTES: smallest per-source gather run as NCCL
     uint32_t next_bid_ = 0;
     bool shut_ = false;
+};
+
+// Virtual-node mode (§3.4; mirrors
+// oracle/cluster.py): N nodes of D devices, one Scheduler each.  The
+// command-graph decisions -- which node pushes what to whom, what each node
+// awaits -- come from replicated bookkeeping kept once here: per buffer the
+// node that last wrote each element (owner) and the set of nodes holding an
+// up-to-date copy (holders).  Readings R17.
+class Cluster {
+public:
+    Cluster(int n_nodes, int devices_per_node, int lookahead, int horizon_step, bool checks,
+            const std::vector<InstrSink*>& sinks, const std::vector<FILE*>& logs);
+    int buffer_create(int dims, const int64_t extent[3], uint32_t elem_size, bool host_init, uint32_t* out);
+    int task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string* err);
+    void wait();
+    // node 0 gathers `box` of `bid` (owners push what it lacks); returns the readback id
+    int readback(uint32_t bid, const Box& box, int64_t* rb_out, std::string* err);
+    int destroy(uint32_t bid, std::string* err);
+    void shutdown();
+    int nodes() const { return N_; }
+    Scheduler& node(int k) { return *s_[k]; }
+    const Scheduler& node(int k) const { return *s_[k]; }
+
+private:
+    struct Track {
+        RegionMap<int64_t> owner;     // -1 never written, -2 host data (every node)
+        RegionMap<uint32_t> holders;  // bit n: node n holds an up-to-date copy
+    };
+    void transfers(const std::vector<std::map<uint32_t, Region>>& need, std::vector<std::vector<Push>>& pushes,
+                   std::vector<std::map<uint32_t, Region>>& awaits) const;
+    int N_, D_;
+    std::vector<std::unique_ptr<Scheduler>> s_;
+    std::map<uint32_t, Track> t_;
 };
 
 }  // namespace cel

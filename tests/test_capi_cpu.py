@@ -166,3 +166,43 @@ def test_errors_and_warnings(cel):
         r.task_submit({"dims": 1, "range": full, "kernel": "probe", "params": {"salt": 3},
                        "accesses": [(a, "write", ("one_to_one",))]})
     r.shutdown()
+
+
+# ------------------------------------------------------------ virtual-node mode
+def cluster_logs(cel, prog, N, D, mode, step=4, tmp="/tmp/cel_cpu_cluster.jsonl"):
+    from oracle.cluster import Cluster
+    o = Cluster(N, D, lookahead=mode, horizon_step=step)
+    run_program(o, prog)
+    r = cel.Runtime(D, execute=False, lookahead=mode, horizon_step=step, instr_log_path=tmp, n_nodes=N)
+    run_program(r, prog)
+    return o, [[json.loads(line) for line in open("%s.%d" % (tmp, k))] for k in range(N)]
+
+
+@pytest.mark.parametrize("N,D", [(2, 1), (2, 2), (3, 2), (4, 1)])
+def test_cluster_config_logs_match_oracle(cel, N, D):
+    for prog in (P.c1_chain(64), P.wavesim(64, 5, rows=40), P.jacobi3d(12, 3), P.rsim(64, 10), P.nbody(100, 2),
+                 P.nbody(256, 2, host_init=True)):
+        for mode in ("none", "auto"):
+            o, c = cluster_logs(cel, prog, N, D, mode)
+            for k in range(N):
+                assert c[k] == o.logs[k], (prog["name"], mode, k)
+
+
+@pytest.mark.parametrize("N,D", [(2, 1), (2, 2), (3, 1), (3, 2)])
+def test_cluster_random_logs_match_oracle(cel, N, D):
+    for s in range(20):
+        prog = P.random_program(5100 + 13 * N + D + s)
+        mode = ["none", "auto", "infinite"][s % 3]
+        o, c = cluster_logs(cel, prog, N, D, mode, step=2 + s % 3)
+        for k in range(N):
+            assert c[k] == o.logs[k], (s, k)
+
+
+def test_cluster_full_size_counts(cel):
+    """N-body 2^20 on 2 nodes x 4 devices and WaveSim 16384^2 on 4 nodes x 2:
+    instruction logs equal at BASELINE sizes (execute=0)."""
+    for prog, N, D in ((P.nbody(1 << 20, 2), 2, 4), (P.wavesim(16384, 6), 4, 2)):
+        o, c = cluster_logs(cel, prog, N, D, "auto")
+        for k in range(N):
+            assert c[k] == o.logs[k]
+        assert sum(1 for r in c[0] if r["kind"] == "send") > 0
