@@ -77,17 +77,7 @@ int after(cel_runtime* rt, int rc) {
         }
     return rc;
 }
-// virtual-node mode: pilots produced by compilation go to the receivers'
-// arbitration right away ("transmitted ... immediately")
-void deliver_pilots(cel_runtime* rt) {
-    if (!rt->cluster || !rt->comm) return;
-    for (int k = 0; k < rt->cluster->nodes(); ++k) {
-        std::vector<Pilot> p = rt->cluster->node(k).take_pilots();
-        if (!p.empty()) rt->comm->add_pilots(p);
-    }
-}
 void drain_all(cel_runtime* rt) {
-    deliver_pilots(rt);
     for (Executor* e : execs(rt)) e->drain();
 }
 }  // namespace
@@ -159,6 +149,12 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
         rt->cluster = std::make_unique<Cluster>(nodes, cfg->n_devices, cfg->lookahead, step, cfg->checks != 0, sinks,
                                                 rt->node_logs);
         for (int k = 0; k < int(rt->node_exec.size()); ++k) rt->node_exec[k]->set_scheduler(&rt->cluster->node(k));
+        if (rt->comm) {
+            // pilots reach the receivers' arbitration as they are compiled
+            std::shared_ptr<Communicator> comm = rt->comm;
+            for (int k = 0; k < nodes; ++k)
+                rt->cluster->node(k).set_pilot_sink([comm](const Pilot& p) { comm->add_pilot(p); });
+        }
         *out = rt.release();
         return CEL_OK;
     }
@@ -269,7 +265,6 @@ int cel_task_submit(cel_runtime* rt, const cel_task_desc* d, cel_task* out) {
     uint64_t tid = 0;
     const uint64_t t0 = now_ns();
     const int rc = rt->cluster ? rt->cluster->task_submit(t, &tid, &err) : rt->sched->task_submit(t, &tid, &err);
-    deliver_pilots(rt);
     rt->gen_ns += now_ns() - t0;
     if (rc < 0) return fail(rc, err);
     if (out) *out = tid;
@@ -308,7 +303,6 @@ int cel_buffer_destroy(cel_runtime* rt, cel_buffer buf) {
     std::string err;
     const int rc = rt->cluster ? rt->cluster->destroy(buf, &err) : rt->sched->destroy(buf, &err);
     if (rc < 0) return fail(rc, err);
-    deliver_pilots(rt);
     for (Executor* e : execs(rt)) e->drop_host_init_later(buf);
     return after(rt, CEL_OK);
 }
@@ -434,6 +428,7 @@ int cel_runtime_destroy(cel_runtime* rt) {
             if (e->error() && rc == CEL_OK) rc = fail(e->error(), e->error_msg());
     } else {
         rc = err;
+        if (rt->comm) rt->comm->abort();   // wake nodes waiting for a failed peer
     }
     rt->sched.reset();
     rt->exec.reset();

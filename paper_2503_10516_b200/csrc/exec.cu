@@ -193,7 +193,6 @@ Executor::~Executor() {
     for (auto& kv : host_init_)
         if (kv.second.second) cudaFreeHost(kv.second.first);
     if (host_arena_.base) cudaFreeHost(host_arena_.base);
-    if (vflags_) cudaFree(vflags_);
 }
 
 void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
@@ -202,6 +201,7 @@ void Executor::check(cudaError_t e, const char* what) {
     if (e == cudaSuccess || err_) return;
     errmsg_ = std::string(what) + ": " + cudaGetErrorString(e);
     err_ = E_CUDA;
+    if (cfg_.comm) cfg_.comm->abort();
 }
 
 void Executor::checkd(CUresult e, const char* what) {
@@ -313,13 +313,7 @@ int Executor::init(std::string* err) {
     }
     if (cfg_.comm) {
         // virtual-node mode: M1 staging arena (pinned, mapped: copy kernels and
-        // the communicator's pulls address it directly) and the flags sends and
-        // receives wait on (device memory of the node's first GPU)
-        g_drv.load();
-        if (!g_drv.wait64 || !g_drv.write64) {
-            *err = "virtual-node mode needs stream memory operations";
-            return E_CUDA;
-        }
+        // the communicator's pulls address it directly)
         void* h = nullptr;
         if (cudaHostAlloc(&h, cfg_.host_arena_bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
             cudaGetLastError();
@@ -329,14 +323,6 @@ int Executor::init(std::string* err) {
         host_arena_.base = static_cast<char*>(h);
         host_arena_.size = cfg_.host_arena_bytes;
         host_arena_.free_[0] = FreeRange{cfg_.host_arena_bytes, Token{}};
-        set_dev(0);
-        if (cudaMalloc(&vflags_, 2 * kRing * sizeof(uint64_t)) != cudaSuccess) {
-            cudaGetLastError();
-            *err = "cannot allocate transfer flags";
-            return E_OOM;
-        }
-        cudaMemset(vflags_, 0, 2 * kRing * sizeof(uint64_t));
-        cfg_.comm->attach(cfg_.node, phys_[0]);
     }
     cudaDeviceSynchronize();
     const char* et = getenv("CEL_EXEC_THREAD");
@@ -691,7 +677,9 @@ void Executor::push(Item&& it) {
     bool wake;
     {
         std::unique_lock<std::mutex> l(qm_);
-        while (q_.size() >= 16384) qfull_cv_.wait(l);   // bounded run-ahead of the scheduler
+        // bounded run-ahead of the scheduler (not in virtual-node mode: a node's
+        // executor may wait for pilots another node's compilation produces)
+        while (q_.size() >= 16384 && !cfg_.comm) qfull_cv_.wait(l);
         q_.push_back(std::move(it));
         qsize_.store(q_.size(), std::memory_order_release);
         wake = sleeping_;
@@ -807,6 +795,7 @@ int Executor::trace_dump(const char* path) {
 
 void Executor::on_instr_impl(const Instr& ins) {
     if (err_) return;
+    if (!pending_send_.empty()) resolve_sends(ins);
     const int od = instr_owner(ins);
     const bool mine = od < 0 || owner_rank(od) == cfg_.rank;
     if (trace_)
@@ -1186,130 +1175,83 @@ void box_seg(CopyArgs& args, const char* sb, const Box& S, char* db, const Box& 
 }
 }  // namespace
 
-Communicator::Communicator(int nodes) : nodes_(nodes), phys_(nodes, -1), stream_(nodes, nullptr) {}
-
-Communicator::~Communicator() {
-    for (int n = 0; n < nodes_; ++n)
-        if (stream_[n]) {
-            cudaSetDevice(phys_[n]);
-            cudaStreamSynchronize(stream_[n]);
-            cudaStreamDestroy(stream_[n]);
-        }
+void Communicator::add_pilot(const Pilot& p) {
+    std::lock_guard<std::mutex> l(m_);
+    pilots_[Key{p.receiver, p.transfer, p.buffer}].push_back(PilotRec{p.sender, p.msg, p.box});
+    cv_.notify_all();
 }
 
-void Communicator::attach(int node, int phys_dev) {
+void Communicator::post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready) {
     std::lock_guard<std::mutex> l(m_);
-    phys_[node] = phys_dev;
-    cudaSetDevice(phys_dev);
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStreamCreateWithPriority(&stream_[node], cudaStreamNonBlocking, hi);
-    // pulls write the peer's completion flags: peer access between the nodes' GPUs
-    for (int k = 0; k < nodes_; ++k) {
-        if (k == node || phys_[k] < 0 || phys_[k] == phys_dev) continue;
-        int can = 0;
-        cudaDeviceCanAccessPeer(&can, phys_dev, phys_[k]);
-        if (can && cudaDeviceEnablePeerAccess(phys_[k], 0) == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        cudaSetDevice(phys_[k]);
-        cudaDeviceCanAccessPeer(&can, phys_[k], phys_dev);
-        if (can && cudaDeviceEnablePeerAccess(phys_dev, 0) == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
-        cudaSetDevice(phys_dev);
-    }
+    sends_[{node, msg}] = Send{src, ready};
+    cv_.notify_all();
 }
 
-void Communicator::add_pilots(const std::vector<Pilot>& ps) {
+void Communicator::abort() {
     std::lock_guard<std::mutex> l(m_);
-    std::vector<Key> touched;
-    for (const Pilot& p : ps) {
-        const Key k{p.receiver, p.transfer, p.buffer};
-        recv_[k].pilots.push_back(PilotRec{p.sender, p.msg, p.box});
-        pilot_key_[{p.sender, p.msg}] = k;
-        touched.push_back(k);
-    }
-    for (const Key& k : touched) try_pulls(k);
+    abort_ = true;
+    cv_.notify_all();
 }
 
-void Communicator::post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready, uint64_t* done,
-                             uint64_t done_val) {
-    std::lock_guard<std::mutex> l(m_);
-    sends_[{node, msg}] = Send{src, ready, done, done_val};
-    auto it = pilot_key_.find({node, msg});
-    if (it != pilot_key_.end()) try_pulls(it->second);
-}
-
-void Communicator::post_dest(int node, int64_t tid, uint32_t buf, const Mem& dst, cudaEvent_t dst_ready) {
-    std::lock_guard<std::mutex> l(m_);
+int Communicator::pull_region(int node, int64_t tid, uint32_t buf, const Region& reg, const Mem& dst,
+                              cudaStream_t stream) {
+    std::unique_lock<std::mutex> l(m_);
     const Key k{node, tid, buf};
-    Recv& r = recv_[k];
-    r.has_dest = true;
-    r.dst = dst;
-    r.dst_ready = dst_ready;
-    try_pulls(k);
-}
-
-void Communicator::post_frag(int node, int64_t tid, uint32_t buf, const Region& reg, uint64_t* counter,
-                             uint64_t base, uint64_t* target, cudaEvent_t* after) {
-    std::lock_guard<std::mutex> l(m_);
-    const Key k{node, tid, buf};
-    Recv& r = recv_[k];
-    // pulls already issued: covered by an event on the communication stream;
-    // later pulls raise the counter
-    uint64_t done = 0;
-    for (const Box& b : r.issued) done += rvolume(rinter(Region{b}, reg));
-    *after = nullptr;
-    if (done) {
-        cudaSetDevice(phys_[node]);
-        cudaEventCreateWithFlags(after, cudaEventDisableTiming);
-        cudaEventRecord(*after, stream_[node]);
+    const uint64_t need = rvolume(reg);
+    // wait until the pilots covering reg are known and their sends issued
+    // (pilots of one transfer are disjoint and tile the awaited region)
+    for (;;) {
+        if (abort_) return E_STATE;
+        uint64_t covered = 0;
+        bool posted = true;
+        auto it = pilots_.find(k);
+        if (it != pilots_.end())
+            for (const PilotRec& p : it->second) {
+                const uint64_t v = rvolume(rinter(Region{p.box}, reg));
+                if (!v) continue;
+                covered += v;
+                if (!p.pulled && !sends_.count({p.sender, p.msg})) posted = false;
+            }
+        if (covered >= need && posted) break;
+        cv_.wait(l);
     }
-    *target = base + (rvolume(reg) - done);
-    r.frags.push_back(Frag{reg, counter, base, 0});
-}
-
-void Communicator::try_pulls(const Key& k) {
-    auto rit = recv_.find(k);
-    if (rit == recv_.end() || !rit->second.has_dest) return;
-    Recv& r = rit->second;
-    for (PilotRec& p : r.pilots) {
-        if (p.issued) continue;
+    for (PilotRec& p : pilots_[k]) {
+        if (p.pulled || rinter(Region{p.box}, reg).empty()) continue;
         auto sit = sends_.find({p.sender, p.msg});
-        if (sit == sends_.end()) continue;
-        pull(k, r, p, sit->second);
-        if (sit->second.ready) cudaEventDestroy(sit->second.ready);
+        Send snd = sit->second;
         sends_.erase(sit);
+        cudaStreamWaitEvent(stream, snd.ready, 0);           // the sender's staged data
+        cudaEventDestroy(snd.ready);
+        CopyArgs args;
+        args.nseg = 0;
+        args.total_units = 0;
+        args.peer = 0;
+        box_seg(args, snd.src.base, snd.src.box, dst.base, dst.box, p.box, dst.es);
+        launch_copy(args, stream);
+        cudaEvent_t done = nullptr;
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, stream);
+        pulled_[{p.sender, p.msg}] = done;
+        p.pulled = true;
+        pulls_++;
+        pull_bytes_ += uint64_t(p.box.volume()) * dst.es;
     }
+    cv_.notify_all();
+    return cudaGetLastError() == cudaSuccess ? E_OK : E_CUDA;
 }
 
-void Communicator::pull(const Key& k, Recv& r, PilotRec& p, Send& snd) {
-    const int node = std::get<0>(k);
-    cudaSetDevice(phys_[node]);
-    cudaStream_t st = stream_[node];
-    cudaStreamWaitEvent(st, snd.ready, 0);                    // the sender's staged data
-    if (r.dst_ready) cudaStreamWaitEvent(st, r.dst_ready, 0); // the receive's own dependencies
-    CopyArgs args;
-    args.nseg = 0;
-    args.total_units = 0;
-    args.peer = 0;
-    box_seg(args, snd.src.base, snd.src.box, r.dst.base, r.dst.box, p.box, r.dst.es);
-    launch_copy(args, st);
-    for (Frag& f : r.frags) {
-        const uint64_t v = rvolume(rinter(Region{p.box}, f.reg));
-        if (!v) continue;
-        f.cum += v;
-        g_drv.write64(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(f.counter), f.base + f.cum,
-                      CU_STREAM_WRITE_VALUE_DEFAULT);
+cudaEvent_t Communicator::wait_pulled(int node, uint64_t msg) {
+    std::unique_lock<std::mutex> l(m_);
+    for (;;) {
+        auto it = pulled_.find({node, msg});
+        if (it != pulled_.end()) {
+            cudaEvent_t e = it->second;
+            pulled_.erase(it);
+            return e;
+        }
+        if (abort_) return nullptr;
+        cv_.wait(l);
     }
-    g_drv.write64(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(snd.done), snd.done_val,
-                  CU_STREAM_WRITE_VALUE_DEFAULT);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess && !err_) {
-        err_ = E_CUDA;
-        errmsg_ = std::string("receive arbitration: ") + cudaGetErrorString(e);
-    }
-    p.issued = true;
-    r.issued.push_back(p.box);
-    pulls_++;
-    pull_bytes_ += uint64_t(p.box.volume()) * r.dst.es;
 }
 
 // Send / receive / split receive / await receive (virtual-node mode, Table 1).
@@ -1318,65 +1260,75 @@ void Executor::exec_transfer(const Instr& ins) {
     const Token deps = local_part(ins.deps);
     const uint32_t es = bufinfo_.at(ins.buffer).es;
     set_dev(0);
-    const int s_sync = S_SYNC, s_send = S_HSIG, s_recv = S_SIG0;   // device 0 of the node
+    const int s_sync = S_SYNC, s_recv = S_SIG0;          // streams of the node's first device
+    const int64_t key = (ins.transfer << 20) ^ int64_t(ins.buffer);
     auto mem = [&](int64_t aid) {
         const AllocRec& a = allocs_.at(aid);
         return Communicator::Mem{base_of(a), a.box, es};
     };
-    auto ready_event = [&]() {          // an event after the instruction's dependencies
-        wait_token(s_sync, deps);
-        cudaEvent_t e = nullptr;
-        check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-        check(cudaEventRecord(e, streams_[s_sync].s), "cudaEventRecord");
-        return e;
-    };
-    auto wait_frag = [&](const Region& reg) {
-        const uint64_t slot = kRing + (frag_seq_ % kRing);
-        const uint64_t base = (++frag_seq_) << 32;
-        uint64_t target = 0;
-        cudaEvent_t after = nullptr;
-        comm.post_frag(cfg_.node, ins.transfer, ins.buffer, reg, vflags_ + slot, base, &target, &after);
-        if (after) {
-            check(cudaStreamWaitEvent(streams_[s_recv].s, after, 0), "cudaStreamWaitEvent");
-            cudaEventDestroy(after);
+    auto pull = [&](const Region& reg, const Communicator::Mem& dst) {
+        wait_token(s_recv, deps);                         // the receive's own dependencies (M1 readers, writers)
+        const int rc = comm.pull_region(cfg_.node, ins.transfer, ins.buffer, reg, dst, streams_[s_recv].s);
+        if (rc != E_OK && !err_) {
+            errmsg_ = "receive arbitration failed";
+            err_ = rc;
         }
-        if (target > base)
-            checkd(g_drv.wait64(reinterpret_cast<CUstream>(streams_[s_recv].s),
-                                reinterpret_cast<CUdeviceptr>(vflags_ + slot), target, CU_STREAM_WAIT_VALUE_GEQ),
-                   "cuStreamWaitValue64");
         return record(s_recv);
     };
     switch (ins.kind) {
     case IKind::Send: {
-        const cudaEvent_t ready = ready_event();
-        const uint64_t slot = send_seq_ % kRing;
-        const uint64_t val = ++send_seq_;
-        comm.post_send(cfg_.node, ins.msg, mem(ins.src_aid), ready, vflags_ + slot, val);
-        // complete once the receiver has pulled the box (the staging copy may then be reused)
-        checkd(g_drv.wait64(reinterpret_cast<CUstream>(streams_[s_send].s),
-                            reinterpret_cast<CUdeviceptr>(vflags_ + slot), val, CU_STREAM_WAIT_VALUE_GEQ),
-               "cuStreamWaitValue64");
-        tok_[ins.iid] = record(s_send);
+        wait_token(s_sync, deps);                         // the staging copy
+        cudaEvent_t ready = nullptr;
+        check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventRecord(ready, streams_[s_sync].s), "cudaEventRecord");
+        comm.post_send(cfg_.node, ins.msg, mem(ins.src_aid), ready);
+        pending_send_[ins.iid] = ins.msg;                 // completes with the receiver's pull
         st_.bytes_copy[5] += uint64_t(ins.box.volume()) * es;
         break;
     }
     case IKind::Receive:
-        comm.post_dest(cfg_.node, ins.transfer, ins.buffer, mem(ins.dst_aid), ready_event());
-        tok_[ins.iid] = wait_frag(ins.region);
+        tok_[ins.iid] = pull(ins.region, mem(ins.dst_aid));
         break;
     case IKind::SplitReceive:
-        comm.post_dest(cfg_.node, ins.transfer, ins.buffer, mem(ins.dst_aid), ready_event());
+        recv_dst_[key] = mem(ins.dst_aid);
         tok_[ins.iid] = deps;
         break;
-    case IKind::AwaitReceive:
-        tok_[ins.iid] = wait_frag(ins.region);
+    case IKind::AwaitReceive: {
+        auto it = recv_dst_.find(key);
+        if (it == recv_dst_.end()) {
+            errmsg_ = "await receive without its split receive";
+            err_ = E_STATE;
+            return;
+        }
+        tok_[ins.iid] = pull(ins.region, it->second);
         break;
+    }
     default:
         break;
     }
-    if (comm.error() && !err_) {
-        errmsg_ = comm.error_msg();
-        err_ = comm.error();
+}
+
+// A send completes when the receiver has pulled its box: resolved when an
+// instruction depending on it is issued (blocking until the receiver has
+// issued the pull -- it only waits for sends of this or earlier tasks).
+void Executor::resolve_sends(const Instr& ins) {
+    for (uint64_t j : ins.deps) {
+        auto it = pending_send_.find(j);
+        if (it == pending_send_.end()) continue;
+        cudaEvent_t e = cfg_.comm->wait_pulled(cfg_.node, it->second);
+        pending_send_.erase(it);
+        if (!e) {
+            if (!err_) {
+                errmsg_ = "communicator aborted";
+                err_ = E_STATE;
+            }
+            return;
+        }
+        const int sidx = S_HSIG;                          // device 0 of the node
+        set_dev(0);
+        check(cudaStreamWaitEvent(streams_[sidx].s, e, 0), "cudaStreamWaitEvent");
+        cudaEventDestroy(e);
+        tok_[j] = record(sidx);
     }
 }
 

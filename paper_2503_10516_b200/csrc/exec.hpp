@@ -50,16 +50,17 @@ struct Token {
 };
 
 // Virtual-node mode: the "communicator" between the node
-// executors of one process.  Sends publish their staged M1 box;
-// receives and await receives register their destination and fragments;
-// pilots arrive from the schedulers at compile time.  Receive
-// arbitration: as soon as a pilot's send has been issued and its transfer's
-// destination is known, the box is pulled into the receiver's M1 allocation by
-// a copy kernel on the receiver's communication stream; the pull then raises
-// the fragment counters the receiver's await-receive waits on (GPU stream
-// memory operations: completion is "as soon as its subregion or a superset
-// thereof has been received") and the sender's completion flag (its
-// staging buffer may be reused).
+// executors of one process.  Pilots arrive from the schedulers at
+// compile time; a send publishes its staged M1 box and the event
+// after its staging copy.  Receive arbitration happens on the receiver's
+// executor thread: a receive (or await receive) waits until the pilots covering
+// its region have arrived and their sends have been issued, then pulls each box
+// into its M1 allocation with a copy kernel on its own stream; completion is
+// "as soon as its subregion or a superset thereof has been received".
+// A send completes with the pull of its box; the sender resolves that event
+// lazily, when an instruction depending on the send is issued.  No GPU-side
+// waits on flags: every cross-node edge is an event of a pull already issued
+// (host-side ordering by task order keeps this deadlock-free).
 class Communicator {
 public:
     struct Mem {
@@ -67,20 +68,17 @@ public:
         Box box;                // allocation box, row-major
         uint32_t es = 0;
     };
-    explicit Communicator(int nodes);
-    ~Communicator();
-    void attach(int node, int phys_dev);
-    void add_pilots(const std::vector<Pilot>& p);
-    void post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready, uint64_t* done, uint64_t done_val);
-    // destination of transfer (tid, buf) on `node`; writes start after `dst_ready`
-    void post_dest(int node, int64_t tid, uint32_t buf, const Mem& dst, cudaEvent_t dst_ready);
-    // a fragment the receiver waits on: counter >= *target, after *after (null if none)
-    void post_frag(int node, int64_t tid, uint32_t buf, const Region& reg, uint64_t* counter, uint64_t base,
-                   uint64_t* target, cudaEvent_t* after);
-    int error() const { return err_; }
-    const std::string& error_msg() const { return errmsg_; }
+    explicit Communicator(int nodes) : nodes_(nodes) {}
+    void add_pilot(const Pilot& p);
+    void post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready);
+    // receiver thread: pull every pilot of transfer (node, tid, buf) that
+    // intersects `reg` and was not pulled yet into `dst`, on `stream`
+    int pull_region(int node, int64_t tid, uint32_t buf, const Region& reg, const Mem& dst, cudaStream_t stream);
+    // sender thread: event after the pull of (node, msg); blocks until issued
+    cudaEvent_t wait_pulled(int node, uint64_t msg);
     uint64_t pulls() const { return pulls_; }
     uint64_t pull_bytes() const { return pull_bytes_; }
+    void abort();                               // wake blocked threads on shutdown / error
 
 private:
     using Key = std::tuple<int, int64_t, uint32_t>;     // (receiver, tid, buffer)
@@ -88,39 +86,19 @@ private:
         int sender;
         uint64_t msg;
         Box box;
-        bool issued = false;
-    };
-    struct Frag {
-        Region reg;
-        uint64_t* counter;
-        uint64_t base;
-        uint64_t cum = 0;
-    };
-    struct Recv {
-        bool has_dest = false;
-        Mem dst;
-        cudaEvent_t dst_ready = nullptr;
-        std::vector<PilotRec> pilots;
-        std::vector<Frag> frags;
-        std::vector<Box> issued;
+        bool pulled = false;
     };
     struct Send {
         Mem src;
         cudaEvent_t ready = nullptr;
-        uint64_t* done = nullptr;
-        uint64_t done_val = 0;
     };
-    void try_pulls(const Key& k);
-    void pull(const Key& k, Recv& r, PilotRec& p, Send& snd);
     std::mutex m_;
+    std::condition_variable cv_;
     int nodes_;
-    std::vector<int> phys_;
-    std::vector<cudaStream_t> stream_;                     // per receiving node
-    std::map<Key, Recv> recv_;
-    std::map<std::pair<int, uint64_t>, Send> sends_;       // (sender, msg)
-    std::map<std::pair<int, uint64_t>, Key> pilot_key_;    // (sender, msg) -> transfer
-    int err_ = 0;
-    std::string errmsg_;
+    bool abort_ = false;
+    std::map<Key, std::vector<PilotRec>> pilots_;
+    std::map<std::pair<int, uint64_t>, Send> sends_;          // posted, not yet pulled
+    std::map<std::pair<int, uint64_t>, cudaEvent_t> pulled_;  // pull done events, until the sender takes them
     uint64_t pulls_ = 0, pull_bytes_ = 0;
 };
 
@@ -366,8 +344,9 @@ private:
     std::unordered_map<uint64_t, std::vector<Instr>> coll_pending_;
     // virtual-node mode: M1 staging arena and the flags sends / receives wait on
     Arena host_arena_;
-    uint64_t* vflags_ = nullptr;                  // [0, kRing) send done flags, [kRing, 2 kRing) fragment counters
-    uint64_t send_seq_ = 0, frag_seq_ = 0;
+    std::unordered_map<uint64_t, uint64_t> pending_send_;      // send iid -> message id, completion not resolved
+    std::unordered_map<int64_t, Communicator::Mem> recv_dst_; // transfer tid * 2^32 + buffer -> split receive destination
+    void resolve_sends(const Instr& ins);
     std::unordered_map<uint64_t, Parts> parts_;
     static constexpr uint64_t kRing = 1u << 16;
 };

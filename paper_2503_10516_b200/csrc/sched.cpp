@@ -932,9 +932,13 @@ void Scheduler::transfers(Cmd& c, std::map<Key, Alloc*>& binding, bool readback_
                 ins.src_aid = m1->aid;
                 ins.src_mem = 1;
                 ins.box = bx;
+                const Pilot pl{node_, ins.msg, target, tid, bid, bx};
+                if (pilot_sink_)
+                    pilot_sink_(pl);
+                else
+                    pilots_.push_back(pl);
                 const uint64_t iid = emit(ins, deps);
                 m1->readers.add(int64_t(iid), Region{bx});
-                pilots_.push_back(Pilot{node_, ins.msg, target, tid, bid, bx});
             }
         }
     }

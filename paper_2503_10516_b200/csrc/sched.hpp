@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <functional>
 #include <map>
 #include <memory>
 #include <set>
@@ -249,6 +250,8 @@ public:
                     const std::map<uint32_t, Region>& awaits);
     void set_node(int n) { node_ = n; }
     int node() const { return node_; }
+    // pilots go to `fn` as they are produced ("transmitted ... ahead of execution time")
+    void set_pilot_sink(std::function<void(const Pilot&)> fn) { pilot_sink_ = std::move(fn); }
     std::vector<Pilot> take_pilots() {
         std::vector<Pilot> p;
         p.swap(pilots_);
@@ -379,6 +382,7 @@ private:
     int node_ = 0;                                    // virtual-node mode: this node's id
     uint64_t next_msg_ = 0;                           // P:L400 "locally unique message id"
     std::vector<Pilot> pilots_;
+    std::function<void(const Pilot&)> pilot_sink_;
     uint64_t coll_min_bytes_ = 1ull << 20;            // CEL_COLL_MIN_BYTES: smallest per-source gather run as NCCL
     uint32_t next_bid_ = 0;
     bool shut_ = false;
