@@ -156,6 +156,8 @@ typedef struct {
                                   staged in pinned host memory (M1), with pilot messages and receive
                                   arbitration.  Node k's instruction log goes to
                                   "<instr_log_path>.<k>"; readbacks gather on node 0.
+                                  Each node's M1 arena is arena_bytes of pinned host
+                                  memory (256 MiB when arena_bytes is 0).
                                   0 or 1 = one node (the default). */
 } cel_config;
 

@@ -132,6 +132,9 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
                 ec.collective = false;
                 ec.node = k;
                 ec.comm = comm;
+                // M1 staging: a pushed or awaited region is staged in one contiguous
+                // allocation over its bounding box, up to a node's whole chunk
+                if (cfg->arena_bytes) ec.host_arena_bytes = cfg->arena_bytes;
                 rt->node_exec.emplace_back(new Executor(ec, nullptr));
                 std::string err;
                 const int rc = rt->node_exec.back()->init(&err);

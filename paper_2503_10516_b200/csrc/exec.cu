@@ -508,6 +508,10 @@ Token Executor::materialize(int dev, const Token& t) {
 }
 
 void Executor::throttle() {
+    // virtual-node mode: never block here -- the oldest event may wait for a
+    // pull another node's executor thread issues only after this thread has
+    // posted a send further down its queue
+    if (cfg_.comm) return;
     for (auto& s : streams_) {
         while (s.inflight.size() > 2048) {
             check(cudaEventSynchronize(s.inflight.front().second), "cudaEventSynchronize");
@@ -736,6 +740,7 @@ void Executor::thread_main() {
         if (it.kind == 0) {
             const uint64_t t0 = now_ns();
             on_instr_impl(it.ins);
+            if (err_ && cfg_.comm) cfg_.comm->abort();   // wake nodes waiting for this one
             st_.exec_ns[int(it.ins.kind)] += now_ns() - t0;
         } else if (it.kind == 1) {
             it.fn();
@@ -921,6 +926,16 @@ void Executor::on_instr_impl(const Instr& ins) {
         // deps older than the applied (previous) horizon are never referenced again.
         Token lt = multi_local_part(ins.deps);
         ltok_[ins.iid] = lt;
+        if (cfg_.comm && prev_horizon_) {
+            // virtual-node mode bounds the run-ahead here (throttle() must not
+            // block): wait for the previous horizon, which only depends on
+            // sends / pulls every node has already issued
+            auto pit = ltok_.find(prev_horizon_);
+            if (pit != ltok_.end())
+                for (const TokEntry& e : pit->second.local)
+                    if (e.seq > streams_[e.stream].done) check(cudaEventSynchronize(e.ev), "horizon wait");
+            st_.host_syncs++;
+        }
         Token t = lt;
         for (int r = 0; r < cfg_.world; ++r)
             if (r != cfg_.rank) t.remote.push_back({r, ins.iid});
