@@ -2,7 +2,7 @@
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Follows PAPER.md §2.4,
 §3 and §4.3 step by step, in the order and notation of the paper; where the
-paper is silent the DESIGN.md reading (R0-R16) is cited.
+paper is silent the DESIGN.md reading (R0-R17) is cited.
 
 Topology (R0, §3.2): one node, G devices D0..D(G-1); memory ids
 M0 = user host, M1 = pinned host (never used: B200/NVSwitch supports d2d,
