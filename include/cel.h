@@ -102,6 +102,11 @@ typedef struct {
     void* base;                /* device pointer of the allocation (element alloc_box.min) */
     cel_box alloc_box;         /* buffer box the allocation covers, dense row-major */
     uint32_t elem_size;
+    cel_box range;             /* the range mapper's region for this chunk: what the kernel may access */
+    long long* oob;            /* bounds checking on (cel_config.bounds_check): device record
+                                  [min z,y,x, max+1 z,y,x] of accesses outside `range`, to be
+                                  updated with cel_check_access() (include/cel_device.cuh);
+                                  NULL when off */
 } cel_accessor;
 
 /* User kernel: called on the scheduling thread with the device's stream; it
@@ -148,6 +153,12 @@ typedef struct {
                                   devices are distinct GPUs; 0: as peer pushes.  The instruction graph
                                   is the same either way.  NCCL (libnccl.so.2) is opened at run time;
                                   a failed communicator setup is CEL_E_NCCL (sticky). */
+    int32_t bounds_check;      /* §4.4 accessor bounds checking: kernels run their
+                                  scalar variants, every element access is checked against the
+                                  range mapper's region, and the bounding box of the accesses
+                                  outside it is reported after the kernel exits as a sticky
+                                  CEL_E_OUT_OF_BOUNDS error ("task T device D accessor A ...").
+                                  Debug aid: slower kernels, results unchanged. */
     int32_t n_nodes;           /* virtual-node mode (§3.4, §4.2): > 1 runs
                                   n_nodes node schedulers of n_devices devices each in this process;
                                   cuda_devices then lists n_nodes * n_devices entries (node-major).

@@ -52,7 +52,8 @@ class cel_kernel_params(C.Structure):
 
 
 class cel_accessor(C.Structure):
-    _fields_ = [("base", C.c_void_p), ("alloc_box", cel_box), ("elem_size", C.c_uint32)]
+    _fields_ = [("base", C.c_void_p), ("alloc_box", cel_box), ("elem_size", C.c_uint32), ("range", cel_box),
+                ("oob", C.c_void_p)]
 
 
 cel_kernel_fn = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(cel_box), C.POINTER(cel_accessor), C.c_int,
@@ -70,7 +71,7 @@ class cel_config(C.Structure):
                 ("lookahead", C.c_int32), ("horizon_step", C.c_int32), ("checks", C.c_int32),
                 ("instr_log_path", C.c_char_p), ("arena_bytes", C.c_uint64), ("rank", C.c_int32),
                 ("world", C.c_int32), ("fast_math", C.c_int32), ("collective", C.c_int32),
-                ("n_nodes", C.c_int32)]
+                ("bounds_check", C.c_int32), ("n_nodes", C.c_int32)]
 
 
 class cel_stats(C.Structure):
@@ -174,7 +175,8 @@ class Runtime:
     """The C-ABI runtime.  Method names follow include/cel.h (cel_ prefix dropped)."""
 
     def __init__(self, n_devices, cuda_devices=None, execute=True, lookahead="auto", horizon_step=4, checks=True,
-                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False, collective=True, n_nodes=1):
+                 instr_log_path=None, arena_bytes=0, rank=0, world=1, fast_math=False, collective=True, n_nodes=1,
+                 bounds_check=False):
         """n_nodes > 1: virtual-node mode, n_nodes nodes of n_devices devices each
         (cuda_devices lists n_nodes * n_devices entries, node-major); node k's
         instruction log is written to instr_log_path + ".k"."""
@@ -194,6 +196,7 @@ class Runtime:
         cfg.fast_math = 1 if fast_math else 0
         cfg.collective = 1 if collective else 0
         cfg.n_nodes = int(n_nodes)
+        cfg.bounds_check = 1 if bounds_check else 0
         h = _P()
         _check(lib.cel_runtime_create(C.byref(cfg), C.byref(h)))
         self.h = h

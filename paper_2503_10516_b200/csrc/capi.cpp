@@ -130,6 +130,7 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
                 ec.arena_bytes = cfg->arena_bytes;
                 ec.fast_math = cfg->fast_math != 0;
                 ec.collective = false;
+                ec.bounds_check = cfg->bounds_check != 0;
                 ec.node = k;
                 ec.comm = comm;
                 // M1 staging: a pushed or awaited region is staged in one contiguous
@@ -173,6 +174,7 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
         ec.arena_bytes = cfg->arena_bytes;
         ec.fast_math = cfg->fast_math != 0;
         ec.collective = cfg->collective != 0;
+        ec.bounds_check = cfg->bounds_check != 0;
         rt->exec = std::make_unique<Executor>(ec, nullptr);
         std::string err;
         const int rc = rt->exec->init(&err);

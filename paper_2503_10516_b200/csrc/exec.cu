@@ -193,6 +193,11 @@ Executor::~Executor() {
     for (auto& kv : host_init_)
         if (kv.second.second) cudaFreeHost(kv.second.first);
     if (host_arena_.base) cudaFreeHost(host_arena_.base);
+    for (auto& r : oob_pending_) cudaEventDestroy(r.ev);
+    for (long long* p : oob_dev_)
+        if (p) cudaFree(p);
+    for (long long* p : oob_host_)
+        if (p) cudaFreeHost(p);
 }
 
 void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
@@ -309,6 +314,23 @@ int Executor::init(std::string* err) {
                 memcpy(nccl_id_, &id, sizeof id);
                 nccl_id_set_ = true;
             }
+        }
+    }
+    if (cfg_.bounds_check) {
+        oob_dev_.assign(G_, nullptr);
+        oob_host_.assign(G_, nullptr);
+        oob_next_.assign(G_, 0);
+        for (int d = 0; d < G_; ++d) {
+            if (!owned(d)) continue;
+            set_dev(d);
+            const size_t bytes = size_t(kOobSlots) * kMaxAcc * 6 * sizeof(long long);
+            void* h = nullptr;
+            if (cudaMalloc(&oob_dev_[d], bytes) != cudaSuccess || cudaHostAlloc(&h, bytes, cudaHostAllocPortable) != cudaSuccess) {
+                cudaGetLastError();
+                *err = "cannot allocate bounds-check records";
+                return E_OOM;
+            }
+            oob_host_[d] = static_cast<long long*>(h);
         }
     }
     if (cfg_.comm) {
@@ -435,6 +457,74 @@ void Executor::poll(bool prune) {
         }
     }
     (void)prune;
+    if (!oob_pending_.empty()) oob_check(false);
+}
+
+// §4.4 accessor bounds checking: claim the next record slot of `dev` and reset it
+long long* Executor::oob_begin(int dev, int sidx, int n_acc) {
+    // the ring slot must have been inspected: wait for its launch if still pending
+    while (!oob_pending_.empty() && int(oob_pending_.size()) >= kOobSlots) {
+        check(cudaEventSynchronize(oob_pending_.front().ev), "bounds-check wait");
+        oob_check(false);
+    }
+    const int slot = oob_next_[dev];
+    long long* rec = oob_dev_[dev] + size_t(slot) * kMaxAcc * 6;
+    launch_oob_init(rec, n_acc, streams_[sidx].s);
+    return rec;
+}
+
+void Executor::oob_end(int dev, int sidx, const Instr& ins, const TaskDesc& d, int n_acc) {
+    const int slot = oob_next_[dev];
+    oob_next_[dev] = (slot + 1) % kOobSlots;
+    const size_t off = size_t(slot) * kMaxAcc * 6;
+    check(cudaMemcpyAsync(oob_host_[dev] + off, oob_dev_[dev] + off, size_t(n_acc) * 6 * sizeof(long long),
+                          cudaMemcpyDeviceToHost, streams_[sidx].s),
+          "bounds-check record copy");
+    OobRec r;
+    r.dev = dev;
+    r.slot = slot;
+    check(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming), "cudaEventCreate");
+    check(cudaEventRecord(r.ev, streams_[sidx].s), "cudaEventRecord");
+    r.iid = ins.iid;
+    r.task = ins.task;
+    r.n_acc = n_acc;
+    for (int i = 0; i < n_acc; ++i) {
+        r.buf[i] = d.acc[i].buf;
+        r.range[i] = map_access(d.acc[i].map, ins.chunk, bufinfo_.at(d.acc[i].buf).extent);
+    }
+    oob_pending_.push_back(r);
+}
+
+// Inspect the records of exited kernels ("report their bounding box in a
+// runtime error message after the kernel exits").
+void Executor::oob_check(bool wait) {
+    while (!oob_pending_.empty()) {
+        OobRec& r = oob_pending_.front();
+        if (wait) {
+            check(cudaEventSynchronize(r.ev), "bounds-check wait");
+        } else {
+            const cudaError_t q = cudaEventQuery(r.ev);
+            if (q == cudaErrorNotReady) return;
+        }
+        const long long* h = oob_host_[r.dev] + size_t(r.slot) * kMaxAcc * 6;
+        for (int i = 0; i < r.n_acc && !err_; ++i) {
+            const long long* b = h + 6 * i;
+            if (b[0] > b[3] - 1) continue;            // nothing recorded
+            char msg[400];
+            const Box& g = r.range[i];
+            snprintf(msg, sizeof msg,
+                     "accessor out of bounds: task %lld, device %d, accessor %d (buffer %u) accessed "
+                     "[[%lld,%lld,%lld],[%lld,%lld,%lld]] outside its range-mapper region "
+                     "[[%lld,%lld,%lld],[%lld,%lld,%lld]]",
+                     (long long)r.task, r.dev, i, r.buf[i], b[0], b[1], b[2], b[3], b[4], b[5], (long long)g.lo[0],
+                     (long long)g.lo[1], (long long)g.lo[2], (long long)g.hi[0], (long long)g.hi[1],
+                     (long long)g.hi[2]);
+            errmsg_ = msg;
+            err_ = E_OUT_OF_BOUNDS;
+        }
+        cudaEventDestroy(r.ev);
+        oob_pending_.pop_front();
+    }
 }
 
 Token Executor::dep_token(uint64_t j) const {
@@ -993,6 +1083,7 @@ void Executor::exec_epoch(const Instr& ins) {
     }
     st_.host_syncs++;
     poll(true);
+    if (!oob_pending_.empty()) oob_check(true);
     for (uint32_t bid : host_drop_) {
         auto it = host_init_.find(bid);
         if (it != host_init_.end()) {
@@ -1638,12 +1729,22 @@ void Executor::exec_kernel(const Instr& ins) {
             auto it = allocs_.find(aid);
             memset(&acc[i], 0, sizeof acc[i]);
             if (it == allocs_.end()) continue;
-            acc[i].base = arenas_[it->second.dev].base + it->second.off;
+            acc[i].base = base_of(it->second);
             for (int k = 0; k < 3; ++k) {
                 acc[i].alloc_box.min[k] = uint64_t(it->second.box.lo[k]);
                 acc[i].alloc_box.max[k] = uint64_t(it->second.box.hi[k]);
             }
             acc[i].elem_size = it->second.es;
+            const Box rg = map_access(d.acc[i].map, ins.chunk, bufinfo_.at(d.acc[i].buf).extent);
+            for (int k = 0; k < 3; ++k) {
+                acc[i].range.min[k] = uint64_t(rg.lo[k]);
+                acc[i].range.max[k] = uint64_t(rg.hi[k]);
+            }
+        }
+        const int n_chk = int(std::min<size_t>(acc.size(), kMaxAcc));
+        if (cfg_.bounds_check && n_chk) {
+            long long* rec = oob_begin(dev, sidx, n_chk);
+            for (int i = 0; i < n_chk; ++i) acc[i].oob = rec + 6 * i;
         }
         cel_box ch;
         for (int k = 0; k < 3; ++k) {
@@ -1651,6 +1752,7 @@ void Executor::exec_kernel(const Instr& ins) {
             ch.max[k] = uint64_t(ins.chunk.hi[k]);
         }
         if (d.fn) d.fn(d.fn_user, dev, &ch, acc.data(), int(acc.size()), streams_[sidx].s);
+        if (cfg_.bounds_check && n_chk) oob_end(dev, sidx, ins, d, n_chk);
         tok_[ins.iid] = record(sidx);
         return;
     }
@@ -1687,7 +1789,7 @@ void Executor::exec_kernel(const Instr& ins) {
         }
         auto it = allocs_.find(ins.bindings[i]);
         if (it != allocs_.end()) {
-            A.base = arenas_[it->second.dev].base + it->second.off;
+            A.base = base_of(it->second);
             for (int k = 0; k < 3; ++k) {
                 A.lo[k] = it->second.box.lo[k];
                 A.n[k] = it->second.box.extent(k);
@@ -1720,6 +1822,13 @@ void Executor::exec_kernel(const Instr& ins) {
         // chain (a launch costs a few microseconds; tiny chunks are latency-bound)
         if (interior.empty() || interior.volume() < (uint64_t(1) << 18)) split = false;
     }
+    long long* oob = nullptr;
+    if (cfg_.bounds_check && a.n_acc) {
+        split = false;                            // one record per instruction, one launch stream
+        oob = oob_begin(dev, sidx, a.n_acc);
+        a.checked = 1;
+        for (int i = 0; i < a.n_acc; ++i) a.acc[i].oob = oob + 6 * i;
+    }
     auto launch = [&](const Box& ch, int stream, bool shell_part) {
         KArgs b = a;
         for (int k = 0; k < 3; ++k) {
@@ -1749,6 +1858,7 @@ void Executor::exec_kernel(const Instr& ins) {
     };
     if (!split) {
         launch(ins.chunk, sidx, false);
+        if (oob) oob_end(dev, sidx, ins, d, a.n_acc);
         tok_[ins.iid] = record(sidx);
         return;
     }

@@ -112,6 +112,7 @@ struct ExecConfig {
     int node = 0;                      // virtual-node mode: this executor's node
     std::shared_ptr<Communicator> comm;
     uint64_t host_arena_bytes = 256ull << 20;   // M1 (pinned, mapped) staging arena, virtual-node mode
+    bool bounds_check = false;                  // §4.4 accessor bounds checking
 };
 
 struct ExecStats {
@@ -267,6 +268,25 @@ private:
     void prune_tokens(uint64_t below);
     void note_use(const Instr& ins);
     void exec_transfer(const Instr& ins);
+    // accessor bounds checking (§4.4): per-launch device records, copied to
+    // pinned host memory after the kernel and inspected once it has exited
+    struct OobRec {
+        int dev;
+        int slot;
+        cudaEvent_t ev;
+        uint64_t iid;
+        int64_t task;
+        int n_acc;
+        uint32_t buf[kMaxAcc];
+        Box range[kMaxAcc];
+    };
+    long long* oob_begin(int dev, int sidx, int n_acc);   // device record of the next launch
+    void oob_end(int dev, int sidx, const Instr& ins, const TaskDesc& d, int n_acc);
+    void oob_check(bool wait);
+    std::vector<long long*> oob_dev_, oob_host_;
+    std::vector<int> oob_next_;
+    std::deque<OobRec> oob_pending_;
+    static constexpr int kOobSlots = 1024;
     void exec_host_copy(const Instr& ins, const Token& deps);
     Arena& arena(int dev) { return dev < 0 ? host_arena_ : arenas_[dev]; }
     char* base_of(const AllocRec& r) { return (r.dev < 0 ? host_arena_.base : arenas_[r.dev].base) + r.off; }

@@ -208,6 +208,33 @@ __device__ __forceinline__ T* ptr(const DAcc& A, int64_t z, int64_t y, int64_t x
 }
 __device__ __forceinline__ int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Accessor bounds checking (§4.4): an element access outside the
+// range-mapper region of its accessor is recorded (bounding box by atomic
+// min / max) and reported by the executor after the kernel exits; the access
+// itself is redirected to the allocation base when it also leaves the
+// allocation, so a wrong range mapper cannot fault the kernel.
+template <class T>
+__device__ __forceinline__ T* at(const DAcc& A, int64_t z, int64_t y, int64_t x) {
+    if (A.oob && (z < A.box.lo[0] || z >= A.box.hi[0] || y < A.box.lo[1] || y >= A.box.hi[1] ||
+                  x < A.box.lo[2] || x >= A.box.hi[2])) {
+        atomicMin(&A.oob[0], (long long)z);
+        atomicMin(&A.oob[1], (long long)y);
+        atomicMin(&A.oob[2], (long long)x);
+        atomicMax(&A.oob[3], (long long)z + 1);
+        atomicMax(&A.oob[4], (long long)y + 1);
+        atomicMax(&A.oob[5], (long long)x + 1);
+        if (z < A.lo[0] || z >= A.lo[0] + A.n[0] || y < A.lo[1] || y >= A.lo[1] + A.n[1] || x < A.lo[2] ||
+            x >= A.lo[2] + A.n[2])
+            return reinterpret_cast<T*>(A.base);
+    }
+    return ptr<T>(A, z, y, x);
+}
+
+__global__ void oob_init_kernel(long long* rec, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 6 * n) rec[i] = (i % 6) < 3 ? 0x7fffffffffffffffLL : (-0x7fffffffffffffffLL - 1);
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -272,10 +299,10 @@ __global__ void stencil3_kernel(const __grid_constant__ KArgs a) {
     const int64_t n = S.ext[0];
     for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
          i += int64_t(gridDim.x) * blockDim.x) {
-        const float xm = *ptr<const float>(S, clampi(i - 1, 0, n - 1), 0, 0);
-        const float xc = *ptr<const float>(S, i, 0, 0);
-        const float xp = *ptr<const float>(S, clampi(i + 1, 0, n - 1), 0, 0);
-        *ptr<float>(D, i, 0, 0) = (0.25f * xm + 0.5f * xc) + 0.25f * xp;
+        const float xm = *at<const float>(S, clampi(i - 1, 0, n - 1), 0, 0);
+        const float xc = *at<const float>(S, i, 0, 0);
+        const float xp = *at<const float>(S, clampi(i + 1, 0, n - 1), 0, 0);
+        *at<float>(D, i, 0, 0) = (0.25f * xm + 0.5f * xc) + 0.25f * xp;
     }
 }
 
@@ -294,12 +321,12 @@ __global__ void wave5_scalar(const __grid_constant__ KArgs a) {
     const int64_t E0 = U.ext[0], E1 = U.ext[1];
     for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < nr * nc; t += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = r0 + t / nc, c = c0 + t % nc;
-        const float uc = *ptr<const float>(U, r, c, 0);
-        const float un = *ptr<const float>(U, clampi(r - 1, 0, E0 - 1), c, 0);
-        const float us = *ptr<const float>(U, clampi(r + 1, 0, E0 - 1), c, 0);
-        const float uw = *ptr<const float>(U, r, clampi(c - 1, 0, E1 - 1), 0);
-        const float ue = *ptr<const float>(U, r, clampi(c + 1, 0, E1 - 1), 0);
-        float* pp = ptr<float>(P, r, c, 0);
+        const float uc = *at<const float>(U, r, c, 0);
+        const float un = *at<const float>(U, clampi(r - 1, 0, E0 - 1), c, 0);
+        const float us = *at<const float>(U, clampi(r + 1, 0, E0 - 1), c, 0);
+        const float uw = *at<const float>(U, r, clampi(c - 1, 0, E1 - 1), 0);
+        const float ue = *at<const float>(U, r, clampi(c + 1, 0, E1 - 1), 0);
+        float* pp = at<float>(P, r, c, 0);
         *pp = wave1(uc, *pp, un, us, uw, ue);
     }
 }
@@ -375,14 +402,14 @@ __global__ void jacobi7_scalar(const __grid_constant__ KArgs a) {
         const int64_t x = ch.lo[2] + t % n2;
         const int64_t y = ch.lo[1] + (t / n2) % n1;
         const int64_t z = ch.lo[0] + t / (n1 * n2);
-        const float c = *ptr<const float>(A, z, y, x);
-        const float zm = *ptr<const float>(A, clampi(z - 1, 0, E0 - 1), y, x);
-        const float zp = *ptr<const float>(A, clampi(z + 1, 0, E0 - 1), y, x);
-        const float ym = *ptr<const float>(A, z, clampi(y - 1, 0, E1 - 1), x);
-        const float yp = *ptr<const float>(A, z, clampi(y + 1, 0, E1 - 1), x);
-        const float xm = *ptr<const float>(A, z, y, clampi(x - 1, 0, E2 - 1));
-        const float xp = *ptr<const float>(A, z, y, clampi(x + 1, 0, E2 - 1));
-        *ptr<float>(B, z, y, x) = jac1(c, zm, zp, ym, yp, xm, xp);
+        const float c = *at<const float>(A, z, y, x);
+        const float zm = *at<const float>(A, clampi(z - 1, 0, E0 - 1), y, x);
+        const float zp = *at<const float>(A, clampi(z + 1, 0, E0 - 1), y, x);
+        const float ym = *at<const float>(A, z, clampi(y - 1, 0, E1 - 1), x);
+        const float yp = *at<const float>(A, z, clampi(y + 1, 0, E1 - 1), x);
+        const float xm = *at<const float>(A, z, y, clampi(x - 1, 0, E2 - 1));
+        const float xp = *at<const float>(A, z, y, clampi(x + 1, 0, E2 - 1));
+        *at<float>(B, z, y, x) = jac1(c, zm, zp, ym, yp, xm, xp);
     }
 }
 
@@ -567,11 +594,11 @@ __global__ void __launch_bounds__(kNbTile) nbody_step_kernel(const __grid_consta
     const bool valid = i < a.chunk.hi[0];
     const int64_t N = P.ext[0];
     float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid) pi = *ptr<const float4>(P, i, 0, 0);
+    if (valid) pi = *at<const float4>(P, i, 0, 0);
     float ax = 0.f, ay = 0.f, az = 0.f;
     for (int64_t j0 = 0; j0 < N; j0 += kNbTile) {
         const int64_t j = j0 + threadIdx.x;
-        sp[threadIdx.x] = j < N ? *ptr<const float4>(P, j, 0, 0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sp[threadIdx.x] = j < N ? *at<const float4>(P, j, 0, 0) : make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
         const int jn = N - j0 < kNbTile ? int(N - j0) : kNbTile;
         for (int k = 0; k < jn; ++k) {
@@ -587,7 +614,7 @@ __global__ void __launch_bounds__(kNbTile) nbody_step_kernel(const __grid_consta
         __syncthreads();
     }
     if (valid) {
-        float4* vp = ptr<float4>(V, i, 0, 0);
+        float4* vp = at<float4>(V, i, 0, 0);
         float4 v = *vp;
         const float c = NB_DT * NB_MASS;
         v.x = v.x + c * ax;
@@ -780,8 +807,8 @@ __global__ void nbody_update_kernel(const __grid_constant__ KArgs a) {
     const DAcc& P = a.acc[1];
     for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
          i += int64_t(gridDim.x) * blockDim.x) {
-        const float4 v = *ptr<const float4>(V, i, 0, 0);
-        float4* pp = ptr<float4>(P, i, 0, 0);
+        const float4 v = *at<const float4>(V, i, 0, 0);
+        float4* pp = at<float4>(P, i, 0, 0);
         float4 p = *pp;
         p.x = p.x + NB_DT * v.x;
         p.y = p.y + NB_DT * v.y;
@@ -803,6 +830,26 @@ __device__ __forceinline__ float ld_policy(const float* p, uint64_t pol) {
     float v;
     asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
     return v;
+}
+
+// Bounds-checked variant: every element access through at() (§4.4).
+__global__ void rsim_row_checked(const __grid_constant__ KArgs a) {
+    const DAcc& R = a.acc[0];
+    const DAcc& Wr = a.acc[1];
+    const int64_t t = a.t;
+    const int64_t W = R.ext[1];
+    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
+         i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int64_t s = 0; s < t; ++s) {
+            int64_t c = i + s;
+            c = c >= W ? c - W : c;
+            acc = acc + *at<const float>(R, s, c, 0);
+        }
+        const float prev = *at<const float>(R, t - 1, i, 0);
+        const float coef = 0.5f / float(t);
+        *at<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
+    }
 }
 
 // Software-pipelined variant: the next group of U loads is issued before the
@@ -1013,7 +1060,7 @@ __global__ void __launch_bounds__(128) rsim_row_kernel(const __grid_constant__ K
 // ------------------------------------------------------------------ integer probe
 __device__ uint32_t probe_sum(const DAcc& A, int64_t z, int64_t y, int64_t x) {
     if (A.mode == 3 || A.map == 0)  // read_write or one_to_one: the element itself
-        return *ptr<const uint32_t>(A, z, y, x);
+        return *at<const uint32_t>(A, z, y, x);
     int64_t lo[3], hi[3];
     if (A.map == 2) {  // all
         for (int d = 0; d < 3; ++d) { lo[d] = 0; hi[d] = A.ext[d]; }
@@ -1029,7 +1076,7 @@ __device__ uint32_t probe_sum(const DAcc& A, int64_t z, int64_t y, int64_t x) {
     uint32_t s = 0;
     for (int64_t a0 = lo[0]; a0 < hi[0]; ++a0)
         for (int64_t a1 = lo[1]; a1 < hi[1]; ++a1)
-            for (int64_t a2 = lo[2]; a2 < hi[2]; ++a2) s += *ptr<const uint32_t>(A, a0, a1, a2);
+            for (int64_t a2 = lo[2]; a2 < hi[2]; ++a2) s += *at<const uint32_t>(A, a0, a1, a2);
     return s;
 }
 
@@ -1049,7 +1096,7 @@ __global__ void probe_kernel(const __grid_constant__ KArgs a, int w) {
             if (A.mode != 1 && A.mode != 3) continue;
             h = fmix32(h ^ probe_sum(A, z, y, x));
         }
-        *ptr<uint32_t>(O, z, y, x) = h;
+        *at<uint32_t>(O, z, y, x) = h;
     }
 }
 
@@ -1076,6 +1123,10 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 }  // namespace
 
 void set_copy_blocks_per_sm(int n) { g_copy_blocks_per_sm = n > 0 ? n : 8; }
+
+void launch_oob_init(long long* rec, int n, cudaStream_t s) {
+    oob_init_kernel<<<1, 64, 0, s>>>(rec, n);
+}
 
 int launch_copy(const CopyArgs& a, cudaStream_t s) {
     if (a.total_units == 0 || a.nseg == 0) return 0;
@@ -1131,7 +1182,7 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         const DAcc& U = a.acc[0];
         const DAcc& P = a.acc[1];
         const int64_t c0 = a.chunk.lo[1], w = a.chunk.hi[1] - c0;
-        const bool vec = U.es == 4 && P.es == 4 && U.n[2] == 1 && P.n[2] == 1 && U.n[1] % 4 == 0 &&
+        const bool vec = !a.checked && U.es == 4 && P.es == 4 && U.n[2] == 1 && P.n[2] == 1 && U.n[1] % 4 == 0 &&
                          P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
                          aligned16(U.base) && aligned16(P.base);
         if (vec) {
@@ -1162,7 +1213,7 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         const DAcc& A = a.acc[0];
         const DAcc& B = a.acc[1];
         const int64_t x0 = a.chunk.lo[2], w = a.chunk.hi[2] - x0;
-        const bool vec = A.es == 4 && B.es == 4 && A.n[2] % 4 == 0 && B.n[2] % 4 == 0 && (x0 - A.lo[2]) % 4 == 0 &&
+        const bool vec = !a.checked && A.es == 4 && B.es == 4 && A.n[2] % 4 == 0 && B.n[2] % 4 == 0 && (x0 - A.lo[2]) % 4 == 0 &&
                          (x0 - B.lo[2]) % 4 == 0 && w % 4 == 0 && aligned16(A.base) && aligned16(B.base);
         static int use_tma = -1;
         static bool attr_set[64] = {};
@@ -1199,7 +1250,9 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             const char* e = getenv("CEL_NBODY");
             variant = (e && e[0] == '1') ? 1 : ((e && e[0] == '2') ? 2 : 3);
         }
-        if (a.fast && variant == 3)
+        if (a.checked)
+            nbody_step_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
+        else if (a.fast && variant == 3)
             nbody_step_fast_x2_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), 128, 0, s>>>(a);
         else if (a.fast && variant == 2)
             nbody_step_fast2_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), 128, 0, s>>>(a);
@@ -1232,6 +1285,10 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             variant = e ? atoi(e) : 5;
         }
         const DAcc& R0 = a.acc[0];
+        if (a.checked) {
+            rsim_row_checked<<<grid_for(cv, 128), 128, 0, s>>>(a);
+            return 1;
+        }
         CUtensorMap tm;
         if (variant == 5 && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
             R0.lo[2] == 0 && R0.es == 4 && R0.ext[1] >= 2 * kRB && R0.lo[0] == 0 &&

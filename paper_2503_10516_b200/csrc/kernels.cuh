@@ -47,6 +47,8 @@ struct DAcc {
     int64_t border[3];
     DBox fixed;
     DBox box;                  // mapped box of this access for the chunk
+    long long* oob;            // accessor bounds checking (§4.4): [min z,y,x, max+1 z,y,x] of
+                               // accesses outside `box`, or null when checking is off
 };
 
 constexpr int kMaxAcc = 6;
@@ -61,6 +63,7 @@ struct KArgs {
     uint32_t salt;
     int fast;                  // fast-math variant (FMA + rsqrt) of ALU-bound kernels
     int strip;                 // rows per CTA of the stencil kernels (0 = default)
+    int checked;               // bounds checking: scalar kernels whose accesses go through at()
     DAcc acc[kMaxAcc];
 };
 
@@ -81,6 +84,8 @@ enum : int {
 
 // Returns the number of kernel launches issued (0 if nothing to do).
 int launch_copy(const CopyArgs& a, cudaStream_t s);
+// bounds-check records: n accessors x [min z,y,x = +inf, max z,y,x = -inf]
+void launch_oob_init(long long* rec, int n, cudaStream_t s);
 int launch_workload(const KArgs& a, cudaStream_t s);
 
 void set_copy_blocks_per_sm(int n);

@@ -306,3 +306,48 @@ def test_rsim_full_width(cel):
     prog = P.rsim(84000, 48)
     for mode in ("none", "auto"):
         run_both(cel, prog, 4, mode, arena=256 << 20)
+
+
+# ------------------------------------------------------------ §4.4 accessor bounds checking
+def test_bounds_check_reports_out_of_range_accesses(cel):
+    """a 3-point stencil declared with a one_to_one read (instead of
+    neighborhood(1)) reads one element past each chunk: the runtime reports the
+    bounding box of the offending accesses after the kernel exits."""
+    n = 4096
+    prog = {"name": "oob", "buffers": [{"dims": 1, "extent": [n], "elem_size": 4, "host_init": None},
+                                       {"dims": 1, "extent": [n], "elem_size": 4, "host_init": None}],
+            "ops": [P._task(1, P.full([n]), "fill_hash", [(0, "write", ("one_to_one",))], {"seed": 7}),
+                    P._task(1, P.full([n]), "stencil3", [(0, "read", ("one_to_one",)),
+                                                         (1, "write", ("one_to_one",))])]}
+    rt = cel.Runtime(2, cuda_devices=[0, 0], arena_bytes=64 << 20, bounds_check=True)
+    for b in prog["buffers"]:
+        rt.buffer_create(b["dims"], b["extent"], b["elem_size"])
+    with pytest.raises(cel.CelError) as e:
+        for op in prog["ops"]:
+            rt.task_submit(op[1])
+        rt.wait()
+    assert e.value.code == -2
+    msg = str(e.value)
+    # device 0 owns [0, 2048): its only out-of-range read is element 2048
+    assert "accessor out of bounds" in msg and "device 0, accessor 0" in msg
+    assert "[[2048,0,0],[2049,1,1]]" in msg and "[[0,0,0],[2048,1,1]]" in msg
+    with pytest.raises(cel.CelError):       # sticky: the runtime is poisoned
+        rt.wait()
+
+
+@pytest.mark.parametrize("G", [1, 2, 3])
+def test_bounds_check_no_false_positives(cel, G):
+    """Zero false positives on the paper's workloads and random probe
+    programs; with checking on the kernels take their scalar paths, so this is
+    also parity of those paths."""
+    progs = [P.c1_chain(4096), P.wavesim(515, 5, rows=130), P.jacobi3d(24, 3), P.nbody(700, 2), P.rsim(1000, 12),
+             P.nbody(300, 2, host_init=True)] + [P.random_program(8800 + 5 * G + s) for s in range(6)]
+    for prog in progs:
+        rt = cel.Runtime(G, cuda_devices=[0] * G, arena_bytes=64 << 20, bounds_check=True)
+        got = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
+        o = OracleRuntime(G)
+        run_program(o, prog)
+        exp = simulate(o)
+        for k, arr in enumerate(got):
+            defined = exp[k] != np.uint32(0x7FC00BAD)
+            assert np.array_equal(arr[defined], exp[k][defined]), prog["name"]
