@@ -245,7 +245,9 @@ int cel_stats_get(cel_runtime* rt, cel_stats* out);
  * k = 12 for the boundary (shell) launches of stencil kernels that are split
  * for halo overlap (their interiors count under the kernel's kind) and k = 13
  * for NCCL all-gather groups (per device, broadcast group start to end).
- * n = array length (14). */
+ * n = array length (14).  cel_profile_enable(rt, k): k = 0 off, k >= 1 times
+ * every k-th launch of each kind (count[] = timed launches, so ms/count stays
+ * the average launch duration with 1/k of the event overhead). */
 int cel_profile_enable(cel_runtime* rt, int32_t on);
 int cel_profile_read(cel_runtime* rt, double* ms, uint64_t* count, int32_t n);
 

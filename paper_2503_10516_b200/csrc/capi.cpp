@@ -383,8 +383,8 @@ int cel_profile_enable(cel_runtime* rt, int32_t on) {
     if (int rc = check_poison(rt)) return rc;
     if (execs(rt).empty()) return fail(CEL_E_STATE, "runtime does not execute");
     for (Executor* e : execs(rt)) {
-        e->set_profile(on != 0);
-        if (on) e->profile_reset();
+        e->set_profile(on > 0 ? on : 0);
+        if (on > 0) e->profile_reset();
     }
     return after(rt, CEL_OK);
 }

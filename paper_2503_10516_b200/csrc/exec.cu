@@ -848,10 +848,12 @@ void Executor::add_buffer(uint32_t bid, const Box& extent, uint32_t es) {
     post([this, bid, extent, es] { bufinfo_[bid] = BufInfo{extent, es}; });
 }
 
-void Executor::set_profile(bool on) {
+void Executor::set_profile(int stride) {
     drain();
-    cfg_.profile = on;
-    if (!on) return;
+    cfg_.profile = stride > 0;
+    prof_stride_ = stride > 0 ? stride : 1;
+    for (auto& c : prof_ctr_) c = 0;
+    if (!cfg_.profile) return;
     // time origin of the trace on every owned device
     trace_ref_.assign(G_, nullptr);
     trace_recs_.clear();
@@ -1538,7 +1540,7 @@ void Executor::exec_copy(const Instr& ins) {
         uint64_t bytes = 0;
         auto flush = [&]() {
             if (args.nseg == 0) return;
-            if (cfg_.profile) {
+            if (cfg_.profile && prof_sample(args.peer ? K_NUM + 1 : K_NUM)) {
                 Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev, ins.iid, sidx, now_ns()};
                 cudaEventRecord(p.a, streams_[sidx].s);
                 st_.kernel_launches += launch_copy(args, streams_[sidx].s);
@@ -1843,7 +1845,7 @@ void Executor::exec_kernel(const Instr& ins) {
             }
         }
         int n;
-        if (cfg_.profile) {
+        if (cfg_.profile && prof_sample(shell_part ? K_NUM + 2 : d.kernel)) {
             Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev, ins.iid, stream, now_ns()};
             cudaEventRecord(p.a, streams_[stream].s);
             n = launch_workload(b, streams_[stream].s);

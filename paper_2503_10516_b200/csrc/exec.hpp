@@ -170,7 +170,9 @@ public:
     const ExecStats& stats() const { return st_; }
 
     // profiling: per kernel kind, accumulated device ms and launch count
-    void set_profile(bool on);
+    // stride k > 0: time every k-th launch of each kind (unbiased average, less
+    // event overhead in the timed region); 0: off
+    void set_profile(int stride);
     int profile_read(double* ms, uint64_t* count, int n);
     // JSONL trace of the profiled launches (S:L528 format): iid, device,
     // stream, kind, start_us, end_us relative to profile_enable, per device
@@ -316,6 +318,9 @@ private:
     std::vector<Prof> prof_pending_;
     double prof_ms_[kProfSlots] = {};    // kernel kinds, K_NUM = local copy, +1 peer copy, +2 shell, +3 collective
     uint64_t prof_n_[kProfSlots] = {};
+    int prof_stride_ = 1;
+    uint64_t prof_ctr_[kProfSlots] = {};
+    bool prof_sample(int kind) { return prof_ctr_[kind]++ % uint64_t(prof_stride_) == 0; }
     std::vector<int> phys_;
     bool memops64_ = false;
     std::atomic<int> err_{0};
