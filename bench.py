@@ -147,9 +147,18 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def gpu_of(v):
+    """Physical GPU of virtual device / rank v.  CEL_BENCH_GPUS=k folds the
+    ranks onto k GPUs (several processes per GPU): a functional rehearsal of
+    N > k runs on a smaller box, not a performance measurement."""
+    k = int(os.environ.get("CEL_BENCH_GPUS", "0") or 0)
+    return v % k if k > 0 else v
+
+
 def make_runtime(cel, G, rank, world, dist, arena, **kw):
+    devs = [gpu_of(v) for v in range(G)]
     if world > 1:
-        rt = cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=arena, rank=rank, world=world, **kw)
+        rt = cel.Runtime(G, cuda_devices=devs, arena_bytes=arena, rank=rank, world=world, **kw)
         blob = rt.ipc_export()
         blobs = [None] * world
         dist.all_gather_object(blobs, blob)
@@ -158,7 +167,7 @@ def make_runtime(cel, G, rank, world, dist, arena, **kw):
                 rt.ipc_import(r, b)
         dist.barrier()
         return rt
-    return cel.Runtime(G, cuda_devices=list(range(G)), arena_bytes=arena, **kw)
+    return cel.Runtime(G, cuda_devices=devs, arena_bytes=arena, **kw)
 
 
 def main():
@@ -189,7 +198,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("gloo")
-    torch.cuda.set_device(local if world > 1 else 0)
+    torch.cuda.set_device(gpu_of(local) if world > 1 else 0)
     n = args.n
     arena = int(2 * (n // G + 2) * n * 4 * 1.05) + (512 << 20)
 

@@ -125,6 +125,7 @@ def main():
             "gpu_launches": st1["kernel_launches"] - st0["kernel_launches"],
             "collective": bool(args.collective),
             "coll_groups": st1["coll_groups"] - st0["coll_groups"],
+            "coll_allgathers": st1["coll_allgathers"] - st0["coll_allgathers"],
             "profile_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()}}
     if args.workload == "jacobi3d":
         cells = 1024 ** 3 / G

@@ -189,6 +189,7 @@ typedef struct {
     uint64_t gather_sets;                 /* coherence copy sets the scheduler found to be all-gathers */
     uint64_t n_send, n_receive, n_split_receive, n_await_receive;   /* virtual-node mode (n_nodes > 1) */
     uint64_t pulls, pull_bytes;           /* virtual-node mode: pilot-matched transfers executed, bytes */
+    uint64_t coll_allgathers;             /* all-gather sets run as one in-place ncclAllGather */
 } cel_stats;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

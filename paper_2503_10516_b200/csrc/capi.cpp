@@ -371,6 +371,7 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
         o->bytes_elided += e.bytes_elided;
         o->coll_groups += e.coll_groups;
         o->coll_copies += e.coll_copies;
+        o->coll_allgathers += e.coll_allgathers;
     }
     if (rt->comm) {
         o->pulls = rt->comm->pulls();

@@ -49,6 +49,7 @@ struct Nccl {
     ncclResult_t (*group_start)() = nullptr;
     ncclResult_t (*group_end)() = nullptr;
     ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*allgather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*errstr)(ncclResult_t) = nullptr;
     int state = 0;   // 0 not tried, 1 loaded, -1 unavailable
     bool load() {
@@ -63,6 +64,7 @@ struct Nccl {
         group_start = reinterpret_cast<decltype(group_start)>(dlsym(h, "ncclGroupStart"));
         group_end = reinterpret_cast<decltype(group_end)>(dlsym(h, "ncclGroupEnd"));
         bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
+        allgather = reinterpret_cast<decltype(allgather)>(dlsym(h, "ncclAllGather"));
         errstr = reinterpret_cast<decltype(errstr)>(dlsym(h, "ncclGetErrorString"));
         if (get_id && init_rank && init_all && destroy && group_start && group_end && bcast && errstr) state = 1;
         return state > 0;
@@ -1182,7 +1184,50 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
             profs.push_back(p);
         }
     uint64_t bytes_total = 0;
+    // address of root s's box in local device v's memory
+    auto addr = [&](int s, int v) -> char* {
+        const std::vector<const Instr*>& xs = roots.at(s);
+        const Box& b = xs[0]->region[0];
+        if (v == s) {
+            const AllocRec& S = allocs_.at(xs[0]->src_aid);
+            return arenas_[S.dev].base + S.off + lin(b, S.box) * es;
+        }
+        for (const Instr* x : xs)
+            if (x->dst_mem - 2 == v) {
+                const AllocRec& D = allocs_.at(x->dst_aid);
+                return arenas_[D.dev].base + D.off + lin(b, D.box) * es;
+            }
+        return nullptr;
+    };
+    // every device a root with an equal-size box at offset root x count of one
+    // contiguous layout (N-body's P): one in-place ncclAllGather per device,
+    // which NCCL may run over NVLink SHARP (NVLS) multicast
+    static const char* agenv = getenv("CEL_COLL_AG");
+    bool ag = g_nccl.allgather && !(agenv && agenv[0] == '0') && int(roots.size()) == G_;
+    size_t count = 0;
+    if (ag) {
+        count = size_t(roots.begin()->second[0]->region[0].volume()) * es;
+        for (auto& rt : roots)
+            if (size_t(rt.second[0]->region[0].volume()) * es != count) ag = false;
+        for (size_t k = 0; k < locals.size() && ag; ++k) {
+            char* b0 = addr(0, locals[k]);
+            for (int sr = 0; sr < G_ && ag; ++sr)
+                if (!b0 || addr(sr, locals[k]) != b0 + size_t(sr) * count) ag = false;
+        }
+    }
     ncclResult_t r = g_nccl.group_start();
+    if (ag) {
+        for (size_t k = 0; k < locals.size() && r == ncclSuccess; ++k) {
+            const int v = locals[k];
+            char* b0 = addr(0, v);
+            const int sidx = v * kStreamsPerDev + S_PUSH;
+            r = g_nccl.allgather(b0 + size_t(v) * count, b0, count, ncclUint8, static_cast<ncclComm_t>(comms_[k]),
+                                 streams_[sidx].s);
+        }
+        bytes_total = count * size_t(G_) * size_t(G_ - 1);
+        st_.coll_allgathers++;
+        roots.clear();                          // nothing left for broadcasts
+    }
     for (auto& rt : roots) {
         const int s = rt.first;
         const Instr& x0 = *rt.second[0];

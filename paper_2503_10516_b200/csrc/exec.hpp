@@ -124,6 +124,7 @@ struct ExecStats {
     uint64_t event_waits = 0, remote_waits = 0, signals = 0;
     uint64_t copies_elided = 0, bytes_elided = 0;   // resize copies made no-ops by in-place growth
     uint64_t coll_groups = 0, coll_copies = 0;      // all-gather copy sets run as NCCL collectives
+    uint64_t coll_allgathers = 0;                   // ... of which as one in-place ncclAllGather
     uint64_t host_syncs = 0;
     uint64_t exec_ns[kNumIKinds] = {}; // host time in on_instr per instruction kind (IKind order)
     uint64_t signal_ns = 0, remote_wait_ns = 0;

@@ -2,7 +2,7 @@
 N=${1:-4}
 for c in 8 32; do
   CUDA_DEVICE_MAX_CONNECTIONS=$c timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N \
-    --master-addr 127.0.0.1 --master-port 297$N$c bench.py --gpus $N --steps 3000 --warmup 20 \
+    --master-addr 127.0.0.1 --master-port 28${N}$c bench.py --gpus $N --steps 3000 --warmup 20 \
     --no-cpu-baseline --no-e2e 2>/dev/null | grep "^{" > gpurun_out/conn_${N}_$c.json
   python - "$c" "$N" <<'PY'
 import json, sys
