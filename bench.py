@@ -25,6 +25,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_FIELD = 16384
+METRIC = "WaveSim steps/s (16384^2 fp32, 1-D row split, halo coherence copies)"
+
+
+def arm_config(G, world, n=N_FIELD):
+    """The `config` both arms (ours and --impl reference) report."""
+    return {"workload": "wavesim_%dx%d_f32" % (n, n), "n_devices": G, "split": "1d rows", "lookahead": "auto",
+            "processes": world,
+            "l2": "inputs larger than L2 (u+up = %.2f GiB per GPU vs 126 MB L2)" % (2 * n * n * 4 / G / 2 ** 30)}
 ALG_BYTES_PER_CELL = 12        # wave5: read u, read up, write up (4 B each)
 PROF_STRIDE = 8
 
@@ -137,10 +145,10 @@ def run_reference(args):
     dt = time.perf_counter() - t0
     full = args.steps * R / N_FIELD
     val = full / dt
-    line = {"impl": "reference", "metric": "WaveSim steps/s (16384^2 fp32)", "value": val, "unit": "steps/s",
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "wavesim_16384x16384_f32", "n_devices": args.gpus, "split": "1d rows"},
+            "config": arm_config(args.gpus, world),
             "cpu_baseline": {"value": val, "unit": "steps/s", "cores": 1, "kind": "oracle",
                              "sample": "oracle wave5 kernel on %d of 16384 rows per step, scaled by rows" % R},
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -321,13 +329,11 @@ def main():
     if G == 1 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
     line = {
-        "metric": "WaveSim steps/s (16384^2 fp32, 1-D row split, halo coherence copies)",
+        "metric": METRIC,
         "value": value, "unit": "steps/s", "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "wavesim_16384x16384_f32", "n_devices": G, "split": "1d rows",
-                   "lookahead": "auto", "processes": world,
-                   "l2": "inputs larger than L2 (u+up = %.2f GiB per GPU vs 126 MB L2)" % (2 * n * n * 4 / G / 2 ** 30)},
+        "config": arm_config(G, world, n),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "wave5_vec", "alg_bytes_per_launch": alg_bytes,
