@@ -531,7 +531,15 @@ void Executor::oob_check(bool wait) {
 
 Token Executor::dep_token(uint64_t j) const {
     auto it = tok_.find(j);
-    return it == tok_.end() ? Token{} : it->second;
+    if (it != tok_.end()) return it->second;
+    // copies and kernels another rank executes are not stored: their token is
+    // the owner's flag (signalled to us through signal_deps on its side)
+    if (cfg_.world > 1 && j >= prune_floor_) {
+        auto k = kind_of_.find(j);
+        if (k != kind_of_.end() && k->second >= 0 && owner_rank(k->second) != cfg_.rank)
+            return Token{{}, {{owner_rank(k->second), j}}};
+    }
+    return Token{};
 }
 
 void Executor::merge(Token& into, const Token& t) const {
@@ -641,6 +649,7 @@ void Executor::note_use(const Instr& ins) {
 }
 
 void Executor::prune_tokens(uint64_t below) {
+    prune_floor_ = below;
     for (auto it = tok_.begin(); it != tok_.end();) {
         if (it->first < below && !live_alloc_iid_.count(it->first))
             it = tok_.erase(it);
@@ -1001,18 +1010,15 @@ void Executor::on_instr_impl(const Instr& ins) {
         return;
     }
     case IKind::Copy:
-        copy_info_[ins.iid] = CopyInfo{ins.src_aid, ins.dst_aid, rbbox(ins.region), ins.region};
-        if (!mine) {
-            tok_[ins.iid] = Token{{}, {{owner_rank(od), ins.iid}}};
-            return;
-        }
+        // the interior / shell split of this rank's kernels inspects copies
+        // into its own allocations too (executed by their producer's rank)
+        if (mine || (ins.dst_mem >= 2 && owner_rank(ins.dst_mem - 2) == cfg_.rank))
+            copy_info_[ins.iid] = CopyInfo{ins.src_aid, ins.dst_aid, rbbox(ins.region), ins.region};
+        if (!mine) return;                        // token: dep_token() -> the owner's flag
         exec_copy(ins);
         break;
     case IKind::Kernel:
-        if (!mine) {
-            tok_[ins.iid] = Token{{}, {{owner_rank(od), ins.iid}}};
-            return;
-        }
+        if (!mine) return;
         exec_kernel(ins);
         break;
     case IKind::Horizon: {

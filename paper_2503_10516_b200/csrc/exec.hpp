@@ -353,6 +353,7 @@ private:
     ExecStats st_;
     uint64_t since_poll_ = 0;
     uint64_t prev_horizon_ = 0;
+    uint64_t prune_floor_ = 0;                    // tokens below it were pruned (complete)
     std::unordered_set<uint64_t> live_alloc_iid_;
     std::vector<uint32_t> host_drop_;
     bool trace_ = false;
