@@ -1,5 +1,6 @@
 // C-ABI (include/cel.h) over the scheduler and executor.
 #include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -186,6 +187,8 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
     const int step = cfg->horizon_step > 0 ? cfg->horizon_step : 4;
     rt->sched = std::make_unique<Scheduler>(cfg->n_devices, cfg->lookahead, step, cfg->checks != 0, rt->exec.get(),
                                             rt->log);
+    const char* nf = getenv("CEL_NO_FILTER");
+    if (world > 1 && !(nf && nf[0] == '1')) rt->sched->set_rank_filter(cfg->rank, world);   // before any instruction is emitted
     if (rt->exec) rt->exec->set_scheduler(rt->sched.get());
     *out = rt.release();
     return CEL_OK;

@@ -535,11 +535,21 @@ Token Executor::dep_token(uint64_t j) const {
     // copies and kernels another rank executes are not stored: their token is
     // the owner's flag (signalled to us through signal_deps on its side)
     if (cfg_.world > 1 && j >= prune_floor_) {
-        auto k = kind_of_.find(j);
-        if (k != kind_of_.end() && k->second >= 0 && owner_rank(k->second) != cfg_.rank)
-            return Token{{}, {{owner_rank(k->second), j}}};
+        int o = 0;
+        if (owner_lookup(j, &o) && o >= 0 && owner_rank(o) != cfg_.rank) return Token{{}, {{owner_rank(o), j}}};
     }
     return Token{};
+}
+
+// Owner device of instruction j: recorded when this executor processed it, else
+// (the scheduler's rank filter never handed it over) from the scheduler's ring.
+bool Executor::owner_lookup(uint64_t j, int* o) const {
+    auto k = kind_of_.find(j);
+    if (k != kind_of_.end()) {
+        *o = k->second;
+        return true;
+    }
+    return sched_ && sched_->ring_owner(j, o);
 }
 
 void Executor::merge(Token& into, const Token& t) const {
@@ -683,14 +693,14 @@ void Executor::prune_tokens(uint64_t below) {
 Token Executor::multi_local_part(const std::vector<uint64_t>& deps) const {
     Token t;
     for (uint64_t j : deps) {
-        auto kit = kind_of_.find(j);
-        if (cfg_.world > 1 && kit != kind_of_.end()) {
-            if (kit->second < 0) {
+        int ko = 0;
+        if (cfg_.world > 1 && owner_lookup(j, &ko)) {
+            if (ko < 0) {
                 auto lt = ltok_.find(j);
                 if (lt != ltok_.end()) merge(t, lt->second);
                 continue;
             }
-            if (owner_rank(kit->second) != cfg_.rank) continue;
+            if (owner_rank(ko) != cfg_.rank) continue;
         }
         merge(t, dep_token(j));
     }
@@ -726,9 +736,8 @@ Token Executor::local_part(const std::vector<uint64_t>& deps) const {
 void Executor::signal_deps(const Instr& ins, int owner_dev) {
     const int o = owner_rank(owner_dev);
     for (uint64_t j : ins.deps) {
-        auto kit = kind_of_.find(j);
-        if (kit == kind_of_.end()) continue;  // complete before any remote dependent existed
-        const int jo = kit->second;           // owner device, -1 = all
+        int jo = 0;                           // owner device, -1 = all
+        if (!owner_lookup(j, &jo)) continue;  // complete before any remote dependent existed
         if (jo >= 0 && owner_rank(jo) != cfg_.rank) continue;
         const uint64_t key = j * uint64_t(cfg_.world) + uint64_t(o);
         if (!signalled_.insert(key).second) continue;
@@ -994,10 +1003,10 @@ void Executor::on_instr_impl(const Instr& ins) {
         if (mine) {
             t = local_part(ins.deps);
             for (uint64_t j : ins.deps) {
-                auto kit = kind_of_.find(j);
-                if (cfg_.world > 1 && kit != kind_of_.end() && kit->second >= 0 &&
-                    owner_rank(kit->second) != cfg_.rank)
-                    t.remote.push_back({owner_rank(kit->second), j});
+                int ko = 0;
+                if (cfg_.world > 1 && owner_lookup(j, &ko) && ko >= 0 && owner_rank(ko) != cfg_.rank &&
+                    std::find(t.remote.begin(), t.remote.end(), std::make_pair(owner_rank(ko), j)) == t.remote.end())
+                    t.remote.push_back({owner_rank(ko), j});
             }
             if (t.remote.size() > 8) t = materialize(r.dev, t);
         } else {

@@ -254,6 +254,7 @@ private:
     void put_event(int dev, cudaEvent_t e);
     void poll(bool prune);
     Token dep_token(uint64_t j) const;
+    bool owner_lookup(uint64_t j, int* o) const;
     void merge(Token& into, const Token& t) const;
     void wait_token(int sidx, const Token& t);
     Token record(int sidx);

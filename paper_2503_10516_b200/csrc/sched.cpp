@@ -596,6 +596,42 @@ void Scheduler::log_instr(const Instr& ins) {
     fprintf(log_, "]}\n");
 }
 
+int Scheduler::instr_owner(const Instr& ins) {
+    switch (ins.kind) {
+    case IKind::Alloc:
+    case IKind::Free:
+        return ins.mem >= 2 ? ins.mem - 2 : -1;
+    case IKind::Kernel:
+        return ins.device;
+    case IKind::Copy:
+        return ins.src_mem >= 2 ? ins.src_mem - 2 : (ins.dst_mem >= 2 ? ins.dst_mem - 2 : -1);
+    default:
+        return -1;
+    }
+}
+
+void Scheduler::set_rank_filter(int rank, int world) {
+    filter_rank_ = rank;
+    filter_world_ = world;
+    if (world > 1) {
+        ring_iid_.assign(kOwnerRing, ~0ull);
+        ring_owner_.assign(kOwnerRing, -1);
+    }
+}
+
+bool Scheduler::owner_of(uint64_t iid, int* owner) const {
+    if (ring_iid_.empty()) return false;
+    const uint64_t k = iid & (kOwnerRing - 1);
+    if (ring_iid_[k] == iid) {
+        *owner = ring_owner_[k];
+        return true;
+    }
+    auto it = alloc_owner_.find(int64_t(iid));
+    if (it == alloc_owner_.end()) return false;
+    *owner = it->second;
+    return true;
+}
+
 uint64_t Scheduler::emit(Instr& ins, std::vector<uint64_t>& deps) {
     std::sort(deps.begin(), deps.end());
     deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
@@ -610,6 +646,23 @@ uint64_t Scheduler::emit(Instr& ins, std::vector<uint64_t>& deps) {
     front_.swap(nf);
     st_.n_by_kind[int(ins.kind)]++;
     log_instr(ins);
+    if (filter_world_ > 1) {
+        // all-gather members may run as a collective that every rank takes part
+        // in (§8 a7): co-owned, like horizons, so their dependents reach everyone
+        const int own = ins.coll_n ? -1 : instr_owner(ins);
+        const uint64_t k = ins.iid & (kOwnerRing - 1);
+        ring_owner_[k] = int8_t(own);
+        ring_iid_[k] = ins.iid;
+        if (ins.kind == IKind::Alloc) alloc_owner_[int64_t(ins.iid)] = own;
+        bool rel = (ins.kind != IKind::Copy && ins.kind != IKind::Kernel) || own < 0 || own == filter_rank_ ||
+                   ins.coll_n != 0 || (ins.kind == IKind::Copy && ins.dst_mem - 2 == filter_rank_);
+        for (size_t i = 0; i < ins.deps.size() && !rel; ++i) {
+            int o = 0;
+            // a dependency this rank executes or co-owns (horizons, epochs): it must signal it
+            if (!owner_of(ins.deps[i], &o) || o < 0 || o == filter_rank_) rel = true;
+        }
+        if (!rel) return ins.iid;                 // other ranks' business: the executor never sees it
+    }
     if (sink_) sink_->on_instr(ins);
     return ins.iid;
 }
@@ -635,6 +688,7 @@ Scheduler::Alloc* Scheduler::new_alloc(uint32_t bid, int mem, const Box& box, in
 }
 
 void Scheduler::free_alloc(Alloc* a, int64_t tid) {
+    if (filter_world_ > 1) alloc_owner_.erase(a->iid);
     std::vector<uint64_t> deps{uint64_t(a->iid)};
     for (auto& p : a->last_writer.e)
         if (p.first >= 0) deps.push_back(uint64_t(p.first));

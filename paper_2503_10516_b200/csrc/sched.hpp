@@ -249,6 +249,24 @@ public:
     void epoch_node(int64_t rb, uint32_t rb_buf, const Box& rb_box, const std::vector<Push>& pushes,
                     const std::map<uint32_t, Region>& awaits);
     void set_node(int n) { node_ = n; }
+    // Multi-process mode (one process per GPU, every rank replays the node's
+    // IDAG): hand this rank's executor only the instructions it executes or
+    // must take part in (allocs, frees, horizons, epochs, collectives, copies
+    // into its memory, and instructions with a dependency it executes or
+    // co-owns, which it must signal); record every instruction's owner device
+    // for the executor (owner_of).
+    void set_rank_filter(int rank, int world);
+    // owner device of instruction `iid` (-1: every rank), false if unknown
+    bool owner_of(uint64_t iid, int* owner) const;
+    // the same from the recent-instruction ring only: safe to call from the
+    // executor thread for instructions emitted before the one it processes
+    bool ring_owner(uint64_t iid, int* owner) const {
+        if (ring_iid_.empty()) return false;
+        const uint64_t k = iid & (kOwnerRing - 1);
+        if (ring_iid_[k] != iid) return false;
+        *owner = ring_owner_[k];
+        return true;
+    }
     int node() const { return node_; }
     // pilots go to `fn` as they are produced ("transmitted ... ahead of execution time")
     void set_pilot_sink(std::function<void(const Pilot&)> fn) { pilot_sink_ = std::move(fn); }
@@ -380,6 +398,12 @@ private:
     int64_t next_rb_ = 0;
     uint64_t next_coll_ = 1;
     int node_ = 0;                                    // virtual-node mode: this node's id
+    int filter_rank_ = -1, filter_world_ = 1;
+    static constexpr uint64_t kOwnerRing = 1ull << 20;
+    std::vector<uint64_t> ring_iid_;                  // iid -> owner device, recent instructions
+    std::vector<int8_t> ring_owner_;
+    std::unordered_map<int64_t, int> alloc_owner_;    // live allocation iid -> device (old, still referenced)
+    static int instr_owner(const Instr& ins);
     uint64_t next_msg_ = 0;                           // P:L400 "locally unique message id"
     std::vector<Pilot> pilots_;
     std::function<void(const Pilot&)> pilot_sink_;
