@@ -106,7 +106,13 @@ def c3fast():
 
 def c4(T=1024, W=84000):
     res = {}
-    for mode in ("auto", "none"):
+    # "none" without in-place growth is the paper's comparison (resize chains
+    # executed); "none_grow" shows what the executor's growth recovers
+    for label, mode, grow in (("auto", "auto", True), ("none", "none", False), ("none_grow", "none", True)):
+        if grow:
+            os.environ.pop("CEL_NO_GROW", None)
+        else:
+            os.environ["CEL_NO_GROW"] = "1"
         rt = cel.Runtime(1, lookahead=mode, arena_bytes=4 << 30)
         prog = P.rsim(W, T)
         rt.buffer_create(2, [T, W], 4)
@@ -119,11 +125,13 @@ def c4(T=1024, W=84000):
         cm = prof.get("copy", (0.0, 0))
         km = prof.get("rsim_row", (0.0, 0))[0] / 1e3
         kbytes = sum(t * W * 4 for t in range(1, T)) + (T - 1) * W * 4
-        res[mode] = {"seconds": dt, "steps_per_s": T / dt, "alloc": st["n_alloc"], "flushes": st["flushes"],
+        res[label] = {"seconds": dt, "resize_copies_elided": st["copies_elided"], "steps_per_s": T / dt, "alloc": st["n_alloc"], "flushes": st["flushes"],
                      "resize_copies": st["copies_resize"], "resize_bytes": st["bytes_resize"],
                      "resize_copy_GBps": (2 * st["bytes_resize"] / (cm[0] / 1e3) / 1e9) if cm[0] else None,
                      "kernel_GBps": kbytes / km / 1e9 if km else None, "profile_ms": {k: v[0] for k, v in prof.items()}}
+    os.environ.pop("CEL_NO_GROW", None)
     res["speedup_auto_vs_none"] = res["none"]["seconds"] / res["auto"]["seconds"]
+    res["speedup_auto_vs_none_grow"] = res["none_grow"]["seconds"] / res["auto"]["seconds"]
     return res
 
 
@@ -151,6 +159,10 @@ def c5(steps=40, n=1024):
 
 def copy_sweep():
     out = {"impl": os.environ.get("CEL_COPY", "lsu")}
+    # measure the copies themselves: in-place growth would turn these resizes
+    # into no-ops (the arena range after the allocation is free)
+    grow = os.environ.get("CEL_NO_GROW")
+    os.environ["CEL_NO_GROW"] = "1"
     # (a) 1 GiB contiguous resize copy: write [0, 2^28), then a task needs [0, 2^28 + 1)
     n = 1 << 28
     for reps in range(2):          # the first run pays lazy module loading; the second is reported
@@ -188,7 +200,9 @@ def copy_sweep():
     if torch.cuda.device_count() >= 2:
         for mib in (16, 256, 1024):
             N = mib * (1 << 20) // 16
-            rt = cel.Runtime(2, cuda_devices=[0, 1], arena_bytes=3 << 30)
+            # collective=False: this row measures the peer-push copy kernel (the
+            # all-gather set would otherwise run as NCCL, measured by c3 / configs)
+            rt = cel.Runtime(2, cuda_devices=[0, 1], arena_bytes=3 << 30, collective=False)
             rt.buffer_create(1, [N], 16)
             rt.buffer_create(1, [N], 16)
             rt.task_submit({"dims": 1, "range": ([0], [N]), "kernel": "fill_const", "params": {"value": 1.0},
@@ -206,6 +220,10 @@ def copy_sweep():
                                             "GBps_per_direction": half / (ms / cnt / 1e3) / 1e9,
                                             "frac_nvlink_nominal": half / (ms / cnt / 1e3) / 1e9 / NVLINK_NOMINAL,
                                             "frac_nvlink_measured_ref": half / (ms / cnt / 1e3) / 1e9 / NVLINK_MEASURED_REF}
+    if grow is None:
+        os.environ.pop("CEL_NO_GROW", None)
+    else:
+        os.environ["CEL_NO_GROW"] = grow
     return out
 
 

@@ -1194,6 +1194,7 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
     if (cfg_.profile)
         for (int v : locals) {
             const int sidx = v * kStreamsPerDev + S_PUSH;
+            set_dev(v);                  // profile events belong to the device's stream
             Prof p{K_NUM + 3, prof_event(v), prof_event(v), v, m[0].iid, sidx, now_ns()};
             cudaEventRecord(p.a, streams_[sidx].s);
             profs.push_back(p);
@@ -1280,6 +1281,7 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
         return;
     }
     for (auto& p : profs) {
+        set_dev(p.dev);
         cudaEventRecord(p.b, streams_[p.stream].s);
         prof_pending_.push_back(p);
     }

@@ -119,6 +119,7 @@ def test_all_gather_collective_vs_pushes(cel, monkeypatch):
     for prog in (P.nbody(3000, 3), P.rsim(3001, 12), P.nbody(777, 2, host_init=True)):
         for coll in (True, False):
             rt = cel.Runtime(n, cuda_devices=devs, arena_bytes=256 << 20, collective=coll)
+            rt.profile_enable(True)         # profile events on every device (collective groups included)
             got = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
             o = OracleRuntime(n)
             run_program(o, prog)
