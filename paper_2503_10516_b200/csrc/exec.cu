@@ -1,91 +1,9 @@
 // Executor implementation (see exec.hpp).  Paper: §4.1 out-of-order dispatch
 // (P:L515-530), allocation instructions, copy instructions
 // (P:L292), epochs, horizons.
-#include "exec.hpp"
-
-#include <algorithm>
-#include <cstdio>
-#include <chrono>
-#include <cstdlib>
-#include <cstring>
-#include <dlfcn.h>
-#include <immintrin.h>
-#include <nccl.h>
-
-#include "../../include/cel.h"
+#include "exec_impl.hpp"
 
 namespace cel {
-
-Box map_access(const Mapper& m, const Box& chunk, const Box& ext);  // sched.cpp
-
-namespace {
-// Driver-API entry points resolved through the runtime (no link-time libcuda
-// dependency, so the library also loads on a host without a driver for the
-// execute=0 scheduling mode).
-struct Drv {
-    CUresult (*wait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
-    CUresult (*write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
-    CUresult (*errstr)(CUresult, const char**) = nullptr;
-    CUresult (*devattr)(int*, CUdevice_attribute, CUdevice) = nullptr;
-    bool loaded = false;
-    void load() {
-        if (loaded) return;
-        loaded = true;
-        cudaDriverEntryPointQueryResult q;
-        cudaGetDriverEntryPoint("cuStreamWaitValue64", reinterpret_cast<void**>(&wait64), cudaEnableDefault, &q);
-        cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&write64), cudaEnableDefault, &q);
-        cudaGetDriverEntryPoint("cuGetErrorString", reinterpret_cast<void**>(&errstr), cudaEnableDefault, &q);
-        cudaGetDriverEntryPoint("cuDeviceGetAttribute", reinterpret_cast<void**>(&devattr), cudaEnableDefault, &q);
-    }
-} g_drv;
-
-// NCCL, opened at run time (the process may already hold torch's copy of
-// libnccl.so.2; the C API is stable across the 2.2x releases in this image).
-struct Nccl {
-    ncclResult_t (*get_id)(ncclUniqueId*) = nullptr;
-    ncclResult_t (*init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-    ncclResult_t (*init_all)(ncclComm_t*, int, const int*) = nullptr;
-    ncclResult_t (*destroy)(ncclComm_t) = nullptr;
-    ncclResult_t (*group_start)() = nullptr;
-    ncclResult_t (*group_end)() = nullptr;
-    ncclResult_t (*bcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-    ncclResult_t (*allgather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-    const char* (*errstr)(ncclResult_t) = nullptr;
-    int state = 0;   // 0 not tried, 1 loaded, -1 unavailable
-    bool load() {
-        if (state) return state > 0;
-        state = -1;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) return false;
-        get_id = reinterpret_cast<decltype(get_id)>(dlsym(h, "ncclGetUniqueId"));
-        init_rank = reinterpret_cast<decltype(init_rank)>(dlsym(h, "ncclCommInitRank"));
-        init_all = reinterpret_cast<decltype(init_all)>(dlsym(h, "ncclCommInitAll"));
-        destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "ncclCommDestroy"));
-        group_start = reinterpret_cast<decltype(group_start)>(dlsym(h, "ncclGroupStart"));
-        group_end = reinterpret_cast<decltype(group_end)>(dlsym(h, "ncclGroupEnd"));
-        bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
-        allgather = reinterpret_cast<decltype(allgather)>(dlsym(h, "ncclAllGather"));
-        errstr = reinterpret_cast<decltype(errstr)>(dlsym(h, "ncclGetErrorString"));
-        if (get_id && init_rank && init_all && destroy && group_start && group_end && bcast && errstr) state = 1;
-        return state > 0;
-    }
-} g_nccl;
-
-inline uint64_t now_ns() {
-    return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
-                        std::chrono::steady_clock::now().time_since_epoch())
-                        .count());
-}
-
-constexpr int kStreamsPerDev = 11;
-// work streams 0..4; 5 = eager horizon / epoch flags; 6..10 = flags released
-// by an event of work stream (k - 6), so each flag stream's FIFO order follows
-// its source stream's completion order (no head-of-line blocking between a
-// long-complete flag and one waiting for recent work)
-enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3, S_HALO = 4, S_HSIG = 5, S_SIG0 = 6 };
-constexpr uint64_t kAlign = 512;
-uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
-}  // namespace
 
 // ------------------------------------------------------------ arena (allocation manager)
 // Deterministic first-fit sub-allocator over one pre-reserved device range per
@@ -1134,841 +1052,6 @@ void Executor::exec_epoch(const Instr& ins) {
             else ++it;
         }
     }
-}
-
-bool Executor::coll_init() {
-    if (coll_state_) return coll_state_ > 0;
-    coll_state_ = -1;
-    if (cfg_.world > 1) {
-        if (!nccl_id_set_) return false;
-        ncclUniqueId id;
-        memcpy(&id, nccl_id_, sizeof id);
-        ncclComm_t c = nullptr;
-        set_dev(cfg_.rank);
-        // collective over all ranks; every rank reaches the same first group
-        if (trace_) fprintf(stderr, "[cel r%d] ncclCommInitRank ...\n", cfg_.rank);
-        if (g_nccl.init_rank(&c, cfg_.world, id, cfg_.rank) != ncclSuccess) return false;
-        if (trace_) fprintf(stderr, "[cel r%d] ncclCommInitRank done\n", cfg_.rank);
-        comms_.assign(1, c);
-    } else {
-        std::vector<ncclComm_t> cs(G_, nullptr);
-        if (g_nccl.init_all(cs.data(), G_, phys_.data()) != ncclSuccess) return false;
-        comms_.assign(cs.begin(), cs.end());
-    }
-    coll_state_ = 1;
-    return true;
-}
-
-// §8 a7: an all-gather copy set (Scheduler::all_gathers) executed as
-// one group of NCCL broadcasts, one per source device, in place in every
-// device's allocation (the `all` mapper; NVLink / NVSwitch
-// collectives instead of G(G-1) separate pushes).
-void Executor::exec_coll(const std::vector<Instr>& m) {
-    const uint32_t es = bufinfo_.at(m[0].buffer).es;
-    if (!coll_init()) {
-        errmsg_ = "NCCL communicator setup failed (set collective = 0 to use peer pushes)";
-        err_ = E_NCCL;
-        return;
-    }
-    // local devices taking part: all G (one process) or this rank's device
-    std::vector<int> locals;
-    if (cfg_.world > 1) locals.push_back(cfg_.rank);
-    else
-        for (int v = 0; v < G_; ++v) locals.push_back(v);
-    auto lin = [](const Box& b, const Box& a) {          // element offset of b.lo in a row-major over a
-        return uint64_t(((b.lo[0] - a.lo[0]) * a.extent(1) + (b.lo[1] - a.lo[1])) * a.extent(2) + (b.lo[2] - a.lo[2]));
-    };
-    std::vector<Token> tv(G_);
-    for (int v : locals) {
-        Token t;
-        for (const Instr& x : m)
-            if (x.src_mem - 2 == v || x.dst_mem - 2 == v) merge(t, local_part(x.deps));
-        const int sidx = v * kStreamsPerDev + S_PUSH;
-        set_dev(v);
-        wait_token(sidx, t);
-    }
-    // roots in ascending device order; a root's region is the same box for all receivers
-    std::map<int, std::vector<const Instr*>> roots;
-    for (const Instr& x : m) roots[x.src_mem - 2].push_back(&x);
-    std::vector<Prof> profs;
-    if (cfg_.profile)
-        for (int v : locals) {
-            const int sidx = v * kStreamsPerDev + S_PUSH;
-            set_dev(v);                  // profile events belong to the device's stream
-            Prof p{K_NUM + 3, prof_event(v), prof_event(v), v, m[0].iid, sidx, now_ns()};
-            cudaEventRecord(p.a, streams_[sidx].s);
-            profs.push_back(p);
-        }
-    uint64_t bytes_total = 0;
-    // address of root s's box in local device v's memory
-    auto addr = [&](int s, int v) -> char* {
-        const std::vector<const Instr*>& xs = roots.at(s);
-        const Box& b = xs[0]->region[0];
-        if (v == s) {
-            const AllocRec& S = allocs_.at(xs[0]->src_aid);
-            return arenas_[S.dev].base + S.off + lin(b, S.box) * es;
-        }
-        for (const Instr* x : xs)
-            if (x->dst_mem - 2 == v) {
-                const AllocRec& D = allocs_.at(x->dst_aid);
-                return arenas_[D.dev].base + D.off + lin(b, D.box) * es;
-            }
-        return nullptr;
-    };
-    // every device a root with an equal-size box at offset root x count of one
-    // contiguous layout (N-body's P): one in-place ncclAllGather per device,
-    // which NCCL may run over NVLink SHARP (NVLS) multicast
-    static const char* agenv = getenv("CEL_COLL_AG");
-    bool ag = g_nccl.allgather && !(agenv && agenv[0] == '0') && int(roots.size()) == G_;
-    size_t count = 0;
-    if (ag) {
-        count = size_t(roots.begin()->second[0]->region[0].volume()) * es;
-        for (auto& rt : roots)
-            if (size_t(rt.second[0]->region[0].volume()) * es != count) ag = false;
-        for (size_t k = 0; k < locals.size() && ag; ++k) {
-            char* b0 = addr(0, locals[k]);
-            for (int sr = 0; sr < G_ && ag; ++sr)
-                if (!b0 || addr(sr, locals[k]) != b0 + size_t(sr) * count) ag = false;
-        }
-    }
-    ncclResult_t r = g_nccl.group_start();
-    if (ag) {
-        for (size_t k = 0; k < locals.size() && r == ncclSuccess; ++k) {
-            const int v = locals[k];
-            char* b0 = addr(0, v);
-            const int sidx = v * kStreamsPerDev + S_PUSH;
-            r = g_nccl.allgather(b0 + size_t(v) * count, b0, count, ncclUint8, static_cast<ncclComm_t>(comms_[k]),
-                                 streams_[sidx].s);
-        }
-        bytes_total = count * size_t(G_) * size_t(G_ - 1);
-        st_.coll_allgathers++;
-        roots.clear();                          // nothing left for broadcasts
-    }
-    for (auto& rt : roots) {
-        const int s = rt.first;
-        const Instr& x0 = *rt.second[0];
-        const Box& b = x0.region[0];
-        const AllocRec& S = allocs_.at(x0.src_aid);
-        const size_t bytes = size_t(b.volume()) * es;
-        bytes_total += bytes * rt.second.size();
-        for (size_t k = 0; k < locals.size() && r == ncclSuccess; ++k) {
-            const int v = locals[k];
-            char* buf = nullptr;
-            if (v == s) {
-                buf = arenas_[S.dev].base + S.off + lin(b, S.box) * es;
-            } else {
-                for (const Instr* x : rt.second)
-                    if (x->dst_mem - 2 == v) {
-                        const AllocRec& D = allocs_.at(x->dst_aid);
-                        buf = arenas_[D.dev].base + D.off + lin(b, D.box) * es;
-                    }
-            }
-            if (!buf) {
-                errmsg_ = "all-gather set without a receiver on a device";
-                err_ = E_STATE;
-                g_nccl.group_end();
-                return;
-            }
-            const int sidx = v * kStreamsPerDev + S_PUSH;
-            r = g_nccl.bcast(buf, buf, bytes, ncclUint8, s, static_cast<ncclComm_t>(comms_[k]), streams_[sidx].s);
-        }
-    }
-    const ncclResult_t r2 = g_nccl.group_end();
-    if (trace_) fprintf(stderr, "[cel r%d] broadcast group of %zu copies issued\n", cfg_.rank, m.size());
-    if (r != ncclSuccess || r2 != ncclSuccess) {
-        errmsg_ = std::string("ncclBroadcast: ") + g_nccl.errstr(r != ncclSuccess ? r : r2);
-        err_ = E_NCCL;
-        return;
-    }
-    for (auto& p : profs) {
-        set_dev(p.dev);
-        cudaEventRecord(p.b, streams_[p.stream].s);
-        prof_pending_.push_back(p);
-    }
-    for (int v : locals) {
-        set_dev(v);                  // events come from the device's pool
-        tv[v] = record(v * kStreamsPerDev + S_PUSH);
-    }
-    for (const Instr& x : m) {
-        const int sd = x.src_mem - 2, dd = x.dst_mem - 2;
-        Token lt;
-        for (int v : locals)
-            if (v == sd || v == dd) merge(lt, tv[v]);
-        if (cfg_.world > 1) {
-            // the source's rank (sendbuff reusable) and the destination's rank
-            // (data arrived) each hold part of the completion
-            ltok_[x.iid] = lt;
-            for (int rk : {owner_rank(sd), owner_rank(dd)})
-                if (rk != cfg_.rank) lt.remote.push_back({rk, x.iid});
-        }
-        tok_[x.iid] = lt;
-    }
-    st_.coll_groups++;
-    st_.coll_copies += m.size();
-    st_.bytes_copy[2] += bytes_total;   // NCCL's kernels are library launches: not in kernel_launches
-}
-
-
-// ------------------------------------------------------------ virtual-node communicator
-namespace {
-// one box of a row-major allocation copied into another: a copy-kernel segment
-void box_seg(CopyArgs& args, const char* sb, const Box& S, char* db, const Box& D, const Box& b, uint32_t es) {
-    const int64_t sn1 = S.extent(1), sn2 = S.extent(2), dn1 = D.extent(1), dn2 = D.extent(2);
-    CopySeg g;
-    const int64_t so = ((b.lo[0] - S.lo[0]) * sn1 + (b.lo[1] - S.lo[1])) * sn2 + (b.lo[2] - S.lo[2]);
-    const int64_t dof = ((b.lo[0] - D.lo[0]) * dn1 + (b.lo[1] - D.lo[1])) * dn2 + (b.lo[2] - D.lo[2]);
-    g.src = sb + so * es;
-    g.dst = db + dof * es;
-    g.row_bytes = uint64_t(b.extent(2)) * es;
-    g.rows = uint32_t(b.extent(1));
-    g.planes = uint32_t(b.extent(0));
-    g.src_row_stride = uint64_t(sn2) * es;
-    g.dst_row_stride = uint64_t(dn2) * es;
-    g.src_plane_stride = uint64_t(sn1 * sn2) * es;
-    g.dst_plane_stride = uint64_t(dn1 * dn2) * es;
-    if (g.row_bytes == g.src_row_stride && g.row_bytes == g.dst_row_stride) {
-        g.row_bytes *= g.rows;
-        g.rows = 1;
-        if (g.row_bytes == g.src_plane_stride && g.row_bytes == g.dst_plane_stride) {
-            g.row_bytes *= g.planes;
-            g.planes = 1;
-        }
-    }
-    uint64_t a = uintptr_t(g.src) | uintptr_t(g.dst) | g.row_bytes;
-    if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
-    if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
-    g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
-    g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
-    g.units_begin = args.total_units;
-    args.seg[args.nseg++] = g;
-    args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
-}
-}  // namespace
-
-void Communicator::add_pilot(const Pilot& p) {
-    std::lock_guard<std::mutex> l(m_);
-    pilots_[Key{p.receiver, p.transfer, p.buffer}].push_back(PilotRec{p.sender, p.msg, p.box});
-    cv_.notify_all();
-}
-
-void Communicator::post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready) {
-    std::lock_guard<std::mutex> l(m_);
-    sends_[{node, msg}] = Send{src, ready};
-    cv_.notify_all();
-}
-
-void Communicator::abort() {
-    std::lock_guard<std::mutex> l(m_);
-    abort_ = true;
-    cv_.notify_all();
-}
-
-int Communicator::pull_region(int node, int64_t tid, uint32_t buf, const Region& reg, const Mem& dst,
-                              cudaStream_t stream) {
-    std::unique_lock<std::mutex> l(m_);
-    const Key k{node, tid, buf};
-    const uint64_t need = rvolume(reg);
-    // wait until the pilots covering reg are known and their sends issued
-    // (pilots of one transfer are disjoint and tile the awaited region)
-    for (;;) {
-        if (abort_) return E_STATE;
-        uint64_t covered = 0;
-        bool posted = true;
-        auto it = pilots_.find(k);
-        if (it != pilots_.end())
-            for (const PilotRec& p : it->second) {
-                const uint64_t v = rvolume(rinter(Region{p.box}, reg));
-                if (!v) continue;
-                covered += v;
-                if (!p.pulled && !sends_.count({p.sender, p.msg})) posted = false;
-            }
-        if (covered >= need && posted) break;
-        cv_.wait(l);
-    }
-    for (PilotRec& p : pilots_[k]) {
-        if (p.pulled || rinter(Region{p.box}, reg).empty()) continue;
-        auto sit = sends_.find({p.sender, p.msg});
-        Send snd = sit->second;
-        sends_.erase(sit);
-        cudaStreamWaitEvent(stream, snd.ready, 0);           // the sender's staged data
-        cudaEventDestroy(snd.ready);
-        CopyArgs args;
-        args.nseg = 0;
-        args.total_units = 0;
-        args.peer = 0;
-        box_seg(args, snd.src.base, snd.src.box, dst.base, dst.box, p.box, dst.es);
-        launch_copy(args, stream);
-        cudaEvent_t done = nullptr;
-        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
-        cudaEventRecord(done, stream);
-        pulled_[{p.sender, p.msg}] = done;
-        p.pulled = true;
-        pulls_++;
-        pull_bytes_ += uint64_t(p.box.volume()) * dst.es;
-    }
-    cv_.notify_all();
-    return cudaGetLastError() == cudaSuccess ? E_OK : E_CUDA;
-}
-
-cudaEvent_t Communicator::wait_pulled(int node, uint64_t msg) {
-    std::unique_lock<std::mutex> l(m_);
-    for (;;) {
-        auto it = pulled_.find({node, msg});
-        if (it != pulled_.end()) {
-            cudaEvent_t e = it->second;
-            pulled_.erase(it);
-            return e;
-        }
-        if (abort_) return nullptr;
-        cv_.wait(l);
-    }
-}
-
-// Send / receive / split receive / await receive (virtual-node mode, Table 1).
-void Executor::exec_transfer(const Instr& ins) {
-    Communicator& comm = *cfg_.comm;
-    const Token deps = local_part(ins.deps);
-    const uint32_t es = bufinfo_.at(ins.buffer).es;
-    set_dev(0);
-    const int s_sync = S_SYNC, s_recv = S_SIG0;          // streams of the node's first device
-    const int64_t key = (ins.transfer << 20) ^ int64_t(ins.buffer);
-    auto mem = [&](int64_t aid) {
-        const AllocRec& a = allocs_.at(aid);
-        return Communicator::Mem{base_of(a), a.box, es};
-    };
-    auto pull = [&](const Region& reg, const Communicator::Mem& dst) {
-        wait_token(s_recv, deps);                         // the receive's own dependencies (M1 readers, writers)
-        const int rc = comm.pull_region(cfg_.node, ins.transfer, ins.buffer, reg, dst, streams_[s_recv].s);
-        if (rc != E_OK && !err_) {
-            errmsg_ = "receive arbitration failed";
-            err_ = rc;
-        }
-        return record(s_recv);
-    };
-    switch (ins.kind) {
-    case IKind::Send: {
-        wait_token(s_sync, deps);                         // the staging copy
-        cudaEvent_t ready = nullptr;
-        check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
-        check(cudaEventRecord(ready, streams_[s_sync].s), "cudaEventRecord");
-        comm.post_send(cfg_.node, ins.msg, mem(ins.src_aid), ready);
-        pending_send_[ins.iid] = ins.msg;                 // completes with the receiver's pull
-        st_.bytes_copy[5] += uint64_t(ins.box.volume()) * es;
-        break;
-    }
-    case IKind::Receive:
-        tok_[ins.iid] = pull(ins.region, mem(ins.dst_aid));
-        break;
-    case IKind::SplitReceive:
-        recv_dst_[key] = mem(ins.dst_aid);
-        tok_[ins.iid] = deps;
-        break;
-    case IKind::AwaitReceive: {
-        auto it = recv_dst_.find(key);
-        if (it == recv_dst_.end()) {
-            errmsg_ = "await receive without its split receive";
-            err_ = E_STATE;
-            return;
-        }
-        tok_[ins.iid] = pull(ins.region, it->second);
-        break;
-    }
-    default:
-        break;
-    }
-}
-
-// A send completes when the receiver has pulled its box: resolved when an
-// instruction depending on it is issued (blocking until the receiver has
-// issued the pull -- it only waits for sends of this or earlier tasks).
-void Executor::resolve_sends(const Instr& ins) {
-    for (uint64_t j : ins.deps) {
-        auto it = pending_send_.find(j);
-        if (it == pending_send_.end()) continue;
-        cudaEvent_t e = cfg_.comm->wait_pulled(cfg_.node, it->second);
-        pending_send_.erase(it);
-        if (!e) {
-            if (!err_) {
-                errmsg_ = "communicator aborted";
-                err_ = E_STATE;
-            }
-            return;
-        }
-        const int sidx = S_HSIG;                          // device 0 of the node
-        set_dev(0);
-        check(cudaStreamWaitEvent(streams_[sidx].s, e, 0), "cudaStreamWaitEvent");
-        cudaEventDestroy(e);
-        tok_[j] = record(sidx);
-    }
-}
-
-// Copies between host-side memories (M0 host data / user pointer and the M1
-// staging arena): plain host copies once the dependencies have completed.
-void Executor::exec_host_copy(const Instr& ins, const Token& deps) {
-    const uint32_t es = bufinfo_.at(ins.buffer).es;
-    for (const TokEntry& e : deps.local)
-        if (e.seq > streams_[e.stream].done) check(cudaEventSynchronize(e.ev), "host copy wait");
-    const char* sb;
-    Box sbox;
-    if (ins.src_mem == 1) {
-        const AllocRec& S = allocs_.at(ins.src_aid);
-        sb = base_of(S);
-        sbox = S.box;
-    } else {
-        auto hi = host_init_.find(ins.buffer);
-        if (hi == host_init_.end()) {
-            errmsg_ = "host copy of a buffer without host data";
-            err_ = E_STATE;
-            return;
-        }
-        sb = hi->second.first;
-        sbox = bufinfo_.at(ins.buffer).extent;
-    }
-    char* db;
-    Box dbox;
-    if (ins.dst_aid == USER_AID) {
-        auto rb = readbacks_.find(ins.readback);
-        if (rb == readbacks_.end()) {
-            errmsg_ = "readback copy without a destination";
-            err_ = E_STATE;
-            return;
-        }
-        db = rb->second.dst;
-        dbox = rb->second.box;
-    } else {
-        const AllocRec& D = allocs_.at(ins.dst_aid);
-        db = base_of(D);
-        dbox = D.box;
-    }
-    for (const Box& b : ins.region)
-        for (int64_t z = b.lo[0]; z < b.hi[0]; ++z)
-            for (int64_t y = b.lo[1]; y < b.hi[1]; ++y) {
-                const int64_t so = ((z - sbox.lo[0]) * sbox.extent(1) + (y - sbox.lo[1])) * sbox.extent(2) +
-                                   (b.lo[2] - sbox.lo[2]);
-                const int64_t dof = ((z - dbox.lo[0]) * dbox.extent(1) + (y - dbox.lo[1])) * dbox.extent(2) +
-                                    (b.lo[2] - dbox.lo[2]);
-                memcpy(db + dof * es, sb + so * es, size_t(b.extent(2)) * es);
-            }
-    st_.bytes_copy[5] += rvolume(ins.region) * es;
-    tok_[ins.iid] = Token{};
-}
-
-void Executor::exec_copy(const Instr& ins) {
-    const uint32_t es = bufinfo_.at(ins.buffer).es;
-    Token deps;
-    for (uint64_t j : ins.deps) {
-        // a copy that reads only rows a split kernel wrote in its shell launch
-        // waits for that launch, not for the interior (computation /
-        // communication overlap)
-        auto pit = parts_.find(j);
-        if (pit != parts_.end() && pit->second.write_aid == ins.src_aid && ins.src_mem >= 2 &&
-            std::find(pit->second.bound.begin(), pit->second.bound.end(), ins.dst_aid) == pit->second.bound.end()) {
-            bool touches = false;
-            for (const Box& b : ins.region)
-                if (!intersect(b, pit->second.interior).empty()) touches = true;
-            if (!touches) {
-                merge(deps, pit->second.shell);
-                continue;
-            }
-        }
-        merge(deps, dep_token(j));
-    }
-    if (ins.src_mem >= 1 && ins.dst_mem >= 1) {
-        // allocation to allocation: device memories, or the pinned + mapped M1
-        // staging arena of virtual-node mode on either side (copy kernel)
-        const AllocRec& S = allocs_.at(ins.src_aid);
-        const AllocRec& D = allocs_.at(ins.dst_aid);
-        if (S.dev == D.dev && S.off == D.off && S.box.lo[0] == D.box.lo[0] && S.box.lo[1] == D.box.lo[1] &&
-            S.box.lo[2] == D.box.lo[2] && S.box.extent(1) == D.box.extent(1) && S.box.extent(2) == D.box.extent(2)) {
-            // in-place growth: source and destination bytes coincide
-            st_.copies_elided++;
-            st_.bytes_elided += rvolume(ins.region) * es;
-            tok_[ins.iid] = deps;
-            return;
-        }
-        const int dev = S.dev >= 0 ? S.dev : (D.dev >= 0 ? D.dev : 0);
-        const bool peer = S.dev >= 0 && D.dev >= 0 && S.dev != D.dev;
-        const int sidx = dev * kStreamsPerDev + (peer ? S_PUSH : S_COPY);
-        set_dev(dev);
-        wait_token(sidx, deps);
-        const char* sb = base_of(S);
-        char* db = base_of(D);
-        CopyArgs args;
-        args.nseg = 0;
-        args.total_units = 0;
-        args.peer = peer && phys_[S.dev] != phys_[D.dev] ? 1 : 0;
-        const int64_t sn1 = S.box.extent(1), sn2 = S.box.extent(2);
-        const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
-        uint64_t bytes = 0;
-        auto flush = [&]() {
-            if (args.nseg == 0) return;
-            if (cfg_.profile && prof_sample(args.peer ? K_NUM + 1 : K_NUM)) {
-                Prof p{args.peer ? K_NUM + 1 : K_NUM, prof_event(dev), prof_event(dev), dev, ins.iid, sidx, now_ns()};
-                cudaEventRecord(p.a, streams_[sidx].s);
-                st_.kernel_launches += launch_copy(args, streams_[sidx].s);
-                cudaEventRecord(p.b, streams_[sidx].s);
-                prof_pending_.push_back(p);
-            } else {
-                st_.kernel_launches += launch_copy(args, streams_[sidx].s);
-            }
-            st_.copy_launches++;
-            args.nseg = 0;
-            args.total_units = 0;
-        };
-        for (const Box& b : ins.region) {
-            CopySeg g;
-            const int64_t so = ((b.lo[0] - S.box.lo[0]) * sn1 + (b.lo[1] - S.box.lo[1])) * sn2 + (b.lo[2] - S.box.lo[2]);
-            const int64_t dof = ((b.lo[0] - D.box.lo[0]) * dn1 + (b.lo[1] - D.box.lo[1])) * dn2 + (b.lo[2] - D.box.lo[2]);
-            g.src = sb + so * es;
-            g.dst = db + dof * es;
-            g.row_bytes = uint64_t(b.extent(2)) * es;
-            g.rows = uint32_t(b.extent(1));
-            g.planes = uint32_t(b.extent(0));
-            g.src_row_stride = uint64_t(sn2) * es;
-            g.dst_row_stride = uint64_t(dn2) * es;
-            g.src_plane_stride = uint64_t(sn1 * sn2) * es;
-            g.dst_plane_stride = uint64_t(dn1 * dn2) * es;
-            if (g.row_bytes == g.src_row_stride && g.row_bytes == g.dst_row_stride) {
-                g.row_bytes *= g.rows;
-                g.rows = 1;
-                if (g.row_bytes == g.src_plane_stride && g.row_bytes == g.dst_plane_stride) {
-                    g.row_bytes *= g.planes;
-                    g.planes = 1;
-                }
-            }
-            uint64_t a = uintptr_t(g.src) | uintptr_t(g.dst) | g.row_bytes;
-            if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
-            if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
-            g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
-            g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
-            // huge planes x rows: split so that units stay below 2^63 (never in practice)
-            if (args.nseg == kMaxSegs) flush();
-            g.units_begin = args.total_units;
-            args.seg[args.nseg++] = g;
-            args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
-            bytes += b.volume() * es;
-        }
-        flush();
-        const int kind = ins.reason == REASON_RESIZE ? 0 : (peer ? (phys_[S.dev] == phys_[D.dev] ? 1 : 2) : 1);
-        st_.bytes_copy[kind] += bytes;
-        tok_[ins.iid] = record(sidx);
-        return;
-    }
-    // host <-> device: DMA (cudaMemcpy3DAsync per box)
-    const bool h2d = ins.src_mem == 0 && ins.dst_mem >= 2;
-    const bool d2h = ins.src_mem >= 2 && ins.dst_aid == USER_AID;
-    if (!h2d && !d2h && (ins.src_mem == 1 || ins.dst_mem == 1)) {
-        exec_host_copy(ins, deps);           // M1 <-> M0 / user pointer (virtual-node mode)
-        return;
-    }
-    if (!h2d && !d2h) {
-        // host implicit allocation -> user pointer: plain host copy
-        auto hi = host_init_.find(ins.buffer);
-        auto rb = readbacks_.find(ins.readback);
-        if (hi == host_init_.end() || rb == readbacks_.end()) {
-            errmsg_ = "host copy without source or destination";
-            err_ = E_STATE;
-            return;
-        }
-        const Box E = bufinfo_.at(ins.buffer).extent;
-        const Box& R = rb->second.box;
-        for (const Box& b : ins.region)
-            for (int64_t z = b.lo[0]; z < b.hi[0]; ++z)
-                for (int64_t y = b.lo[1]; y < b.hi[1]; ++y) {
-                    const int64_t so = ((z * E.extent(1)) + y) * E.extent(2) + b.lo[2];
-                    const int64_t dof = (((z - R.lo[0]) * R.extent(1)) + (y - R.lo[1])) * R.extent(2) + (b.lo[2] - R.lo[2]);
-                    memcpy(rb->second.dst + dof * es, hi->second.first + so * es, size_t(b.extent(2)) * es);
-                }
-        st_.bytes_copy[5] += rvolume(ins.region) * es;
-        tok_[ins.iid] = Token{};
-        return;
-    }
-    const int dev = h2d ? ins.dst_mem - 2 : ins.src_mem - 2;
-    const int sidx = dev * kStreamsPerDev + S_COPY;
-    set_dev(dev);
-    wait_token(sidx, deps);
-    char* hbase;
-    Box hbox;
-    char* dbase;
-    Box dbox;
-    if (h2d) {
-        auto hi = host_init_.find(ins.buffer);
-        if (hi == host_init_.end()) {
-            errmsg_ = "H2D copy of a buffer without host data";
-            err_ = E_STATE;
-            return;
-        }
-        hbase = hi->second.first;
-        hbox = bufinfo_.at(ins.buffer).extent;
-        const AllocRec& D = allocs_.at(ins.dst_aid);
-        dbase = arenas_[D.dev].base + D.off;
-        dbox = D.box;
-    } else {
-        auto rb = readbacks_.find(ins.readback);
-        if (rb == readbacks_.end()) {
-            errmsg_ = "readback copy without a destination";
-            err_ = E_STATE;
-            return;
-        }
-        hbase = rb->second.dst;
-        hbox = rb->second.box;
-        const AllocRec& S = allocs_.at(ins.src_aid);
-        dbase = arenas_[S.dev].base + S.off;
-        dbox = S.box;
-    }
-    for (const Box& b : ins.region) {
-        // DMA: collapse to one linear copy when the box is contiguous in both
-        // layouts (full rows / planes), else a 2-D copy per plane, else 3-D
-        const size_t hrow = size_t(hbox.extent(2)) * es, drow = size_t(dbox.extent(2)) * es;
-        const size_t width = size_t(b.extent(2)) * es;
-        auto hoff = [&](int64_t z, int64_t y) {
-            return ((size_t(z - hbox.lo[0]) * size_t(hbox.extent(1)) + size_t(y - hbox.lo[1])) * hrow) +
-                   size_t(b.lo[2] - hbox.lo[2]) * es;
-        };
-        auto doff = [&](int64_t z, int64_t y) {
-            return ((size_t(z - dbox.lo[0]) * size_t(dbox.extent(1)) + size_t(y - dbox.lo[1])) * drow) +
-                   size_t(b.lo[2] - dbox.lo[2]) * es;
-        };
-        char* hp0 = hbase + hoff(b.lo[0], b.lo[1]);
-        char* dp0 = dbase + doff(b.lo[0], b.lo[1]);
-        const bool rows_contig = width == hrow && width == drow;
-        const bool planes_contig = rows_contig && b.extent(1) == hbox.extent(1) && b.extent(1) == dbox.extent(1);
-        const cudaStream_t st = streams_[sidx].s;
-        if (planes_contig || (rows_contig && b.extent(0) == 1)) {
-            const size_t bytes = width * size_t(b.extent(1)) * size_t(b.extent(0));
-            check(h2d ? cudaMemcpyAsync(dp0, hp0, bytes, cudaMemcpyHostToDevice, st)
-                      : cudaMemcpyAsync(hp0, dp0, bytes, cudaMemcpyDeviceToHost, st),
-                  "cudaMemcpyAsync");
-            st_.memcpy_calls++;
-            continue;
-        }
-        if (b.extent(0) == 1) {
-            check(h2d ? cudaMemcpy2DAsync(dp0, drow, hp0, hrow, width, size_t(b.extent(1)), cudaMemcpyHostToDevice, st)
-                      : cudaMemcpy2DAsync(hp0, hrow, dp0, drow, width, size_t(b.extent(1)), cudaMemcpyDeviceToHost, st),
-                  "cudaMemcpy2DAsync");
-            st_.memcpy_calls++;
-            continue;
-        }
-        cudaMemcpy3DParms p;
-        memset(&p, 0, sizeof p);
-        cudaPitchedPtr hp = make_cudaPitchedPtr(hbase, hrow, hrow, size_t(hbox.extent(1)));
-        cudaPitchedPtr dp = make_cudaPitchedPtr(dbase, drow, drow, size_t(dbox.extent(1)));
-        cudaPos hpos = make_cudaPos(size_t(b.lo[2] - hbox.lo[2]) * es, size_t(b.lo[1] - hbox.lo[1]),
-                                    size_t(b.lo[0] - hbox.lo[0]));
-        cudaPos dpos = make_cudaPos(size_t(b.lo[2] - dbox.lo[2]) * es, size_t(b.lo[1] - dbox.lo[1]),
-                                    size_t(b.lo[0] - dbox.lo[0]));
-        if (h2d) {
-            p.srcPtr = hp;
-            p.srcPos = hpos;
-            p.dstPtr = dp;
-            p.dstPos = dpos;
-            p.kind = cudaMemcpyHostToDevice;
-        } else {
-            p.srcPtr = dp;
-            p.srcPos = dpos;
-            p.dstPtr = hp;
-            p.dstPos = hpos;
-            p.kind = cudaMemcpyDeviceToHost;
-        }
-        p.extent = make_cudaExtent(width, size_t(b.extent(1)), size_t(b.extent(0)));
-        check(cudaMemcpy3DAsync(&p, st), "cudaMemcpy3DAsync");
-        st_.memcpy_calls++;
-    }
-    st_.bytes_copy[h2d ? 3 : 4] += rvolume(ins.region) * es;
-    tok_[ins.iid] = record(sidx);
-}
-
-void Executor::exec_kernel(const Instr& ins) {
-    const TaskDesc& d = *ins.desc;
-    const int dev = ins.device;
-    const int sidx = dev * kStreamsPerDev + S_COMPUTE;
-    set_dev(dev);
-    Token deps;
-    for (uint64_t j : ins.deps) merge(deps, dep_token(j));
-    wait_token(sidx, deps);
-    if (d.kernel == K_CALLBACK) {
-        std::vector<cel_accessor> acc(d.acc.size());
-        for (size_t i = 0; i < d.acc.size(); ++i) {
-            const int64_t aid = ins.bindings[i];
-            auto it = allocs_.find(aid);
-            memset(&acc[i], 0, sizeof acc[i]);
-            if (it == allocs_.end()) continue;
-            acc[i].base = base_of(it->second);
-            for (int k = 0; k < 3; ++k) {
-                acc[i].alloc_box.min[k] = uint64_t(it->second.box.lo[k]);
-                acc[i].alloc_box.max[k] = uint64_t(it->second.box.hi[k]);
-            }
-            acc[i].elem_size = it->second.es;
-            const Box rg = map_access(d.acc[i].map, ins.chunk, bufinfo_.at(d.acc[i].buf).extent);
-            for (int k = 0; k < 3; ++k) {
-                acc[i].range.min[k] = uint64_t(rg.lo[k]);
-                acc[i].range.max[k] = uint64_t(rg.hi[k]);
-            }
-        }
-        const int n_chk = int(std::min<size_t>(acc.size(), kMaxAcc));
-        if (cfg_.bounds_check && n_chk) {
-            long long* rec = oob_begin(dev, sidx, n_chk);
-            for (int i = 0; i < n_chk; ++i) acc[i].oob = rec + 6 * i;
-        }
-        cel_box ch;
-        for (int k = 0; k < 3; ++k) {
-            ch.min[k] = uint64_t(ins.chunk.lo[k]);
-            ch.max[k] = uint64_t(ins.chunk.hi[k]);
-        }
-        if (d.fn) d.fn(d.fn_user, dev, &ch, acc.data(), int(acc.size()), streams_[sidx].s);
-        if (cfg_.bounds_check && n_chk) oob_end(dev, sidx, ins, d, n_chk);
-        tok_[ins.iid] = record(sidx);
-        return;
-    }
-    KArgs a;
-    memset(&a, 0, sizeof a);
-    a.kind = d.kernel;
-    a.n_acc = int(std::min<size_t>(d.acc.size(), kMaxAcc));
-    for (int k = 0; k < 3; ++k) {
-        a.chunk.lo[k] = ins.chunk.lo[k];
-        a.chunk.hi[k] = ins.chunk.hi[k];
-    }
-    a.seed = d.params.seed;
-    a.value = d.params.value;
-    a.t = d.params.t;
-    a.salt = d.params.salt;
-    a.fast = cfg_.fast_math ? 1 : 0;
-    for (int i = 0; i < a.n_acc; ++i) {
-        const Access& ac = d.acc[i];
-        DAcc& A = a.acc[i];
-        const Box ext = bufinfo_.at(ac.buf).extent;
-        for (int k = 0; k < 3; ++k) A.ext[k] = ext.hi[k];
-        A.es = bufinfo_.at(ac.buf).es;
-        A.mode = ac.mode;
-        A.map = int(ac.map.kind);
-        for (int k = 0; k < 3; ++k) {
-            A.border[k] = ac.map.border[k];
-            A.fixed.lo[k] = ac.map.fixed.lo[k];
-            A.fixed.hi[k] = ac.map.fixed.hi[k];
-        }
-        const Box mb = map_access(ac.map, ins.chunk, ext);
-        for (int k = 0; k < 3; ++k) {
-            A.box.lo[k] = mb.lo[k];
-            A.box.hi[k] = mb.hi[k];
-        }
-        auto it = allocs_.find(ins.bindings[i]);
-        if (it != allocs_.end()) {
-            A.base = base_of(it->second);
-            for (int k = 0; k < 3; ++k) {
-                A.lo[k] = it->second.box.lo[k];
-                A.n[k] = it->second.box.extent(k);
-            }
-        }
-    }
-    // Shell / interior split of stencil launches: the boundary bands that
-    // neighbouring devices read (halo rows) are computed first on a
-    // high-priority stream, so their coherence copies leave while the interior
-    // is still running.  Same instruction, same result; only the launch order
-    // and the per-part completion events change.
-    Box interior = ins.chunk;
-    bool split = false;
-    if (split_ && (d.kernel == K_WAVE5 || d.kernel == K_JACOBI7 || d.kernel == K_STENCIL3)) {
-        for (const Access& ac : d.acc) {
-            if (ac.map.kind != MapKind::Neighborhood || (ac.mode != MODE_READ && ac.mode != MODE_READ_WRITE)) continue;
-            const Box rb = map_access(ac.map, ins.chunk, bufinfo_.at(ac.buf).extent);
-            for (int k = 0; k < 3; ++k) {
-                if (rb.lo[k] < ins.chunk.lo[k]) {
-                    interior.lo[k] = std::max(interior.lo[k], ins.chunk.lo[k] + ac.map.border[k]);
-                    split = true;
-                }
-                if (rb.hi[k] > ins.chunk.hi[k]) {
-                    interior.hi[k] = std::min(interior.hi[k], ins.chunk.hi[k] - ac.map.border[k]);
-                    split = true;
-                }
-            }
-        }
-        // only worth it when the interior is big enough to hide the halo
-        // chain (a launch costs a few microseconds; tiny chunks are latency-bound)
-        if (interior.empty() || interior.volume() < (uint64_t(1) << 18)) split = false;
-    }
-    long long* oob = nullptr;
-    if (cfg_.bounds_check && a.n_acc) {
-        split = false;                            // one record per instruction, one launch stream
-        oob = oob_begin(dev, sidx, a.n_acc);
-        a.checked = 1;
-        for (int i = 0; i < a.n_acc; ++i) a.acc[i].oob = oob + 6 * i;
-    }
-    auto launch = [&](const Box& ch, int stream, bool shell_part) {
-        KArgs b = a;
-        for (int k = 0; k < 3; ++k) {
-            b.chunk.lo[k] = ch.lo[k];
-            b.chunk.hi[k] = ch.hi[k];
-        }
-        for (int i = 0; i < b.n_acc; ++i) {
-            const Box mb = map_access(d.acc[i].map, ch, bufinfo_.at(d.acc[i].buf).extent);
-            for (int k = 0; k < 3; ++k) {
-                b.acc[i].box.lo[k] = mb.lo[k];
-                b.acc[i].box.hi[k] = mb.hi[k];
-            }
-        }
-        int n;
-        if (cfg_.profile && prof_sample(shell_part ? K_NUM + 2 : d.kernel)) {
-            Prof p{shell_part ? K_NUM + 2 : d.kernel, prof_event(dev), prof_event(dev), dev, ins.iid, stream, now_ns()};
-            cudaEventRecord(p.a, streams_[stream].s);
-            n = launch_workload(b, streams_[stream].s);
-            cudaEventRecord(p.b, streams_[stream].s);
-            prof_pending_.push_back(p);
-        } else {
-            n = launch_workload(b, streams_[stream].s);
-        }
-        check(cudaGetLastError(), "kernel launch");
-        st_.kernel_launches += n;
-        st_.workload_launches += n;
-    };
-    if (!split) {
-        launch(ins.chunk, sidx, false);
-        if (oob) oob_end(dev, sidx, ins, d, a.n_acc);
-        tok_[ins.iid] = record(sidx);
-        return;
-    }
-    // shell launches: every dependency (they read the incoming halos)
-    const int hidx = dev * kStreamsPerDev + S_HALO;
-    wait_token(hidx, deps);
-    std::vector<Box> shell;
-    subtract_into(ins.chunk, interior, shell);
-    for (const Box& b : shell) launch(b, hidx, true);
-    Token tshell = record(hidx);
-    // interior launch: only dependencies whose accesses conflict with the
-    // interior's (copies into halo rows it never reads are skipped)
-    Token ideps;
-    for (uint64_t j : ins.deps) {
-        auto ci = copy_info_.find(j);
-        bool conflict = true;
-        if (ci != copy_info_.end()) {
-            conflict = false;
-            for (size_t i = 0; i < d.acc.size() && !conflict; ++i) {
-                const Access& ac = d.acc[i];
-                const int64_t aid = ins.bindings[i];
-                const Box ib = map_access(ac.map, interior, bufinfo_.at(ac.buf).extent);
-                auto hits = [&](const CopyInfo& c) {
-                    if (intersect(c.bb, ib).empty()) return false;
-                    for (const Box& b : c.region)
-                        if (!intersect(b, ib).empty()) return true;
-                    return false;
-                };
-                if (ci->second.dst_aid == aid && hits(ci->second)) conflict = true;             // RAW / WAW
-                if (ci->second.src_aid == aid && (ac.mode & MODE_WRITE) && hits(ci->second)) conflict = true;  // WAR
-            }
-        }
-        if (conflict) merge(ideps, dep_token(j));
-    }
-    wait_token(sidx, ideps);
-    // the interior must also follow the shell launches' own predecessors on
-    // the halo stream only through real conflicts, which `ideps` carries
-    launch(interior, sidx, false);
-    Token tint = record(sidx);
-    Token all = tint;
-    merge(all, tshell);
-    tok_[ins.iid] = all;
-    int64_t waid = 0;
-    for (size_t i = 0; i < d.acc.size(); ++i)
-        if (d.acc[i].mode & MODE_WRITE) waid = ins.bindings[i];
-    parts_[ins.iid] = Parts{tshell, interior, waid, ins.bindings};
 }
 
 cudaEvent_t Executor::prof_event(int dev) {

@@ -1,0 +1,200 @@
+// Executor: virtual-node mode transfers -- Communicator (receive arbitration,
+// P:L534-544), send / receive / split receive / await receive (Table 1, §3.4).
+#include "exec_impl.hpp"
+
+namespace cel {
+
+// ------------------------------------------------------------ virtual-node communicator
+namespace {
+// one box of a row-major allocation copied into another: a copy-kernel segment
+void box_seg(CopyArgs& args, const char* sb, const Box& S, char* db, const Box& D, const Box& b, uint32_t es) {
+    const int64_t sn1 = S.extent(1), sn2 = S.extent(2), dn1 = D.extent(1), dn2 = D.extent(2);
+    CopySeg g;
+    const int64_t so = ((b.lo[0] - S.lo[0]) * sn1 + (b.lo[1] - S.lo[1])) * sn2 + (b.lo[2] - S.lo[2]);
+    const int64_t dof = ((b.lo[0] - D.lo[0]) * dn1 + (b.lo[1] - D.lo[1])) * dn2 + (b.lo[2] - D.lo[2]);
+    g.src = sb + so * es;
+    g.dst = db + dof * es;
+    g.row_bytes = uint64_t(b.extent(2)) * es;
+    g.rows = uint32_t(b.extent(1));
+    g.planes = uint32_t(b.extent(0));
+    g.src_row_stride = uint64_t(sn2) * es;
+    g.dst_row_stride = uint64_t(dn2) * es;
+    g.src_plane_stride = uint64_t(sn1 * sn2) * es;
+    g.dst_plane_stride = uint64_t(dn1 * dn2) * es;
+    if (g.row_bytes == g.src_row_stride && g.row_bytes == g.dst_row_stride) {
+        g.row_bytes *= g.rows;
+        g.rows = 1;
+        if (g.row_bytes == g.src_plane_stride && g.row_bytes == g.dst_plane_stride) {
+            g.row_bytes *= g.planes;
+            g.planes = 1;
+        }
+    }
+    uint64_t a = uintptr_t(g.src) | uintptr_t(g.dst) | g.row_bytes;
+    if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
+    if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
+    g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
+    g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
+    g.units_begin = args.total_units;
+    args.seg[args.nseg++] = g;
+    args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
+}
+}  // namespace
+
+void Communicator::add_pilot(const Pilot& p) {
+    std::lock_guard<std::mutex> l(m_);
+    pilots_[Key{p.receiver, p.transfer, p.buffer}].push_back(PilotRec{p.sender, p.msg, p.box});
+    cv_.notify_all();
+}
+
+void Communicator::post_send(int node, uint64_t msg, const Mem& src, cudaEvent_t ready) {
+    std::lock_guard<std::mutex> l(m_);
+    sends_[{node, msg}] = Send{src, ready};
+    cv_.notify_all();
+}
+
+void Communicator::abort() {
+    std::lock_guard<std::mutex> l(m_);
+    abort_ = true;
+    cv_.notify_all();
+}
+
+int Communicator::pull_region(int node, int64_t tid, uint32_t buf, const Region& reg, const Mem& dst,
+                              cudaStream_t stream) {
+    std::unique_lock<std::mutex> l(m_);
+    const Key k{node, tid, buf};
+    const uint64_t need = rvolume(reg);
+    // wait until the pilots covering reg are known and their sends issued
+    // (pilots of one transfer are disjoint and tile the awaited region)
+    for (;;) {
+        if (abort_) return E_STATE;
+        uint64_t covered = 0;
+        bool posted = true;
+        auto it = pilots_.find(k);
+        if (it != pilots_.end())
+            for (const PilotRec& p : it->second) {
+                const uint64_t v = rvolume(rinter(Region{p.box}, reg));
+                if (!v) continue;
+                covered += v;
+                if (!p.pulled && !sends_.count({p.sender, p.msg})) posted = false;
+            }
+        if (covered >= need && posted) break;
+        cv_.wait(l);
+    }
+    for (PilotRec& p : pilots_[k]) {
+        if (p.pulled || rinter(Region{p.box}, reg).empty()) continue;
+        auto sit = sends_.find({p.sender, p.msg});
+        Send snd = sit->second;
+        sends_.erase(sit);
+        cudaStreamWaitEvent(stream, snd.ready, 0);           // the sender's staged data
+        cudaEventDestroy(snd.ready);
+        CopyArgs args;
+        args.nseg = 0;
+        args.total_units = 0;
+        args.peer = 0;
+        box_seg(args, snd.src.base, snd.src.box, dst.base, dst.box, p.box, dst.es);
+        launch_copy(args, stream);
+        cudaEvent_t done = nullptr;
+        cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+        cudaEventRecord(done, stream);
+        pulled_[{p.sender, p.msg}] = done;
+        p.pulled = true;
+        pulls_++;
+        pull_bytes_ += uint64_t(p.box.volume()) * dst.es;
+    }
+    cv_.notify_all();
+    return cudaGetLastError() == cudaSuccess ? E_OK : E_CUDA;
+}
+
+cudaEvent_t Communicator::wait_pulled(int node, uint64_t msg) {
+    std::unique_lock<std::mutex> l(m_);
+    for (;;) {
+        auto it = pulled_.find({node, msg});
+        if (it != pulled_.end()) {
+            cudaEvent_t e = it->second;
+            pulled_.erase(it);
+            return e;
+        }
+        if (abort_) return nullptr;
+        cv_.wait(l);
+    }
+}
+
+// Send / receive / split receive / await receive (virtual-node mode, Table 1).
+void Executor::exec_transfer(const Instr& ins) {
+    Communicator& comm = *cfg_.comm;
+    const Token deps = local_part(ins.deps);
+    const uint32_t es = bufinfo_.at(ins.buffer).es;
+    set_dev(0);
+    const int s_sync = S_SYNC, s_recv = S_SIG0;          // streams of the node's first device
+    const int64_t key = (ins.transfer << 20) ^ int64_t(ins.buffer);
+    auto mem = [&](int64_t aid) {
+        const AllocRec& a = allocs_.at(aid);
+        return Communicator::Mem{base_of(a), a.box, es};
+    };
+    auto pull = [&](const Region& reg, const Communicator::Mem& dst) {
+        wait_token(s_recv, deps);                         // the receive's own dependencies (M1 readers, writers)
+        const int rc = comm.pull_region(cfg_.node, ins.transfer, ins.buffer, reg, dst, streams_[s_recv].s);
+        if (rc != E_OK && !err_) {
+            errmsg_ = "receive arbitration failed";
+            err_ = rc;
+        }
+        return record(s_recv);
+    };
+    switch (ins.kind) {
+    case IKind::Send: {
+        wait_token(s_sync, deps);                         // the staging copy
+        cudaEvent_t ready = nullptr;
+        check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
+        check(cudaEventRecord(ready, streams_[s_sync].s), "cudaEventRecord");
+        comm.post_send(cfg_.node, ins.msg, mem(ins.src_aid), ready);
+        pending_send_[ins.iid] = ins.msg;                 // completes with the receiver's pull
+        st_.bytes_copy[5] += uint64_t(ins.box.volume()) * es;
+        break;
+    }
+    case IKind::Receive:
+        tok_[ins.iid] = pull(ins.region, mem(ins.dst_aid));
+        break;
+    case IKind::SplitReceive:
+        recv_dst_[key] = mem(ins.dst_aid);
+        tok_[ins.iid] = deps;
+        break;
+    case IKind::AwaitReceive: {
+        auto it = recv_dst_.find(key);
+        if (it == recv_dst_.end()) {
+            errmsg_ = "await receive without its split receive";
+            err_ = E_STATE;
+            return;
+        }
+        tok_[ins.iid] = pull(ins.region, it->second);
+        break;
+    }
+    default:
+        break;
+    }
+}
+
+// A send completes when the receiver has pulled its box: resolved when an
+// instruction depending on it is issued (blocking until the receiver has
+// issued the pull -- it only waits for sends of this or earlier tasks).
+void Executor::resolve_sends(const Instr& ins) {
+    for (uint64_t j : ins.deps) {
+        auto it = pending_send_.find(j);
+        if (it == pending_send_.end()) continue;
+        cudaEvent_t e = cfg_.comm->wait_pulled(cfg_.node, it->second);
+        pending_send_.erase(it);
+        if (!e) {
+            if (!err_) {
+                errmsg_ = "communicator aborted";
+                err_ = E_STATE;
+            }
+            return;
+        }
+        const int sidx = S_HSIG;                          // device 0 of the node
+        set_dev(0);
+        check(cudaStreamWaitEvent(streams_[sidx].s, e, 0), "cudaStreamWaitEvent");
+        cudaEventDestroy(e);
+        tok_[j] = record(sidx);
+    }
+}
+
+}  // namespace cel
