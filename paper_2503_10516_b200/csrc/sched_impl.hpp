@@ -1,0 +1,16 @@
+// Private declarations shared by sched.cpp and cluster.cpp.
+#pragma once
+
+#include <vector>
+
+#include "sched.hpp"
+
+namespace cel {
+namespace detail {
+void split_1d(const Box& rng, int n, int dim, std::vector<Box>& out);
+std::vector<Box> split(const Box& rng, int n, int kind);        // R4: 0 = 1D, 1 = 2D
+int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out);   // R5
+bool is_read(int mode);
+bool is_write(int mode);
+}  // namespace detail
+}  // namespace cel
