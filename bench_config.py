@@ -30,7 +30,9 @@ FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", required=True, choices=["jacobi3d", "nbody", "rsim"])
+    ap.add_argument("--workload", required=True, choices=["jacobi3d", "nbody", "rsim", "wavesim"])
+    ap.add_argument("--split", default="1d", help="wavesim: 1d | 2d")
+    ap.add_argument("--mapper", default="neighborhood", help="wavesim: neighborhood | neighborhood_axes")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=0)
     ap.add_argument("--warmup", type=int, default=3)
@@ -59,6 +61,19 @@ def main():
         descs = [cel.task_desc(P.jacobi_step(n, k)[1]) for k in (0, 1)]
         submit = lambda s: rt.submit_desc(descs[s % 2][0])  # noqa: E731
         kernel = "jacobi7"
+    elif args.workload == "wavesim":
+        # NEXT-3 variants of C2: 2-D split and the axis-only neighbourhood
+        n = 16384
+        steps = args.steps or 1000
+        arena = int(2 * n * n * 4 / G * 1.1) + (1 << 30)
+        rt = bench.make_runtime(cel, G, rank, world, dist, arena)
+        rt.buffer_create(2, [n, n], 4)
+        rt.buffer_create(2, [n, n], 4)
+        for op in P.wavesim_init(n, split=args.split):
+            rt.task_submit(op[1])
+        descs = [cel.task_desc(P.wavesim_step(n, k, split=args.split, mapper=args.mapper)[1]) for k in (0, 1)]
+        submit = lambda s: rt.submit_desc(descs[s % 2][0])  # noqa: E731
+        kernel = "wave5"
     elif args.workload == "nbody":
         N = 1 << 20
         steps = args.steps or 3
@@ -139,6 +154,10 @@ def main():
                             "achieved": 20 * inter / (km / 1e3) / 1e12, "fast_math": args.fast_math}
         line["roofline"]["frac"] = line["roofline"]["achieved"] / FP32_NOMINAL_TFLOPS
         line["interactions_per_s"] = (1 << 40) * steps / (ms / 1e3)
+    elif args.workload == "wavesim":
+        line["split"] = args.split
+        line["mapper"] = args.mapper
+        line["coherence_copies_per_step"] = (st1["copies_coherence"] - st0["copies_coherence"]) / steps
     else:
         line["lookahead"] = args.lookahead
         line["alloc"] = st1["n_alloc"] - st0["n_alloc"]

@@ -64,7 +64,17 @@ typedef struct {
  *   REMAP        buffer dim k takes the chunk's interval of kernel dim
  *                from_kernel_dim[k], or fixed's interval if that is -1
  *                (e.g. RSim "append row t": fixed=[t,t+1)x., map={-1,0,-1}) */
-typedef enum { CEL_ONE_TO_ONE = 0, CEL_NEIGHBORHOOD = 1, CEL_ALL = 2, CEL_FIXED = 3, CEL_REMAP = 4 } cel_mapper_kind;
+/* CEL_NEIGHBORHOOD_AXES: the axis-only neighbourhood -- the chunk inflated by
+ * border[d] along one dimension d at a time (a cross, no corners), e.g. a
+ * 5-point stencil; the allocation still spans the cross's bounding box. */
+typedef enum {
+    CEL_ONE_TO_ONE = 0,
+    CEL_NEIGHBORHOOD = 1,
+    CEL_ALL = 2,
+    CEL_FIXED = 3,
+    CEL_REMAP = 4,
+    CEL_NEIGHBORHOOD_AXES = 5
+} cel_mapper_kind;
 
 typedef struct {
     int32_t kind;              /* cel_mapper_kind */

@@ -32,7 +32,7 @@ R17 [readings] (DESIGN.md):
 """
 
 from . import geometry as g
-from .program import CelError, READS, WRITES, apply_mapper, split
+from .program import CelError, READS, WRITES, mapper_region, split
 from .scheduler import Runtime, _Cmd, _norm_mapper
 
 NONE = -1
@@ -78,13 +78,13 @@ class Cluster:
         if g.is_empty(chunk):
             return reads, writes
         for (bid, mode, mapper) in spec["accesses"]:
-            bx = apply_mapper(mapper, chunk, self.nodes[0].bufs[bid].extent)
-            if g.is_empty(bx):
+            reg = mapper_region(mapper, chunk, self.nodes[0].bufs[bid].extent)
+            if not reg:
                 continue
             if mode in READS:
-                reads[bid] = g.region_union(reads.get(bid, ()), (bx,))
+                reads[bid] = g.region_union(reads.get(bid, ()), reg)
             if mode in WRITES:
-                writes[bid] = g.region_union(writes.get(bid, ()), (bx,))
+                writes[bid] = g.region_union(writes.get(bid, ()), reg)
         return reads, writes
 
     def _transfers(self, need_by_node):

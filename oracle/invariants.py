@@ -21,7 +21,7 @@ Values are symbolic tokens (the producing kernel's iid), not bytes.
 import numpy as np
 
 from . import geometry as g
-from .program import apply_mapper, READS, WRITES
+from .program import mapper_region, READS, WRITES
 from .scheduler import HOST_AID, USER_AID, _norm_mapper
 
 
@@ -169,13 +169,11 @@ def check(log, buf_meta, tasks):
             chunk = _tobox(rec["chunk"])
             reads, writes = {}, {}
             for (bid, mode, mp), aid in zip(spec["accesses"], rec["bindings"]):
-                bx = apply_mapper(_norm_mapper(mp), chunk, buf_meta[bid]["extent"])
-                if g.is_empty(bx):
-                    continue
-                if mode in READS:
-                    reads.setdefault((bid, aid), []).append(bx)
-                if mode in WRITES:
-                    writes.setdefault((bid, aid), []).append(bx)
+                for bx in mapper_region(_norm_mapper(mp), chunk, buf_meta[bid]["extent"]):
+                    if mode in READS:
+                        reads.setdefault((bid, aid), []).append(bx)
+                    if mode in WRITES:
+                        writes.setdefault((bid, aid), []).append(bx)
             for (bid, aid), bxs in sorted(reads.items()):
                 A = get(aid, bid, i)
                 for bx in bxs:

@@ -98,6 +98,12 @@ def apply_mapper(mapper, chunk, extent):
         mn = tuple(chunk[0][d] - border[d] for d in range(3))
         mx = tuple(chunk[1][d] + border[d] for d in range(3))
         return g.box_intersect((mn, mx), extent)
+    if kind == "neighborhood_axes":
+        # the bounding box of the cross (mapper_region is the region itself)
+        border = tuple(mapper[1]) + (0,) * (3 - len(mapper[1]))
+        mn = tuple(chunk[0][d] - border[d] for d in range(3))
+        mx = tuple(chunk[1][d] + border[d] for d in range(3))
+        return g.box_intersect((mn, mx), extent)
     if kind == "all":
         return extent
     if kind == "fixed":
@@ -123,6 +129,24 @@ def apply_mapper(mapper, chunk, extent):
             raise CelError(CelError.OUT_OF_BOUNDS, "remap box outside buffer extent")
         return b
     raise CelError(CelError.INVALID, "unknown mapper %r" % (kind,))
+
+
+def mapper_region(mapper, chunk, extent):
+    """R5 / SURVEY NEXT-3: the buffer region a chunk accesses.  Equal to the
+    mapper's box for every kind except `neighborhood_axes`, the axis-only
+    neighbourhood (a stencil that reads no corners): the union over dims d of
+    the chunk inflated by border[d] in dim d alone, clamped to the extent."""
+    if mapper[0] != "neighborhood_axes":
+        bx = apply_mapper(mapper, chunk, extent)
+        return () if g.is_empty(bx) else (bx,)
+    if g.is_empty(chunk):
+        return ()
+    border = tuple(mapper[1]) + (0,) * (3 - len(mapper[1]))
+    parts = [chunk]
+    for d in range(3):
+        if border[d] > 0:
+            parts.append(g._with_dim(chunk, d, chunk[0][d] - border[d], chunk[1][d] + border[d]))
+    return g.region_intersect(g.region_union(*[(p,) for p in parts]), (extent,))
 
 
 READS = ("read", "read_write")

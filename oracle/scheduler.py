@@ -29,7 +29,7 @@ R2 canonical order.
 """
 
 from . import geometry as g
-from .program import CelError, READS, WRITES, apply_mapper, split
+from .program import CelError, READS, WRITES, apply_mapper, mapper_region, split
 
 NONE = -1          # "no writer" (uninitialised) in writer maps
 HOST_AID = -1      # implicit M0 allocation of a host-initialised buffer (R6)
@@ -343,13 +343,13 @@ class Runtime:
             if g.is_empty(ch):
                 continue
             for (bid, mode, mapper) in spec["accesses"]:
-                bx = apply_mapper(mapper, ch, self.bufs[bid].extent)
-                if g.is_empty(bx):
+                reg = mapper_region(mapper, ch, self.bufs[bid].extent)
+                if not reg:
                     continue
                 if mode in READS:
-                    cmd.reads[(d, bid)] = g.region_union(cmd.reads.get((d, bid), ()), (bx,))
+                    cmd.reads[(d, bid)] = g.region_union(cmd.reads.get((d, bid), ()), reg)
                 if mode in WRITES:
-                    cmd.writes[(d, bid)] = g.region_union(cmd.writes.get((d, bid), ()), (bx,))
+                    cmd.writes[(d, bid)] = g.region_union(cmd.writes.get((d, bid), ()), reg)
         # §4.4 Overlapping-write detection: error, state unchanged
         for bid in sorted({b for (_, b) in cmd.writes}):
             ws = [(d, cmd.writes[(d, bid)]) for d in range(self.G) if (d, bid) in cmd.writes]
@@ -770,8 +770,8 @@ def _norm_mapper(mp):
         mn = tuple(mp[1][0]) + (0,) * (3 - len(mp[1][0]))
         mx = tuple(mp[1][1]) + (1,) * (3 - len(mp[1][1]))
         return ("remap", (mn, mx), kd)
-    if kind == "neighborhood":
-        return ("neighborhood", tuple(mp[1]) + (0,) * (3 - len(mp[1])))
+    if kind in ("neighborhood", "neighborhood_axes"):
+        return (kind, tuple(mp[1]) + (0,) * (3 - len(mp[1])))
     return (kind,)
 
 

@@ -20,7 +20,7 @@ lib = C.CDLL(LIB_PATH)
 OK, W_UNINIT_READ = 0, 1
 E_INVALID, E_OUT_OF_BOUNDS, E_OVERLAPPING_WRITE, E_OOM, E_CUDA, E_NCCL, E_STATE = -1, -2, -3, -4, -5, -6, -7
 
-MAPPERS = {"one_to_one": 0, "neighborhood": 1, "all": 2, "fixed": 3, "remap": 4}
+MAPPERS = {"one_to_one": 0, "neighborhood": 1, "all": 2, "fixed": 3, "remap": 4, "neighborhood_axes": 5}
 MODES = {"read": 1, "write": 2, "read_write": 3}
 SPLITS = {"1d": 0, "2d": 1}
 KERNELS = {"fill_hash": 0, "fill_const": 1, "stencil3": 2, "wave5": 3, "jacobi7": 4, "nbody_step": 5,
@@ -139,7 +139,7 @@ def _mapper(mp):
     m = cel_range_mapper()
     m.kind = MAPPERS[mp[0]]
     m.from_kernel_dim[:] = [-1, -1, -1]
-    if mp[0] == "neighborhood":
+    if mp[0] in ("neighborhood", "neighborhood_axes"):
         bd = list(mp[1]) + [0] * (3 - len(mp[1]))
         m.border[:] = [int(x) for x in bd]
     elif mp[0] in ("fixed", "remap"):

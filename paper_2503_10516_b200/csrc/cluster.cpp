@@ -73,15 +73,15 @@ int Cluster::task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string* e
     for (int n = 0; n < N_; ++n) {
         if (chunks[n].empty()) continue;
         for (const Access& a : desc.acc) {
-            Box bx;
-            const int rc = apply_mapper(a.map, chunks[n], s_[0]->extent(a.buf), &bx);
+            Region reg;
+            const int rc = mapper_region(a.map, chunks[n], s_[0]->extent(a.buf), &reg);
             if (rc != E_OK) {
                 if (err) *err = "range mapper result outside the buffer extent";
                 return rc;
             }
-            if (bx.empty()) continue;
-            if (is_read(a.mode)) rd[n][a.buf] = runion(rd[n][a.buf], Region{bx});
-            if (is_write(a.mode)) wr[n][a.buf] = runion(wr[n][a.buf], Region{bx});
+            if (reg.empty()) continue;
+            if (is_read(a.mode)) rd[n][a.buf] = runion(rd[n][a.buf], reg);
+            if (is_write(a.mode)) wr[n][a.buf] = runion(wr[n][a.buf], reg);
         }
     }
     // §4.4 overlapping writes across nodes

@@ -71,6 +71,8 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     split_ = !(ns && ns[0] == '1');
     const char* ng = getenv("CEL_NO_GROW");
     no_grow_ = ng && ng[0] == '1';
+    const char* np = getenv("CEL_NO_PAD");
+    no_pad_ = np && np[0] == '1';
     grown_ = !no_grow_;
 }
 
@@ -121,6 +123,19 @@ Executor::~Executor() {
 }
 
 void Executor::set_dev(int dev) { cudaSetDevice(phys_[dev]); }
+
+Box Executor::padded_box(const Box& b, uint32_t buffer, uint32_t es) const {
+    if (no_pad_ || (es != 4 && es != 8) || b.empty()) return b;
+    const Box& ext = bufinfo_.at(buffer).extent;
+    int d = 2;                                   // innermost dimension the buffer uses
+    while (d > 0 && ext.hi[d] - ext.lo[d] <= 1) --d;
+    if (d == 0) return b;                        // 1-D: whole rows are contiguous already
+    const int64_t a = 16 / int64_t(es);
+    Box p = b;
+    p.lo[d] = b.lo[d] - (b.lo[d] % a);           // coordinates are >= 0
+    p.hi[d] = p.lo[d] + (b.hi[d] - p.lo[d] + a - 1) / a * a;
+    return p;
+}
 
 void Executor::check(cudaError_t e, const char* what) {
     if (e == cudaSuccess || err_) return;
@@ -864,7 +879,13 @@ void Executor::on_instr_impl(const Instr& ins) {
     case IKind::Alloc: {
         const int dev = ins.mem - 2;
         const uint32_t es = bufinfo_.at(ins.buffer).es;
-        const uint64_t bytes = ins.box.volume() * es;
+        // Physical layout: the allocation's innermost dimension is padded to
+        // 16-byte boundaries (lower end rounded down, width rounded up), so rows
+        // start aligned even when the box begins at a halo column (2-D split):
+        // the vectorised kernels and 16-byte copy paths then apply.  The IDAG's
+        // box is unchanged; every address is computed from the padded box.
+        const Box pbox = padded_box(ins.box, ins.buffer, es);
+        const uint64_t bytes = pbox.volume() * es;
         uint64_t off = 0;
         Token t;
         // In-place growth: a resize that keeps a live
@@ -879,8 +900,8 @@ void Executor::on_instr_impl(const Instr& ins) {
             AllocRec& o = kv.second;
             if (no_grow_ || o.dev != dev || o.buffer != ins.buffer || o.absorbed_into) continue;
             const Box& ob = o.box;
-            if (ob.lo[0] == ins.box.lo[0] && ob.lo[1] == ins.box.lo[1] && ob.lo[2] == ins.box.lo[2] &&
-                ob.hi[1] == ins.box.hi[1] && ob.hi[2] == ins.box.hi[2] && ob.hi[0] <= ins.box.hi[0]) {
+            if (ob.lo[0] == pbox.lo[0] && ob.lo[1] == pbox.lo[1] && ob.lo[2] == pbox.lo[2] &&
+                ob.hi[1] == pbox.hi[1] && ob.hi[2] == pbox.hi[2] && ob.hi[0] <= pbox.hi[0]) {
                 grow = &o;
                 break;
             }
@@ -900,7 +921,7 @@ void Executor::on_instr_impl(const Instr& ins) {
             err_ = E_OOM;
             return;
         }
-        allocs_[ins.aid] = AllocRec{dev, off, bytes, ins.box, es, ins.iid, ins.buffer};
+        allocs_[ins.aid] = AllocRec{dev, off, bytes, pbox, es, ins.iid, ins.buffer};
         live_alloc_iid_.insert(ins.iid);
         Token mt;
         if (mine) merge(mt, t);

@@ -360,6 +360,8 @@ private:
     bool trace_ = false;
     bool split_ = true;
     bool no_grow_ = false;                      // CEL_NO_GROW=1: disable in-place growth (A/B)
+    bool no_pad_ = false;                       // CEL_NO_PAD=1: allocations exactly as the IDAG's boxes
+    Box padded_box(const Box& b, uint32_t buffer, uint32_t es) const;
     bool grown_ = true;                           // track allocation uses for in-place growth
     std::unordered_map<uint64_t, CopyInfo> copy_info_;
     // §8 a7 all-gather as a collective: members are held until the whole set

@@ -142,12 +142,12 @@ void Executor::exec_copy(const Instr& ins) {
             if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
             if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
             g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
-            g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
+
             // huge planes x rows: split so that units stay below 2^63 (never in practice)
             if (args.nseg == kMaxSegs) flush();
             g.units_begin = args.total_units;
             args.seg[args.nseg++] = g;
-            args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
+            args.total_units += seg_units(args.seg[args.nseg - 1]);
             bytes += b.volume() * es;
         }
         flush();

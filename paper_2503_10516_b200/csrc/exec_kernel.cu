@@ -95,7 +95,9 @@ void Executor::exec_kernel(const Instr& ins) {
     bool split = false;
     if (split_ && (d.kernel == K_WAVE5 || d.kernel == K_JACOBI7 || d.kernel == K_STENCIL3)) {
         for (const Access& ac : d.acc) {
-            if (ac.map.kind != MapKind::Neighborhood || (ac.mode != MODE_READ && ac.mode != MODE_READ_WRITE)) continue;
+            if ((ac.map.kind != MapKind::Neighborhood && ac.map.kind != MapKind::NeighborhoodAxes) ||
+                (ac.mode != MODE_READ && ac.mode != MODE_READ_WRITE))
+                continue;
             const Box rb = map_access(ac.map, ins.chunk, bufinfo_.at(ac.buf).extent);
             for (int k = 0; k < 3; ++k) {
                 if (rb.lo[k] < ins.chunk.lo[k]) {

@@ -33,10 +33,10 @@ void box_seg(CopyArgs& args, const char* sb, const Box& S, char* db, const Box& 
     if (g.rows > 1) a |= g.src_row_stride | g.dst_row_stride;
     if (g.planes > 1) a |= g.src_plane_stride | g.dst_plane_stride;
     g.vec = (a & 15) == 0 ? 16 : (a & 7) == 0 ? 8 : (a & 3) == 0 ? 4 : (a & 1) == 0 ? 2 : 1;
-    g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
     g.units_begin = args.total_units;
+    const uint64_t units = seg_units(g);
     args.seg[args.nseg++] = g;
-    args.total_units += uint64_t(g.units_per_row) * g.rows * g.planes;
+    args.total_units += units;
 }
 }  // namespace
 

@@ -121,13 +121,38 @@ __device__ __forceinline__ void copy_span_realign(const char* __restrict__ src, 
 // One CTA per 8 KiB unit (a flat grid: measured faster than a persistent
 // grid-stride loop and than cudaMemcpy / torch copy_ on B200, see
 // tools/copy_micro.cu); units beyond 2^31 CTAs loop.
-__global__ void __launch_bounds__(256) copy_kernel(const __grid_constant__ CopyArgs a) {
+__global__ void __launch_bounds__(256, 8) copy_kernel(const __grid_constant__ CopyArgs a) {   // 8 CTAs/SM: <= 32 registers
     __shared__ uint32_t sm[kCopyUnit / 4 + 8];
     for (uint64_t u = blockIdx.x; u < a.total_units; u += gridDim.x) {
         int s = 0;
         while (s + 1 < a.nseg && a.seg[s + 1].units_begin <= u) ++s;
         const CopySeg& g = a.seg[s];
         const uint64_t lu = u - g.units_begin;
+        if (g.narrow) {
+            // short rows (e.g. a column halo, one element per row): a thread per row
+            const uint64_t rl = lu * g.narrow + threadIdx.x;
+            if (threadIdx.x < g.narrow && rl < uint64_t(g.rows) * g.planes) {
+                const uint64_t plane = rl / g.rows, row = rl - plane * g.rows;
+                const char* sp = g.src + plane * g.src_plane_stride + row * g.src_row_stride;
+                char* dp = g.dst + plane * g.dst_plane_stride + row * g.dst_row_stride;
+                const uint32_t nb = uint32_t(g.row_bytes);
+                switch (g.vec) {
+                case 16:
+                    for (uint32_t o = 0; o < nb; o += 16) *reinterpret_cast<uint4*>(dp + o) = *reinterpret_cast<const uint4*>(sp + o);
+                    break;
+                case 8:
+                    for (uint32_t o = 0; o < nb; o += 8) *reinterpret_cast<uint2*>(dp + o) = *reinterpret_cast<const uint2*>(sp + o);
+                    break;
+                case 4:
+                    for (uint32_t o = 0; o < nb; o += 4) *reinterpret_cast<uint32_t*>(dp + o) = *reinterpret_cast<const uint32_t*>(sp + o);
+                    break;
+                default:
+                    for (uint32_t o = 0; o < nb; ++o) dp[o] = sp[o];
+                    break;
+                }
+            }
+            continue;
+        }
         const uint64_t row_lin = lu / g.units_per_row;
         const uint32_t chunk = uint32_t(lu - row_lin * g.units_per_row);
         const uint64_t plane = row_lin / g.rows;
@@ -1182,7 +1207,7 @@ int launch_copy(const CopyArgs& a, cudaStream_t s) {
         use_tma = (e && e[0] == 't') ? 1 : 0;
     }
     bool all16 = true;
-    for (int i = 0; i < a.nseg; ++i) all16 = all16 && a.seg[i].vec == 16;
+    for (int i = 0; i < a.nseg; ++i) all16 = all16 && a.seg[i].vec == 16 && !a.seg[i].narrow;
     if (use_tma && all16 && !a.peer) {
         int dev = 0;
         cudaGetDevice(&dev);

@@ -19,9 +19,11 @@ struct CopySeg {
     uint64_t units_begin;      // prefix sum of work units (exclusive)
     uint32_t units_per_row;
     uint32_t vec;              // 16, 8, 4, 2 or 1 byte accesses
+    uint32_t narrow;           // > 0: rows of <= kNarrowBytes, a unit = `narrow` whole rows, one per thread
 };
 
 constexpr int kMaxSegs = 24;
+constexpr uint64_t kNarrowBytes = 256;     // rows this short are packed 256 per CTA (e.g. column halos)
 constexpr uint32_t kCopyUnit = 8192;      // bytes of one row chunk = one CTA (256 threads x 2 x 16 B)
 
 struct CopyArgs {
@@ -81,6 +83,20 @@ enum : int {
     K_CALLBACK = 9,
     K_NUM = 10,
 };
+
+// Work units of a segment (fields src .. vec set): a unit is one <= kCopyUnit
+// chunk of a row, or, for many short rows, 256 whole rows (one per thread).
+inline uint64_t seg_units(CopySeg& g) {
+    const uint64_t nrows = uint64_t(g.rows) * g.planes;
+    if (g.row_bytes <= kNarrowBytes && nrows >= 64) {
+        g.narrow = 256;
+        g.units_per_row = 0;
+        return (nrows + g.narrow - 1) / g.narrow;
+    }
+    g.narrow = 0;
+    g.units_per_row = uint32_t((g.row_bytes + kCopyUnit - 1) / kCopyUnit);
+    return uint64_t(g.units_per_row) * nrows;
+}
 
 // Returns the number of kernel launches issued (0 if nothing to do).
 int launch_copy(const CopyArgs& a, cudaStream_t s);

@@ -71,7 +71,8 @@ int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out) {
         if (!ext.contains(chunk)) return E_OUT_OF_BOUNDS;
         *out = chunk;
         return E_OK;
-    case MapKind::Neighborhood: {
+    case MapKind::Neighborhood:
+    case MapKind::NeighborhoodAxes: {
         Box b;
         for (int d = 0; d < 3; ++d) {
             b.lo[d] = chunk.lo[d] - m.border[d];
@@ -111,6 +112,30 @@ int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out) {
     }
     }
     return E_INVALID;
+}
+
+int mapper_region(const Mapper& m, const Box& chunk, const Box& ext, Region* out) {
+    Box bx;
+    const int rc = apply_mapper(m, chunk, ext, &bx);
+    if (rc != E_OK) return rc;
+    out->clear();
+    if (bx.empty()) return E_OK;
+    if (m.kind != MapKind::NeighborhoodAxes) {
+        *out = Region{bx};
+        return E_OK;
+    }
+    // union over dims d of the chunk inflated by border[d] in dim d alone
+    Region r{intersect(chunk, ext)};
+    for (int d = 0; d < 3; ++d) {
+        if (m.border[d] <= 0) continue;
+        Box b = chunk;
+        b.lo[d] -= m.border[d];
+        b.hi[d] += m.border[d];
+        b = intersect(b, ext);
+        if (!b.empty()) r = runion(r, Region{b});
+    }
+    *out = std::move(r);
+    return E_OK;
 }
 
 bool is_read(int mode) { return mode == MODE_READ || mode == MODE_READ_WRITE; }
@@ -268,7 +293,7 @@ int Scheduler::prepare(const TaskDesc& d, Cmd& c, std::string* err, const Box* n
             if (err) *err = "bad access mode";
             return E_INVALID;
         }
-        if (int(a.map.kind) < 0 || int(a.map.kind) > 4) {
+        if (int(a.map.kind) < 0 || int(a.map.kind) > 5) {
             if (err) *err = "bad range mapper";
             return E_INVALID;
         }
@@ -278,16 +303,16 @@ int Scheduler::prepare(const TaskDesc& d, Cmd& c, std::string* err, const Box* n
         const Box& ch = c.chunks[dev];
         if (ch.empty()) continue;
         for (const Access& a : d.acc) {
-            Box bx;
-            const int rc = apply_mapper(a.map, ch, bufs_.at(a.buf)->extent, &bx);
+            Region reg;
+            const int rc = mapper_region(a.map, ch, bufs_.at(a.buf)->extent, &reg);
             if (rc != E_OK) {
                 if (err) *err = "range mapper result outside the buffer extent";
                 return rc;
             }
-            if (bx.empty()) continue;
+            if (reg.empty()) continue;
             const Key k{dev, a.buf};
-            if (is_read(a.mode)) c.reads[k] = runion(c.reads[k], Region{bx});
-            if (is_write(a.mode)) c.writes[k] = runion(c.writes[k], Region{bx});
+            if (is_read(a.mode)) c.reads[k] = runion(c.reads[k], reg);
+            if (is_write(a.mode)) c.writes[k] = runion(c.writes[k], reg);
         }
     }
     // §4.4 overlapping-write detection
@@ -837,7 +862,16 @@ std::map<uint32_t, uint32_t> Scheduler::all_gathers(
                 const int s = ms - 2;
                 const Box& b = p.second[0];
                 const Alloc* src = allocs_.at(std::get<2>(p.first)).get();
-                if (!contiguous_in(b, src->box) || !contiguous_in(b, bit->second->box)) {
+                // one contiguous byte run in both allocations, robust to the
+                // executor padding the innermost dimension of multi-dimensional
+                // allocations: 1-D buffers, or a single row segment
+                const Box& ext = bufs_.at(bid)->extent;
+                int inner = 2;
+                while (inner > 0 && ext.extent(inner) <= 1) --inner;
+                bool row = true;
+                for (int k = 0; k < inner; ++k)
+                    if (b.extent(k) != 1) row = false;
+                if (!contiguous_in(b, src->box) || !contiguous_in(b, bit->second->box) || !row) {
                     ok = false;
                     break;
                 }

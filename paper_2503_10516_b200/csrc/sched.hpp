@@ -31,7 +31,9 @@ enum : int {
     E_STATE = -7,
 };
 
-enum class MapKind : int { OneToOne = 0, Neighborhood = 1, All = 2, Fixed = 3, Remap = 4 };
+// NeighborhoodAxes: the axis-only neighbourhood (a stencil reading no corners,
+// SURVEY NEXT-3); its box is the cross's bounding box, mapper_region the cross
+enum class MapKind : int { OneToOne = 0, Neighborhood = 1, All = 2, Fixed = 3, Remap = 4, NeighborhoodAxes = 5 };
 
 struct Mapper {
     MapKind kind = MapKind::OneToOne;

@@ -10,6 +10,8 @@ namespace detail {
 void split_1d(const Box& rng, int n, int dim, std::vector<Box>& out);
 std::vector<Box> split(const Box& rng, int n, int kind);        // R4: 0 = 1D, 1 = 2D
 int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out);   // R5
+// the region a chunk accesses: the mapper's box, except the cross of NeighborhoodAxes
+int mapper_region(const Mapper& m, const Box& chunk, const Box& ext, Region* out);
 bool is_read(int mode);
 bool is_write(int mode);
 }  // namespace detail

@@ -206,3 +206,20 @@ def test_cluster_full_size_counts(cel):
         for k in range(N):
             assert c[k] == o.logs[k]
         assert sum(1 for r in c[0] if r["kind"] == "send") > 0
+
+
+def test_axis_neighborhood_and_2d_wavesim_logs(cel):
+    """WaveSim with the axis-only neighbourhood and the 2-D split:
+    C++ logs equal the oracle's, and no corner element is ever copied."""
+    for G in (2, 4, 6, 8):
+        for split in ("1d", "2d"):
+            prog = P.wavesim(96, 5, rows=72, split=split, mapper="neighborhood_axes")
+            for mode in ("none", "auto"):
+                o, c = both_logs(cel, prog, G, mode)
+                assert_same(o, c)
+                check(c, o.buf_meta, o.tasks)
+    # 2-D split, 4 devices: the box neighbourhood also moves the 4 corner elements per step
+    box = both_logs(cel, P.wavesim(96, 4, rows=72, split="2d"), 4, "auto")[1]
+    axes = both_logs(cel, P.wavesim(96, 4, rows=72, split="2d", mapper="neighborhood_axes"), 4, "auto")[1]
+    ncopy = lambda log: sum(1 for r in log if r["kind"] == "copy" and r["reason"] == "coherence")  # noqa: E731
+    assert ncopy(box) - ncopy(axes) == 4 * 4

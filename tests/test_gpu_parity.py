@@ -352,3 +352,12 @@ def test_bounds_check_no_false_positives(cel, G):
         for k, arr in enumerate(got):
             defined = exp[k] != np.uint32(0x7FC00BAD)
             assert np.array_equal(arr[defined], exp[k][defined]), prog["name"]
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_wavesim_2d_split_axis_neighborhood(cel, G):
+    """WaveSim with the 2-D split, box and axis-only
+    neighbourhoods, bit-exact against the oracle (ragged tiles)."""
+    for mp in ("neighborhood", "neighborhood_axes"):
+        run_both(cel, P.wavesim(515, 5, rows=130, split="2d", mapper=mp), G)
+        run_both(cel, P.wavesim(516, 4, rows=260, split="2d", mapper=mp), G)

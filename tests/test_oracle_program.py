@@ -95,3 +95,23 @@ def test_mapper_monotone():
         c1 = B([r.randrange(c2[0][d], c2[1][d]) for d in range(3)], [c2[1][d] for d in range(3)])
         for mp in [("one_to_one",), ("neighborhood", (1, 2, 0)), ("all",), ("fixed", B([1, 1, 1], [3, 3, 3]))]:
             assert g.box_contains(apply_mapper(mp, c2, ext), apply_mapper(mp, c1, ext))
+
+
+def test_axis_neighborhood_region():
+    """The axis-only neighbourhood is the union of the chunk
+    inflated along each dimension alone: a cross; volume by inclusion-exclusion,
+    and brute force on a small grid."""
+    from oracle.program import mapper_region
+    ext = g.box([0, 0], [10, 10])
+    ch = g.box([2, 3], [5, 7])
+    r = mapper_region(("neighborhood_axes", (1, 1, 0)), ch, ext)
+    assert g.region_volume(r) == 5 * 4 + 3 * 6 - 3 * 4
+    pts = {(z, y) for z in range(10) for y in range(10)
+           if (2 <= z < 5 and 2 <= y < 8) or (1 <= z < 6 and 3 <= y < 7)}
+    got = {(z, y) for b in r for z in range(b[0][0], b[1][0]) for y in range(b[0][1], b[1][1])}
+    assert got == pts
+    # clamped at the extent, and equal to the box mapper in 1-D
+    r0 = mapper_region(("neighborhood_axes", (2, 2, 0)), g.box([0, 0], [3, 3]), ext)
+    assert g.region_bbox(r0) == g.box([0, 0], [5, 5]) and g.region_volume(r0) == 9 + 2 * 6
+    assert mapper_region(("neighborhood_axes", (1, 0, 0)), g.box([3], [5]), g.box([0], [9])) == \
+        mapper_region(("neighborhood", (1, 0, 0)), g.box([3], [5]), g.box([0], [9]))

@@ -9,7 +9,7 @@ the product binding alike:
   spec = {"dims", "range": (mins, maxs), "split": "1d" | "2d",
           "kernel": name, "params": {...},
           "accesses": [(bid, "read" | "write" | "read_write", mapper)]}
-  mapper = ("one_to_one",) | ("neighborhood", (b0, b1, b2)) | ("all",) |
+  mapper = ("one_to_one",) | ("neighborhood", (b0, b1, b2)) | ("neighborhood_axes", (b0, b1, b2)) | ("all",) |
            ("fixed", (mins, maxs)) | ("remap", (mins, maxs), (k0, k1, k2))
 
 Input recipe: every value is either produced on the
@@ -62,28 +62,31 @@ def listing5(n=64, seed=1):
 
 
 # ---------------------------------------------------------------- C2
-def wavesim_init(n, seed=2, rows=None):
+def wavesim_init(n, seed=2, rows=None, split="1d"):
     rows = n if rows is None else rows
     u, up = 0, 1
     r = full([rows, n])
     return [
-        _task(2, r, "fill_hash", [(u, "write", ("one_to_one",))], {"seed": seed}),
-        _task(2, r, "fill_hash", [(up, "write", ("one_to_one",))], {"seed": seed}),
+        _task(2, r, "fill_hash", [(u, "write", ("one_to_one",))], {"seed": seed}, split=split),
+        _task(2, r, "fill_hash", [(up, "write", ("one_to_one",))], {"seed": seed}, split=split),
     ]
 
 
-def wavesim_step(n, k, rows=None):
-    """Step k of WaveSim: up = wave5(u, up); then the roles swap."""
+def wavesim_step(n, k, rows=None, split="1d", mapper="neighborhood"):
+    """Step k of WaveSim: up = wave5(u, up); then the roles swap.
+    mapper "neighborhood_axes" declares the 5-point stencil's cross exactly
+    (no corners); split "2d" tiles the grid over the devices."""
     rows = n if rows is None else rows
     u, up = (0, 1) if k % 2 == 0 else (1, 0)
     return _task(2, full([rows, n]), "wave5",
-                 [(u, "read", ("neighborhood", (1, 1))), (up, "read_write", ("one_to_one",))])
+                 [(u, "read", (mapper, (1, 1))), (up, "read_write", ("one_to_one",))], split=split)
 
 
-def wavesim(n=16384, steps=4, seed=2, rows=None):
-    """Config 2: WaveSim 2-D 5-point stencil, rows x n fp32, 1-D row split."""
+def wavesim(n=16384, steps=4, seed=2, rows=None, split="1d", mapper="neighborhood"):
+    """Config 2: WaveSim 2-D 5-point stencil, rows x n fp32, 1-D row split
+    (split / mapper: the NEXT-3 variants, see wavesim_step)."""
     rows = n if rows is None else rows
-    ops = wavesim_init(n, seed, rows) + [wavesim_step(n, k, rows) for k in range(steps)]
+    ops = wavesim_init(n, seed, rows, split) + [wavesim_step(n, k, rows, split, mapper) for k in range(steps)]
     ops += [("read", 0, full([rows, n])), ("read", 1, full([rows, n]))]
     bufs = [{"dims": 2, "extent": [rows, n], "elem_size": 4, "host_init": None} for _ in range(2)]
     return {"name": "wavesim", "buffers": bufs, "ops": ops}
