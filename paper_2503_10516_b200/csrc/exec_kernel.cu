@@ -98,14 +98,22 @@ void Executor::exec_kernel(const Instr& ins) {
             if ((ac.map.kind != MapKind::Neighborhood && ac.map.kind != MapKind::NeighborhoodAxes) ||
                 (ac.mode != MODE_READ && ac.mode != MODE_READ_WRITE))
                 continue;
-            const Box rb = map_access(ac.map, ins.chunk, bufinfo_.at(ac.buf).extent);
+            const Box& ext = bufinfo_.at(ac.buf).extent;
+            const Box rb = map_access(ac.map, ins.chunk, ext);
+            // bands along the innermost dimension are widened to 16 bytes, so
+            // the interior keeps the chunk's alignment (vectorised kernels)
+            int inner = 2;
+            while (inner > 0 && ext.extent(inner) <= 1) --inner;
+            const int64_t es = int64_t(bufinfo_.at(ac.buf).es);
             for (int k = 0; k < 3; ++k) {
+                int64_t bw = ac.map.border[k];
+                if (k == inner && k > 0 && (es == 4 || es == 8)) bw = (bw + 16 / es - 1) / (16 / es) * (16 / es);
                 if (rb.lo[k] < ins.chunk.lo[k]) {
-                    interior.lo[k] = std::max(interior.lo[k], ins.chunk.lo[k] + ac.map.border[k]);
+                    interior.lo[k] = std::max(interior.lo[k], ins.chunk.lo[k] + bw);
                     split = true;
                 }
                 if (rb.hi[k] > ins.chunk.hi[k]) {
-                    interior.hi[k] = std::min(interior.hi[k], ins.chunk.hi[k] - ac.map.border[k]);
+                    interior.hi[k] = std::min(interior.hi[k], ins.chunk.hi[k] - bw);
                     split = true;
                 }
             }
