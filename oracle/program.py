@@ -16,7 +16,9 @@ R5  Range mappers: one_to_one -> chunk (error if not
     neighborhood"); all -> extent ("always spans the entire buffer range",
     P:L163); fixed(box) -> box (error if outside); remap(box, kdims)
     [reading, for RSim P:L632]: buffer dim k takes the chunk's interval in
-    kernel dim kdims[k], or box's interval when kdims[k] == -1.
+    kernel dim kdims[k], or box's interval when kdims[k] == -1;
+    neighborhood_axes(b) [SURVEY NEXT-3] -> the cross: the chunk inflated by
+    b[d] along one dim d at a time (mapper_region); its box is the bbox.
 """
 
 from . import geometry as g
