@@ -890,16 +890,43 @@ __global__ void nbody_update_kernel(const __grid_constant__ KArgs a) {
 // ------------------------------------------------------------------ C4 RSim row
 // Row t = 0.5 * row[t-1] + 0.5/t * sum_{s<t} row[s][(i+s) mod W], the sum taken
 // in ascending s with sequential adds (R16).  HBM bound: t*W*4 B per launch.
-// Each thread keeps U independent loads in flight (memory-level parallelism:
-// ~18 warps per SM at W = 84,000, so U = 16 puts ~36 KB per SM in flight).
-// Rows below `keep` are loaded with an L2 evict_last policy and the rest with
-// evict_first: every launch re-reads all earlier rows, a cyclic sweep larger
-// than L2 that plain LRU never hits; pinning a fixed prefix of rows makes that
-// prefix hit in every later launch.
-__device__ __forceinline__ float ld_policy(const float* p, uint64_t pol) {
-    float v;
-    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-    return v;
+// Register fallback (when the TMA variant's layout preconditions fail): each
+// thread keeps U = 16 independent loads in flight (~18 warps per SM at
+// W = 84,000; 8 loads in flight ran 56 ms per 1024 rows, 16 ran 42.5 ms).
+// Evict-last / evict-first L2 hints for a pinned prefix of rows were measured
+// and dropped (within 2%).
+template <int U>
+__global__ void __launch_bounds__(128) rsim_row_kernel(const __grid_constant__ KArgs a) {
+    const DAcc& R = a.acc[0];
+    const DAcc& Wr = a.acc[1];
+    const int64_t t = a.t;
+    const int64_t W = R.ext[1];
+    const float* base = ptr<const float>(R, 0, 0, 0);
+    const int64_t pitch = R.n[1];
+    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
+         i += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        int64_t s = 0;
+        for (; s + U <= t; s += U) {
+            float v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                int64_t c = i + s + k;
+                c = c >= W ? c - W : c;
+                v[k] = __ldg(base + (s + k) * pitch + c);
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) acc = acc + v[k];
+        }
+        for (; s < t; ++s) {
+            int64_t c = i + s;
+            c = c >= W ? c - W : c;
+            acc = acc + __ldg(base + s * pitch + c);
+        }
+        const float prev = *ptr<const float>(R, t - 1, i, 0);
+        const float coef = 0.5f / float(t);
+        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
+    }
 }
 
 // Bounds-checked variant: every element access through at() (§4.4).
@@ -919,48 +946,6 @@ __global__ void rsim_row_checked(const __grid_constant__ KArgs a) {
         const float prev = *at<const float>(R, t - 1, i, 0);
         const float coef = 0.5f / float(t);
         *at<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
-    }
-}
-
-// Software-pipelined variant: the next group of U loads is issued before the
-// current group is summed, so 2U loads per thread stay in flight.
-template <int U>
-__global__ void rsim_row_pipe_kernel(const __grid_constant__ KArgs a) {
-    const DAcc& R = a.acc[0];
-    const DAcc& Wr = a.acc[1];
-    const int64_t t = a.t;
-    const int64_t W = R.ext[1];
-    const float* base = ptr<const float>(R, 0, 0, 0);
-    const int64_t pitch = R.n[1];
-    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
-         i += int64_t(gridDim.x) * blockDim.x) {
-        float acc = 0.f;
-        const int64_t full = t / U * U;
-        float cur[U], nxt[U];
-        auto load = [&](float* v, int64_t s0) {
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                int64_t c = i + s0 + k;
-                c = c >= W ? c - W : c;
-                v[k] = __ldg(base + (s0 + k) * pitch + c);
-            }
-        };
-        if (full > 0) load(cur, 0);
-        for (int64_t s = 0; s < full; s += U) {
-            if (s + U < full) load(nxt, s + U);
-#pragma unroll
-            for (int k = 0; k < U; ++k) acc = acc + cur[k];
-#pragma unroll
-            for (int k = 0; k < U; ++k) cur[k] = nxt[k];
-        }
-        for (int64_t s = full; s < t; ++s) {
-            int64_t c = i + s;
-            c = c >= W ? c - W : c;
-            acc = acc + __ldg(base + s * pitch + c);
-        }
-        const float prev = *ptr<const float>(R, t - 1, i, 0);
-        const float coef = 0.5f / float(t);
-        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
     }
 }
 
@@ -1089,43 +1074,6 @@ bool rsim_tensor_map(const DAcc& A, CUtensorMap* out) {
     return true;
 }
 
-template <int U>
-__global__ void __launch_bounds__(128) rsim_row_kernel(const __grid_constant__ KArgs a, int64_t keep) {
-    const DAcc& R = a.acc[0];
-    const DAcc& Wr = a.acc[1];
-    const int64_t t = a.t;
-    const int64_t W = R.ext[1];
-    uint64_t pol_keep, pol_stream;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
-    const float* base = ptr<const float>(R, 0, 0, 0);
-    const int64_t pitch = R.n[1];
-    for (int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < a.chunk.hi[0];
-         i += int64_t(gridDim.x) * blockDim.x) {
-        float acc = 0.f;
-        int64_t s = 0;
-        for (; s + U <= t; s += U) {
-            float v[U];
-            const uint64_t pol = s + U <= keep ? pol_keep : pol_stream;
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                int64_t c = i + s + k;
-                c = c >= W ? c - W : c;
-                v[k] = ld_policy(base + (s + k) * pitch + c, pol);
-            }
-#pragma unroll
-            for (int k = 0; k < U; ++k) acc = acc + v[k];
-        }
-        for (; s < t; ++s) {
-            int64_t c = i + s;
-            c = c >= W ? c - W : c;
-            acc = acc + ld_policy(base + s * pitch + c, s < keep ? pol_keep : pol_stream);
-        }
-        const float prev = *ptr<const float>(R, t - 1, i, 0);
-        const float coef = 0.5f / float(t);
-        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
-    }
-}
 
 // ------------------------------------------------------------------ integer probe
 __device__ uint32_t probe_sum(const DAcc& A, int64_t z, int64_t y, int64_t x) {
@@ -1336,22 +1284,11 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         if (cv == 0) return 0;
         nbody_update_kernel<<<grid_for(cv, 256), 256, 0, s>>>(a);
         return 1;
-    case K_RSIM_ROW:
+    case K_RSIM_ROW: {
         if (cv == 0) return 0;
-    {
-        static int unroll = 0;
-        static int64_t keep_bytes = -1;
-        if (!unroll) {
-            const char* e = getenv("CEL_RSIM_UNROLL");
-            unroll = e ? atoi(e) : 16;
-            const char* k = getenv("CEL_RSIM_KEEP_MB");
-            keep_bytes = (k ? atoll(k) : 48) << 20;
-        }
-        const int64_t row_bytes = a.acc[0].n[1] * 4;
-        const int64_t keep = row_bytes > 0 ? keep_bytes / row_bytes : 0;
         static int variant = -1;
         if (variant < 0) {
-            const char* e = getenv("CEL_RSIM");
+            const char* e = getenv("CEL_RSIM");          // 0: force the register kernel (A/B)
             variant = e ? atoi(e) : 5;
         }
         const DAcc& R0 = a.acc[0];
@@ -1360,35 +1297,14 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             return 1;
         }
         CUtensorMap tm;
-        if (variant == 5 && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
+        if (variant != 0 && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
             R0.lo[2] == 0 && R0.es == 4 && R0.ext[1] >= 2 * kRB && R0.lo[0] == 0 &&
             (reinterpret_cast<uintptr_t>(R0.base) & 15) == 0 && a.t > 0 && rsim_tensor_map(R0, &tm)) {
             const unsigned grid = unsigned((cv + kRC - 1) / kRC);
             rsim_row_tma<<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a);
             return 1;
         }
-        if (variant == 1) {         // pipelined, 64-thread CTAs
-            rsim_row_pipe_kernel<16><<<grid_for(cv, 64), 64, 0, s>>>(a);
-            return 1;
-        }
-        if (variant == 2) {         // pipelined, 128-thread CTAs
-            rsim_row_pipe_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a);
-            return 1;
-        }
-        if (variant == 3) {         // pipelined U=8, 64-thread CTAs
-            rsim_row_pipe_kernel<8><<<grid_for(cv, 64), 64, 0, s>>>(a);
-            return 1;
-        }
-        if (variant == 4) {         // burst U=16, 64-thread CTAs
-            rsim_row_kernel<16><<<grid_for(cv, 64), 64, 0, s>>>(a, keep);
-            return 1;
-        }
-        if (unroll == 8)
-            rsim_row_kernel<8><<<grid_for(cv, 128), 128, 0, s>>>(a, keep);
-        else if (unroll == 32)
-            rsim_row_kernel<32><<<grid_for(cv, 128), 128, 0, s>>>(a, keep);
-        else
-            rsim_row_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a, keep);
+        rsim_row_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a);
         return 1;
     }
     case K_PROBE: {
