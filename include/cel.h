@@ -182,6 +182,9 @@ typedef struct {
                                   0 or 1 = one node (the default). */
 } cel_config;
 
+/* Counters since runtime creation.  Instruction counts are the node's IDAG
+ * (every rank of a multi-process run replays the whole node's graph); executor
+ * counters are this process's.  Virtual-node mode: totals over the nodes. */
 typedef struct {
     uint64_t n_alloc, n_free, n_copy, n_kernel, n_horizon, n_epoch;
     uint64_t copies_resize, copies_coherence, copies_readback;
