@@ -126,6 +126,16 @@ def test_all_gather_detection(cel, monkeypatch):
         assert _gather_sets(cel, P.jacobi3d(16, 2), G)[0] == 0
         assert _gather_sets(cel, P.c1_chain(64), G)[0] == 0
     assert _gather_sets(cel, P.nbody(1000, 2), 1) == (0, 0)
+    # a 2-D buffer gathered in multi-row boxes is not flagged: the executor pads
+    # allocation rows to 16 bytes, so such boxes need not be one byte run
+    n = 64
+    prog = {"name": "all2d", "buffers": [{"dims": 2, "extent": [n, n], "elem_size": 4, "host_init": None},
+                                         {"dims": 2, "extent": [n, n], "elem_size": 4, "host_init": None}],
+            "ops": [P._task(2, P.full([n, n]), "fill_hash", [(0, "write", ("one_to_one",))], {"seed": 1}),
+                    P._task(2, P.full([n, n]), "probe", [(0, "read", ("all",)), (1, "write", ("one_to_one",))],
+                            {"salt": 2})]}
+    for G in (2, 4):
+        assert _gather_sets(cel, prog, G)[0] == 0
     # the default threshold (1 MiB per source) keeps small gathers on peer pushes
     monkeypatch.delenv("CEL_COLL_MIN_BYTES")
     assert _gather_sets(cel, P.nbody(1000, 2), 4)[0] == 0
