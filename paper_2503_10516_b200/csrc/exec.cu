@@ -67,6 +67,11 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     G_ = int(cfg_.cuda_devices.size());
     const char* tr = getenv("CEL_TRACE");
     trace_ = tr && tr[0] == '1';
+    // small contiguous pushes to another GPU go to a copy engine: a 64 KiB halo
+    // push as an SM kernel took SM time from the running stencil (kernel share
+    // 0.940 -> 0.986 of the step at 4 GPUs with DMA); CEL_PEER_DMA=0 for A/B
+    const char* pd = getenv("CEL_PEER_DMA");
+    peer_dma_ = !(pd && pd[0] == '0');
     const char* ns = getenv("CEL_NO_SPLIT");
     split_ = !(ns && ns[0] == '1');
     const char* ng = getenv("CEL_NO_GROW");

@@ -101,6 +101,31 @@ void Executor::exec_copy(const Instr& ins) {
         args.peer = peer && phys_[S.dev] != phys_[D.dev] ? 1 : 0;
         const int64_t sn1 = S.box.extent(1), sn2 = S.box.extent(2);
         const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
+        if (args.peer && peer_dma_) {
+            // small pushes to another GPU on a copy engine (DMA): no SM time taken
+            // from the running stencil; each box must be one byte run in both
+            bool runs = ins.region.size() <= 4;
+            uint64_t total = 0;
+            for (const Box& b : ins.region) {
+                const bool cs = b.extent(2) == sn2 && (b.extent(1) == sn1 || b.extent(0) == 1);
+                const bool cd = b.extent(2) == dn2 && (b.extent(1) == dn1 || b.extent(0) == 1);
+                if (!(cs && cd) && !(b.extent(0) == 1 && b.extent(1) == 1)) runs = false;
+                total += b.volume() * es;
+            }
+            if (runs && total <= peer_dma_max_) {
+                for (const Box& b : ins.region) {
+                    const int64_t so = ((b.lo[0] - S.box.lo[0]) * sn1 + (b.lo[1] - S.box.lo[1])) * sn2 + (b.lo[2] - S.box.lo[2]);
+                    const int64_t dof = ((b.lo[0] - D.box.lo[0]) * dn1 + (b.lo[1] - D.box.lo[1])) * dn2 + (b.lo[2] - D.box.lo[2]);
+                    check(cudaMemcpyAsync(db + dof * es, sb + so * es, size_t(b.volume()) * es, cudaMemcpyDeviceToDevice,
+                                          streams_[sidx].s),
+                          "cudaMemcpyAsync (peer DMA)");
+                    st_.memcpy_calls++;
+                }
+                st_.bytes_copy[2] += total;
+                tok_[ins.iid] = record(sidx);
+                return;
+            }
+        }
         uint64_t bytes = 0;
         auto flush = [&]() {
             if (args.nseg == 0) return;
