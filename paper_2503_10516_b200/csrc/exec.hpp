@@ -360,7 +360,7 @@ private:
     bool trace_ = false;
     bool split_ = true;
     bool peer_dma_ = true;                        // small contiguous pushes on a copy engine (CEL_PEER_DMA=0: off)
-    uint64_t peer_dma_max_ = 1ull << 20;
+    uint64_t peer_dma_max_ = 4ull << 20;
     bool no_grow_ = false;                      // CEL_NO_GROW=1: disable in-place growth (A/B)
     bool no_pad_ = false;                       // CEL_NO_PAD=1: allocations exactly as the IDAG's boxes
     Box padded_box(const Box& b, uint32_t buffer, uint32_t es) const;

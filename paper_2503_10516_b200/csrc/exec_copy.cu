@@ -103,22 +103,53 @@ void Executor::exec_copy(const Instr& ins) {
         const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
         if (args.peer && peer_dma_) {
             // small pushes to another GPU on a copy engine (DMA): no SM time taken
-            // from the running stencil; each box must be one byte run in both
-            bool runs = ins.region.size() <= 4;
+            // from the running stencil.  Each box must be one byte run in both
+            // allocations, or one run per row at a constant pitch in each
+            // (a 2-D copy: e.g. a y-face of a 3-D halo, 256 rows of 4 KiB)
+            struct Dma {
+                int64_t so, dof;
+                size_t width, height, spitch, dpitch;
+            };
+            SmallVec<Dma, 4> plan;
+            bool ok = ins.region.size() <= 4;
             uint64_t total = 0;
             for (const Box& b : ins.region) {
+                if (!ok) break;
+                Dma m;
+                m.so = ((b.lo[0] - S.box.lo[0]) * sn1 + (b.lo[1] - S.box.lo[1])) * sn2 + (b.lo[2] - S.box.lo[2]);
+                m.dof = ((b.lo[0] - D.box.lo[0]) * dn1 + (b.lo[1] - D.box.lo[1])) * dn2 + (b.lo[2] - D.box.lo[2]);
                 const bool cs = b.extent(2) == sn2 && (b.extent(1) == sn1 || b.extent(0) == 1);
                 const bool cd = b.extent(2) == dn2 && (b.extent(1) == dn1 || b.extent(0) == 1);
-                if (!(cs && cd) && !(b.extent(0) == 1 && b.extent(1) == 1)) runs = false;
+                if ((cs && cd) || (b.extent(0) == 1 && b.extent(1) == 1)) {
+                    m.width = size_t(b.volume()) * es;       // one run
+                    m.height = 1;
+                    m.spitch = m.dpitch = m.width;
+                } else if (b.extent(0) == 1) {                // rows of one plane
+                    m.width = size_t(b.extent(2)) * es;
+                    m.height = size_t(b.extent(1));
+                    m.spitch = size_t(sn2) * es;
+                    m.dpitch = size_t(dn2) * es;
+                } else if (b.extent(1) == 1) {                // one row per plane
+                    m.width = size_t(b.extent(2)) * es;
+                    m.height = size_t(b.extent(0));
+                    m.spitch = size_t(sn1 * sn2) * es;
+                    m.dpitch = size_t(dn1 * dn2) * es;
+                } else {
+                    ok = false;
+                }
+                plan.push_back(m);
                 total += b.volume() * es;
             }
-            if (runs && total <= peer_dma_max_) {
-                for (const Box& b : ins.region) {
-                    const int64_t so = ((b.lo[0] - S.box.lo[0]) * sn1 + (b.lo[1] - S.box.lo[1])) * sn2 + (b.lo[2] - S.box.lo[2]);
-                    const int64_t dof = ((b.lo[0] - D.box.lo[0]) * dn1 + (b.lo[1] - D.box.lo[1])) * dn2 + (b.lo[2] - D.box.lo[2]);
-                    check(cudaMemcpyAsync(db + dof * es, sb + so * es, size_t(b.volume()) * es, cudaMemcpyDeviceToDevice,
-                                          streams_[sidx].s),
-                          "cudaMemcpyAsync (peer DMA)");
+            if (ok && total <= peer_dma_max_) {
+                for (const Dma& m : plan) {
+                    if (m.height == 1)
+                        check(cudaMemcpyAsync(db + m.dof * es, sb + m.so * es, m.width, cudaMemcpyDeviceToDevice,
+                                              streams_[sidx].s),
+                              "cudaMemcpyAsync (peer DMA)");
+                    else
+                        check(cudaMemcpy2DAsync(db + m.dof * es, m.dpitch, sb + m.so * es, m.spitch, m.width, m.height,
+                                                cudaMemcpyDeviceToDevice, streams_[sidx].s),
+                              "cudaMemcpy2DAsync (peer DMA)");
                     st_.memcpy_calls++;
                 }
                 st_.bytes_copy[2] += total;
