@@ -151,3 +151,43 @@ def test_configs_match_sequential(N, D):
         for mode in ("none", "auto"):
             cl = run(prog, N, D, mode)
             assert bytes_match(cl, prog), (prog["name"], mode)
+
+
+def pushed_elements(cl):
+    return sum(g.volume(p["box"]) for p in cl.pilots())
+
+
+@pytest.mark.parametrize("N,D", [(2, 1), (3, 2), (4, 1), (4, 2)])
+@pytest.mark.parametrize("mapper", ["neighborhood", "neighborhood_axes"])
+def test_wavesim_halo_volume_closed_form(N, D, mapper):
+    """Closed form of the inter-node traffic of a radius-1 stencil under the
+    1-D node split (§3.4 push / await-push; R17): every step each
+    of the N-1 interior boundaries exchanges one full row each way
+    (2(N-1) rows of n cells; the buffer read was rewritten by its owners in the
+    previous step, so no halo is still valid), the devices inside a node
+    add nothing, and the final readback of both buffers makes node 0 pull the
+    R - R/N rows it does not own, twice, less the one halo row of the buffer
+    the last step read, which node 0 received then and still holds (R17
+    holders: not rewritten since)."""
+    R, n, steps = 6 * N, 10, 3
+    cl = run(P.wavesim(n, steps, rows=R, mapper=mapper), N, D)
+    assert pushed_elements(cl) == steps * 2 * (N - 1) * n + (2 * (R - R // N) - 1) * n
+    # every step push is one row, from an adjacent node
+    for p in cl.pilots():
+        (lo, hi) = p["box"]
+        if hi[0] - lo[0] == 1:
+            assert abs(p["sender"] - p["receiver"]) == 1
+
+
+@pytest.mark.parametrize("N", [2, 3, 4])
+@pytest.mark.parametrize("host_init", [False, True])
+def test_nbody_allgather_volume_closed_form(N, host_init):
+    """Closed form for the all-gather of Listing 1 ("all" mapper):
+    a timestep makes every node receive the n - n/N bodies it does not own,
+    (N-1) n in total, except the first one when the positions are host data
+    present on every node (R17 ALL); the readback of P and V pulls n - n/N
+    bodies of each to node 0."""
+    n, steps = 12 * N, 3
+    cl = run(P.nbody(n, steps, host_init=host_init), N, 1)
+    gathers = steps - (1 if host_init else 0)
+    assert pushed_elements(cl) == gathers * (N - 1) * n + 2 * (n - n // N)
