@@ -1022,10 +1022,7 @@ void Scheduler::transfers(Cmd& c, std::map<Key, Alloc*>& binding, bool readback_
                 ins.src_mem = 1;
                 ins.box = bx;
                 const Pilot pl{node_, ins.msg, target, tid, bid, bx};
-                if (pilot_sink_)
-                    pilot_sink_(pl);
-                else
-                    pilots_.push_back(pl);
+                if (pilot_sink_) pilot_sink_(pl);
                 const uint64_t iid = emit(ins, deps);
                 m1->readers.add(int64_t(iid), Region{bx});
             }

@@ -270,13 +270,9 @@ public:
         return true;
     }
     int node() const { return node_; }
-    // pilots go to `fn` as they are produced ("transmitted ... ahead of execution time")
+    // pilots go to `fn` as they are produced ("transmitted ... ahead of execution time");
+    // without a sink (execute=0) they are dropped: the send instruction in the log carries them
     void set_pilot_sink(std::function<void(const Pilot&)> fn) { pilot_sink_ = std::move(fn); }
-    std::vector<Pilot> take_pilots() {
-        std::vector<Pilot> p;
-        p.swap(pilots_);
-        return p;
-    }
     int64_t alloc_readback_id() { return next_rb_++; }
     void wait();
     int readback(uint32_t bid, const Box& box, int64_t* rb_out, std::string* err);
@@ -407,7 +403,6 @@ private:
     std::unordered_map<int64_t, int> alloc_owner_;    // live allocation iid -> device (old, still referenced)
     static int instr_owner(const Instr& ins);
     uint64_t next_msg_ = 0;                           // P:L400 "locally unique message id"
-    std::vector<Pilot> pilots_;
     std::function<void(const Pilot&)> pilot_sink_;
     uint64_t coll_min_bytes_ = 1ull << 20;            // CEL_COLL_MIN_BYTES: smallest per-source gather run as NCCL
     uint32_t next_bid_ = 0;
