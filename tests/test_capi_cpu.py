@@ -233,3 +233,19 @@ def test_axis_neighborhood_and_2d_wavesim_logs(cel):
     axes = both_logs(cel, P.wavesim(96, 4, rows=72, split="2d", mapper="neighborhood_axes"), 4, "auto")[1]
     ncopy = lambda log: sum(1 for r in log if r["kind"] == "copy" and r["reason"] == "coherence")  # noqa: E731
     assert ncopy(box) - ncopy(axes) == 4 * 4
+
+
+def degenerate_cases():
+    """Fewer rows / bodies / cells than devices (empty chunks, R4), 1x1 grids,
+    one-element buffers, 2-D split on a 2x4 grid."""
+    return [(P.wavesim(5, 3, rows=3), 4), (P.wavesim(1, 3, rows=1), 2), (P.nbody(1, 2), 2), (P.nbody(3, 2), 4),
+            (P.jacobi3d(2, 2), 3), (P.rsim(3, 4), 4), (P.c1_chain(2), 4),
+            (P.wavesim(4, 2, rows=2, split="2d", mapper="neighborhood_axes"), 4)]
+
+
+@pytest.mark.parametrize("mode", ["none", "auto"])
+def test_degenerate_shapes_logs_match_oracle(cel, mode):
+    for prog, G in degenerate_cases():
+        o, c = both_logs(cel, prog, G, mode)
+        assert_same(o, c)
+        check(c, o.buf_meta, o.tasks)          # and the brute-force checker
