@@ -361,3 +361,15 @@ def test_wavesim_2d_split_axis_neighborhood(cel, G):
     for mp in ("neighborhood", "neighborhood_axes"):
         run_both(cel, P.wavesim(515, 5, rows=130, split="2d", mapper=mp), G)
         run_both(cel, P.wavesim(516, 4, rows=260, split="2d", mapper=mp), G)
+
+
+@pytest.mark.parametrize("mode", ["none", "auto"])
+def test_degenerate_shapes(cel, mode):
+    """Empty device chunks (fewer rows / bodies than devices), 1x1 grids,
+    one-element buffers and a 2x4 grid under the 2-D split: bit-exact, and the
+    same instruction log as the oracle."""
+    cases = [(P.wavesim(5, 3, rows=3), 4), (P.wavesim(1, 3, rows=1), 2), (P.nbody(1, 2), 2), (P.nbody(3, 2), 4),
+             (P.jacobi3d(2, 2), 3), (P.rsim(3, 4), 4), (P.c1_chain(2), 4),
+             (P.wavesim(4, 2, rows=2, split="2d", mapper="neighborhood_axes"), 4)]
+    for prog, G in cases:
+        run_both(cel, prog, G, mode, arena=8 << 20)
