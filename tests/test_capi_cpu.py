@@ -249,3 +249,20 @@ def test_degenerate_shapes_logs_match_oracle(cel, mode):
         o, c = both_logs(cel, prog, G, mode)
         assert_same(o, c)
         check(c, o.buf_meta, o.tasks)          # and the brute-force checker
+
+
+def test_cluster_degenerate_shapes(cel):
+    """More nodes than rows / bodies (nodes with empty command chunks, R17
+    1-D node split), 1x1 grids and one-element buffers: every node's C++ log
+    equals the oracle's and the oracle's bytes equal the sequential definition."""
+    import numpy as np
+    from oracle.simulate import sequential, simulate_cluster
+    cases = [(P.wavesim(5, 3, rows=3), 4, 1), (P.wavesim(1, 3, rows=1), 2, 2), (P.nbody(1, 2), 2, 1),
+             (P.nbody(3, 2), 2, 2), (P.jacobi3d(2, 2), 3, 1), (P.rsim(3, 4), 4, 1), (P.c1_chain(2), 3, 2)]
+    for prog, N, D in cases:
+        for mode in ("none", "auto"):
+            o, c = cluster_logs(cel, prog, N, D, mode)
+            assert c == o.logs
+            res = simulate_cluster(o)
+            exp, mask = sequential(prog)
+            assert all(np.array_equal(res[k][mask[k]], exp[k][mask[k]]) for k in exp)
