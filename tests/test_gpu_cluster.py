@@ -97,3 +97,12 @@ def test_nodes_on_distinct_gpus(cel):
         devs = list(range(N * D))
         for prog in (P.nbody(2048, 2), P.wavesim(1024, 5, rows=300), P.random_program(6200 + N)):
             run_both(cel, prog, N, D, devices=devs)
+
+
+def test_degenerate_shapes(cel):
+    """Nodes with empty command chunks, 1x1 grids, one-element buffers."""
+    cases = [(P.wavesim(5, 3, rows=3), 4, 1), (P.wavesim(1, 3, rows=1), 2, 2), (P.nbody(1, 2), 2, 1),
+             (P.nbody(3, 2), 2, 2), (P.jacobi3d(2, 2), 3, 1), (P.rsim(3, 4), 4, 1), (P.c1_chain(2), 3, 2)]
+    for prog, N, D in cases:
+        for mode in ("none", "auto"):
+            run_both(cel, prog, N, D, mode)
