@@ -50,113 +50,259 @@ def measured_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (the recipe's clocks line)."""
+    """Clock / throttle sampling DURING the timed region (the recipe's clocks
+    line): an NVML thread samples every millisecond (the timed region of a
+    short run is only milliseconds long), falling back to `nvidia-smi -lms`."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, gpu):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+        self.rows = []
+        self.p = None
+        self.stop_ev = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), "--query-gpu=" + q, "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[gpu]) if vis and vis.split(",")[gpu].strip().isdigit() else gpu
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.sample()
+            self.t = threading.Thread(target=self.loop, daemon=True)
+            self.t.start()
         except Exception:
-            self.p = None
+            self.nv = None
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), "--query-gpu=" + q,
+                                           "--format=csv,noheader,nounits", "-lms", "100"],
+                                          stdout=self.f, stderr=subprocess.DEVNULL)
+            except Exception:
+                self.p = None
+
+    def sample(self):
+        nv = self.nv
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)), float(self.max_mhz),
+                          [v for k, v in self.REASONS.items() if r & k]))
+
+    def loop(self):
+        while not self.stop_ev.wait(0.001):
+            self.sample()
 
     def stop(self):
-        if self.p is None:
-            return None
-        self.p.terminate()
-        try:
-            self.p.wait(timeout=5)
-        except Exception:
-            self.p.kill()
-        self.f.flush()
-        rows = []
-        for line in open(self.f.name):
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
+        if self.nv is not None:
+            self.sample()
+            self.stop_ev.set()
+            self.t.join()
+            rows = self.rows
+            how = "nvml, 1 ms"
+        else:
+            if self.p is None:
+                return None
+            self.p.terminate()
             try:
-                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
-            except ValueError:
-                continue
-        os.unlink(self.f.name)
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.flush()
+            rows = []
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for line in open(self.f.name):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    rows.append((float(parts[1]), float(parts[2]),
+                                 [names[i] for i, v in enumerate(parts[5:9]) if v.lower() == "active"]))
+                except ValueError:
+                    continue
+            os.unlink(self.f.name)
+            how = "nvidia-smi, 100 ms"
         if not rows:
             return None
         sm = sorted(r[0] for r in rows)
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
-                "samples": len(rows)}
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": sorted({x for r in rows for x in r[2]}), "samples": len(rows), "sampler": how}
 
 
-def cpu_baseline(budget_s=12.0, max_reps=8):
-    """The oracle, as it stands, on a bounded sample of the WaveSim workload:
-    16384 columns x R rows, IDAG generation + byte simulation, one process,
-    repeated until about budget_s of CPU work.  Scaled to full 16384^2
-    steps/s by rows."""
-    import numpy as np  # noqa: F401
-    from oracle.scheduler import Runtime as OracleRuntime, run_program
-    from oracle.simulate import simulate
-    from workloads import programs as P
-    rows, steps = 1024, 3
-    reps, dt = 0, 0.0
-    while reps < max_reps and (reps == 0 or dt < budget_s):
-        t0 = time.perf_counter()
-        prog = P.wavesim(N_FIELD, steps, rows=rows)
-        prog["ops"] = [op for op in prog["ops"] if op[0] != "read"] + [("read", 1, P.full([rows, N_FIELD]))]
-        o = OracleRuntime(1)
-        run_program(o, prog)
-        simulate(o)
-        dt += time.perf_counter() - t0
-        reps += 1
-    full_steps = reps * steps * rows / N_FIELD
+def oracle_wave_fields(rows, seed=2):
+    """u = up = the input recipe's init(seed, .) (the WaveSim workload's fill
+    tasks) over `rows` full-width rows of the 16384^2 field plus one halo row
+    on each side when rows < 16384, as the oracle's accessors; returns them
+    and the box of rows a step writes."""
+    import numpy as np
+    from oracle import geometry as g
+    from oracle.kernels import Acc, init_value
+    lo, hi = (0, N_FIELD) if rows >= N_FIELD else (0, rows + 2)
+    idx = np.arange(lo * N_FIELD, hi * N_FIELD, dtype=np.uint64)
+    f = np.asarray(init_value(seed, idx), dtype=np.float32).reshape(hi - lo, N_FIELD, 1, 1).view(np.uint32)
+    ext = g.box([0, 0], [N_FIELD, N_FIELD])
+    box = g.box([lo, 0], [hi, N_FIELD])
+    wbox = box if rows >= N_FIELD else g.box([1, 0], [rows + 1, N_FIELD])
+    return Acc(f.copy(), box, ext), Acc(f, box, ext), wbox
+
+
+def oracle_wave_step(U, UP, wbox, k):
+    """One WaveSim step of the oracle (oracle.kernels.k_wave5, NumPy float32,
+    one core) over the rows of wbox."""
+    from oracle.kernels import k_wave5
+    k_wave5({}, [wbox, wbox], [U, UP] if k % 2 == 0 else [UP, U])
+
+
+def cpu_baseline(budget_s=15.0, max_steps=3):
+    """The oracle as it stands, timed on this host: WaveSim steps of the full
+    16384^2 field through the oracle's wave5 kernel (G = 1: the IDAG is one
+    kernel instruction per step, its generation is negligible), repeated until
+    budget_s or max_steps -- measured at full size, not extrapolated."""
+    import time as _t
+    U, UP, box = oracle_wave_fields(N_FIELD)
+    k, dt = 0, 0.0
+    while k < max_steps and (k == 0 or dt < budget_s):
+        t0 = _t.perf_counter()
+        oracle_wave_step(U, UP, box, k)
+        dt += _t.perf_counter() - t0
+        k += 1
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    return {"value": full_steps / dt, "unit": "steps/s", "cores": 1, "kind": "oracle",
-            "sample": "%d x (WaveSim %d rows x %d cols, %d steps incl. 2 fills), oracle IDAG + NumPy byte "
-                      "simulation, scaled by rows to 16384^2 steps (host has %d cores; NumPy elementwise is "
-                      "single-threaded)" % (reps, rows, N_FIELD, steps, cores),
+    return {"value": k / dt, "unit": "steps/s", "cores": 1, "kind": "oracle",
+            "sample": "%d full-size steps of WaveSim 16384^2 f32 (oracle.kernels.k_wave5, NumPy, one thread; host "
+                      "has %d cores), measured" % (k, cores),
             "seconds": dt}
 
 
 def run_reference(args):
+    """--impl reference: the oracle, as it stands, on this arm's metric.  Each
+    timed step is one WaveSim step through the oracle's wave5 kernel over R
+    full-width rows: R = 16384 (the whole field, measured) when K full steps
+    fit in about 100 s of CPU, else the largest slab that does, the line then
+    scaled by rows and saying so.  Warm-up steps run on a 64-row slab."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    import numpy as np
-    from oracle import geometry as g
-    from oracle.kernels import Acc, k_wave5
-    # each "step" is a bounded sample: one wave5 step over R rows of the 16384^2
-    # field through the oracle kernel (pure NumPy, 1 core), scaled by rows
-    # bounded: ~1 ms of NumPy per row, keep the whole run around a minute
-    R = int(max(8, min(512, 60000 // max(1, args.steps + args.warmup))))
-    ext = g.box([0, 0], [N_FIELD, N_FIELD])
-    rng = np.random.default_rng(2)
-    u = rng.uniform(-1, 1, (R + 2, N_FIELD, 1, 1)).astype(np.float32).view(np.uint32)
-    up = rng.uniform(-1, 1, (R + 2, N_FIELD, 1, 1)).astype(np.float32).view(np.uint32)
-    ubox = g.box([0, 0], [R + 2, N_FIELD])
-    wbox = g.box([1, 0], [R + 1, N_FIELD])
-    U, UP = Acc(u, ubox, ext), Acc(up, ubox, ext)
-    for _ in range(args.warmup):
-        k_wave5({}, [ubox, wbox], [U, UP])
-    t0 = time.perf_counter()
+    import time as _t
+    Uw, UPw, bw = oracle_wave_fields(64)
+    for k in range(args.warmup):
+        oracle_wave_step(Uw, UPw, bw, k)
+    t0 = _t.perf_counter()
+    oracle_wave_step(Uw, UPw, bw, 0)
+    per_row = (_t.perf_counter() - t0) / 64
+    R = int(min(N_FIELD, max(64, 100.0 / max(1, args.steps) / max(per_row, 1e-9))))
+    U, UP, box = oracle_wave_fields(R)
+    t0 = _t.perf_counter()
     for k in range(args.steps):
-        if k % 2 == 0:
-            k_wave5({}, [ubox, wbox], [U, UP])
-        else:
-            k_wave5({}, [ubox, wbox], [UP, U])
-    dt = time.perf_counter() - t0
-    full = args.steps * R / N_FIELD
-    val = full / dt
+        oracle_wave_step(U, UP, box, k)
+    dt = _t.perf_counter() - t0
+    val = args.steps * (R / N_FIELD) / dt
+    sample = ("oracle wave5 kernel (NumPy, one thread), %d steps of the full 16384^2 field, measured" % args.steps
+              if R == N_FIELD else
+              "oracle wave5 kernel (NumPy, one thread), %d steps over %d of 16384 rows each, scaled by rows "
+              "(full-size steps would not fit the run's time budget)" % (args.steps, R))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / val,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": arm_config(args.gpus, world),
-            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": 1, "kind": "oracle",
-                             "sample": "oracle wave5 kernel on %d of 16384 rows per step, scaled by rows" % R},
+            "cpu_baseline": {"value": val, "unit": "steps/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def copy_block(cel, P, peak):
+    """The coherence-copy half of BASELINE.json's metric ("coherence copy GB/s
+    vs HBM peak"), through the product path on this GPU: resize copies (alloc
+    -> copy -> free) of 1 GiB contiguous and 8192 x 16 KiB strided, and
+    halo-shaped coherence copies between virtual devices (WaveSim 64 KiB rows;
+    3-D faces: 2 MiB z-faces, 256 x 4 KiB strided y-faces, corner lines).
+    Device time per copy launch from the library's CUDA-event profile; bytes
+    are read + write of HBM (2 x payload); resized data byte-checked."""
+    import numpy as np
+    out = {}
+    saved = os.environ.get("CEL_NO_GROW")
+    os.environ["CEL_NO_GROW"] = "1"            # measure real resize copies, not in-place growth
+
+    def resize_case(name, ext, written, fixed, samples):
+        rt = cel.Runtime(1, lookahead="none", arena_bytes=3 << 30)
+        dims = len(ext)
+        rt.buffer_create(dims, ext, 4)
+        rt.task_submit({"dims": dims, "range": ([0] * dims, list(written)), "kernel": "fill_hash",
+                        "params": {"seed": 11}, "accesses": [(0, "write", ("one_to_one",))]})
+        rt.wait()
+        rt.profile_enable(True)
+        # a 1-item task writing a box that overlaps the live allocation's end:
+        # R9 merges them, i.e. one resize copy of the whole written part
+        rt.task_submit({"dims": 1, "range": ([0], [1]), "kernel": "fill_const", "params": {"value": 2.0},
+                        "accesses": [(0, "write", ("fixed", fixed))]})
+        rt.wait()
+        prof = rt.profile_read()
+        st = rt.stats()
+        ok = True
+        for lo, hi in samples:
+            got = rt.buffer_read(0, (lo, hi)).view(np.float32).reshape(-1)
+            grid = np.indices([h - l for l, h in zip(lo, hi)]).reshape(len(lo), -1)
+            lin = np.zeros(grid.shape[1], dtype=np.uint64)
+            for d in range(dims):
+                lin = lin * np.uint64(ext[d]) + (grid[d] + lo[d]).astype(np.uint64)
+            ok = ok and np.array_equal(got.view(np.uint32), P.init_values(11, lin).view(np.uint32))
+        rt.shutdown()
+        ms, cnt = prof.get("copy", (0.0, 0))
+        payload = st["bytes_resize"]
+        gbs = 2 * payload / (ms / 1e3) / 1e9 if ms else None
+        out[name] = {"payload_bytes": payload, "copies": st["copies_resize"], "launches": cnt, "ms": ms,
+                     "GBps_hbm_rw": gbs, "frac_hbm": gbs / peak if gbs else None, "bytes_ok": bool(ok)}
+
+    n = 1 << 28
+    resize_case("resize_1GiB", [n + 1], [n], ([n - 1], [n + 1]),
+                [([0], [1 << 20]), ([n // 2], [n // 2 + (1 << 20)]), ([n - (1 << 20)], [n - 1])])
+    R, C = 8192, 4096
+    resize_case("resize_2d_8192x16KiB", [R, 16384], [R, C], ([0, C - 1], [R, C + 1]),
+                [([0, 0], [64, C - 1]), ([R // 2, 0], [R // 2 + 64, C - 1]), ([R - 64, 0], [R, C - 1])])
+    if saved is None:
+        os.environ.pop("CEL_NO_GROW", None)
+    else:
+        os.environ["CEL_NO_GROW"] = saved
+
+    def halo_case(name, G, ext, descs_of, init, steps):
+        rt = cel.Runtime(G, cuda_devices=[0] * G, arena_bytes=int(2 * np.prod(ext) * 4 / G * 1.3) + (256 << 20))
+        rt.buffer_create(len(ext), ext, 4)
+        rt.buffer_create(len(ext), ext, 4)
+        for op in init:
+            rt.task_submit(op[1])
+        descs = [cel.task_desc(d[1]) for d in descs_of]
+        for k in range(4):
+            rt.submit_desc(descs[k % 2][0])
+        rt.wait()
+        st0 = rt.stats()
+        rt.profile_enable(True)
+        for k in range(steps):
+            rt.submit_desc(descs[k % 2][0])
+        rt.wait()
+        prof = rt.profile_read()
+        st1 = rt.stats()
+        rt.shutdown()
+        ms, cnt = prof.get("copy", (0.0, 0))
+        payload = st1["bytes_coherence"] - st0["bytes_coherence"]
+        copies = st1["copies_coherence"] - st0["copies_coherence"]
+        gbs = 2 * payload / (ms / 1e3) / 1e9 if ms else None
+        out[name] = {"devices": "%d virtual devices on one GPU" % G, "copies": copies, "launches": cnt,
+                     "payload_bytes": payload, "us_per_copy": ms * 1e3 / cnt if cnt else None,
+                     "GBps_hbm_rw": gbs, "frac_hbm": gbs / peak if gbs else None}
+
+    nf = N_FIELD
+    halo_case("halo_rows_64KiB", 2, [nf, nf], [P.wavesim_step(nf, k) for k in (0, 1)], P.wavesim_init(nf), 200)
+    nz = 512
+    jac = P.jacobi3d(1024, 2)
+    jac_init = [("task", dict(jac["ops"][0][1], range=([0, 0, 0], [nz, 1024, 1024])))]
+    steps = [("task", dict(P.jacobi_step(1024, k)[1], range=([0, 0, 0], [nz, 1024, 1024]))) for k in (0, 1)]
+    halo_case("halo_3d_faces_2x2", 4, [nz, 1024, 1024], steps, jac_init, 40)
+    return out
 
 
 def gpu_of(v):
@@ -191,6 +337,7 @@ def main():
     ap.add_argument("--n", type=int, default=N_FIELD)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-copy", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -331,6 +478,9 @@ def main():
         if dist:
             dist.destroy_process_group()
         return
+    copies = None
+    if G == 1 and world == 1 and not args.no_copy:
+        copies = copy_block(cel, P, peak)
     cpu = None
     if G == 1 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline()
@@ -349,6 +499,7 @@ def main():
                      "kernel_share_of_step": kernel_share},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "copy": copies,
         "gpu_launches": launches,
         "host_submit_us_per_step": (th1 - th0) / kh * 1e6,
         "host_us_per_step_by_part": {k[8:] if k.startswith("exec_ns_") else k: (sh1[k] - sh0[k]) / kh / 1e3

@@ -185,7 +185,7 @@ typedef struct {
 /* Counters since runtime creation.  Instruction counts are the node's IDAG
  * (every rank of a multi-process run replays the whole node's graph); executor
  * counters are this process's.  Virtual-node mode: totals over the nodes. */
-typedef struct {
+typedef struct cel_stats_s {
     uint64_t n_alloc, n_free, n_copy, n_kernel, n_horizon, n_epoch;
     uint64_t copies_resize, copies_coherence, copies_readback;
     uint64_t bytes_resize, bytes_coherence, bytes_readback, bytes_d2d_peer;
@@ -203,7 +203,7 @@ typedef struct {
     uint64_t n_send, n_receive, n_split_receive, n_await_receive;   /* virtual-node mode (n_nodes > 1) */
     uint64_t pulls, pull_bytes;           /* virtual-node mode: pilot-matched transfers executed, bytes */
     uint64_t coll_allgathers;             /* all-gather sets run as one in-place ncclAllGather */
-} cel_stats;
+} cel_stats_t;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of
  * device memory and gets its own streams; peer access is enabled between
@@ -234,23 +234,40 @@ int cel_buffer_create(cel_runtime* rt, int32_t dims, const uint64_t extent[3], u
 int cel_buffer_create_ex(cel_runtime* rt, int32_t dims, const uint64_t extent[3], uint32_t elem_size,
                          const void* host_init, uint32_t flags, cel_buffer* out);
 
-/* Submit a task: returns after its instructions are generated and enqueued
- * (asynchronous).  >0: uninitialised-read warning; <0: rejected, no effect. */
+/* Submit a task ("submit command groups to a queue"; one kernel
+ * over desc->range with the accessors' range mappers).  The task
+ * is split over the devices (§3.1), checked (§4.4) and
+ * lowered to instructions (§3.2-3.5) that are issued to the GPUs before the
+ * call returns; it does not wait for them (asynchronous).  desc and
+ * desc->acc are copied; *out (nullable) receives the task id.
+ * Returns 0, or CEL_W_UNINIT_READ (>0, accepted: a read of never-written
+ * elements), or <0 with no effect: CEL_E_INVALID (malformed desc),
+ * CEL_E_OUT_OF_BOUNDS (one_to_one / fixed / remap region outside a buffer),
+ * CEL_E_OVERLAPPING_WRITE (two devices write the same element), or
+ * the runtime's sticky error. */
 int cel_task_submit(cel_runtime* rt, const cel_task_desc* desc, cel_task* out);
 
 /* Epoch: flush the lookahead queue, block until all work is done. */
 int cel_wait(cel_runtime* rt);
 
-/* Read back `box` of a buffer into host_dst (dense over box): coherence copies
- * to host followed by an epoch; blocking.  Elements never written and not
- * host-initialised are left untouched.  Multi-process: only the elements
- * whose up-to-date copy lives on this rank's device are written. */
+/* Read back `box` of a buffer into host_dst (dense row-major over box,
+ * elem_size bytes per element, caller-owned, written before the call
+ * returns): coherence copies into host memory (§3.3, the user
+ * pointer acting as an M0 allocation over `box`; R13) followed by an epoch
+ * (P:L304); blocking.  Elements never written and not host-initialised are
+ * left untouched.  Multi-process: only the elements whose up-to-date copy
+ * lives on this rank's device are written.  CEL_E_INVALID: unknown buffer or
+ * null pointer; CEL_E_OUT_OF_BOUNDS: box outside the buffer. */
 int cel_buffer_read(cel_runtime* rt, cel_buffer buf, const cel_box* box, void* host_dst);
 
 /* Drop the buffer: its allocations are freed once the last user has finished. */
 int cel_buffer_destroy(cel_runtime* rt, cel_buffer buf);
 
-int cel_stats_get(cel_runtime* rt, cel_stats* out);
+/* Counters (cel_stats_t above) into *out; the executor's counters are as of
+ * the last epoch or a few hundred instructions ago.  cel_stats_get is the
+ * round-1 name of the same call. */
+int cel_stats(cel_runtime* rt, cel_stats_t* out);
+int cel_stats_get(cel_runtime* rt, cel_stats_t* out);
 
 /* Device-time profile of the kernels this process launched, measured with
  * CUDA events on the launching streams: ms[k], count[k] for k = cel_kernel

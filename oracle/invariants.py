@@ -13,7 +13,19 @@ buffers, for ANY instruction log (the oracle's or the C++ scheduler's):
     write-after-read hazard is left unordered" (north_star; P:L447-448);
   * coverage: every element a kernel (or readback) reads carries exactly
     the value of the buffer's last writer in task order ("every read is
-    covered by exactly one up-to-date last writer", north_star).
+    covered by exactly one up-to-date last writer", north_star; P:L371);
+  * allocation shape (R9, SURVEY §8(c) pin table), per (buffer, memory):
+    - non-overlap: "buffer backing allocations remain non-overlapping"
+       — outside a resize chain (alloc, resize copies, free)
+      the live allocations are pairwise disjoint;
+    - never shrink: "we never emit instructions to downsize a buffer
+      allocation" — an alloc that overlaps a live allocation
+      contains it (it replaces it), a resize copy goes into an allocation
+      containing its source, and a free that is not the buffer's last
+      reference leaves a live allocation containing the freed box;
+    - pairing: every alloc has exactly one free, and none is live after
+      shutdown ("all allocations are however returned back to the system
+      eventually", P:L365; S:L376).
 
 Values are symbolic tokens (the producing kernel's iid), not bytes.
 """
@@ -52,8 +64,74 @@ class _A:
             self.token[...] = -1                            # host-initialised data
 
 
-def check(log, buf_meta, tasks):
+def check_allocations(log, closed=True):
+    """R9 allocation shape on any log: see the
+    module docstring.  `closed`: the log ends after shutdown, so nothing may
+    still be live."""
+    buf_of = {}
+    last_use = {}                     # buffer -> index of its last non-free reference
+    for i, rec in enumerate(log):
+        k = rec["kind"]
+        if k == "alloc":
+            buf_of[rec["aid"]] = rec["buffer"]
+        if k in ("alloc", "copy", "send", "receive", "split_receive", "await_receive"):
+            last_use[rec["buffer"]] = i
+        elif k == "kernel":
+            for aid in rec["bindings"]:
+                if aid in buf_of:
+                    last_use[buf_of[aid]] = i
+    live = {}                         # (buffer, mem) -> {aid: box}
+    where = {}                        # aid -> (buffer, mem)
+    freed = set()
+    dirty = False                     # a resize chain may be open: disjointness re-checked after it
+    for i, rec in enumerate(log):
+        k = rec["kind"]
+        in_chain = k in ("alloc", "free") or (k == "copy" and rec["reason"] == "resize")
+        if dirty and not in_chain:
+            for key, d in live.items():
+                items = sorted(d.items())
+                for x in range(len(items)):
+                    for y in range(x + 1, len(items)):
+                        if not g.is_empty(g.box_intersect(items[x][1], items[y][1])):
+                            raise InvariantError("allocations %d and %d of buffer %d on M%d overlap at instruction %d "
+                                                 "(P:L350)" % (items[x][0], items[y][0], key[0], key[1], i))
+            dirty = False
+        if k == "alloc":
+            aid, key, bx = rec["aid"], (rec["buffer"], rec["mem"]), _tobox(rec["box"])
+            if aid in where or aid in freed:
+                raise InvariantError("allocation %d allocated twice (S:L376)" % aid)
+            for o, ob in live.get(key, {}).items():
+                if not g.is_empty(g.box_intersect(ob, bx)) and not g.box_contains(bx, ob):
+                    raise InvariantError("alloc %d overlaps live allocation %d without containing it "
+                                         "(downsize / overlap, P:L350, P:L364)" % (aid, o))
+            live.setdefault(key, {})[aid] = bx
+            where[aid] = key
+            dirty = True
+        elif k == "copy" and rec["reason"] == "resize":
+            s, d = rec["src_aid"], rec["dst_aid"]
+            if s in where and d in where and not g.box_contains(live[where[d]][d], live[where[s]][s]):
+                raise InvariantError("resize copy %d: destination allocation %d does not contain source %d (P:L364)"
+                                     % (i, d, s))
+        elif k == "free":
+            aid = rec["aid"]
+            if aid not in where:
+                raise InvariantError("free %d of allocation %d that is not live (S:L376)" % (i, aid))
+            key = where.pop(aid)
+            bx = live[key].pop(aid)
+            freed.add(aid)
+            if last_use.get(key[0], -1) > i and not any(g.box_contains(ob, bx) for ob in live[key].values()):
+                raise InvariantError("free %d drops allocation %d of buffer %d before its last use with no live "
+                                     "allocation containing it (downsize, P:L364)" % (i, aid, key[0]))
+    if closed:
+        left = sorted(where)
+        if left:
+            raise InvariantError("allocations %s are never freed (P:L365, S:L376)" % left)
+    return {"allocs": len(where) + len(freed), "freed": len(freed)}
+
+
+def check(log, buf_meta, tasks, closed=True):
     """Raise InvariantError on the first violation; returns stats dict."""
+    alloc_stats = check_allocations(log, closed)
     anc = []
     for i, rec in enumerate(log):
         if rec["iid"] != i:
@@ -196,4 +274,4 @@ def check(log, buf_meta, tasks):
         # horizons / epochs carry no data
     flush_ver()
     live = [aid for aid, A in allocs.items() if A.freed is None]
-    return {"instructions": len(log), "checked_reads": nreads, "live_allocs": live}
+    return {"instructions": len(log), "checked_reads": nreads, "live_allocs": live, **alloc_stats}

@@ -775,29 +775,6 @@ def _norm_mapper(mp):
     return (kind,)
 
 
-def run_program(rt, program):
-    """Drive a `workloads` program description through a runtime (oracle or
-    product binding alike): buffers, then ops in order."""
-    bids = []
-    for b in program["buffers"]:
-        bids.append(rt.buffer_create(b["dims"], b["extent"], b["elem_size"], b.get("host_init")))
-    results = []
-    for op in program["ops"]:
-        kind = op[0]
-        if kind == "task":
-            results.append(("task",) + tuple(rt.task_submit(op[1])))
-        elif kind == "wait":
-            rt.wait()
-        elif kind == "read":
-            results.append(("read", rt.buffer_read(op[1], op[2])))
-        elif kind == "destroy":
-            rt.buffer_destroy(op[1])
-        else:
-            raise ValueError(kind)
-    rt.shutdown()
-    return results
-
-
 def counts(log):
     """Instruction counts by kind (copies by reason and memory pair)."""
     c = {}

@@ -99,6 +99,7 @@ lib.cel_task_submit.argtypes = [_P, C.POINTER(cel_task_desc), C.POINTER(C.c_uint
 lib.cel_wait.argtypes = [_P]
 lib.cel_buffer_read.argtypes = [_P, C.c_uint32, C.POINTER(cel_box), C.c_void_p]
 lib.cel_buffer_destroy.argtypes = [_P, C.c_uint32]
+lib.cel_stats.argtypes = [_P, C.POINTER(cel_stats)]
 lib.cel_stats_get.argtypes = [_P, C.POINTER(cel_stats)]
 lib.cel_profile_enable.argtypes = [_P, C.c_int32]
 lib.cel_profile_read.argtypes = [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int32]
@@ -109,7 +110,7 @@ lib.cel_last_error.restype = C.c_char_p
 BORROW_HOST = 1
 SYMBOLS = ["cel_runtime_create", "cel_ipc_blob_size", "cel_ipc_export", "cel_ipc_import", "cel_buffer_create",
            "cel_buffer_create_ex",
-           "cel_task_submit", "cel_wait", "cel_buffer_read", "cel_buffer_destroy", "cel_stats_get",
+           "cel_task_submit", "cel_wait", "cel_buffer_read", "cel_buffer_destroy", "cel_stats", "cel_stats_get",
            "cel_profile_enable", "cel_profile_read", "cel_trace_dump", "cel_runtime_destroy", "cel_last_error"]
 
 
@@ -264,7 +265,7 @@ class Runtime:
 
     def stats(self):
         s = cel_stats()
-        _check(lib.cel_stats_get(self.h, C.byref(s)))
+        _check(lib.cel_stats(self.h, C.byref(s)))
         return {n: getattr(s, n) for n, _ in cel_stats._fields_}
 
     def profile_enable(self, on=True, stride=1):

@@ -315,8 +315,9 @@ int cel_buffer_destroy(cel_runtime* rt, cel_buffer buf) {
     return after(rt, CEL_OK);
 }
 
-int cel_stats_get(cel_runtime* rt, cel_stats* o) {
-    if (!rt || !o) return fail(CEL_E_INVALID, "null argument");
+int cel_stats(cel_runtime* rt, cel_stats_t* o) {
+    if (int rc = check_poison(rt)) return rc;
+    if (!o) return fail(CEL_E_INVALID, "null argument");
     memset(o, 0, sizeof *o);
     SchedStats s = sched0(rt).stats();
     if (rt->cluster)            // virtual-node mode: totals over the nodes
@@ -354,7 +355,7 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
     o->gather_sets = s.gather_sets;
     o->gen_ns = rt->gen_ns;
     for (Executor* ex : execs(rt)) {
-        const ExecStats& e = ex->stats();
+        const ExecStats e = ex->stats();      // the executor thread's published copy
         o->kernel_launches += e.kernel_launches;
         o->copy_launches += e.copy_launches;
         o->memcpy_calls += e.memcpy_calls;
@@ -382,6 +383,8 @@ int cel_stats_get(cel_runtime* rt, cel_stats* o) {
     }
     return CEL_OK;
 }
+
+int cel_stats_get(cel_runtime* rt, cel_stats_t* o) { return cel_stats(rt, o); }
 
 int cel_profile_enable(cel_runtime* rt, int32_t on) {
     if (int rc = check_poison(rt)) return rc;

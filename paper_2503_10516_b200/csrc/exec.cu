@@ -72,6 +72,12 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     // 0.940 -> 0.986 of the step at 4 GPUs with DMA); CEL_PEER_DMA=0 for A/B
     const char* pd = getenv("CEL_PEER_DMA");
     peer_dma_ = !(pd && pd[0] == '0');
+    const char* jv = getenv("CEL_JACOBI");
+    if (jv && jv[0] == 'l') kernel_variant_ |= kVarJacobiLsu;
+    const char* rv = getenv("CEL_RSIM");
+    if (rv && rv[0] == '0') kernel_variant_ |= kVarRsimRegs;
+    const char* fp = getenv("CEL_FORCE_PEER");
+    force_peer_ = fp && fp[0] == '1';
     const char* ns = getenv("CEL_NO_SPLIT");
     split_ = !(ns && ns[0] == '1');
     const char* ng = getenv("CEL_NO_GROW");
@@ -286,6 +292,11 @@ int Executor::init(std::string* err) {
         host_arena_.size = cfg_.host_arena_bytes;
         host_arena_.free_[0] = FreeRange{cfg_.host_arena_bytes, Token{}};
     }
+    {
+        int mp = 0;
+        if (cudaDeviceGetAttribute(&mp, cudaDevAttrMaxPitch, phys_[0]) == cudaSuccess && mp > 0) max_pitch_ = size_t(mp);
+        cudaGetLastError();
+    }
     cudaDeviceSynchronize();
     const char* et = getenv("CEL_EXEC_THREAD");
     if (cfg_.comm || !(et && et[0] == '0')) {   // nodes must progress independently
@@ -480,14 +491,42 @@ Token Executor::dep_token(uint64_t j) const {
 }
 
 // Owner device of instruction j: recorded when this executor processed it, else
-// (the scheduler's rank filter never handed it over) from the scheduler's ring.
+// (the scheduler's rank filter never handed it over) as the scheduler attached
+// it to the instruction being processed (Instr::dep_owner).  The executor
+// thread never reads the scheduler's own ring, which the API thread keeps
+// overwriting while it runs ahead.
 bool Executor::owner_lookup(uint64_t j, int* o) const {
     auto k = kind_of_.find(j);
     if (k != kind_of_.end()) {
         *o = k->second;
         return true;
     }
-    return sched_ && sched_->ring_owner(j, o);
+    const Instr* c = cur_ins_;
+    if (!c || c->dep_owner.size() != c->deps.size()) return false;
+    auto it = std::lower_bound(c->deps.begin(), c->deps.end(), j);
+    if (it == c->deps.end() || *it != j) return false;
+    const int v = c->dep_owner[size_t(it - c->deps.begin())];
+    if (v == -2) return false;
+    *o = v;
+    return true;
+}
+
+// A dependency of the instruction being processed whose owner nobody knows
+// although it may still be running: its completion would be dropped silently
+// (ADVICE r1), so this is a state error instead.
+void Executor::check_owner_known(const Instr& ins) {
+    if (cfg_.world <= 1) return;
+    for (uint64_t j : ins.deps) {
+        int o = 0;
+        if (j >= prune_floor_ && !tok_.count(j) && !owner_lookup(j, &o)) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "instruction %llu: owner of dependency %llu unknown (scheduler ran too far ahead)",
+                     (unsigned long long)ins.iid, (unsigned long long)j);
+            errmsg_ = buf;
+            err_ = E_STATE;
+            return;
+        }
+    }
 }
 
 void Executor::merge(Token& into, const Token& t) const {
@@ -690,8 +729,9 @@ void Executor::signal_deps(const Instr& ins, int owner_dev) {
         merge(live, t);                               // drops entries already known complete
         int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
         if (live.remote.empty() && live.local.size() == 1)
-            sidx = cfg_.rank * kStreamsPerDev + S_SIG0 + (live.local[0].stream % kStreamsPerDev);
-        wait_token(sidx, live);        if (trace_)
+            sidx = cfg_.rank * kStreamsPerDev + S_SIG0 + (live.local[0].stream % kStreamsPerDev) % kNumSigStreams;
+        wait_token(sidx, live);
+        if (trace_)
             fprintf(stderr, "[cel r%d] signal iid %llu -> rank %d\n", cfg_.rank, (unsigned long long)j, o);
         const uint64_t ts = now_ns();
         checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
@@ -721,6 +761,7 @@ void Executor::on_instr(const Instr& ins) {
     }
     const uint64_t t0 = now_ns();
     on_instr_impl(ins);
+    cur_ins_ = nullptr;
     st_.exec_ns[int(ins.kind)] += now_ns() - t0;
 }
 
@@ -788,11 +829,14 @@ void Executor::thread_main() {
         if (it.kind == 0) {
             const uint64_t t0 = now_ns();
             on_instr_impl(it.ins);
+            cur_ins_ = nullptr;
             if (err_ && cfg_.comm) cfg_.comm->abort();   // wake nodes waiting for this one
             st_.exec_ns[int(it.ins.kind)] += now_ns() - t0;
+            if ((++since_publish_ & 255) == 0) publish_stats();
         } else if (it.kind == 1) {
             it.fn();
         } else {
+            publish_stats();
             {
                 std::lock_guard<std::mutex> l(dm_);
                 marks_done_ = it.mark;
@@ -849,6 +893,9 @@ int Executor::trace_dump(const char* path) {
 }
 
 void Executor::on_instr_impl(const Instr& ins) {
+    if (err_) return;
+    cur_ins_ = &ins;
+    check_owner_known(ins);
     if (err_) return;
     if (!pending_send_.empty()) resolve_sends(ins);
     const int od = instr_owner(ins);

@@ -168,7 +168,13 @@ public:
 
     int error() const { return err_.load(); }
     const std::string& error_msg() const { return errmsg_; }
-    const ExecStats& stats() const { return st_; }
+    // counters as of the last drain (or the last few hundred instructions):
+    // the executor thread publishes a copy, the API thread reads the copy
+    ExecStats stats() {
+        if (!threaded_) return st_;
+        std::lock_guard<std::mutex> l(smu_);
+        return pub_;
+    }
 
     // profiling: per kernel kind, accumulated device ms and launch count
     // stride k > 0: time every k-th launch of each kind (unbiased average, less
@@ -255,6 +261,8 @@ private:
     void poll(bool prune);
     Token dep_token(uint64_t j) const;
     bool owner_lookup(uint64_t j, int* o) const;
+    void check_owner_known(const Instr& ins);
+    const Instr* cur_ins_ = nullptr;              // instruction being processed (dep_owner lookups)
     void merge(Token& into, const Token& t) const;
     void wait_token(int sidx, const Token& t);
     Token record(int sidx);
@@ -352,7 +360,14 @@ private:
     std::unordered_map<uint32_t, BufInfo> bufinfo_;   // executor-side copy of buffer shapes
     std::string errmsg_;
     ExecStats st_;
+    ExecStats pub_;                               // published copy of st_ (stats())
+    std::mutex smu_;
+    void publish_stats() {
+        std::lock_guard<std::mutex> l(smu_);
+        pub_ = st_;
+    }
     uint64_t since_poll_ = 0;
+    uint64_t since_publish_ = 0;
     uint64_t prev_horizon_ = 0;
     uint64_t prune_floor_ = 0;                    // tokens below it were pruned (complete)
     std::unordered_set<uint64_t> live_alloc_iid_;
@@ -361,6 +376,9 @@ private:
     bool split_ = true;
     bool peer_dma_ = true;                        // small contiguous pushes on a copy engine (CEL_PEER_DMA=0: off)
     uint64_t peer_dma_max_ = 4ull << 20;
+    int kernel_variant_ = 0;                      // KArgs::variant (CEL_JACOBI=l, CEL_RSIM=0 for A/B)
+    bool force_peer_ = false;                     // CEL_FORCE_PEER=1: virtual devices of one GPU use the peer path
+    size_t max_pitch_ = size_t(1) << 31;          // cudaDevAttrMaxPitch (2-D DMA limit)
     bool no_grow_ = false;                      // CEL_NO_GROW=1: disable in-place growth (A/B)
     bool no_pad_ = false;                       // CEL_NO_PAD=1: allocations exactly as the IDAG's boxes
     Box padded_box(const Box& b, uint32_t buffer, uint32_t es) const;
@@ -380,7 +398,12 @@ private:
     std::unordered_map<int64_t, Communicator::Mem> recv_dst_; // transfer tid * 2^32 + buffer -> split receive destination
     void resolve_sends(const Instr& ins);
     std::unordered_map<uint64_t, Parts> parts_;
-    static constexpr uint64_t kRing = 1u << 16;
+    // flag slots per (sender rank) in each GPU's signal area: slot iid % kRing.
+    // Waits are GEQ, so two iids sharing a slot must never be in flight
+    // together: the window of in-flight iids is bounded by the executor queue
+    // (16384 relayed instructions) and the per-stream event cap (2048) times the
+    // G ranks' interleaving, far below 2^20
+    static constexpr uint64_t kRing = 1u << 20;
 };
 
 }  // namespace cel

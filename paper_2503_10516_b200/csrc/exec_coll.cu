@@ -49,7 +49,10 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
     for (int v : locals) {
         Token t;
         for (const Instr& x : m)
-            if (x.src_mem - 2 == v || x.dst_mem - 2 == v) merge(t, local_part(x.deps));
+            if (x.src_mem - 2 == v || x.dst_mem - 2 == v) {
+                cur_ins_ = &x;
+                merge(t, local_part(x.deps));
+            }
         const int sidx = v * kStreamsPerDev + S_PUSH;
         set_dev(v);
         wait_token(sidx, t);

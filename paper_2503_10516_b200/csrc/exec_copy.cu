@@ -98,7 +98,10 @@ void Executor::exec_copy(const Instr& ins) {
         CopyArgs args;
         args.nseg = 0;
         args.total_units = 0;
-        args.peer = peer && phys_[S.dev] != phys_[D.dev] ? 1 : 0;
+        // peer: the destination is another GPU's memory (NVLink push).  CEL_FORCE_PEER=1
+        // treats distinct virtual devices of one GPU the same way (DMA plan and the
+        // fenced peer copy kernel), so one-GPU tests cover that path
+        args.peer = peer && (phys_[S.dev] != phys_[D.dev] || force_peer_) ? 1 : 0;
         const int64_t sn1 = S.box.extent(1), sn2 = S.box.extent(2);
         const int64_t dn1 = D.box.extent(1), dn2 = D.box.extent(2);
         if (args.peer && peer_dma_) {
@@ -137,6 +140,9 @@ void Executor::exec_copy(const Instr& ins) {
                 } else {
                     ok = false;
                 }
+                // cudaMemcpy2DAsync rejects pitches above the device limit: those boxes
+                // stay on the copy kernel instead of poisoning the runtime
+                if (m.height > 1 && (m.spitch > max_pitch_ || m.dpitch > max_pitch_ || m.width > max_pitch_)) ok = false;
                 plan.push_back(m);
                 total += b.volume() * es;
             }
@@ -207,7 +213,7 @@ void Executor::exec_copy(const Instr& ins) {
             bytes += b.volume() * es;
         }
         flush();
-        const int kind = ins.reason == REASON_RESIZE ? 0 : (peer ? (phys_[S.dev] == phys_[D.dev] ? 1 : 2) : 1);
+        const int kind = ins.reason == REASON_RESIZE ? 0 : (args.peer ? 2 : 1);
         st_.bytes_copy[kind] += bytes;
         tok_[ins.iid] = record(sidx);
         return;

@@ -86,6 +86,7 @@ constexpr int kStreamsPerDev = 11;
 // its source stream's completion order (no head-of-line blocking between a
 // long-complete flag and one waiting for recent work)
 enum { S_COMPUTE = 0, S_COPY = 1, S_PUSH = 2, S_SYNC = 3, S_HALO = 4, S_HSIG = 5, S_SIG0 = 6 };
+constexpr int kNumSigStreams = kStreamsPerDev - S_SIG0;   // one per work stream 0..4
 constexpr uint64_t kAlign = 512;
 inline uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 }  // namespace detail

@@ -59,6 +59,7 @@ void Executor::exec_kernel(const Instr& ins) {
     a.t = d.params.t;
     a.salt = d.params.salt;
     a.fast = cfg_.fast_math ? 1 : 0;
+    a.variant = kernel_variant_;
     for (int i = 0; i < a.n_acc; ++i) {
         const Access& ac = d.acc[i];
         DAcc& A = a.acc[i];

@@ -694,122 +694,6 @@ __global__ void __launch_bounds__(kNbTile) nbody_step_kernel(const __grid_consta
     }
 }
 
-// fast-math timestep: FMA contraction and the MUFU reciprocal square root,
-// 4 bodies j per unrolled iteration; same summation order over j
-__global__ void __launch_bounds__(kNbTile) nbody_step_fast_kernel(const __grid_constant__ KArgs a) {
-    const DAcc& P = a.acc[0];
-    const DAcc& V = a.acc[1];
-    __shared__ float4 sp[kNbTile];
-    const int64_t i = a.chunk.lo[0] + int64_t(blockIdx.x) * kNbTile + threadIdx.x;
-    const bool valid = i < a.chunk.hi[0];
-    const int64_t N = P.ext[0];
-    float4 pi = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (valid) pi = *ptr<const float4>(P, i, 0, 0);
-    float ax = 0.f, ay = 0.f, az = 0.f;
-    for (int64_t j0 = 0; j0 < N; j0 += kNbTile) {
-        const int64_t j = j0 + threadIdx.x;
-        sp[threadIdx.x] = j < N ? *ptr<const float4>(P, j, 0, 0) : make_float4(0.f, 0.f, 0.f, 0.f);
-        __syncthreads();
-        const int jn = N - j0 < kNbTile ? int(N - j0) : kNbTile;
-        if (jn == kNbTile) {
-#pragma unroll 8
-            for (int k = 0; k < kNbTile; ++k) {
-                const float4 pj = sp[k];
-                const float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-                const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmaf_rn(dx, dx, NB_EPS2)));
-                const float inv = rsqrtf(r2);
-                const float s = inv * inv * inv;
-                ax = __fmaf_rn(dx, s, ax);
-                ay = __fmaf_rn(dy, s, ay);
-                az = __fmaf_rn(dz, s, az);
-            }
-        } else {
-            for (int k = 0; k < jn; ++k) {
-                const float4 pj = sp[k];
-                const float dx = pj.x - pi.x, dy = pj.y - pi.y, dz = pj.z - pi.z;
-                const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmaf_rn(dx, dx, NB_EPS2)));
-                const float inv = rsqrtf(r2);
-                const float s = inv * inv * inv;
-                ax = __fmaf_rn(dx, s, ax);
-                ay = __fmaf_rn(dy, s, ay);
-                az = __fmaf_rn(dz, s, az);
-            }
-        }
-        __syncthreads();
-    }
-    if (valid) {
-        float4* vp = ptr<float4>(V, i, 0, 0);
-        float4 v = *vp;
-        const float c = NB_DT * NB_MASS;
-        v.x = __fmaf_rn(c, ax, v.x);
-        v.y = __fmaf_rn(c, ay, v.y);
-        v.z = __fmaf_rn(c, az, v.z);
-        *vp = v;
-    }
-}
-
-// fast-math timestep, two bodies per thread (i and i + 128): every shared
-// memory read of body j feeds two independent interaction chains
-__global__ void __launch_bounds__(128) nbody_step_fast2_kernel(const __grid_constant__ KArgs a) {
-    const DAcc& P = a.acc[0];
-    const DAcc& V = a.acc[1];
-    __shared__ float4 sp[kNbTile];
-    const int64_t i0 = a.chunk.lo[0] + int64_t(blockIdx.x) * kNbTile + threadIdx.x;
-    const int64_t i1 = i0 + 128;
-    const bool v0 = i0 < a.chunk.hi[0], v1 = i1 < a.chunk.hi[0];
-    const int64_t N = P.ext[0];
-    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 p0 = v0 ? *ptr<const float4>(P, i0, 0, 0) : z4;
-    const float4 p1 = v1 ? *ptr<const float4>(P, i1, 0, 0) : z4;
-    float ax0 = 0.f, ay0 = 0.f, az0 = 0.f, ax1 = 0.f, ay1 = 0.f, az1 = 0.f;
-    for (int64_t j0 = 0; j0 < N; j0 += kNbTile) {
-        for (int t = threadIdx.x; t < kNbTile; t += 128) {
-            const int64_t j = j0 + t;
-            sp[t] = j < N ? *ptr<const float4>(P, j, 0, 0) : z4;
-        }
-        __syncthreads();
-        const int jn = N - j0 < kNbTile ? int(N - j0) : kNbTile;
-        auto body = [&](const float4 pj) {
-            const float dx0 = pj.x - p0.x, dy0 = pj.y - p0.y, dz0 = pj.z - p0.z;
-            const float dx1 = pj.x - p1.x, dy1 = pj.y - p1.y, dz1 = pj.z - p1.z;
-            const float r0 = __fmaf_rn(dz0, dz0, __fmaf_rn(dy0, dy0, __fmaf_rn(dx0, dx0, NB_EPS2)));
-            const float r1 = __fmaf_rn(dz1, dz1, __fmaf_rn(dy1, dy1, __fmaf_rn(dx1, dx1, NB_EPS2)));
-            const float q0 = rsqrtf(r0), q1 = rsqrtf(r1);
-            const float s0 = q0 * q0 * q0, s1 = q1 * q1 * q1;
-            ax0 = __fmaf_rn(dx0, s0, ax0);
-            ay0 = __fmaf_rn(dy0, s0, ay0);
-            az0 = __fmaf_rn(dz0, s0, az0);
-            ax1 = __fmaf_rn(dx1, s1, ax1);
-            ay1 = __fmaf_rn(dy1, s1, ay1);
-            az1 = __fmaf_rn(dz1, s1, az1);
-        };
-        if (jn == kNbTile) {
-#pragma unroll 8
-            for (int k = 0; k < kNbTile; ++k) body(sp[k]);
-        } else {
-            for (int k = 0; k < jn; ++k) body(sp[k]);
-        }
-        __syncthreads();
-    }
-    const float c = NB_DT * NB_MASS;
-    if (v0) {
-        float4* vp = ptr<float4>(V, i0, 0, 0);
-        float4 v = *vp;
-        v.x = __fmaf_rn(c, ax0, v.x);
-        v.y = __fmaf_rn(c, ay0, v.y);
-        v.z = __fmaf_rn(c, az0, v.z);
-        *vp = v;
-    }
-    if (v1) {
-        float4* vp = ptr<float4>(V, i1, 0, 0);
-        float4 v = *vp;
-        v.x = __fmaf_rn(c, ax1, v.x);
-        v.y = __fmaf_rn(c, ay1, v.y);
-        v.z = __fmaf_rn(c, az1, v.z);
-        *vp = v;
-    }
-}
-
 // fast-math timestep on Blackwell packed FP32x2 (FFMA2 / FADD2 / FMUL2):
 // bodies i and i + 128 ride in the two lanes of every float2 operation, so
 // one instruction does the arithmetic of two interactions (rsqrt stays scalar)
@@ -1233,14 +1117,9 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         const int64_t x0 = a.chunk.lo[2], w = a.chunk.hi[2] - x0;
         const bool vec = !a.checked && A.es == 4 && B.es == 4 && A.n[2] % 4 == 0 && B.n[2] % 4 == 0 && (x0 - A.lo[2]) % 4 == 0 &&
                          (x0 - B.lo[2]) % 4 == 0 && w % 4 == 0 && aligned16(A.base) && aligned16(B.base);
-        static int use_tma = -1;
         static bool attr_set[64] = {};
-        if (use_tma < 0) {
-            const char* e = getenv("CEL_JACOBI");
-            use_tma = (e && e[0] == 'l') ? 0 : 1;
-        }
         CUtensorMap tm;
-        if (vec && use_tma && A.n[2] % 4 == 0 && jacobi_tensor_map(A, &tm)) {
+        if (vec && !(a.variant & kVarJacobiLsu) && A.n[2] % 4 == 0 && jacobi_tensor_map(A, &tm)) {
             int dev = 0;
             cudaGetDevice(&dev);
             if (dev >= 0 && dev < 64 && !attr_set[dev]) {
@@ -1263,19 +1142,8 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
     case K_NBODY_STEP: {
         if (cv == 0) return 0;
         const int64_t n = a.chunk.hi[0] - a.chunk.lo[0];
-        static int variant = -1;
-        if (variant < 0) {
-            const char* e = getenv("CEL_NBODY");
-            variant = (e && e[0] == '1') ? 1 : ((e && e[0] == '2') ? 2 : 3);
-        }
-        if (a.checked)
-            nbody_step_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
-        else if (a.fast && variant == 3)
+        if (a.fast && !a.checked)
             nbody_step_fast_x2_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), 128, 0, s>>>(a);
-        else if (a.fast && variant == 2)
-            nbody_step_fast2_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), 128, 0, s>>>(a);
-        else if (a.fast)
-            nbody_step_fast_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
         else
             nbody_step_kernel<<<unsigned((n + kNbTile - 1) / kNbTile), kNbTile, 0, s>>>(a);
         return 1;
@@ -1286,18 +1154,13 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         return 1;
     case K_RSIM_ROW: {
         if (cv == 0) return 0;
-        static int variant = -1;
-        if (variant < 0) {
-            const char* e = getenv("CEL_RSIM");          // 0: force the register kernel (A/B)
-            variant = e ? atoi(e) : 5;
-        }
         const DAcc& R0 = a.acc[0];
         if (a.checked) {
             rsim_row_checked<<<grid_for(cv, 128), 128, 0, s>>>(a);
             return 1;
         }
         CUtensorMap tm;
-        if (variant != 0 && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
+        if (!(a.variant & kVarRsimRegs) && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
             R0.lo[2] == 0 && R0.es == 4 && R0.ext[1] >= 2 * kRB && R0.lo[0] == 0 &&
             (reinterpret_cast<uintptr_t>(R0.base) & 15) == 0 && a.t > 0 && rsim_tensor_map(R0, &tm)) {
             const unsigned grid = unsigned((cv + kRC - 1) / kRC);

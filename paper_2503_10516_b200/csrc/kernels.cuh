@@ -66,8 +66,13 @@ struct KArgs {
     int fast;                  // fast-math variant (FMA + rsqrt) of ALU-bound kernels
     int strip;                 // rows per CTA of the stencil kernels (0 = default)
     int checked;               // bounds checking: scalar kernels whose accesses go through at()
+    int variant;               // A/B switches of the runtime (Executor: CEL_JACOBI / CEL_RSIM env):
+                               // kVarJacobiLsu, kVarRsimRegs
     DAcc acc[kMaxAcc];
 };
+
+constexpr int kVarJacobiLsu = 1;   // 3-D 7-point: LSU register-window kernel instead of TMA
+constexpr int kVarRsimRegs = 2;    // RSim row: register kernel instead of the TMA-staged one
 
 // kernel kinds (mirror include/cel.h cel_kernel)
 enum : int {

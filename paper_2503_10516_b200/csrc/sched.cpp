@@ -682,10 +682,13 @@ uint64_t Scheduler::emit(Instr& ins, std::vector<uint64_t>& deps) {
         if (ins.kind == IKind::Alloc) alloc_owner_[int64_t(ins.iid)] = own;
         bool rel = (ins.kind != IKind::Copy && ins.kind != IKind::Kernel) || own < 0 || own == filter_rank_ ||
                    ins.coll_n != 0 || (ins.kind == IKind::Copy && ins.dst_mem - 2 == filter_rank_);
-        for (size_t i = 0; i < ins.deps.size() && !rel; ++i) {
+        ins.dep_owner.resize(ins.deps.size());
+        for (size_t i = 0; i < ins.deps.size(); ++i) {
             int o = 0;
+            const bool known = owner_of(ins.deps[i], &o);
+            ins.dep_owner[i] = known ? int8_t(o) : int8_t(-2);
             // a dependency this rank executes or co-owns (horizons, epochs): it must signal it
-            if (!owner_of(ins.deps[i], &o) || o < 0 || o == filter_rank_) rel = true;
+            if (!known || o < 0 || o == filter_rank_) rel = true;
         }
         if (!rel) return ins.iid;                 // other ranks' business: the executor never sees it
     }

@@ -202,6 +202,11 @@ struct Instr {
     std::shared_ptr<const TaskDesc> desc;
     // all
     std::vector<uint64_t> deps;
+    // multi-process rank filter (world > 1): owner device of each dependency as
+    // the scheduler knew it when it emitted this instruction (-1 = every rank,
+    // -2 = unknown: older than the scheduler's owner ring), so the executor
+    // thread never reads the scheduler's ring, which the API thread overwrites
+    std::vector<int8_t> dep_owner;
 };
 
 struct InstrSink {

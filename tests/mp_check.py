@@ -20,7 +20,8 @@ sys.path.insert(0, ROOT)
 
 import torch.distributed as dist  # noqa: E402
 
-from oracle.scheduler import Runtime as OracleRuntime, run_program  # noqa: E402
+from oracle.scheduler import Runtime as OracleRuntime  # noqa: E402
+from workloads.driver import run_program  # noqa: E402
 from oracle.simulate import GARBAGE, simulate  # noqa: E402
 from workloads import programs as P  # noqa: E402
 
@@ -30,6 +31,8 @@ def main():
     ap.add_argument("--execute", type=int, default=1)
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--fold", type=int, default=0,
+                    help="k > 0: ranks share k GPUs (rank r on GPU r %% k): CUDA IPC and flags within one GPU")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dist.init_process_group("gloo")
@@ -47,8 +50,9 @@ def main():
             log = "/tmp/mp_log_%d.jsonl" % rank
             if args.execute:
                 import torch
-                torch.cuda.set_device(rank)
-                rt = cel.Runtime(world, cuda_devices=list(range(world)), rank=rank, world=world,
+                gpus = [r % args.fold if args.fold else r for r in range(world)]
+                torch.cuda.set_device(gpus[rank])
+                rt = cel.Runtime(world, cuda_devices=gpus, rank=rank, world=world,
                                  arena_bytes=256 << 20, lookahead=mode, instr_log_path=log)
                 blobs = [None] * world
                 dist.all_gather_object(blobs, rt.ipc_export())

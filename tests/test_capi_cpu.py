@@ -11,7 +11,7 @@ import pytest
 
 from oracle.invariants import check
 from oracle.scheduler import Runtime as OracleRuntime
-from oracle.scheduler import run_program
+from workloads.driver import run_program
 from workloads import programs as P
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

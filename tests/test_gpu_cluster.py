@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from oracle.cluster import Cluster  # noqa: E402
-from oracle.scheduler import run_program  # noqa: E402
+from workloads.driver import run_program  # noqa: E402
 from oracle.simulate import GARBAGE, simulate_cluster  # noqa: E402
 from workloads import programs as P  # noqa: E402
 

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 from oracle import geometry as g  # noqa: E402
 from oracle.kernels import Acc, init_value, k_wave5, nbody_accel_one  # noqa: E402
 from oracle.scheduler import Runtime as OracleRuntime  # noqa: E402
-from oracle.scheduler import run_program  # noqa: E402
+from workloads.driver import run_program  # noqa: E402
 from oracle.simulate import simulate  # noqa: E402
 from workloads import programs as P  # noqa: E402
 
@@ -106,6 +106,56 @@ def test_nbody(cel, G):
 @pytest.mark.parametrize("G,mode", [(1, "auto"), (2, "auto"), (2, "none"), (4, "none"), (3, "infinite")])
 def test_rsim(cel, G, mode):
     run_both(cel, P.rsim(1000, 24), G, mode)
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_rsim_tma_ring_cycles(cel, G):
+    """rsim_row_tma's 4-stage mbarrier ring (16 rows per stage) refills and
+    flips phase once t > 48: T = 140 rows runs ceil(139/16) = 9 stages per
+    launch at the end, > 2 full ring cycles, at W = 1000 >= 2 * 148 (the TMA
+    kernel's precondition), bit-exact against the oracle."""
+    run_both(cel, P.rsim(1000, 140), G, "auto")
+
+
+def test_rsim_register_kernel(cel, monkeypatch):
+    """The register fallback rsim_row_kernel<16> (CEL_RSIM=0 selects it for the
+    runtime; otherwise taken when the TMA preconditions fail): rows t >= 16
+    run its unrolled 16-load loop plus the tail, bit-exact."""
+    monkeypatch.setenv("CEL_RSIM", "0")
+    run_both(cel, P.rsim(1000, 40), 2, "auto")
+    run_both(cel, P.rsim(301, 37), 1, "none")
+
+
+def test_jacobi_lsu_kernel(cel, monkeypatch):
+    """The LSU fallback jacobi7_vec (CEL_JACOBI=l; otherwise taken when the
+    allocation is not TMA-compatible), bit-exact."""
+    monkeypatch.setenv("CEL_JACOBI", "l")
+    run_both(cel, P.jacobi3d(36, 4), 4)
+    run_both(cel, P.jacobi3d(20, 3), 1)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("dma", [True, False])
+def test_forced_peer_path(cel, G, dma, monkeypatch):
+    """CEL_FORCE_PEER=1: copies between virtual devices of one GPU take the
+    path of copies between GPUs -- with dma, the copy-engine plan (1-D runs
+    and pitched 2-D boxes <= 4 MiB: cudaMemcpyAsync / cudaMemcpy2DAsync pitch
+    arithmetic), without (CEL_PEER_DMA=0, what pushes > 4 MiB take) the fenced
+    persistent-grid peer copy kernel -- so one B200 covers that code: 3-D halo
+    faces, ragged and 2-D-split WaveSim, N-body / RSim gathers and random
+    programs, bit-exact and with the oracle's instruction log."""
+    monkeypatch.setenv("CEL_FORCE_PEER", "1")
+    if not dma:
+        monkeypatch.setenv("CEL_PEER_DMA", "0")
+    run_both(cel, P.jacobi3d(36, 4), G)
+    run_both(cel, P.jacobi3d(20, 3), G + 1)
+    run_both(cel, P.wavesim(1040, 7, rows=300), G)
+    run_both(cel, P.wavesim(515, 5, rows=130, split="2d", mapper="neighborhood_axes"), G)
+    st = run_both(cel, P.nbody(1000, 2), G).final_stats
+    assert st["copies_coherence"] > 0 and (st["copy_launches"] == 0) == dma
+    run_both(cel, P.rsim(1000, 24), G, "none")
+    for s in range(6):
+        run_both(cel, P.random_program(7100 + 11 * G + s), G, arena=32 << 20)
 
 
 def test_all_gather_collective_vs_pushes(cel, monkeypatch):
@@ -230,10 +280,10 @@ def test_nbody_full_size_sampled(cel):
 
 
 def test_nbody_fast_math_within_tolerance(cel):
-    """fast_math (FMA + rsqrt) N-body: not bit-exact by design (R16); every
-    velocity component must lie within 2^-16 of the sum of |contributions|
-    (rsqrt ~2 ulp + FMA rounding per term, accumulated over N terms) of the
-    oracle's exact sequential float32 result."""
+    """fast_math (FMA + rsqrt) N-body: not bit-exact by design (R16).  The
+    bar is R16's performance-build tolerance, north_star's "1e-6 relative"
+    read as |g - o| <= 1e-6 * max(|o|, max |field|) per component, against
+    the oracle's exact sequential float32 result."""
     N = 4096
     prog = P.nbody(N, 1)
     rt = cel.Runtime(2, cuda_devices=[0, 0], arena_bytes=64 << 20, fast_math=True)
@@ -241,15 +291,14 @@ def test_nbody_fast_math_within_tolerance(cel):
     o = OracleRuntime(2)
     run_program(o, prog)
     exp = simulate(o)
-    pos = init_value(3, np.arange(4 * N, dtype=np.uint64)).reshape(N, 4)[:, :3].astype(np.float64)
-    d = pos[None, :, :] - pos[:, None, :]
-    r2 = (d ** 2).sum(-1) + 2.0 ** -10
-    l1 = (np.abs(d) / r2[..., None] ** 1.5).sum(1)            # sum of |contributions| per body
-    c = 2.0 ** -27
-    vg = got[1].view(np.float32)[:, 0, 0, :3].astype(np.float64)
-    vo = exp[1].view(np.float32)[:, 0, 0, :3].astype(np.float64)
-    assert np.all(np.abs(vg - vo) <= c * l1 * 2.0 ** -16 + 1e-30)
-    assert not np.array_equal(vg, vo) or True
+    for k in (0, 1):                                          # P and V after the step
+        vg = got[k].view(np.float32)[:, 0, 0, :3].astype(np.float64)
+        vo = exp[k].view(np.float32)[:, 0, 0, :3].astype(np.float64)
+        scale = np.maximum(np.abs(vo), np.abs(vo).max())
+        err = (np.abs(vg - vo) / scale).max()
+        print("fast_math readback %d: max |g-o| / max(|o|, max|field|) = %.3g" % (k, err))
+        assert err <= 1e-6, err
+    assert not np.array_equal(got[1], exp[1]), "fast_math path did not run (bit-identical to the exact kernel)"
 
 
 def light_cone_jacobi(z_lo, z_hi, n, steps, seed=5):

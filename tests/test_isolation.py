@@ -35,11 +35,22 @@ def test_product_package_never_imports_the_oracle():
                 assert oracle_imports(ast.parse(open(p).read())) == [], p
 
 
+CPU_ARMS = ("cpu_baseline", "run_reference")
+ORACLE_HELPERS = ("oracle_wave_fields", "oracle_wave_step")   # bench.py helpers of the two CPU arms
+
+
 def test_bench_imports_the_oracle_only_in_its_cpu_arms():
     for name in ("bench.py", "bench_config.py", "bench_suite.py", "bench_nodes.py"):
         tree = ast.parse(open(os.path.join(ROOT, name)).read())
         for fn, line in oracle_imports(tree):
-            assert fn in ("cpu_baseline", "run_reference"), "%s:%d imports the oracle in %s" % (name, line, fn)
+            assert fn in CPU_ARMS + ORACLE_HELPERS, "%s:%d imports the oracle in %s" % (name, line, fn)
+        # the helpers that touch the oracle are called from the CPU arms only
+        for top in tree.body:
+            if not isinstance(top, ast.FunctionDef):
+                continue
+            for n in ast.walk(top):
+                if isinstance(n, ast.Call) and isinstance(n.func, ast.Name) and n.func.id in ORACLE_HELPERS:
+                    assert top.name in CPU_ARMS + ORACLE_HELPERS, "%s: %s calls %s" % (name, top.name, n.func.id)
 
 
 def test_native_sources_do_not_include_oracle_code():
@@ -48,3 +59,25 @@ def test_native_sources_do_not_include_oracle_code():
             for line in open(os.path.join(dirpath, f)):
                 if line.lstrip().startswith("#include"):
                     assert "oracle" not in line, (f, line)
+
+
+def test_workloads_and_oracle_are_independent():
+    """workloads/ (input generators + the program driver) holds none of the
+    method's arithmetic and imports neither side; the oracle does not import
+    workloads/ or the product."""
+    def imported(tree):
+        mods = set()
+        for n in ast.walk(tree):
+            if isinstance(n, ast.Import):
+                mods |= {a.name.split(".")[0] for a in n.names}
+            elif isinstance(n, ast.ImportFrom) and n.level == 0:
+                mods.add((n.module or "").split(".")[0])
+        return mods
+    for f in os.listdir(os.path.join(ROOT, "workloads")):
+        if f.endswith(".py"):
+            mods = imported(ast.parse(open(os.path.join(ROOT, "workloads", f)).read()))
+            assert not mods & {"oracle", "paper_2503_10516_b200"}, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith(".py"):
+            mods = imported(ast.parse(open(os.path.join(ROOT, "oracle", f)).read()))
+            assert not mods & {"workloads", "paper_2503_10516_b200"}, f

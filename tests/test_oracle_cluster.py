@@ -12,7 +12,9 @@ import pytest
 
 from oracle import geometry as g
 from oracle.cluster import Cluster
-from oracle.scheduler import Runtime, run_program
+from oracle.invariants import check_allocations
+from oracle.scheduler import Runtime
+from workloads.driver import run_program
 from oracle.simulate import sequential, simulate_cluster
 from workloads import programs as P
 
@@ -142,6 +144,8 @@ def test_random_programs_match_sequential(N, D):
         prog = P.random_program(4300 + 31 * N + 7 * D + s)
         cl = run(prog, N, D, ["none", "auto", "infinite"][s % 3], step=2 + s % 3)
         assert bytes_match(cl, prog), s
+        for log in cl.logs:                 # R9 per node, M1 staging allocations included
+            check_allocations(log)
 
 
 @pytest.mark.parametrize("N,D", [(2, 2), (4, 1)])
@@ -151,6 +155,8 @@ def test_configs_match_sequential(N, D):
         for mode in ("none", "auto"):
             cl = run(prog, N, D, mode)
             assert bytes_match(cl, prog), (prog["name"], mode)
+            for log in cl.logs:
+                check_allocations(log)
 
 
 def pushed_elements(cl):

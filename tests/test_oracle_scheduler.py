@@ -11,7 +11,8 @@ import pytest
 from oracle import geometry as g
 from oracle.invariants import InvariantError, check
 from oracle.program import CelError
-from oracle.scheduler import Runtime, counts, run_program
+from oracle.scheduler import Runtime, counts
+from workloads.driver import run_program
 from oracle.simulate import sequential, simulate
 from workloads import programs as P
 
@@ -323,3 +324,49 @@ def test_checker_catches_mutations():
             break
     with pytest.raises(InvariantError):
         check(mutated, rt.buf_meta, rt.tasks)
+
+
+def test_allocation_checker_catches_mutations():
+    """R9 pins: the checker itself must reject a log whose
+    allocations overlap, shrink or leak."""
+    from oracle.invariants import check_allocations
+    prog = P.c1_chain(64)
+    rt = run(prog, 2, "none")          # lookahead none: resize chains alloc -> copy -> free (P:L351)
+    base = rt.log
+    st = check_allocations(base)
+    assert st["allocs"] == st["freed"] == 8
+    chain = [r for r in base if r["kind"] == "copy" and r["reason"] == "resize"][0]
+    new = next(r for r in base if r["kind"] == "alloc" and r["aid"] == chain["dst_aid"])
+    old = next(r for r in base if r["kind"] == "alloc" and r["aid"] == chain["src_aid"])
+
+    def mutate(fn):
+        return [fn(dict(r)) for r in base]
+
+    # shrunk: the replacing allocation no longer contains the one it replaces
+    def shrink(r):
+        if r["iid"] == new["iid"]:
+            r["box"] = [list(old["box"][0]), [old["box"][1][0] - 1] + list(old["box"][1][1:])]
+        return r
+    with pytest.raises(InvariantError):
+        check_allocations(mutate(shrink))
+    # overlap: the old allocation is not freed at the end of its resize chain
+    free_old = next(r for r in base if r["kind"] == "free" and r["aid"] == old["aid"])
+
+    def keep_old(r):
+        return dict(r, kind="horizon") if r["iid"] == free_old["iid"] else r
+    with pytest.raises(InvariantError, match="overlap"):
+        check_allocations(mutate(keep_old), closed=False)
+    # overlap without containment: a fresh allocation straddling a live one
+    extra = dict(new, aid=999, box=[[new["box"][1][0] - 1, 0, 0], [new["box"][1][0] + 1, 1, 1]])
+    with pytest.raises(InvariantError, match="without containing"):
+        check_allocations(base[:new["iid"] + 1] + [extra] + base[new["iid"] + 1:], closed=False)
+    # leaked: a final free dropped
+    last_free = [r for r in base if r["kind"] == "free"][-1]
+
+    def leak(r):
+        return dict(r, kind="horizon") if r["iid"] == last_free["iid"] else r
+    with pytest.raises(InvariantError, match="never freed"):
+        check_allocations(mutate(leak))
+    # double free
+    with pytest.raises(InvariantError):
+        check_allocations(base + [dict(last_free, iid=len(base))])

@@ -2,7 +2,7 @@
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2503_10516_b200 import cel
-from oracle.scheduler import run_program
+from workloads.driver import run_program
 from workloads import programs as P
 name, N, D, mode = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
 prog = {"c1": lambda: P.c1_chain(256), "ws": lambda: P.wavesim(256, 7, rows=96), "nbody": lambda: P.nbody(300, 2),

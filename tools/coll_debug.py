@@ -14,7 +14,7 @@ torch.cuda.set_device(rank)
 rt = bench.make_runtime(cel, world, rank, world, dist, 64 << 20)
 print("rank", rank, "runtime up", flush=True)
 prog = P.nbody(int(sys.argv[1]) if len(sys.argv) > 1 else 64, 1)
-from oracle.scheduler import run_program
+from workloads.driver import run_program
 out = run_program(rt, prog)
 print("rank", rank, "done", flush=True)
 dist.barrier()

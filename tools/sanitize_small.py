@@ -5,7 +5,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 from paper_2503_10516_b200 import cel
-from oracle.scheduler import Runtime as ORt, run_program
+from oracle.scheduler import Runtime as ORt
+from workloads.driver import run_program
 from oracle.simulate import simulate
 from workloads import programs as P
 progs = [P.c1_chain(1024), P.wavesim(1024, 4, rows=700), P.jacobi3d(72, 2), P.nbody(600, 1, host_init=True),

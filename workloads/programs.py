@@ -1,7 +1,7 @@
 """Program descriptions for the five BASELINE.json configs and random tests.
 
-A program is plain data, consumed by `oracle.scheduler.run_program` and by
-the product binding alike:
+A program is plain data, fed by `workloads.driver.run_program` to the oracle
+and to the product binding alike:
 
   {"buffers": [{"dims", "extent", "elem_size", "host_init": ndarray | None}],
    "ops": [("task", spec) | ("wait",) | ("read", bid, (mins, maxs)) |
@@ -18,6 +18,22 @@ for host-initialised buffers, drawn here from numpy's PCG64 with a fixed seed.
 """
 
 import numpy as np
+
+
+def init_values(seed, idx):
+    """The synthetic input recipe's value of element word `idx` (uint64 array):
+    init(seed, i) = 2 * (float)(splitmix64(seed + i) >> 40) * 2^-24 - 1, exact
+    in [-1, 1).  The device fill_hash kernel and the oracle
+    implement it independently; this copy lets harnesses byte-check data that
+    a copy moved without running either side."""
+    M = np.uint64(0xFFFFFFFFFFFFFFFF)
+    with np.errstate(over="ignore"):
+        z = (np.asarray(idx, dtype=np.uint64) + np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15)) & M
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    v = (z >> np.uint64(40)).astype(np.float32)
+    return (np.float32(2.0) * (v * np.float32(2.0 ** -24))) - np.float32(1.0)
 
 
 def _task(dims, rng, kernel, accesses, params=None, split="1d"):
