@@ -8,6 +8,9 @@ region, CUDA events, max over ranks).  Prints one JSON line on rank 0.
   jacobi3d  C5: 1024^3 fp32 7-point, 2-D split (z, y), strided y-face halos
   nbody     C3: 2^20 float4 bodies, 'all' read of P -> G(G-1) peer pushes per step
   rsim      C4: W = 84,000, T rows (default 1024): whole program timed (value = rows/s)
+  gather    C3's communication stage alone: every step rewrites P (2^20 float4 = 16 MiB) on
+            its owners and runs a task reading it through `all`, i.e. one all-gather set of
+            G (G-1) copies; value = gathers/s, GB/s received per device vs NVLink
 """
 
 import argparse
@@ -30,7 +33,7 @@ FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--workload", required=True, choices=["jacobi3d", "nbody", "rsim", "wavesim"])
+    ap.add_argument("--workload", required=True, choices=["jacobi3d", "nbody", "rsim", "wavesim", "gather"])
     ap.add_argument("--split", default="1d", help="wavesim: 1d | 2d")
     ap.add_argument("--mapper", default="neighborhood", help="wavesim: neighborhood | neighborhood_axes")
     ap.add_argument("--gpus", type=int, default=1)
@@ -90,6 +93,24 @@ def main():
             rt.submit_desc(descs[0][0])
             rt.submit_desc(descs[1][0])
         kernel = "nbody_step"
+    elif args.workload == "gather":
+        N = 1 << 20
+        steps = args.steps or 200
+        rt = bench.make_runtime(cel, G, rank, world, dist, 1 << 30, collective=bool(args.collective))
+        rt.buffer_create(1, [N], 16)
+        rt.buffer_create(1, [N], 16)
+        full = ([0], [N])
+        # the owners rewrite P, then a task declares an `all` read of P (its kernel
+        # writes V only): the coherence diff makes that read one all-gather set
+        produce = cel.task_desc({"dims": 1, "range": full, "kernel": "fill_const", "params": {"value": 1.0},
+                                 "accesses": [(0, "write", ("one_to_one",))]})
+        consume = cel.task_desc({"dims": 1, "range": full, "kernel": "fill_const", "params": {"value": 2.0},
+                                 "accesses": [(1, "write", ("one_to_one",)), (0, "read", ("all",))]})
+
+        def submit(s):
+            rt.submit_desc(produce[0])
+            rt.submit_desc(consume[0])
+        kernel = "fill_const"
     else:
         W, T = 84000, args.rows
         steps = T
@@ -158,6 +179,14 @@ def main():
         line["split"] = args.split
         line["mapper"] = args.mapper
         line["coherence_copies_per_step"] = (st1["copies_coherence"] - st0["copies_coherence"]) / steps
+    elif args.workload == "gather":
+        recv = (G - 1) / G * 16 * (1 << 20)
+        line["gather_bytes_received_per_device"] = recv
+        line["GBps_received_per_device"] = recv / (ms / 1e3 / steps) / 1e9
+        line["frac_nvlink_measured_ref"] = line["GBps_received_per_device"] / 770.0
+        line["coll_multicast"] = st1["coll_multicast"] - st0["coll_multicast"]
+        line["gather_sets"] = st1["gather_sets"] - st0["gather_sets"]
+        line["note"] = "step = rewrite P (fill kernel) + the gather; the fill's ~5 us is inside ms_per_step"
     else:
         line["lookahead"] = args.lookahead
         line["alloc"] = st1["n_alloc"] - st0["n_alloc"]

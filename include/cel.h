@@ -203,6 +203,12 @@ typedef struct cel_stats_s {
     uint64_t n_send, n_receive, n_split_receive, n_await_receive;   /* virtual-node mode (n_nodes > 1) */
     uint64_t pulls, pull_bytes;           /* virtual-node mode: pilot-matched transfers executed, bytes */
     uint64_t coll_allgathers;             /* all-gather sets run as one in-place ncclAllGather */
+    uint64_t tma_copy_launches;           /* copy launches of the TMA tensor-map kernel (strided boxes) */
+    uint64_t vmm_maps, vmm_mapped_bytes;  /* VMM allocations: physical granules mapped (creation + in-place growth) */
+    uint64_t coll_multicast;              /* all-gather sets run as NVLS multicast stores (CEL_COLL_MC=1) */
+    uint64_t staging_elided;              /* virtual-node mode: push staging copies (device -> M1) not executed:
+                                             their sends published the device allocation (device-direct) */
+    uint64_t staging_materialized;        /* ... of which executed late (their M1 bytes were needed after all) */
 } cel_stats_t;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

@@ -84,7 +84,8 @@ class cel_stats(C.Structure):
         "exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon", "exec_ns_epoch",
         "signal_ns", "remote_wait_ns", "copies_elided", "bytes_elided", "coll_groups", "coll_copies",
         "gather_sets", "n_send", "n_receive", "n_split_receive", "n_await_receive", "pulls", "pull_bytes",
-        "coll_allgathers")]
+        "coll_allgathers", "tma_copy_launches", "vmm_maps", "vmm_mapped_bytes", "coll_multicast", "staging_elided",
+        "staging_materialized")]
 
 
 _P = C.c_void_p

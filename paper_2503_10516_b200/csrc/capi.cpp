@@ -134,6 +134,8 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
                 ec.bounds_check = cfg->bounds_check != 0;
                 ec.node = k;
                 ec.comm = comm;
+                for (int v = 0; v < nodes * cfg->n_devices; ++v)
+                    ec.all_devices.push_back(cfg->cuda_devices ? cfg->cuda_devices[v] : v);
                 // M1 staging: a pushed or awaited region is staged in one contiguous
                 // allocation over its bounding box, up to a node's whole chunk
                 if (cfg->arena_bytes) ec.host_arena_bytes = cfg->arena_bytes;
@@ -190,6 +192,7 @@ int cel_runtime_create(const cel_config* cfg, cel_runtime** out) {
     const char* nf = getenv("CEL_NO_FILTER");
     if (world > 1 && !(nf && nf[0] == '1')) rt->sched->set_rank_filter(cfg->rank, world);   // before any instruction is emitted
     if (rt->exec) rt->exec->set_scheduler(rt->sched.get());
+    if (rt->exec && rt->exec->gathers_any_size()) rt->sched->set_coll_min_bytes(0);
     *out = rt.release();
     return CEL_OK;
 }
@@ -376,6 +379,12 @@ int cel_stats(cel_runtime* rt, cel_stats_t* o) {
         o->coll_groups += e.coll_groups;
         o->coll_copies += e.coll_copies;
         o->coll_allgathers += e.coll_allgathers;
+        o->tma_copy_launches += e.tma_copy_launches;
+        o->vmm_maps += e.vmm_maps;
+        o->vmm_mapped_bytes += e.vmm_mapped_bytes;
+        o->coll_multicast += e.coll_multicast;
+        o->staging_elided += e.staging_elided;
+        o->staging_materialized += e.staging_materialized;
     }
     if (rt->comm) {
         o->pulls = rt->comm->pulls();

@@ -62,6 +62,101 @@ void Executor::Arena::release(uint64_t off, uint64_t bytes, Token tok) {
     free_[off] = FreeRange{bytes, std::move(tok)};
 }
 
+// ------------------------------------------------------------ VMM allocations
+// SURVEY NEXT-3, P:L549-556 ("allocations are very slow ... resizing"): in a
+// single process every allocation of at least one granule gets its own
+// reserved virtual address range, sized for growth to the buffer's end along
+// dim 0, with physical memory mapped as needed.  A resize that keeps the
+// rows as a prefix (R9 growth at the end of dim 0) maps more granules behind
+// the old ones: no copy, no matter what else was allocated since (the arena
+// form of growth needs the range right after the allocation to be free).
+std::shared_ptr<Executor::VmmRegion> Executor::vmm_create(int dev, uint64_t bytes, uint64_t reserve) {
+    auto v = std::make_shared<VmmRegion>();
+    v->dev = dev;
+    v->reserved = round_up(std::max(reserve, bytes), vmm_gran_);
+    if (g_drv.reserve(&v->va, v->reserved, vmm_gran_, 0, 0) != CUDA_SUCCESS) {
+        v->reserved = round_up(bytes, vmm_gran_);             // no room to grow: reserve what is needed now
+        if (g_drv.reserve(&v->va, v->reserved, vmm_gran_, 0, 0) != CUDA_SUCCESS) return nullptr;
+    }
+    if (!vmm_map_more(*v, bytes)) {
+        vmm_release(*v);
+        return nullptr;
+    }
+    return v;
+}
+
+bool Executor::vmm_map_more(VmmRegion& v, uint64_t bytes) {
+    const uint64_t want = round_up(bytes, vmm_gran_);
+    if (want <= v.mapped) return true;
+    if (want > v.reserved) return false;
+    const uint64_t add = want - v.mapped;
+    CUmemAllocationProp prop;
+    memset(&prop, 0, sizeof prop);
+    prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop.location.id = phys_[v.dev];
+    CUmemGenericAllocationHandle h;
+    if (g_drv.create(&h, add, &prop, 0) != CUDA_SUCCESS) return false;
+    if (g_drv.map(v.va + v.mapped, add, 0, h, 0) != CUDA_SUCCESS) {
+        g_drv.release(h);
+        return false;
+    }
+    // every GPU of this process may read or push into it (peer access by mapping)
+    std::vector<CUmemAccessDesc> acc;
+    for (int p : cfg_.all_devices.empty() ? phys_ : cfg_.all_devices) {
+        bool seen = false;
+        for (auto& a : acc) seen = seen || a.location.id == p;
+        if (seen) continue;
+        CUmemAccessDesc d;
+        d.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        d.location.id = p;
+        d.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        acc.push_back(d);
+    }
+    if (g_drv.set_access(v.va + v.mapped, add, acc.data(), acc.size()) != CUDA_SUCCESS) {
+        g_drv.unmap(v.va + v.mapped, add);
+        g_drv.release(h);
+        return false;
+    }
+    v.chunks.push_back({h, add});
+    v.mapped = want;
+    st_.vmm_mapped_bytes += add;
+    st_.vmm_maps++;
+    return true;
+}
+
+void Executor::vmm_release(VmmRegion& v) {
+    if (!mc_groups_.empty()) mc_forget(&v);     // unbind multicast objects before the memory goes
+    uint64_t o = 0;
+    for (auto& c : v.chunks) {
+        g_drv.unmap(v.va + o, c.second);
+        g_drv.release(c.first);
+        o += c.second;
+    }
+    v.chunks.clear();
+    if (v.va) g_drv.addr_free(v.va, v.reserved);
+    v.va = 0;
+    v.mapped = 0;
+}
+
+// Unmap freed VMM allocations whose free instruction has completed (all: the
+// device is idle, e.g. at destruction).
+void Executor::vmm_reap(bool all) {
+    for (auto it = vmm_free_.begin(); it != vmm_free_.end();) {
+        bool done = all;
+        if (!done) {
+            done = true;
+            for (const TokEntry& e : it->second.local) done = done && e.seq <= streams_[e.stream].done;
+        }
+        if (done) {
+            vmm_release(*it->first);
+            it = vmm_free_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
 // ------------------------------------------------------------ setup
 Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(sched) {
     G_ = int(cfg_.cuda_devices.size());
@@ -76,12 +171,20 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     if (jv && jv[0] == 'l') kernel_variant_ |= kVarJacobiLsu;
     const char* rv = getenv("CEL_RSIM");
     if (rv && rv[0] == '0') kernel_variant_ |= kVarRsimRegs;
+    const char* ds = getenv("CEL_DIRECT_SENDS");
+    direct_sends_ = cfg_.comm && !(ds && ds[0] == '0');
+    const char* cmb = getenv("CEL_COLL_MIN_BYTES");
+    if (cmb && cmb[0]) coll_min_bytes_ = strtoull(cmb, nullptr, 10);
+    const char* cv = getenv("CEL_COPY");
+    tma_copy_ = cv && cv[0] == 't';
     const char* fp = getenv("CEL_FORCE_PEER");
     force_peer_ = fp && fp[0] == '1';
     const char* ns = getenv("CEL_NO_SPLIT");
     split_ = !(ns && ns[0] == '1');
     const char* ng = getenv("CEL_NO_GROW");
     no_grow_ = ng && ng[0] == '1';
+    const char* ra = getenv("CEL_ROW_ALIGN");
+    if (ra && atoi(ra) >= 16 && (atoi(ra) & (atoi(ra) - 1)) == 0) row_align_ = uint32_t(atoi(ra));
     const char* np = getenv("CEL_NO_PAD");
     no_pad_ = np && np[0] == '1';
     grown_ = !no_grow_;
@@ -99,6 +202,13 @@ Executor::~Executor() {
         threaded_ = false;
     }
     if (err_ == 0) sync_all();
+    else
+        for (auto& s : streams_)
+            if (s.s) cudaStreamSynchronize(s.s);
+    mc_teardown();
+    vmm_reap(true);
+    for (auto& kv : allocs_)
+        if (kv.second.vmm && !kv.second.absorbed_into && kv.second.vmm->va) vmm_release(*kv.second.vmm);
     for (auto& p : prof_pending_) {
         cudaEventDestroy(p.a);
         cudaEventDestroy(p.b);
@@ -141,7 +251,7 @@ Box Executor::padded_box(const Box& b, uint32_t buffer, uint32_t es) const {
     int d = 2;                                   // innermost dimension the buffer uses
     while (d > 0 && ext.hi[d] - ext.lo[d] <= 1) --d;
     if (d == 0) return b;                        // 1-D: whole rows are contiguous already
-    const int64_t a = 16 / int64_t(es);
+    const int64_t a = int64_t(row_align_) / int64_t(es);
     Box p = b;
     p.lo[d] = b.lo[d] - (b.lo[d] % a);           // coordinates are >= 0
     p.hi[d] = p.lo[d] + (b.hi[d] - p.lo[d] + a - 1) / a * a;
@@ -186,16 +296,19 @@ int Executor::init(std::string* err) {
     uint64_t arena = cfg_.arena_bytes ? cfg_.arena_bytes : (16ull << 30);
     const uint64_t sig_bytes = cfg_.world > 1 ? uint64_t(cfg_.world) * kRing * 8 : 0;
     const uint64_t data_off = round_up(sig_bytes, 2u << 20);
-    // peer access between distinct physical devices (NVLink 5 / NVSwitch)
+    // peer access between distinct physical devices (NVLink 5 / NVSwitch);
+    // virtual-node mode: with every GPU of the process (device-direct sends
+    // are pulled from another node's device memory)
+    const std::vector<int>& peers = cfg_.all_devices.empty() ? phys_ : cfg_.all_devices;
     for (int a = 0; a < G_; ++a) {
         if (!owned(a)) continue;
-        for (int b = 0; b < G_; ++b) {
-            if (phys_[a] == phys_[b]) continue;
+        for (int pb : peers) {
+            if (phys_[a] == pb) continue;
             int can = 0;
-            cudaDeviceCanAccessPeer(&can, phys_[a], phys_[b]);
+            cudaDeviceCanAccessPeer(&can, phys_[a], pb);
             if (can) {
                 cudaSetDevice(phys_[a]);
-                cudaError_t e = cudaDeviceEnablePeerAccess(phys_[b], 0);
+                cudaError_t e = cudaDeviceEnablePeerAccess(pb, 0);
                 if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
             }
         }
@@ -243,6 +356,33 @@ int Executor::init(std::string* err) {
             return E_CUDA;
         }
     }
+    // VMM allocations: one process owning all devices (multi-process runs
+    // replay one deterministic arena layout instead, so every rank knows every
+    // address without exchanging memory handles)
+    const char* nv = getenv("CEL_NO_VMM");
+    if (cfg_.world == 1 && !(nv && nv[0] == '1')) {
+        g_drv.load();
+        int sup = 1;
+        for (int p : phys_) {
+            int v = 0;
+            if (!g_drv.devattr || g_drv.devattr(&v, CU_DEVICE_ATTRIBUTE_VIRTUAL_MEMORY_MANAGEMENT_SUPPORTED, CUdevice(p)) !=
+                                      CUDA_SUCCESS)
+                v = 0;
+            sup = sup && v;
+        }
+        if (sup && g_drv.vmm()) {
+            CUmemAllocationProp prop;
+            memset(&prop, 0, sizeof prop);
+            prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+            prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+            prop.location.id = phys_[0];
+            size_t gr = 0;
+            if (g_drv.granularity(&gr, &prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM) == CUDA_SUCCESS && gr > 0) {
+                vmm_gran_ = gr;
+                vmm_ = true;
+            }
+        }
+    }
     if (cfg_.collective && G_ >= 2) {
         // one NCCL rank per GPU: the virtual devices must be distinct GPUs
         bool distinct = true;
@@ -252,6 +392,9 @@ int Executor::init(std::string* err) {
         const char* cv = getenv("CEL_COLL");
         if (cv && cv[0] == '0') distinct = false;
         coll_ = distinct && g_nccl.load();
+        // NVLS multicast gathers: one process, distinct GPUs, VMM allocations
+        const char* mc = getenv("CEL_COLL_MC");
+        mc_enabled_ = distinct && vmm_ && cfg_.world == 1 && mc && mc[0] == '1';
         if (coll_ && cfg_.world > 1 && cfg_.rank == 0) {
             ncclUniqueId id;
             if (g_nccl.get_id(&id) != ncclSuccess) {
@@ -408,6 +551,7 @@ void Executor::poll(bool prune) {
         }
     }
     (void)prune;
+    if (!vmm_free_.empty()) vmm_reap(false);
     if (!oob_pending_.empty()) oob_check(false);
 }
 
@@ -897,13 +1041,14 @@ void Executor::on_instr_impl(const Instr& ins) {
     cur_ins_ = &ins;
     check_owner_known(ins);
     if (err_) return;
+    if (!staged_.empty()) settle_staged(ins);
     if (!pending_send_.empty()) resolve_sends(ins);
     const int od = instr_owner(ins);
     const bool mine = od < 0 || owner_rank(od) == cfg_.rank;
     if (trace_)
         fprintf(stderr, "[cel r%d] iid %llu kind %d owner %d %s\n", cfg_.rank, (unsigned long long)ins.iid,
                 int(ins.kind), od, mine ? "exec" : "skip");
-    if (coll_ && ins.kind == IKind::Copy && ins.coll_n) {
+    if ((coll_ || mc_enabled_) && ins.kind == IKind::Copy && ins.coll_n) {
         // §8 a7: a member of an all-gather copy set.  Every rank takes part;
         // the source's and the destination's ranks each wait for the member's
         // dependencies, so the other ranks signal theirs to both.
@@ -958,22 +1103,51 @@ void Executor::on_instr_impl(const Instr& ins) {
                 break;
             }
         }
-        if (grow && arena(dev).extend(grow->off, grow->bytes, bytes, &t)) {
-            // the grown allocation's users write memory the old one's readers
+        // Placement (single process with VMM; multi-process runs use the arena
+        // only, the layout every rank replays):
+        //  1. growing a VMM allocation: map granules behind its rows, in place;
+        //  2. growing an arena allocation whose successor range is free: in place;
+        //  3. growing otherwise: a VMM allocation reserved up to the buffer's end
+        //     along dim 0 (one copy now, later growth in place);
+        //  4. anything else from the pre-reserved arena (allocation instructions
+        //     cost nothing on the hot path), VMM when the arena is full -- the
+        //     arena size is no cap on the buffers' allocations.
+        std::shared_ptr<VmmRegion> vreg;
+        const bool vmm_ok = vmm_ && dev >= 0;
+        auto vmm_new = [&](bool growth) {
+            uint64_t reserve = bytes;
+            if (growth) {        // R9 growth keeps lo and the row pitch: room to the buffer's end along dim 0
+                const uint64_t slice = bytes / uint64_t(std::max<int64_t>(1, pbox.extent(0)));
+                const int64_t rows_max = bufinfo_.at(ins.buffer).extent.hi[0] - pbox.lo[0];
+                reserve = std::min<uint64_t>(slice * uint64_t(std::max<int64_t>(rows_max, 1)), 1ull << 40);
+            }
+            vreg = vmm_create(dev, bytes, reserve);
+            return vreg != nullptr;
+        };
+        if (vmm_ok && grow && grow->vmm && vmm_map_more(*grow->vmm, bytes)) {
+            vreg = grow->vmm;                                           // 1
+            grow->absorbed_into = ins.aid;
+            if (mine) merge(t, grow->use);
+        } else if (grow && !grow->vmm && arena(dev).extend(grow->off, grow->bytes, bytes, &t)) {
+            // 2: the grown allocation's users write memory the old one's readers
             // may still read: follow every local use of the old allocation
             // (remote ranks only write it, and those writes reach the new
             // allocation's users through the resize copies' dependencies)
             off = grow->off;
             grow->absorbed_into = ins.aid;
             if (mine) merge(t, grow->use);
-        } else if (!arena(dev).alloc(bytes, &off, &t)) {
+        } else if (vmm_ok && grow && vmm_new(true)) {
+            // 3
+        } else if (!arena(dev).alloc(bytes, &off, &t) && !(vmm_ok && vmm_new(false))) {
             char buf[200];
-            snprintf(buf, sizeof buf, "device %d arena exhausted allocating %.3f GiB", dev, double(bytes) / (1ull << 30));
+            snprintf(buf, sizeof buf, "device %d: cannot allocate %.3f GiB (arena exhausted%s)", dev,
+                     double(bytes) / (1ull << 30), vmm_ok ? ", VMM mapping failed" : "");
             errmsg_ = buf;
             err_ = E_OOM;
             return;
         }
         allocs_[ins.aid] = AllocRec{dev, off, bytes, pbox, es, ins.iid, ins.buffer};
+        if (vreg) allocs_[ins.aid].vmm = vreg;
         live_alloc_iid_.insert(ins.iid);
         Token mt;
         if (mine) merge(mt, t);
@@ -1003,7 +1177,12 @@ void Executor::on_instr_impl(const Instr& ins) {
         } else {
             t.remote.push_back({owner_rank(r.dev), ins.iid});
         }
-        if (!r.absorbed_into) arena(r.dev).release(r.off, r.bytes, t);   // else: lives on in the grown one
+        if (!r.absorbed_into) {                   // else: lives on in the grown one
+            if (r.vmm)
+                vmm_free_.push_back({r.vmm, t});  // unmapped once the free's dependencies have completed
+            else
+                arena(r.dev).release(r.off, r.bytes, t);
+        }
         tok_[ins.iid] = t;
         live_alloc_iid_.erase(r.iid);
         allocs_.erase(it);
@@ -1102,6 +1281,7 @@ void Executor::exec_epoch(const Instr& ins) {
         }
     }
     host_drop_.clear();
+    if (pending_send_.empty()) msg_tok_.clear();
     Token mine;
     for (int r = 0; r < cfg_.world; ++r)
         if (r != cfg_.rank) mine.remote.push_back({r, ins.iid});

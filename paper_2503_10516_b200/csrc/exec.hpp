@@ -111,6 +111,7 @@ struct ExecConfig {
     bool collective = true;            // run all-gather copy sets as grouped NCCL broadcasts (§8 a7)
     int node = 0;                      // virtual-node mode: this executor's node
     std::shared_ptr<Communicator> comm;
+    std::vector<int> all_devices;               // virtual-node mode: every node's GPUs (peer access for device-direct sends)
     uint64_t host_arena_bytes = 256ull << 20;   // M1 (pinned, mapped) staging arena, virtual-node mode
     bool bounds_check = false;                  // §4.4 accessor bounds checking
 };
@@ -119,6 +120,10 @@ struct ExecStats {
     uint64_t kernel_launches = 0;      // our CUDA kernels (workload + copy + signal)
     uint64_t workload_launches = 0;
     uint64_t copy_launches = 0;
+    uint64_t tma_copy_launches = 0;    // ... of which TMA tensor-map copy kernels
+    uint64_t vmm_maps = 0, vmm_mapped_bytes = 0;   // VMM: physical granule mappings and their bytes
+    uint64_t coll_multicast = 0;                    // all-gather sets run as NVLS multicast stores
+    uint64_t staging_elided = 0, staging_materialized = 0;   // device-direct sends (virtual-node mode)
     uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
     uint64_t event_waits = 0, remote_waits = 0, signals = 0;
@@ -186,6 +191,8 @@ public:
     int trace_dump(const char* path);
     void profile_reset();
     int device_count() const { return G_; }
+    // multicast gathers run sets of any size: the scheduler should flag small ones too
+    bool gathers_any_size() const { return mc_enabled_; }
     int owned(int d) const { return owner_rank(d) == cfg_.rank; }
     void sync_all();
 
@@ -213,6 +220,14 @@ private:
         bool extend(uint64_t off, uint64_t old_bytes, uint64_t new_bytes, Token* tok);
         void release(uint64_t off, uint64_t bytes, Token tok);
     };
+    // VMM allocation: its own reserved VA range,
+    // physical memory mapped in granules as the allocation grows in place
+    struct VmmRegion {
+        CUdeviceptr va = 0;
+        uint64_t reserved = 0, mapped = 0;
+        int dev = 0;
+        std::vector<std::pair<CUmemGenericAllocationHandle, uint64_t>> chunks;   // (handle, bytes) in VA order
+    };
     struct AllocRec {
         int dev;
         uint64_t off;
@@ -223,6 +238,7 @@ private:
         uint32_t buffer = 0;
         int64_t absorbed_into = 0;                // in-place growth: memory now owned by this aid
         Token use;                                // local work that read / wrote it (in-place growth)
+        std::shared_ptr<VmmRegion> vmm;           // VMM allocation (else arena range [off, off + bytes))
     };
     struct Prof {
         int kind;
@@ -274,6 +290,7 @@ private:
     Token multi_local_part(const std::vector<uint64_t>& deps) const;
     char* alloc_ptr(int64_t aid);
     void exec_copy(const Instr& ins);
+    bool exec_copy_tma(const Instr& ins, const AllocRec& S, const AllocRec& D, uint32_t es, int sidx, int dev);
     void exec_kernel(const Instr& ins);
     void exec_epoch(const Instr& ins);
     void throttle();
@@ -301,7 +318,44 @@ private:
     static constexpr int kOobSlots = 1024;
     void exec_host_copy(const Instr& ins, const Token& deps);
     Arena& arena(int dev) { return dev < 0 ? host_arena_ : arenas_[dev]; }
-    char* base_of(const AllocRec& r) { return (r.dev < 0 ? host_arena_.base : arenas_[r.dev].base) + r.off; }
+    char* base_of(const AllocRec& r) {
+        if (r.vmm) return reinterpret_cast<char*>(r.vmm->va);
+        return (r.dev < 0 ? host_arena_.base : arenas_[r.dev].base) + r.off;
+    }
+    // NVLS multicast all-gather (exec_mc.cu)
+    struct McGroup {
+        CUmemGenericAllocationHandle h = 0;       // multicast object bound to the set's G allocations
+        CUdeviceptr va = 0;
+        uint64_t size = 0;
+        std::vector<std::shared_ptr<VmmRegion>> regions;
+        uint64_t slot = 0;                        // flag word of this group
+        uint64_t expected = 0;                    // flag value once every round so far has landed
+    };
+    bool mc_enabled_ = false;                     // CEL_COLL_MC=1 (single process, distinct GPUs, VMM)
+    uint64_t coll_min_bytes_ = 1ull << 20;        // smallest per-source set for NCCL (CEL_COLL_MIN_BYTES)
+    int mc_state_ = 0;                            // 0 not set up, 1 ready, -1 unavailable
+    uint64_t mc_gran_ = 0;
+    CUmemGenericAllocationHandle mc_flag_h_ = 0;
+    CUdeviceptr mc_flag_va_ = 0;
+    std::vector<std::shared_ptr<VmmRegion>> mc_flag_dev_;
+    std::vector<void*> mc_ctr_;
+    std::map<std::vector<int64_t>, McGroup> mc_groups_;
+    uint64_t mc_next_slot_ = 0;
+    bool mc_setup();
+    bool mc_map(CUmemGenericAllocationHandle h, uint64_t size, CUdeviceptr* va);
+    void mc_group_destroy(McGroup& g);
+    void mc_teardown();
+    void mc_forget(const VmmRegion* r);
+    bool exec_coll_mc(const std::vector<Instr>& m);
+    void sync_streams();
+    // VMM (single process): reserve / map / grow / release
+    bool vmm_ = false;
+    uint64_t vmm_gran_ = 2ull << 20;
+    std::vector<std::pair<std::shared_ptr<VmmRegion>, Token>> vmm_free_;   // released once the token completes
+    bool vmm_map_more(VmmRegion& v, uint64_t bytes);
+    std::shared_ptr<VmmRegion> vmm_create(int dev, uint64_t bytes, uint64_t reserve);
+    void vmm_release(VmmRegion& v);
+    void vmm_reap(bool all);
     void exec_coll(const std::vector<Instr>& members);
     bool coll_init();
     Token materialize(int dev, const Token& t);
@@ -377,10 +431,12 @@ private:
     bool peer_dma_ = true;                        // small contiguous pushes on a copy engine (CEL_PEER_DMA=0: off)
     uint64_t peer_dma_max_ = 4ull << 20;
     int kernel_variant_ = 0;                      // KArgs::variant (CEL_JACOBI=l, CEL_RSIM=0 for A/B)
+    bool tma_copy_ = false;                       // strided local boxes by TMA tensor maps (CEL_COPY=tma)
     bool force_peer_ = false;                     // CEL_FORCE_PEER=1: virtual devices of one GPU use the peer path
     size_t max_pitch_ = size_t(1) << 31;          // cudaDevAttrMaxPitch (2-D DMA limit)
     bool no_grow_ = false;                      // CEL_NO_GROW=1: disable in-place growth (A/B)
     bool no_pad_ = false;                       // CEL_NO_PAD=1: allocations exactly as the IDAG's boxes
+    uint32_t row_align_ = 16;                   // bytes the innermost dimension's rows are padded to (CEL_ROW_ALIGN)
     Box padded_box(const Box& b, uint32_t buffer, uint32_t es) const;
     bool grown_ = true;                           // track allocation uses for in-place growth
     std::unordered_map<uint64_t, CopyInfo> copy_info_;
@@ -394,7 +450,22 @@ private:
     std::unordered_map<uint64_t, std::vector<Instr>> coll_pending_;
     // virtual-node mode: M1 staging arena and the flags sends / receives wait on
     Arena host_arena_;
-    std::unordered_map<uint64_t, uint64_t> pending_send_;      // send iid -> message id, completion not resolved
+    std::unordered_map<uint64_t, std::vector<uint64_t>> pending_send_;   // iid -> messages whose pulls complete it
+    std::unordered_map<uint64_t, Token> msg_tok_;              // message -> its pull's completion (resolved once)
+    // device-direct sends (P:L785 RDMA future work): a staging
+    // copy device -> M1 whose data only leaves through sends is not executed;
+    // the sends publish the device allocation itself and the receiver pulls
+    // from it over NVLink.  Materialised (executed late) if anything else needs
+    // the M1 bytes, or before its source allocation is freed.
+    struct Staged {
+        Instr ins;                                 // the elided copy
+        Token deps;                                // its dependencies' completion
+        bool consumed = false;                     // a send published its source
+    };
+    std::map<uint64_t, Staged> staged_;
+    bool direct_sends_ = false;                    // CEL_DIRECT_SENDS=0 turns it off
+    void settle_staged(const Instr& ins);
+    void materialize_staged(uint64_t iid);
     std::unordered_map<int64_t, Communicator::Mem> recv_dst_; // transfer tid * 2^32 + buffer -> split receive destination
     void resolve_sends(const Instr& ins);
     std::unordered_map<uint64_t, Parts> parts_;

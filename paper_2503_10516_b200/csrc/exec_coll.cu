@@ -32,6 +32,21 @@ bool Executor::coll_init() {
 // collectives instead of G(G-1) separate pushes).
 void Executor::exec_coll(const std::vector<Instr>& m) {
     const uint32_t es = bufinfo_.at(m[0].buffer).es;
+    if (exec_coll_mc(m)) return;                  // NVLS multicast stores (exec_mc.cu)
+    uint64_t min_bytes = ~0ull;
+    for (const Instr& x : m) min_bytes = std::min<uint64_t>(min_bytes, rvolume(x.region) * es);
+    if (cfg_.world == 1 && (!coll_ || min_bytes < coll_min_bytes_)) {
+        // one process, and no NCCL or a set too small for it (flagged for the
+        // multicast path, which did not apply): the members run as the peer
+        // pushes they are.  (Multi-process runs only flag sets the scheduler's
+        // identical threshold admits, so every rank joins the same groups.)
+        for (const Instr& x : m) {
+            cur_ins_ = &x;
+            exec_copy(x);
+            if (grown_) note_use(x);
+        }
+        return;
+    }
     if (!coll_init()) {
         errmsg_ = "NCCL communicator setup failed (set collective = 0 to use peer pushes)";
         err_ = E_NCCL;
@@ -76,12 +91,12 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
         const Box& b = xs[0]->region[0];
         if (v == s) {
             const AllocRec& S = allocs_.at(xs[0]->src_aid);
-            return arenas_[S.dev].base + S.off + lin(b, S.box) * es;
+            return base_of(S) + lin(b, S.box) * es;
         }
         for (const Instr* x : xs)
             if (x->dst_mem - 2 == v) {
                 const AllocRec& D = allocs_.at(x->dst_aid);
-                return arenas_[D.dev].base + D.off + lin(b, D.box) * es;
+                return base_of(D) + lin(b, D.box) * es;
             }
         return nullptr;
     };
@@ -125,12 +140,12 @@ void Executor::exec_coll(const std::vector<Instr>& m) {
             const int v = locals[k];
             char* buf = nullptr;
             if (v == s) {
-                buf = arenas_[S.dev].base + S.off + lin(b, S.box) * es;
+                buf = base_of(S) + lin(b, S.box) * es;
             } else {
                 for (const Instr* x : rt.second)
                     if (x->dst_mem - 2 == v) {
                         const AllocRec& D = allocs_.at(x->dst_aid);
-                        buf = arenas_[D.dev].base + D.off + lin(b, D.box) * es;
+                        buf = base_of(D) + lin(b, D.box) * es;
                     }
             }
             if (!buf) {

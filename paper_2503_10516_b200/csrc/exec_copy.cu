@@ -55,6 +55,55 @@ void Executor::exec_host_copy(const Instr& ins, const Token& deps) {
     tok_[ins.iid] = Token{};
 }
 
+// Strided boxes (rows at a pitch, or one row per plane) of a copy between
+// device allocations of one GPU by TMA tensor maps (north_star "TMA tensor-map
+// box loads and stores for 2D/3D strided regions"; SASS UTMALDG / UTMASTG).
+// All-or-nothing per instruction: false (nothing launched) if any box is one
+// contiguous run or not expressible, and the LSU copy kernel takes it.
+bool Executor::exec_copy_tma(const Instr& ins, const AllocRec& S, const AllocRec& D, uint32_t es, int sidx, int dev) {
+    std::vector<TmaBox> boxes;
+    for (const Box& b : ins.region) {
+        TmaBox t;
+        t.src = base_of(S);
+        t.dst = base_of(D);
+        t.es = es;
+        for (int k = 0; k < 3; ++k) {
+            t.sn[k] = S.box.extent(k);
+            t.dn[k] = D.box.extent(k);
+            t.so[k] = b.lo[k] - S.box.lo[k];
+            t.dof[k] = b.lo[k] - D.box.lo[k];
+            t.ext[k] = b.extent(k);
+        }
+        boxes.push_back(t);
+    }
+    std::vector<TmaCopyArgs> launches(1);
+    memset(&launches.back(), 0, sizeof(TmaCopyArgs));
+    for (const TmaBox& t : boxes) {
+        int r = tma_copy_add(launches.back(), t);
+        if (r == 0 && launches.back().nseg == kMaxTmaSegs) {
+            launches.emplace_back();
+            memset(&launches.back(), 0, sizeof(TmaCopyArgs));
+            r = tma_copy_add(launches.back(), t);
+        }
+        if (r != 1) return false;                 // a contiguous run or not expressible: LSU for the instruction
+    }
+    for (const TmaCopyArgs& a : launches) {
+        if (cfg_.profile && prof_sample(K_NUM)) {
+            Prof p{K_NUM, prof_event(dev), prof_event(dev), dev, ins.iid, sidx, now_ns()};
+            cudaEventRecord(p.a, streams_[sidx].s);
+            st_.kernel_launches += launch_copy_tma(a, streams_[sidx].s);
+            cudaEventRecord(p.b, streams_[sidx].s);
+            prof_pending_.push_back(p);
+        } else {
+            st_.kernel_launches += launch_copy_tma(a, streams_[sidx].s);
+        }
+        st_.copy_launches++;
+        st_.tma_copy_launches++;
+    }
+    st_.bytes_copy[ins.reason == REASON_RESIZE ? 0 : 1] += rvolume(ins.region) * es;
+    return true;
+}
+
 void Executor::exec_copy(const Instr& ins) {
     const uint32_t es = bufinfo_.at(ins.buffer).es;
     Token deps;
@@ -75,12 +124,21 @@ void Executor::exec_copy(const Instr& ins) {
         }
         merge(deps, dep_token(j));
     }
+    if (direct_sends_ && ins.src_mem >= 2 && ins.dst_mem == 1 && ins.reason == REASON_COHERENCE && ins.src_aid >= 0 &&
+        !staged_.count(ins.iid)) {
+        // a push's staging copy: elided; its sends publish the device
+        // allocation (settle_staged / exec_transfer)
+        staged_[ins.iid] = Staged{ins, deps, false};
+        tok_[ins.iid] = deps;
+        st_.staging_elided++;
+        return;
+    }
     if (ins.src_mem >= 1 && ins.dst_mem >= 1) {
         // allocation to allocation: device memories, or the pinned + mapped M1
         // staging arena of virtual-node mode on either side (copy kernel)
         const AllocRec& S = allocs_.at(ins.src_aid);
         const AllocRec& D = allocs_.at(ins.dst_aid);
-        if (S.dev == D.dev && S.off == D.off && S.box.lo[0] == D.box.lo[0] && S.box.lo[1] == D.box.lo[1] &&
+        if (S.dev == D.dev && base_of(S) == base_of(D) && S.box.lo[0] == D.box.lo[0] && S.box.lo[1] == D.box.lo[1] &&
             S.box.lo[2] == D.box.lo[2] && S.box.extent(1) == D.box.extent(1) && S.box.extent(2) == D.box.extent(2)) {
             // in-place growth: source and destination bytes coincide
             st_.copies_elided++;
@@ -164,6 +222,10 @@ void Executor::exec_copy(const Instr& ins) {
             }
         }
         uint64_t bytes = 0;
+        if (tma_copy_ && !args.peer && S.dev >= 0 && D.dev >= 0 && exec_copy_tma(ins, S, D, es, sidx, dev)) {
+            tok_[ins.iid] = record(sidx);
+            return;
+        }
         auto flush = [&]() {
             if (args.nseg == 0) return;
             if (cfg_.profile && prof_sample(args.peer ? K_NUM + 1 : K_NUM)) {
@@ -265,7 +327,7 @@ void Executor::exec_copy(const Instr& ins) {
         hbase = hi->second.first;
         hbox = bufinfo_.at(ins.buffer).extent;
         const AllocRec& D = allocs_.at(ins.dst_aid);
-        dbase = arenas_[D.dev].base + D.off;
+        dbase = base_of(D);
         dbox = D.box;
     } else {
         auto rb = readbacks_.find(ins.readback);
@@ -277,7 +339,7 @@ void Executor::exec_copy(const Instr& ins) {
         hbase = rb->second.dst;
         hbox = rb->second.box;
         const AllocRec& S = allocs_.at(ins.src_aid);
-        dbase = arenas_[S.dev].base + S.off;
+        dbase = base_of(S);
         dbox = S.box;
     }
     for (const Box& b : ins.region) {

@@ -28,11 +28,46 @@ struct Drv {
     CUresult (*write64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int) = nullptr;
     CUresult (*errstr)(CUresult, const char**) = nullptr;
     CUresult (*devattr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+    // virtual memory management (in-place growth by mapping)
+    CUresult (*reserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+    CUresult (*addr_free)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*create)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+    CUresult (*release)(CUmemGenericAllocationHandle) = nullptr;
+    CUresult (*map)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+    CUresult (*unmap)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*set_access)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+    CUresult (*granularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+    // multicast objects (NVLS all-gather)
+    CUresult (*mc_create)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+    CUresult (*mc_add_device)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+    CUresult (*mc_bind_mem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                            unsigned long long) = nullptr;
+    CUresult (*mc_unbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+    CUresult (*mc_granularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
     bool loaded = false;
+    bool vmm() const { return reserve && addr_free && create && release && map && unmap && set_access && granularity; }
+    bool multicast() const { return vmm() && mc_create && mc_add_device && mc_bind_mem && mc_unbind && mc_granularity; }
     void load() {
         if (loaded) return;
         loaded = true;
         cudaDriverEntryPointQueryResult q;
+        auto get = [&](const char* name, auto** fn) {
+            cudaGetDriverEntryPoint(name, reinterpret_cast<void**>(fn), cudaEnableDefault, &q);
+            if (q != cudaDriverEntryPointSuccess) *fn = nullptr;
+        };
+        get("cuMemAddressReserve", &reserve);
+        get("cuMemAddressFree", &addr_free);
+        get("cuMemCreate", &create);
+        get("cuMemRelease", &release);
+        get("cuMemMap", &map);
+        get("cuMemUnmap", &unmap);
+        get("cuMemSetAccess", &set_access);
+        get("cuMemGetAllocationGranularity", &granularity);
+        get("cuMulticastCreate", &mc_create);
+        get("cuMulticastAddDevice", &mc_add_device);
+        get("cuMulticastBindMem", &mc_bind_mem);
+        get("cuMulticastUnbind", &mc_unbind);
+        get("cuMulticastGetGranularity", &mc_granularity);
         cudaGetDriverEntryPoint("cuStreamWaitValue64", reinterpret_cast<void**>(&wait64), cudaEnableDefault, &q);
         cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&write64), cudaEnableDefault, &q);
         cudaGetDriverEntryPoint("cuGetErrorString", reinterpret_cast<void**>(&errstr), cudaEnableDefault, &q);

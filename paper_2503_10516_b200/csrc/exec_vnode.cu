@@ -142,12 +142,26 @@ void Executor::exec_transfer(const Instr& ins) {
     };
     switch (ins.kind) {
     case IKind::Send: {
-        wait_token(s_sync, deps);                         // the staging copy
+        wait_token(s_sync, deps);                         // the staging copy (or, elided, its inputs)
         cudaEvent_t ready = nullptr;
         check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
         check(cudaEventRecord(ready, streams_[s_sync].s), "cudaEventRecord");
-        comm.post_send(cfg_.node, ins.msg, mem(ins.src_aid), ready);
-        pending_send_[ins.iid] = ins.msg;                 // completes with the receiver's pull
+        // device-direct: the box was staged by an elided copy -> publish the
+        // device allocation it came from; the receiver pulls over NVLink
+        Communicator::Mem src = mem(ins.src_aid);
+        for (uint64_t j : ins.deps) {
+            auto it = staged_.find(j);
+            if (it == staged_.end() || it->second.ins.dst_aid != ins.src_aid) continue;
+            bool inside = false;
+            for (const Box& b : it->second.ins.region) inside = inside || b.contains(ins.box);
+            if (!inside) continue;
+            src = mem(it->second.ins.src_aid);
+            it->second.consumed = true;
+            pending_send_[j].push_back(ins.msg);          // the source's readers: after the pull
+            break;
+        }
+        comm.post_send(cfg_.node, ins.msg, src, ready);
+        pending_send_[ins.iid].push_back(ins.msg);        // completes with the receiver's pull
         st_.bytes_copy[5] += uint64_t(ins.box.volume()) * es;
         break;
     }
@@ -180,21 +194,70 @@ void Executor::resolve_sends(const Instr& ins) {
     for (uint64_t j : ins.deps) {
         auto it = pending_send_.find(j);
         if (it == pending_send_.end()) continue;
-        cudaEvent_t e = cfg_.comm->wait_pulled(cfg_.node, it->second);
+        const std::vector<uint64_t> msgs = it->second;
         pending_send_.erase(it);
-        if (!e) {
-            if (!err_) {
-                errmsg_ = "communicator aborted";
-                err_ = E_STATE;
+        Token t = tok_.count(j) ? tok_[j] : Token{};
+        for (uint64_t msg : msgs) {
+            auto mt = msg_tok_.find(msg);
+            if (mt == msg_tok_.end()) {
+                cudaEvent_t e = cfg_.comm->wait_pulled(cfg_.node, msg);
+                if (!e) {
+                    if (!err_) {
+                        errmsg_ = "communicator aborted";
+                        err_ = E_STATE;
+                    }
+                    return;
+                }
+                const int sidx = S_HSIG;                  // device 0 of the node
+                set_dev(0);
+                check(cudaStreamWaitEvent(streams_[sidx].s, e, 0), "cudaStreamWaitEvent");
+                cudaEventDestroy(e);
+                mt = msg_tok_.emplace(msg, record(sidx)).first;
             }
-            return;
+            merge(t, mt->second);
         }
-        const int sidx = S_HSIG;                          // device 0 of the node
-        set_dev(0);
-        check(cudaStreamWaitEvent(streams_[sidx].s, e, 0), "cudaStreamWaitEvent");
-        cudaEventDestroy(e);
-        tok_[j] = record(sidx);
+        tok_[j] = t;
     }
+}
+
+// Before `ins` runs: an elided staging copy it depends on that no send has
+// consumed must exist for real (something other than a send reads its M1
+// bytes); before an allocation is freed, the staged copies sourced from it
+// are materialised (a later send from the same M1 bytes, with no new staging
+// copy, must find them there).
+void Executor::settle_staged(const Instr& ins) {
+    std::vector<uint64_t> todo;
+    for (uint64_t j : ins.deps) {
+        auto it = staged_.find(j);
+        if (it == staged_.end()) continue;
+        const bool send_of_it = ins.kind == IKind::Send && ins.src_aid == it->second.ins.dst_aid;
+        if (!send_of_it && !it->second.consumed) todo.push_back(j);
+    }
+    if (ins.kind == IKind::Free)
+        for (auto& kv : staged_)
+            if (kv.second.ins.src_aid == ins.aid) todo.push_back(kv.first);
+    if (ins.kind == IKind::Free)                          // the M1 allocation goes: nothing to keep
+        for (auto it = staged_.begin(); it != staged_.end();)
+            it = it->second.ins.dst_aid == ins.aid ? staged_.erase(it) : std::next(it);
+    std::sort(todo.begin(), todo.end());
+    todo.erase(std::unique(todo.begin(), todo.end()), todo.end());
+    for (uint64_t j : todo) materialize_staged(j);
+}
+
+void Executor::materialize_staged(uint64_t iid) {
+    auto it = staged_.find(iid);
+    if (it == staged_.end()) return;
+    const Instr c = it->second.ins;
+    staged_.erase(it);
+    const Token before = tok_.count(iid) ? tok_[iid] : Token{};
+    const Instr* saved = cur_ins_;
+    cur_ins_ = &c;
+    exec_copy(c);                                         // not in staged_ any more: really copies
+    cur_ins_ = saved;
+    Token t = tok_[iid];
+    merge(t, before);                                     // e.g. the pull that read the source
+    tok_[iid] = t;
+    st_.staging_materialized++;
 }
 
 }  // namespace cel

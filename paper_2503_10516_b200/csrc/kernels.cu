@@ -185,13 +185,7 @@ __global__ void __launch_bounds__(256, 8) copy_kernel(const __grid_constant__ Co
     if (a.peer) __threadfence_system();
 }
 
-// ------------------------------------------------------------------ copy (TMA bulk engine)
-// One elected thread per CTA drives the Tensor Memory Accelerator's bulk
-// copies (cp.async.bulk, SASS UBLKCP): global -> shared (completion on an
-// mbarrier) -> global, 8 stages x 16 KiB in flight per SM.  Used for local
-// copies whose segments are all 16-byte aligned (see launch_copy).
-constexpr int kTmaStages = 8;
-
+// ------------------------------------------------------------------ copy (TMA tensor maps)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -203,69 +197,122 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
         : "memory");
 }
 
-__global__ void __launch_bounds__(32) copy_kernel_tma(const __grid_constant__ CopyArgs a) {
-    extern __shared__ __align__(128) unsigned char stage_buf[];
-    __shared__ __align__(8) uint64_t bar[kTmaStages];
+constexpr int kTmStages = 6;                 // x 16 KiB tiles in flight per CTA
+constexpr int kTmPend = 3;                   // of which up to 3 stores still reading shared memory
+constexpr uint32_t kTmTileBytes = 16384;
+
+// One elected thread per CTA streams tiles: TMA tensor load into a stage of the
+// shared-memory ring (completion on the stage's mbarrier), then a TMA tensor
+// store of the stage into the destination map.  A stage is refilled one tile
+// later than the store that drains it, so a store and kTmStages - 1 loads are
+// in flight at any time.  Tiles t = blockIdx.x + k * gridDim.x.
+__global__ void __launch_bounds__(32) copy_kernel_tmap(const __grid_constant__ TmaCopyArgs a) {
+    extern __shared__ __align__(128) unsigned char tbuf[];
+    __shared__ __align__(8) uint64_t tbar[kTmStages];
     if (threadIdx.x != 0) return;
-    for (int k = 0; k < kTmaStages; ++k)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[k])) : "memory");
+    for (int k = 0; k < kTmStages; ++k)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tbar[k])) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    auto unit_addr = [&](uint64_t u, const char** src, char** dst, uint32_t* nbytes) {
+    struct Tile {
+        int s, x, y, z;
+    };
+    auto tile = [&](uint64_t t) {
         int s = 0;
-        while (s + 1 < a.nseg && a.seg[s + 1].units_begin <= u) ++s;
-        const CopySeg& g = a.seg[s];
-        const uint64_t lu = u - g.units_begin;
-        const uint64_t row_lin = lu / g.units_per_row;
-        const uint32_t chunk = uint32_t(lu - row_lin * g.units_per_row);
-        const uint64_t plane = row_lin / g.rows;
-        const uint64_t row = row_lin - plane * g.rows;
-        const uint64_t off = uint64_t(chunk) * kCopyUnit;
-        *src = g.src + plane * g.src_plane_stride + row * g.src_row_stride + off;
-        *dst = g.dst + plane * g.dst_plane_stride + row * g.dst_row_stride + off;
-        const uint64_t rem = g.row_bytes - off;
-        *nbytes = rem < kCopyUnit ? uint32_t(rem) : kCopyUnit;
+        while (s + 1 < a.nseg && a.seg[s + 1].tiles_begin <= t) ++s;
+        const TmaSeg& g = a.seg[s];
+        uint64_t l = t - g.tiles_begin;
+        Tile r;
+        r.s = s;
+        const uint32_t tx = uint32_t(l % g.tiles_x);
+        l /= g.tiles_x;
+        const uint32_t ty = uint32_t(l % g.tiles_y);
+        const uint32_t tz = uint32_t(l / g.tiles_y);
+        r.x = int(tx) * g.tw;
+        r.y = int(ty) * g.th;
+        r.z = int(tz);
+        return r;
     };
-    auto issue_load = [&](uint64_t u, int st) {
-        const char* src;
-        char* dst;
-        uint32_t nb;
-        unit_addr(u, &src, &dst, &nb);
-        const uint32_t b = smem_u32(&bar[st]);
-        const uint32_t d = smem_u32(stage_buf + size_t(st) * kCopyUnit);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(nb) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
-                     "l"(src), "r"(nb), "r"(b)
+    auto load = [&](uint64_t t, int st) {
+        const Tile q = tile(t);
+        const TmaSeg& g = a.seg[q.s];
+        const uint32_t b = smem_u32(&tbar[st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(uint32_t(g.tw * g.th * 4))
                      : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+                smem_u32(tbuf + size_t(st) * kTmTileBytes)),
+            "l"(reinterpret_cast<uint64_t>(&a.map[2 * q.s])), "r"(g.s0[0] + q.x), "r"(g.s0[1] + q.y), "r"(g.s0[2] + q.z),
+            "r"(b)
+            : "memory");
     };
-    // units of this CTA: u_k = blockIdx.x + k * gridDim.x
-    const uint64_t first = blockIdx.x, step = gridDim.x;
-    for (int k = 0; k < kTmaStages; ++k) {
-        const uint64_t u = first + uint64_t(k) * step;
-        if (u >= a.total_units) break;
-        issue_load(u, k);
-    }
-    for (uint64_t k = 0;; ++k) {
-        const uint64_t u = first + k * step;
-        if (u >= a.total_units) break;
-        const int st = int(k % kTmaStages);
-        mbar_wait(smem_u32(&bar[st]), uint32_t((k / kTmaStages) & 1));
-        const char* src;
-        char* dst;
-        uint32_t nb;
-        unit_addr(u, &src, &dst, &nb);
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                     "r"(smem_u32(stage_buf + size_t(st) * kCopyUnit)), "r"(nb)
+    auto store = [&](uint64_t t, int st) {
+        const Tile q = tile(t);
+        const TmaSeg& g = a.seg[q.s];
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                         reinterpret_cast<uint64_t>(&a.map[2 * q.s + 1])),
+                     "r"(g.d0[0] + q.x), "r"(g.d0[1] + q.y), "r"(g.d0[2] + q.z),
+                     "r"(smem_u32(tbuf + size_t(st) * kTmTileBytes))
                      : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        const uint64_t un = first + (k + kTmaStages) * step;
-        if (un < a.total_units) {
-            // the stage may be refilled once the store has read it out of shared memory
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            issue_load(un, st);
+    };
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    for (int k = 0; k < kTmStages; ++k) {
+        const uint64_t t = first + uint64_t(k) * step;
+        if (t >= a.total_tiles) break;
+        load(t, k);
+    }
+    // kTmPend stores may still be reading their stages: the stage refilled
+    // after storing tile k is that of tile k - (kTmPend - 1), whose store is
+    // kTmPend - 1 bulk groups old (waiting for the store just issued would
+    // serialise every tile on the store path's latency)
+    for (uint64_t k = 0;; ++k) {
+        const uint64_t t = first + k * step;
+        if (t >= a.total_tiles) break;
+        const int st = int(k % kTmStages);
+        mbar_wait(smem_u32(&tbar[st]), uint32_t((k / kTmStages) & 1));
+        store(t, st);
+        if (k + 1 >= uint64_t(kTmPend)) {
+            const uint64_t j = k + 1 - kTmPend;
+            const uint64_t tn = first + (j + kTmStages) * step;
+            if (tn < a.total_tiles) {
+                asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kTmPend - 1) : "memory");
+                load(tn, int(j % kTmStages));
+            }
         }
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ multicast gather
+// one store per 16 bytes to the multicast address (SASS: a
+// plain STG.E.128 -- the multicast mapping makes NVSwitch replicate it into
+// every bound allocation); the source reads with coherent loads because the
+// same kernel's multicast stores also land (with equal bytes) in its own chunk.
+__global__ void __launch_bounds__(256) mc_gather_kernel(const char* __restrict__ src, char* mc, uint64_t bytes,
+                                                        unsigned long long* flag, unsigned* ctr) {
+    const uint64_t n16 = bytes / 16;
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, nth = uint64_t(gridDim.x) * blockDim.x;
+    for (uint64_t i = tid; i < n16; i += nth) {
+        const uint4 v = *reinterpret_cast<const uint4*>(src + 16 * i);
+        asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc + 16 * i), "f"(__uint_as_float(v.x)),
+                     "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)), "f"(__uint_as_float(v.w))
+                     : "memory");
+    }
+    for (uint64_t i = n16 * 4 + tid; i < bytes / 4; i += nth) {
+        const uint32_t v = reinterpret_cast<const uint32_t*>(src)[i];
+        asm volatile("multimem.st.global.f32 [%0], %1;" ::"l"(mc + 4 * i), "f"(__uint_as_float(v)) : "memory");
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            *ctr = 0;                                       // the next launch on this stream starts at 0
+            __threadfence_system();
+            asm volatile("multimem.red.release.sys.global.add.u64 [%0], %1;" ::"l"(flag), "l"(1ull) : "memory");
+        }
+    }
 }
 
 // ------------------------------------------------------------------ helpers
@@ -1030,29 +1077,163 @@ void launch_oob_init(long long* rec, int n, cudaStream_t s) {
     oob_init_kernel<<<1, 64, 0, s>>>(rec, n);
 }
 
+namespace {
+EncodeFn encoder() {
+    static EncodeFn enc = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&enc), cudaEnableDefault, &q);
+    }
+    return enc;
+}
+
+// 3-D map of 4-byte words: dims (d0 words, d1, d2), byte strides (p1, p2),
+// box (tw, th, 1); cached (halo copies repeat every step)
+bool word_map(const char* base, const uint64_t dims[3], const uint64_t strides[2], int tw, int th, CUtensorMap* out) {
+    EncodeFn enc = encoder();
+    if (!enc) return false;
+    using Key = std::tuple<const char*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, int, int>;
+    static std::map<Key, CUtensorMap> cache;
+    const Key key{base, dims[0], dims[1], dims[2], strides[0], strides[1], tw, th};
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return true;
+    }
+    CUtensorMap m;
+    const cuuint64_t gd[3] = {dims[0], dims[1], dims[2]};
+    const cuuint64_t gs[2] = {strides[0], strides[1]};
+    const cuuint32_t box[3] = {cuuint32_t(tw), cuuint32_t(th), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<char*>(base), gd, gs, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    if (cache.size() > 4096) cache.clear();
+    cache[key] = m;
+    *out = m;
+    return true;
+}
+}  // namespace
+
+int tma_copy_add(TmaCopyArgs& args, const TmaBox& b) {
+    if (b.es % 4 != 0) return 0;
+    // the box as dims (planes, rows, words), each with its origin and byte
+    // stride in both allocations; normalised by (1) merging a dim into the
+    // next inner one where that inner one spans whole rows of both
+    // allocations, (2) folding dims of extent 1 into the base addresses
+    struct Dim {
+        int64_t n, so, dof, ss, ds;
+    };
+    const int64_t w = int64_t(b.es / 4), es = int64_t(b.es);
+    Dim d[3] = {{b.ext[0], b.so[0], b.dof[0], b.sn[1] * b.sn[2] * es, b.dn[1] * b.dn[2] * es},
+                {b.ext[1], b.so[1], b.dof[1], b.sn[2] * es, b.dn[2] * es},
+                {b.ext[2] * w, b.so[2] * w, b.dof[2] * w, 4, 4}};
+    int nd = 3;
+    const char* src = b.src;
+    char* dst = b.dst;
+    for (int k = nd - 2; k >= 0; --k) {            // (1) merge dim k into dim k + 1
+        Dim& in = d[k + 1];
+        if (in.so == 0 && in.dof == 0 && d[k].ss == in.n * in.ss && d[k].ds == in.n * in.ds) {
+            in.so = d[k].so * in.n;
+            in.dof = d[k].dof * in.n;
+            in.n *= d[k].n;
+            for (int j = k; j + 1 < nd; ++j) d[j] = d[j + 1];
+            --nd;
+        }
+    }
+    Dim o[3];
+    int no = 0;
+    for (int k = 0; k < nd; ++k) {                  // (2) fold extent-1 outer dims into the bases
+        if (k + 1 < nd && d[k].n == 1) {
+            src += d[k].so * d[k].ss;
+            dst += d[k].dof * d[k].ds;
+        } else {
+            o[no++] = d[k];
+        }
+    }
+    if (no == 1) return -1;                         // one run: the LSU kernel is at the copy peak
+    if (args.nseg >= kMaxTmaSegs) return 0;
+    if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return 0;
+    // TMA order: dim 0 = words (innermost), 1, 2; a missing dim 2 is extent 1
+    const Dim& x = o[no - 1];
+    const Dim& y = o[no - 2];
+    const Dim z = no == 3 ? o[0] : Dim{1, 0, 0, y.ss * (y.so + y.n), y.ds * (y.dof + y.n)};
+    for (const Dim* q : {&y, &z})
+        if (q->ss % 16 || q->ds % 16 || q->ss >= (int64_t(1) << 40) || q->ds >= (int64_t(1) << 40)) return 0;
+    const int64_t W = x.n;
+    const int tw = int(W >= 256 ? 256 : (W + 3) / 4 * 4);
+    int64_t th = int64_t(kTmTileBytes / 4) / tw;
+    if (th > y.n) th = y.n;
+    if (th > 256) th = 256;
+    // TMA moves the innermost dimension in 16-byte steps: measured on B200, a
+    // tile starting at a word that is not a multiple of 4 faulted (illegal
+    // instruction) and a store clipped at such a word wrote past it.  So the
+    // box must start on 16-byte boundaries of its rows in both allocations and
+    // end on one in the destination; other boxes stay on the LSU kernel
+    if ((x.so % 4) || (x.dof % 4) || ((x.dof + x.n) % 4) || x.dof + x.n < tw) return 0;
+    // maps cut at the box's far corner (the source's rounded up to 16 bytes:
+    // what a tile reads beyond the box is never stored): stores beyond it are
+    // clipped by TMA
+    const int64_t sx = (x.so + x.n + 3) / 4 * 4;
+    const uint64_t sd[3] = {uint64_t(sx < tw ? tw : sx), uint64_t(y.so + y.n), uint64_t(z.so + z.n)};
+    const uint64_t dd[3] = {uint64_t(x.dof + x.n), uint64_t(y.dof + y.n), uint64_t(z.dof + z.n)};
+    const uint64_t ss[2] = {uint64_t(y.ss), uint64_t(z.ss)};
+    const uint64_t ds[2] = {uint64_t(y.ds), uint64_t(z.ds)};
+    for (int k = 0; k < 3; ++k)
+        if (sd[k] >= (uint64_t(1) << 31) || dd[k] >= (uint64_t(1) << 31)) return 0;
+    if (ss[1] < ss[0] * sd[1] || ds[1] < ds[0] * dd[1] || ss[0] < 4 * sd[0] || ds[0] < 4 * dd[0]) return 0;
+    if (sd[1] < uint64_t(th) || dd[1] < uint64_t(th)) return 0;
+    const int s = args.nseg;
+    if (!word_map(src, sd, ss, tw, int(th), &args.map[2 * s]) || !word_map(dst, dd, ds, tw, int(th), &args.map[2 * s + 1]))
+        return 0;
+    TmaSeg& g = args.seg[s];
+    g.s0[0] = int32_t(x.so);
+    g.s0[1] = int32_t(y.so);
+    g.s0[2] = int32_t(z.so);
+    g.d0[0] = int32_t(x.dof);
+    g.d0[1] = int32_t(y.dof);
+    g.d0[2] = int32_t(z.dof);
+    g.tw = tw;
+    g.th = int32_t(th);
+    g.tiles_x = uint32_t((W + tw - 1) / tw);
+    g.tiles_y = uint32_t((y.n + th - 1) / th);
+    g.planes = uint32_t(z.n);
+    g.tiles_begin = args.total_tiles;
+    args.total_tiles += uint64_t(g.tiles_x) * g.tiles_y * g.planes;
+    args.nseg++;
+    return 1;
+}
+
+int launch_copy_tma(const TmaCopyArgs& a, cudaStream_t s) {
+    if (a.total_tiles == 0 || a.nseg == 0) return 0;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !attr_set[dev]) {   // function attributes are per device
+        cudaFuncSetAttribute(copy_kernel_tmap, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmStages * kTmTileBytes));
+        attr_set[dev] = true;
+    }
+    // two CTAs per SM (2 x 96 KiB of stages), persistent over the tiles
+    int64_t grid = int64_t(num_sms()) * 2;
+    if (int64_t(a.total_tiles) < grid) grid = int64_t(a.total_tiles);
+    copy_kernel_tmap<<<unsigned(grid), 32, kTmStages * kTmTileBytes, s>>>(a);
+    return 1;
+}
+
+int launch_mc_gather(const char* src, char* mc_dst, uint64_t bytes, unsigned long long* mc_flag, unsigned* ctr,
+                     cudaStream_t s) {
+    const uint64_t units = (bytes / 16 + 255) / 256;
+    int64_t grid = int64_t(units ? units : 1);
+    if (grid > int64_t(num_sms()) * 4) grid = int64_t(num_sms()) * 4;
+    mc_gather_kernel<<<unsigned(grid), 256, 0, s>>>(src, mc_dst, bytes, mc_flag, ctr);
+    return 1;
+}
+
 int launch_copy(const CopyArgs& a, cudaStream_t s) {
     if (a.total_units == 0 || a.nseg == 0) return 0;
-    static int use_tma = -1;
-    static bool attr_set[64] = {};
-    if (use_tma < 0) {
-        const char* e = getenv("CEL_COPY");
-        use_tma = (e && e[0] == 't') ? 1 : 0;
-    }
-    bool all16 = true;
-    for (int i = 0; i < a.nseg; ++i) all16 = all16 && a.seg[i].vec == 16 && !a.seg[i].narrow;
-    if (use_tma && all16 && !a.peer) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (dev >= 0 && dev < 64 && !attr_set[dev]) {   // function attributes are per device
-            cudaFuncSetAttribute(copy_kernel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 int(kTmaStages * kCopyUnit));
-            attr_set[dev] = true;
-        }
-        int64_t grid = num_sms();
-        if (int64_t(a.total_units) < grid) grid = int64_t(a.total_units);
-        copy_kernel_tma<<<unsigned(grid), 32, kTmaStages * kCopyUnit, s>>>(a);
-        return 1;
-    }
     // local copies: flat grid (one CTA per unit); peer pushes over NVLink: a
     // persistent grid of 8 CTAs per SM (fewer outstanding remote CTAs measured faster)
     int64_t grid = int64_t(a.total_units);

@@ -2,6 +2,7 @@
 // called by the executor; no torch types anywhere.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -32,6 +33,50 @@ struct CopyArgs {
     int peer;                  // destination is another GPU's memory: fence before exit
     uint64_t total_units;
 };
+
+// ---- TMA tensor-map copy of strided boxes (north_star: "TMA tensor-map box
+// loads and stores for 2D/3D strided regions").  Each box of a copy region is
+// described by two 3-D tensor maps of 4-byte words, one over the source and
+// one over the destination allocation, both cut at the box's far corner (TMA
+// stores clip there, so a tile hanging over the box edge never writes outside
+// it); a tile is (tw words x th rows x 1 plane), moved global -> shared ->
+// global by cp.async.bulk.tensor (SASS UTMALDG / UTMASTG).
+constexpr int kMaxTmaSegs = 8;
+struct TmaSeg {
+    int32_t s0[3];             // box origin in the source map (words, rows, planes)
+    int32_t d0[3];             // box origin in the destination map
+    uint32_t tiles_x, tiles_y, planes;
+    int32_t tw, th;            // tile = tensor-map box (tw words, th rows, 1 plane)
+    uint64_t tiles_begin;      // prefix sum of tiles (exclusive)
+};
+struct TmaCopyArgs {
+    CUtensorMap map[2 * kMaxTmaSegs];   // 2 s: source of segment s, 2 s + 1: its destination
+    TmaSeg seg[kMaxTmaSegs];
+    int nseg;
+    uint64_t total_tiles;
+};
+// One strided box of a local copy: allocation bases (16-byte aligned), their
+// extents and the box (planes, rows, elements), element size (multiple of 4).
+struct TmaBox {
+    const char* src;
+    char* dst;
+    int64_t sn[3], dn[3];      // allocation extents (planes, rows, elements)
+    int64_t so[3], dof[3];     // box origin inside each allocation
+    int64_t ext[3];            // box extent
+    uint32_t es;
+};
+// Adds the box to args (encoding / reusing its tensor maps): 1 added; -1 the
+// box is one contiguous run (not strided: left to the LSU kernel); 0 TMA
+// cannot express it (alignment, pitch or size limits) or args is full.
+int tma_copy_add(TmaCopyArgs& args, const TmaBox& b);
+int launch_copy_tma(const TmaCopyArgs& a, cudaStream_t s);
+
+// NVLS all-gather: `bytes` (multiple of 4; src and mc_dst
+// 16-byte aligned) from this device's chunk to the multicast address of the
+// set's allocations; the last CTA then adds 1 to the multicast flag (release,
+// system scope).  ctr: a zeroed per-device word the CTAs count on.
+int launch_mc_gather(const char* src, char* mc_dst, uint64_t bytes, unsigned long long* mc_flag, unsigned* ctr,
+                     cudaStream_t s);
 
 // ---- accessor (allocation pointer interpolated into the accessor)
 struct DBox {

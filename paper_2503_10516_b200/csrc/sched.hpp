@@ -410,6 +410,10 @@ private:
     uint64_t next_msg_ = 0;                           // P:L400 "locally unique message id"
     std::function<void(const Pilot&)> pilot_sink_;
     uint64_t coll_min_bytes_ = 1ull << 20;            // CEL_COLL_MIN_BYTES: smallest per-source gather run as NCCL
+public:
+    // the executor runs gathers of any size as a collective (multicast): flag them all
+    void set_coll_min_bytes(uint64_t b) { coll_min_bytes_ = b; }
+private:
     uint32_t next_bid_ = 0;
     bool shut_ = false;
 };

@@ -106,3 +106,26 @@ def test_degenerate_shapes(cel):
     for prog, N, D in cases:
         for mode in ("none", "auto"):
             run_both(cel, prog, N, D, mode)
+
+
+@pytest.mark.parametrize("direct", [True, False])
+def test_device_direct_sends(cel, direct, monkeypatch):
+    """SURVEY NEXT-1 as written (the paper's RDMA future work): a
+    push's staging copy into M1 is not executed; its sends publish the
+    device allocation and the receiver pulls from it (NVLink between GPUs).
+    Logs are unchanged (the instruction graph still has the staging copy);
+    bytes bit-exact; CEL_DIRECT_SENDS=0 stages through M1 as the paper does."""
+    if not direct:
+        monkeypatch.setenv("CEL_DIRECT_SENDS", "0")
+    n = torch.cuda.device_count()
+    devs2 = [0, 1 % n]
+    for prog, N, D, devs in ((P.wavesim(1024, 7, rows=300), 2, 1, devs2), (P.nbody(2048, 2), 2, 1, devs2),
+                             (P.nbody(512, 2, host_init=True), 2, 2, None), (P.rsim(512, 10), 3, 1, None),
+                             (P.jacobi3d(20, 3), 2, 2, None)):
+        st = run_both(cel, prog, N, D, devices=devs)
+        if direct:
+            assert st["staging_elided"] > st["staging_materialized"], (prog["name"], st["staging_elided"])
+        else:
+            assert st["staging_elided"] == 0
+    for s in range(8):
+        run_both(cel, P.random_program(6400 + s), 2 + s % 2, 1 + s % 2, ["none", "auto"][s % 2])

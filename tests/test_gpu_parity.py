@@ -158,6 +158,26 @@ def test_forced_peer_path(cel, G, dma, monkeypatch):
         run_both(cel, P.random_program(7100 + 11 * G + s), G, arena=32 << 20)
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_tma_tensor_map_copies(cel, G, monkeypatch):
+    """CEL_COPY=tma: strided boxes of copies within a GPU whose rows start and
+    end on 16-byte boundaries (3-D y-faces, resize copies of rows at a pitch)
+    move by TMA tensor maps (UTMALDG / UTMASTG, tiles clipped at the box edge
+    by maps cut there); the rest of each program stays on the LSU kernel;
+    bit-exact with the oracle's bytes and log."""
+    monkeypatch.setenv("CEL_COPY", "tma")
+    monkeypatch.setenv("CEL_NO_GROW", "1")
+    st = run_both(cel, P.jacobi3d(36, 4), G).final_stats
+    assert (st["tma_copy_launches"] > 0) == (G == 4)          # 2 x 1 tiles have contiguous z-faces only
+    run_both(cel, P.jacobi3d(20, 3), G + 1)
+    # 2-D tiles: row halos are one run, column halos one element wide (TMA
+    # needs 16-byte aligned row segments): these stay on the LSU kernel
+    run_both(cel, P.wavesim(515, 5, rows=130, split="2d", mapper="neighborhood_axes"), G)
+    run_both(cel, P.wavesim(516, 4, rows=260, split="2d"), G, "none")
+    for s in range(6):
+        run_both(cel, P.random_program(7300 + 11 * G + s), G, "none", arena=32 << 20)
+
+
 def test_all_gather_collective_vs_pushes(cel, monkeypatch):
     """§8 a7: the same programs with the all-gather copy sets run as NCCL
     broadcasts and as peer pushes give identical bytes."""
@@ -179,6 +199,33 @@ def test_all_gather_collective_vs_pushes(cel, monkeypatch):
                 assert np.array_equal(arr[defined], exp[k][defined]), (prog["name"], coll, k)
 
 
+def test_all_gather_multicast(cel, monkeypatch):
+    """with CEL_COLL_MC=1 (one process, distinct GPUs, VMM
+    allocations) every all-gather set runs as multicast stores through one
+    NVLS object bound to the G receiving allocations, completed by a
+    multicast flag: RSim rows (84 KB-class sets) bit-exact against the oracle,
+    and N-body at 2^17 bodies (2 MiB of positions per device) bit-identical to
+    the single-GPU run of the same program (the oracle-sampled path)."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    monkeypatch.setenv("CEL_COLL_MC", "1")
+    devs = list(range(n))
+    st = run_both(cel, P.rsim(8000, 80), n, devices=devs).final_stats
+    assert st["coll_multicast"] == st["gather_sets"] > 0
+    st = run_both(cel, P.rsim(8000, 40), n, "none", devices=devs).final_stats
+    assert st["coll_multicast"] > 0
+    N = 1 << 17
+    prog = P.nbody(N, 2)
+    rt = cel.Runtime(n, cuda_devices=devs, arena_bytes=256 << 20)
+    got = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
+    monkeypatch.setenv("CEL_COLL_MC", "0")
+    rt1 = cel.Runtime(1, arena_bytes=256 << 20)
+    ref = [r[1] for r in run_program(rt1, prog) if r[0] == "read"]
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("grow", [True, False])
 def test_rsim_in_place_growth(cel, grow, monkeypatch):
     """Without lookahead every RSim row resizes the allocation (alloc -> copy ->
@@ -191,6 +238,38 @@ def test_rsim_in_place_growth(cel, grow, monkeypatch):
         assert st["copies_resize"] > 0
         assert (st["copies_elided"] > 0) == grow
         assert st["copies_elided"] <= st["copies_resize"]
+
+
+@pytest.mark.parametrize("vmm", [True, False])
+def test_vmm_growth_interleaved(cel, vmm, monkeypatch):
+    """SURVEY NEXT-3 / P:L549-556: two buffers growing in turn without
+    lookahead.  The arena can only grow an allocation in place when the range
+    right after it is free, which the other buffer's allocation blocks: every
+    resize copies.  With VMM (single process) a resize that cannot grow in
+    the arena gets an allocation with its own address range reserved up to
+    the buffer's end, so after one real copy per buffer every later resize
+    maps granules behind the rows and its copy is elided.  Same instruction
+    log and bytes either way."""
+    if not vmm:
+        monkeypatch.setenv("CEL_NO_VMM", "1")
+    st = run_both(cel, P.rsim_pair(600000, 10), 1, "none", arena=512 << 20).final_stats
+    info = (st["copies_resize"], st["copies_elided"], st["vmm_maps"])
+    assert st["copies_resize"] > 0, info
+    # (a resize copies one fragment per original producer of the old rows, R9)
+    if vmm:
+        assert st["copies_elided"] >= 0.8 * st["copies_resize"] and st["vmm_maps"] > 2, info
+    else:
+        assert st["copies_elided"] <= 0.5 * st["copies_resize"] and st["vmm_maps"] == 0, info
+    st = run_both(cel, P.rsim(600000, 12), 2, "none", arena=512 << 20).final_stats
+    info = (st["copies_resize"], st["copies_elided"], st["vmm_maps"])
+    assert st["copies_elided"] >= 0.8 * st["copies_resize"], info
+
+
+def test_arena_overflow_maps_vmm(cel):
+    """The arena size caps nothing in one process: allocations that do not fit
+    the arena are VMM-mapped (here a 64 MiB arena and two 128 MiB fields)."""
+    st = run_both(cel, P.wavesim(8192, 3, rows=4096), 2, arena=64 << 20).final_stats
+    assert st["vmm_maps"] > 0
 
 
 def test_physical_multi_gpu(cel, monkeypatch):

@@ -150,6 +150,24 @@ def rsim(W=84000, T=1024, seed=4):
     return {"name": "rsim", "buffers": bufs, "ops": ops}
 
 
+def rsim_pair(W, T, seed=4):
+    """Two RSim-shaped buffers growing in turn (row t of A, then row t of B):
+    without lookahead every task resizes its buffer's allocation while the
+    other buffer's allocation sits right behind it."""
+    ops = []
+    for b in (0, 1):
+        ops.append(_task(1, full([W]), "fill_hash", [(b, "write", ("remap", ([0, 0], [1, 0]), (-1, 0, -1)))],
+                         {"seed": seed + b}))
+    for t in range(1, T):
+        for b in (0, 1):
+            ops.append(_task(1, full([W]), "rsim_row",
+                             [(b, "read", ("fixed", ([0, 0], [t, W]))),
+                              (b, "write", ("remap", ([t, 0], [t + 1, 0]), (-1, 0, -1)))], {"t": t}))
+    ops += [("read", 0, full([T, W])), ("read", 1, full([T, W]))]
+    bufs = [{"dims": 2, "extent": [T, W], "elem_size": 4, "host_init": None} for _ in range(2)]
+    return {"name": "rsim_pair", "buffers": bufs, "ops": ops}
+
+
 # ---------------------------------------------------------------- C5
 def jacobi_step(n, k):
     a, b = (0, 1) if k % 2 == 0 else (1, 0)
