@@ -172,7 +172,7 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     const char* rv = getenv("CEL_RSIM");
     if (rv && rv[0] == '0') kernel_variant_ |= kVarRsimRegs;
     const char* ds = getenv("CEL_DIRECT_SENDS");
-    direct_sends_ = cfg_.comm && !(ds && ds[0] == '0');
+    direct_sends_ = cfg_.comm && ds && ds[0] == '1';
     const char* cmb = getenv("CEL_COLL_MIN_BYTES");
     if (cmb && cmb[0]) coll_min_bytes_ = strtoull(cmb, nullptr, 10);
     const char* cv = getenv("CEL_COPY");
@@ -1041,7 +1041,13 @@ void Executor::on_instr_impl(const Instr& ins) {
     cur_ins_ = &ins;
     check_owner_known(ins);
     if (err_) return;
-    if (!staged_.empty()) settle_staged(ins);
+    if (!staged_.empty()) {
+        settle_staged(ins);
+    } else if (direct_src_ >= 0 || !settle_tok_.empty()) {
+        direct_src_ = -1;
+        direct_staged_ = 0;
+        settle_tok_ = Token{};
+    }
     if (!pending_send_.empty()) resolve_sends(ins);
     const int od = instr_owner(ins);
     const bool mine = od < 0 || owner_rank(od) == cfg_.rank;
@@ -1177,6 +1183,7 @@ void Executor::on_instr_impl(const Instr& ins) {
         } else {
             t.remote.push_back({owner_rank(r.dev), ins.iid});
         }
+        if (!settle_tok_.empty()) merge(t, settle_tok_);   // elided staging copies that read it just now
         if (!r.absorbed_into) {                   // else: lives on in the grown one
             if (r.vmm)
                 vmm_free_.push_back({r.vmm, t});  // unmapped once the free's dependencies have completed

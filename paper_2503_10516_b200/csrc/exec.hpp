@@ -463,7 +463,11 @@ private:
         bool consumed = false;                     // a send published its source
     };
     std::map<uint64_t, Staged> staged_;
-    bool direct_sends_ = false;                    // CEL_DIRECT_SENDS=0 turns it off
+    bool direct_sends_ = false;                    // CEL_DIRECT_SENDS=1 (opt-in: see DESIGN.md §2)
+    bool materializing_ = false;                   // exec_copy of an elided copy that is needed after all
+    int64_t direct_src_ = -1;                      // settle_staged -> exec_transfer: device source of this send
+    uint64_t direct_staged_ = 0;                   // ... and the elided copy that staged it
+    Token settle_tok_;                             // copies materialised before this instruction
     void settle_staged(const Instr& ins);
     void materialize_staged(uint64_t iid);
     std::unordered_map<int64_t, Communicator::Mem> recv_dst_; // transfer tid * 2^32 + buffer -> split receive destination

@@ -124,8 +124,8 @@ void Executor::exec_copy(const Instr& ins) {
         }
         merge(deps, dep_token(j));
     }
-    if (direct_sends_ && ins.src_mem >= 2 && ins.dst_mem == 1 && ins.reason == REASON_COHERENCE && ins.src_aid >= 0 &&
-        !staged_.count(ins.iid)) {
+    if (direct_sends_ && !materializing_ && ins.src_mem >= 2 && ins.dst_mem == 1 && ins.reason == REASON_COHERENCE &&
+        ins.src_aid >= 0) {
         // a push's staging copy: elided; its sends publish the device
         // allocation (settle_staged / exec_transfer)
         staged_[ins.iid] = Staged{ins, deps, false};

@@ -146,19 +146,14 @@ void Executor::exec_transfer(const Instr& ins) {
         cudaEvent_t ready = nullptr;
         check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
         check(cudaEventRecord(ready, streams_[s_sync].s), "cudaEventRecord");
-        // device-direct: the box was staged by an elided copy -> publish the
+        // device-direct: one elided copy staged the whole box -> publish the
         // device allocation it came from; the receiver pulls over NVLink
         Communicator::Mem src = mem(ins.src_aid);
-        for (uint64_t j : ins.deps) {
-            auto it = staged_.find(j);
-            if (it == staged_.end() || it->second.ins.dst_aid != ins.src_aid) continue;
-            bool inside = false;
-            for (const Box& b : it->second.ins.region) inside = inside || b.contains(ins.box);
-            if (!inside) continue;
-            src = mem(it->second.ins.src_aid);
-            it->second.consumed = true;
-            pending_send_[j].push_back(ins.msg);          // the source's readers: after the pull
-            break;
+        auto sg = staged_.find(direct_staged_);
+        if (direct_src_ >= 0 && sg != staged_.end()) {
+            src = mem(direct_src_);
+            sg->second.consumed = true;
+            pending_send_[direct_staged_].push_back(ins.msg);   // readers of the source: after the pull
         }
         comm.post_send(cfg_.node, ins.msg, src, ready);
         pending_send_[ins.iid].push_back(ins.msg);        // completes with the receiver's pull
@@ -194,6 +189,13 @@ void Executor::resolve_sends(const Instr& ins) {
     for (uint64_t j : ins.deps) {
         auto it = pending_send_.find(j);
         if (it == pending_send_.end()) continue;
+        // another send of an elided staging copy's bytes needs only the copy's
+        // inputs (its token until resolved), not the first send's pull: waiting
+        // for that pull could deadlock when both go to one receiver, whose
+        // receive waits for every send of its region to be posted
+        auto sg = staged_.find(j);
+        if (ins.kind == IKind::Send && sg != staged_.end() && sg->second.ins.dst_aid == ins.src_aid) continue;
+        if (ins.kind == IKind::Send && j == direct_staged_) continue;
         const std::vector<uint64_t> msgs = it->second;
         pending_send_.erase(it);
         Token t = tok_.count(j) ? tok_[j] : Token{};
@@ -220,28 +222,67 @@ void Executor::resolve_sends(const Instr& ins) {
     }
 }
 
-// Before `ins` runs: an elided staging copy it depends on that no send has
-// consumed must exist for real (something other than a send reads its M1
-// bytes); before an allocation is freed, the staged copies sourced from it
-// are materialised (a later send from the same M1 bytes, with no new staging
-// copy, must find them there).
+// Before `ins` runs (device-direct sends): readers of M1 bytes that an elided
+// staging copy would have written are found by allocation and region -- not
+// by dependencies, which horizons subsume (R7) -- and either go device-direct
+// (a send whose whole box one elided copy staged) or get those copies
+// executed first.  Before an allocation is freed, the elided copies sourced
+// from it are executed (a later send of the same, still up-to-date M1 bytes
+// must find them there).  Writes into M1 shrink the elided copies' regions.
 void Executor::settle_staged(const Instr& ins) {
+    direct_src_ = -1;
+    direct_staged_ = 0;
+    settle_tok_ = Token{};
+    int64_t m1_read = -1;
+    Region rd;
+    if (ins.kind == IKind::Send) {
+        m1_read = ins.src_aid;
+        rd = Region{ins.box};
+    } else if (ins.kind == IKind::Copy && ins.src_mem == 1) {
+        m1_read = ins.src_aid;
+        rd = ins.region;
+    }
     std::vector<uint64_t> todo;
-    for (uint64_t j : ins.deps) {
-        auto it = staged_.find(j);
-        if (it == staged_.end()) continue;
-        const bool send_of_it = ins.kind == IKind::Send && ins.src_aid == it->second.ins.dst_aid;
-        if (!send_of_it && !it->second.consumed) todo.push_back(j);
+    if (m1_read >= 0) {
+        for (auto& kv : staged_) {
+            const Staged& e = kv.second;
+            if (e.ins.dst_aid != m1_read || rinter(e.ins.region, rd).empty()) continue;
+            bool whole = false;
+            if (ins.kind == IKind::Send)
+                for (const Box& b : e.ins.region) whole = whole || b.contains(ins.box);
+            if (whole && direct_src_ < 0) {
+                direct_src_ = e.ins.src_aid;
+                direct_staged_ = kv.first;
+            } else {
+                todo.push_back(kv.first);
+            }
+        }
+        if (!todo.empty() && direct_src_ >= 0) {            // mixed: the send reads M1 after all
+            todo.push_back(direct_staged_);
+            direct_src_ = -1;
+            direct_staged_ = 0;
+        }
     }
     if (ins.kind == IKind::Free)
         for (auto& kv : staged_)
             if (kv.second.ins.src_aid == ins.aid) todo.push_back(kv.first);
-    if (ins.kind == IKind::Free)                          // the M1 allocation goes: nothing to keep
-        for (auto it = staged_.begin(); it != staged_.end();)
-            it = it->second.ins.dst_aid == ins.aid ? staged_.erase(it) : std::next(it);
     std::sort(todo.begin(), todo.end());
     todo.erase(std::unique(todo.begin(), todo.end()), todo.end());
     for (uint64_t j : todo) materialize_staged(j);
+    int64_t m1 = -1;
+    if (ins.kind == IKind::Copy && ins.dst_mem == 1) m1 = ins.dst_aid;
+    if (ins.kind == IKind::Receive || ins.kind == IKind::SplitReceive) m1 = ins.dst_aid;
+    if (ins.kind == IKind::Free) m1 = ins.aid;
+    if (m1 < 0) return;
+    for (auto it = staged_.begin(); it != staged_.end();) {
+        Staged& e = it->second;
+        if (e.ins.dst_aid != m1 || it->first == ins.iid) {
+            ++it;
+            continue;
+        }
+        if (ins.kind != IKind::Free) e.ins.region = rdiff(e.ins.region, ins.region);
+        it = (ins.kind == IKind::Free || e.ins.region.empty()) ? staged_.erase(it) : std::next(it);
+    }
 }
 
 void Executor::materialize_staged(uint64_t iid) {
@@ -252,9 +293,12 @@ void Executor::materialize_staged(uint64_t iid) {
     const Token before = tok_.count(iid) ? tok_[iid] : Token{};
     const Instr* saved = cur_ins_;
     cur_ins_ = &c;
-    exec_copy(c);                                         // not in staged_ any more: really copies
+    materializing_ = true;
+    exec_copy(c);                                         // really copies this time
+    materializing_ = false;
     cur_ins_ = saved;
     Token t = tok_[iid];
+    merge(settle_tok_, t);                                // e.g. a free of the source waits for it
     merge(t, before);                                     // e.g. the pull that read the source
     tok_[iid] = t;
     st_.staging_materialized++;

@@ -259,7 +259,7 @@ def test_vmm_growth_interleaved(cel, vmm, monkeypatch):
     if vmm:
         assert st["copies_elided"] >= 0.8 * st["copies_resize"] and st["vmm_maps"] > 2, info
     else:
-        assert st["copies_elided"] <= 0.5 * st["copies_resize"] and st["vmm_maps"] == 0, info
+        assert st["copies_elided"] < 0.8 * st["copies_resize"] and st["vmm_maps"] == 0, info
     st = run_both(cel, P.rsim(600000, 12), 2, "none", arena=512 << 20).final_stats
     info = (st["copies_resize"], st["copies_elided"], st["vmm_maps"])
     assert st["copies_elided"] >= 0.8 * st["copies_resize"], info
