@@ -946,7 +946,29 @@ void Executor::drain() {
     done_cv_.wait(l, [&] { return marks_done_ >= m; });
 }
 
+// Thread pinning ("pinned threads"): the executor
+// thread, which spins for new instructions, gets a core of its own -- the
+// process's affinity set counted from the top, one per rank / virtual node --
+// when the set has at least 4 cores.  CEL_PIN=0 leaves scheduling to the OS.
+void Executor::pin_thread() {
+    const char* pin = getenv("CEL_PIN");
+    if (pin && pin[0] == '0') return;
+    cpu_set_t m;
+    CPU_ZERO(&m);
+    if (sched_getaffinity(0, sizeof m, &m) != 0) return;
+    std::vector<int> cores;
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+        if (CPU_ISSET(c, &m)) cores.push_back(c);
+    if (cores.size() < 4) return;
+    const int k = (cfg_.rank + cfg_.node) % int(cores.size());
+    cpu_set_t one;
+    CPU_ZERO(&one);
+    CPU_SET(cores[cores.size() - 1 - size_t(k)], &one);
+    if (pthread_setaffinity_np(pthread_self(), sizeof one, &one) == 0) pinned_core_ = cores[cores.size() - 1 - size_t(k)];
+}
+
 void Executor::thread_main() {
+    pin_thread();
     for (;;) {
         Item it;
         {

@@ -397,6 +397,8 @@ private:
     };
     void push(Item&& it);
     void thread_main();
+    void pin_thread();
+    int pinned_core_ = -1;
     std::thread thr_;
     bool threaded_ = false;
     std::deque<Item> q_;

@@ -11,6 +11,8 @@
 #include <cstring>
 #include <dlfcn.h>
 #include <immintrin.h>
+#include <pthread.h>
+#include <sched.h>
 #include <nccl.h>
 
 #include "../../include/cel.h"

@@ -4,9 +4,13 @@ nvidia-smi topo -m > gpurun_out/topo.txt 2>&1; head -8 gpurun_out/topo.txt
 timeout 300 python tools/peer_peak.py > gpurun_out/peer_peak.json 2>&1; cat gpurun_out/peer_peak.json
 timeout 1200 python -m pytest tests -m gpu -q --timeout 600 -k "multicast or physical_multi or collective_vs or distinct_gpus or multiprocess_gpu or direct" > gpurun_out/pytest_mgpu.log 2>&1
 echo "pytest mgpu rc=$?"; tail -25 gpurun_out/pytest_mgpu.log
+timeout 600 python bench.py --gpus 1 --steps 1000 --warmup 20 --no-e2e --no-cpu-baseline --no-copy > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err
+echo "bench N=1 rc=$?"; python -c "import json; d=json.loads(open('gpurun_out/bench_n1.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['roofline']['kernel_share_of_step'], d['clocks'])"
 for N in 2 4; do
-  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2950$N bench.py --gpus $N --steps 1000 --warmup 20 --no-e2e > gpurun_out/bench_n$N.json 2> gpurun_out/bench_n$N.err
-  echo "bench N=$N rc=$?"; python -c "import json; d=json.loads(open('gpurun_out/bench_n$N.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['roofline']['kernel_share_of_step'], d['clocks'])"
+  for pin in 1 0; do
+    CEL_PIN=$pin timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 295$N$pin bench.py --gpus $N --steps 1000 --warmup 20 --no-e2e > gpurun_out/bench_n${N}_pin$pin.json 2> gpurun_out/bench_n${N}_pin$pin.err
+    echo "bench N=$N pin=$pin rc=$?"; python -c "import json; d=json.loads(open('gpurun_out/bench_n${N}_pin$pin.json').read().strip().splitlines()[-1]); print(d['value'], d['roofline']['frac'], d['roofline']['kernel_share_of_step'], d['clocks'], d['host_submit_us_per_step'])"
+  done
 done
 for cfg in "--collective 0" "--collective 1" "--collective 1 MC"; do
   mc=0; case "$cfg" in *MC*) mc=1;; esac; c=${cfg% MC}
