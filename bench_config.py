@@ -158,6 +158,10 @@ def main():
             "value": steps / (ms / 1e3), "unit": "rows/s" if args.workload == "rsim" else "steps/s",
             "ms_per_step": ms / steps, "host_ms_per_step": host_s * 1e3 / steps,
             "gen_us_per_step": (st1["gen_ns"] - st0["gen_ns"]) / 1e3 / steps,
+            "exec_us_per_step": {k[8:]: (st1[k] - st0[k]) / 1e3 / steps for k in
+                                 ("exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon",
+                                  "exec_ns_epoch")},
+            "coll_p2p": st1["coll_p2p"] - st0["coll_p2p"],
             "gpu_launches": st1["kernel_launches"] - st0["kernel_launches"],
             "collective": bool(args.collective),
             "coll_groups": st1["coll_groups"] - st0["coll_groups"],

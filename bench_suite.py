@@ -108,11 +108,18 @@ def c4(T=1024, W=84000):
     res = {}
     # "none" without in-place growth is the paper's comparison (resize chains
     # executed); "none_grow" shows what the executor's growth recovers
-    for label, mode, grow in (("auto", "auto", True), ("none", "none", False), ("none_grow", "none", True)):
+    # none_grow: in-place growth as configured (arena extension, else VMM
+    # mapping in one process); none_grow_arena: arena extension only
+    for label, mode, grow in (("auto", "auto", True), ("none", "none", False), ("none_grow", "none", True),
+                              ("none_grow_arena", "none", True)):
         if grow:
             os.environ.pop("CEL_NO_GROW", None)
         else:
             os.environ["CEL_NO_GROW"] = "1"
+        if label == "none_grow_arena":
+            os.environ["CEL_NO_VMM"] = "1"
+        else:
+            os.environ.pop("CEL_NO_VMM", None)
         rt = cel.Runtime(1, lookahead=mode, arena_bytes=4 << 30)
         prog = P.rsim(W, T)
         rt.buffer_create(2, [T, W], 4)
@@ -126,10 +133,12 @@ def c4(T=1024, W=84000):
         km = prof.get("rsim_row", (0.0, 0))[0] / 1e3
         kbytes = sum(t * W * 4 for t in range(1, T)) + (T - 1) * W * 4
         res[label] = {"seconds": dt, "resize_copies_elided": st["copies_elided"], "steps_per_s": T / dt, "alloc": st["n_alloc"], "flushes": st["flushes"],
+                     "vmm_maps": st["vmm_maps"],
                      "resize_copies": st["copies_resize"], "resize_bytes": st["bytes_resize"],
                      "resize_copy_GBps": (2 * st["bytes_resize"] / (cm[0] / 1e3) / 1e9) if cm[0] else None,
                      "kernel_GBps": kbytes / km / 1e9 if km else None, "profile_ms": {k: v[0] for k, v in prof.items()}}
     os.environ.pop("CEL_NO_GROW", None)
+    os.environ.pop("CEL_NO_VMM", None)
     res["speedup_auto_vs_none"] = res["none"]["seconds"] / res["auto"]["seconds"]
     res["speedup_auto_vs_none_grow"] = res["none_grow"]["seconds"] / res["auto"]["seconds"]
     return res

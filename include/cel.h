@@ -209,6 +209,7 @@ typedef struct cel_stats_s {
     uint64_t staging_elided;              /* virtual-node mode: push staging copies (device -> M1) not executed:
                                              their sends published the device allocation (device-direct) */
     uint64_t staging_materialized;        /* ... of which executed late (their M1 bytes were needed after all) */
+    uint64_t coll_p2p;                    /* all-gather sets run as P2P gather kernels (stores into every receiver) */
 } cel_stats_t;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

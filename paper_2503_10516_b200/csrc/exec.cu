@@ -295,7 +295,9 @@ int Executor::init(std::string* err) {
     arenas_.resize(G_);
     uint64_t arena = cfg_.arena_bytes ? cfg_.arena_bytes : (16ull << 30);
     const uint64_t sig_bytes = cfg_.world > 1 ? uint64_t(cfg_.world) * kRing * 8 : 0;
-    const uint64_t data_off = round_up(sig_bytes, 2u << 20);
+    gather_off_ = round_up(sig_bytes, 4096);                  // then 4 KiB of gather counters
+    const uint64_t data_off = round_up(gather_off_ + 4096, 2u << 20);
+    gather_exp_.assign(G_, 0);
     // peer access between distinct physical devices (NVLink 5 / NVSwitch);
     // virtual-node mode: with every GPU of the process (device-direct sends
     // are pulled from another node's device memory)
@@ -343,7 +345,7 @@ int Executor::init(std::string* err) {
             *err = buf;
             return E_OOM;
         }
-        if (sig_bytes) cudaMemset(A.base, 0, sig_bytes);
+        cudaMemset(A.base, 0, gather_off_ + 4096);         // flags and gather counters start at 0
     }
     if (cfg_.world > 1) {
         int v = 0;
@@ -393,6 +395,15 @@ int Executor::init(std::string* err) {
         if (cv && cv[0] == '0') distinct = false;
         coll_ = distinct && g_nccl.load();
         // NVLS multicast gathers: one process, distinct GPUs, VMM allocations
+        const char* p2 = getenv("CEL_COLL_P2P");
+        p2p_gather_ = !(p2 && p2[0] == '0');
+        if (p2p_gather_) {                                    // receivers wait with 64-bit stream memory ops
+            g_drv.load();
+            int v = 0;
+            if (g_drv.devattr)
+                g_drv.devattr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, CUdevice(phys_[owned(0) ? 0 : cfg_.rank]));
+            p2p_gather_ = v != 0 && g_drv.wait64;
+        }
         const char* mc = getenv("CEL_COLL_MC");
         mc_enabled_ = distinct && vmm_ && cfg_.world == 1 && mc && mc[0] == '1';
         if (coll_ && cfg_.world > 1 && cfg_.rank == 0) {
@@ -1076,7 +1087,7 @@ void Executor::on_instr_impl(const Instr& ins) {
     if (trace_)
         fprintf(stderr, "[cel r%d] iid %llu kind %d owner %d %s\n", cfg_.rank, (unsigned long long)ins.iid,
                 int(ins.kind), od, mine ? "exec" : "skip");
-    if ((coll_ || mc_enabled_) && ins.kind == IKind::Copy && ins.coll_n) {
+    if ((coll_ || mc_enabled_ || p2p_gather_) && ins.kind == IKind::Copy && ins.coll_n) {
         // §8 a7: a member of an all-gather copy set.  Every rank takes part;
         // the source's and the destination's ranks each wait for the member's
         // dependencies, so the other ranks signal theirs to both.
@@ -1156,7 +1167,8 @@ void Executor::on_instr_impl(const Instr& ins) {
             vreg = grow->vmm;                                           // 1
             grow->absorbed_into = ins.aid;
             if (mine) merge(t, grow->use);
-        } else if (grow && !grow->vmm && arena(dev).extend(grow->off, grow->bytes, bytes, &t)) {
+        } else if (grow && !grow->vmm && !(vmm_ok && mc_enabled_ && bytes >= vmm_gran_) &&
+                   arena(dev).extend(grow->off, grow->bytes, bytes, &t)) {
             // 2: the grown allocation's users write memory the old one's readers
             // may still read: follow every local use of the old allocation
             // (remote ranks only write it, and those writes reach the new
@@ -1166,6 +1178,8 @@ void Executor::on_instr_impl(const Instr& ins) {
             if (mine) merge(t, grow->use);
         } else if (vmm_ok && grow && vmm_new(true)) {
             // 3
+        } else if (vmm_ok && mc_enabled_ && bytes >= vmm_gran_ && vmm_new(false)) {
+            // multicast gathers bind VMM memory: large allocations are mapped
         } else if (!arena(dev).alloc(bytes, &off, &t) && !(vmm_ok && vmm_new(false))) {
             char buf[200];
             snprintf(buf, sizeof buf, "device %d: cannot allocate %.3f GiB (arena exhausted%s)", dev,

@@ -123,6 +123,7 @@ struct ExecStats {
     uint64_t tma_copy_launches = 0;    // ... of which TMA tensor-map copy kernels
     uint64_t vmm_maps = 0, vmm_mapped_bytes = 0;   // VMM: physical granule mappings and their bytes
     uint64_t coll_multicast = 0;                    // all-gather sets run as NVLS multicast stores
+    uint64_t coll_p2p = 0;                          // ... as P2P gather kernels
     uint64_t staging_elided = 0, staging_materialized = 0;   // device-direct sends (virtual-node mode)
     uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
@@ -192,7 +193,7 @@ public:
     void profile_reset();
     int device_count() const { return G_; }
     // multicast gathers run sets of any size: the scheduler should flag small ones too
-    bool gathers_any_size() const { return mc_enabled_; }
+    bool gathers_any_size() const { return mc_enabled_ || p2p_gather_; }
     int owned(int d) const { return owner_rank(d) == cfg_.rank; }
     void sync_all();
 
@@ -347,6 +348,10 @@ private:
     void mc_teardown();
     void mc_forget(const VmmRegion* r);
     bool exec_coll_mc(const std::vector<Instr>& m);
+    bool exec_coll_p2p(const std::vector<Instr>& m);
+    bool p2p_gather_ = false;                     // gather sets as P2P gather kernels (CEL_COLL_P2P=0: off)
+    uint64_t gather_off_ = 0;                     // per device arena: gather counter word (+64: CTA counter)
+    std::vector<uint64_t> gather_exp_;            // per device: chunks received by P2P gathers so far
     void sync_streams();
     // VMM (single process): reserve / map / grow / release
     bool vmm_ = false;

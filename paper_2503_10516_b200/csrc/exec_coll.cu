@@ -30,9 +30,115 @@ bool Executor::coll_init() {
 // one group of NCCL broadcasts, one per source device, in place in every
 // device's allocation (the `all` mapper; NVLink / NVSwitch
 // collectives instead of G(G-1) separate pushes).
+// §8 a7 / §8(e) as a hand-written kernel: each source device stores its chunk
+// into every receiver's allocation (P2P stores over NVLink / NVSwitch, into
+// IPC-mapped arenas across processes) and bumps each receiver's gather
+// counter; each receiver's stream waits until its counter has counted every
+// chunk sent to it so far (cuStreamWaitValue64 GEQ, no host round trip).  One
+// launch and one wait per device per set, instead of G - 1 pushes with their
+// events and flags each, or an NCCL group.  Every rank keeps the same
+// expected counts: they follow from the replicated instruction graph.
+bool Executor::exec_coll_p2p(const std::vector<Instr>& m) {
+    if (!p2p_gather_) return false;
+    const uint32_t es = bufinfo_.at(m[0].buffer).es;
+    if (es % 4) return false;
+    std::map<int, std::vector<const Instr*>> roots;
+    for (const Instr& x : m) {
+        if (x.region.size() != 1 || x.src_mem < 2 || x.dst_mem < 2) return false;
+        roots[x.src_mem - 2].push_back(&x);
+    }
+    for (auto& rt : roots) {
+        if (int(rt.second.size()) > kMaxGatherDst) return false;
+        for (const Instr* x : rt.second)
+            if (!(x->region[0] == rt.second[0]->region[0])) return false;   // one box per source
+    }
+    auto lin = [](const Box& b, const Box& a) {
+        return uint64_t(((b.lo[0] - a.lo[0]) * a.extent(1) + (b.lo[1] - a.lo[1])) * a.extent(2) + (b.lo[2] - a.lo[2]));
+    };
+    std::vector<int> locals;
+    if (cfg_.world > 1) locals.push_back(cfg_.rank);
+    else
+        for (int v = 0; v < G_; ++v) locals.push_back(v);
+    // wait for the dependencies of every member a local device sends or receives
+    for (int v : locals) {
+        Token t;
+        for (const Instr& x : m)
+            if (x.src_mem - 2 == v || x.dst_mem - 2 == v) {
+                cur_ins_ = &x;
+                merge(t, local_part(x.deps));
+            }
+        set_dev(v);
+        wait_token(v * kStreamsPerDev + S_PUSH, t);
+    }
+    uint64_t bytes_total = 0;
+    for (auto& rt : roots) {
+        const int s = rt.first;
+        const Box& b = rt.second[0]->region[0];
+        bytes_total += b.volume() * es * rt.second.size();
+        if (owner_rank(s) != cfg_.rank) continue;
+        P2PGatherArgs a;
+        memset(&a, 0, sizeof a);
+        const AllocRec& S = allocs_.at(rt.second[0]->src_aid);
+        a.src = base_of(S) + lin(b, S.box) * es;
+        a.bytes = b.volume() * es;
+        uintptr_t al = reinterpret_cast<uintptr_t>(a.src) | uintptr_t(a.bytes);
+        for (const Instr* x : rt.second) {
+            const AllocRec& D = allocs_.at(x->dst_aid);
+            const int dd = x->dst_mem - 2;
+            a.dst[a.ndst] = base_of(D) + lin(b, D.box) * es;
+            a.counter[a.ndst] = reinterpret_cast<unsigned long long*>(arenas_[dd].base + gather_off_);
+            al |= reinterpret_cast<uintptr_t>(a.dst[a.ndst]);
+            a.ndst++;
+        }
+        a.vec4 = (al & 15) == 0;
+        a.ctr = reinterpret_cast<unsigned*>(arenas_[s].base + gather_off_ + 64);
+        const int sidx = s * kStreamsPerDev + S_PUSH;
+        set_dev(s);
+        if (cfg_.profile && prof_sample(K_NUM + 3)) {
+            Prof p{K_NUM + 3, prof_event(s), prof_event(s), s, m[0].iid, sidx, now_ns()};
+            cudaEventRecord(p.a, streams_[sidx].s);
+            st_.kernel_launches += launch_p2p_gather(a, streams_[sidx].s);
+            cudaEventRecord(p.b, streams_[sidx].s);
+            prof_pending_.push_back(p);
+        } else {
+            st_.kernel_launches += launch_p2p_gather(a, streams_[sidx].s);
+        }
+        check(cudaGetLastError(), "P2P gather launch");
+    }
+    for (const Instr& x : m) gather_exp_[x.dst_mem - 2]++;
+    std::vector<Token> tv(G_);
+    for (int v : locals) {
+        const int sidx = v * kStreamsPerDev + S_PUSH;
+        set_dev(v);
+        checkd(g_drv.wait64(reinterpret_cast<CUstream>(streams_[sidx].s),
+                            reinterpret_cast<CUdeviceptr>(arenas_[v].base + gather_off_), gather_exp_[v],
+                            CU_STREAM_WAIT_VALUE_GEQ),
+               "cuStreamWaitValue64 (gather counter)");
+        tv[v] = record(sidx);
+    }
+    for (const Instr& x : m) {
+        const int sd = x.src_mem - 2, dd = x.dst_mem - 2;
+        Token lt;
+        for (int v : locals)
+            if (v == sd || v == dd) merge(lt, tv[v]);
+        if (cfg_.world > 1) {
+            ltok_[x.iid] = lt;
+            for (int rk : {owner_rank(sd), owner_rank(dd)})
+                if (rk != cfg_.rank) lt.remote.push_back({rk, x.iid});
+        }
+        tok_[x.iid] = lt;
+    }
+    st_.coll_groups++;
+    st_.coll_copies += m.size();
+    st_.coll_p2p++;
+    st_.bytes_copy[2] += bytes_total;
+    return true;
+}
+
 void Executor::exec_coll(const std::vector<Instr>& m) {
     const uint32_t es = bufinfo_.at(m[0].buffer).es;
     if (exec_coll_mc(m)) return;                  // NVLS multicast stores (exec_mc.cu)
+    if (exec_coll_p2p(m)) return;                 // P2P gather kernels
     uint64_t min_bytes = ~0ull;
     for (const Instr& x : m) min_bytes = std::min<uint64_t>(min_bytes, rvolume(x.region) * es);
     if (cfg_.world == 1 && (!coll_ || min_bytes < coll_min_bytes_)) {

@@ -315,6 +315,41 @@ __global__ void __launch_bounds__(256) mc_gather_kernel(const char* __restrict__
     }
 }
 
+// ------------------------------------------------------------------ P2P gather
+// The chunk is read once (16-byte loads) and stored to each receiver; the
+// stores to other GPUs travel over NVLink.  Completion: every CTA fences at
+// system scope; the last one bumps each receiver's counter (atomicAdd_system
+// on its memory), which the receiver's stream waits for.
+__global__ void __launch_bounds__(256) p2p_gather_kernel(const __grid_constant__ P2PGatherArgs a) {
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, nth = uint64_t(gridDim.x) * blockDim.x;
+    if (a.vec4) {
+        const uint64_t n16 = a.bytes / 16;
+        for (uint64_t i = tid; i < n16; i += nth) {
+            const uint4 v = *reinterpret_cast<const uint4*>(a.src + 16 * i);
+            for (int k = 0; k < a.ndst; ++k) st_na_v4(a.dst[k] + 16 * i, v);
+        }
+        for (uint64_t i = n16 * 4 + tid; i < a.bytes / 4; i += nth) {
+            const uint32_t v = reinterpret_cast<const uint32_t*>(a.src)[i];
+            for (int k = 0; k < a.ndst; ++k) reinterpret_cast<uint32_t*>(a.dst[k])[i] = v;
+        }
+    } else {
+        for (uint64_t i = tid; i < a.bytes / 4; i += nth) {
+            const uint32_t v = reinterpret_cast<const uint32_t*>(a.src)[i];
+            for (int k = 0; k < a.ndst; ++k) reinterpret_cast<uint32_t*>(a.dst[k])[i] = v;
+        }
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned prev = atomicAdd(a.ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            *a.ctr = 0;
+            __threadfence_system();
+            for (int k = 0; k < a.ndst; ++k) atomicAdd_system(a.counter[k], 1ull);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ int64_t off_of(const DAcc& A, int64_t z, int64_t y, int64_t x) {
     return ((z - A.lo[0]) * A.n[1] + (y - A.lo[1])) * A.n[2] + (x - A.lo[2]);
@@ -448,7 +483,7 @@ __global__ void wave5_scalar(const __grid_constant__ KArgs a) {
     }
 }
 
-constexpr int kWaveRows = 16;
+constexpr int kWaveRows = 8;                  // strip height cap of the automatic choice (sweep r02: 8 beat 16 by 3-4%)
 
 // vector path: 128 threads x float4 = 512 columns per CTA, a strip of kWaveRows
 // rows marched top to bottom with a 3-row register window; west/east
@@ -1232,6 +1267,14 @@ int launch_mc_gather(const char* src, char* mc_dst, uint64_t bytes, unsigned lon
     return 1;
 }
 
+int launch_p2p_gather(const P2PGatherArgs& a, cudaStream_t s) {
+    const uint64_t units = (a.bytes / 16 + 255) / 256;
+    int64_t grid = int64_t(units ? units : 1);
+    if (grid > int64_t(num_sms()) * 4) grid = int64_t(num_sms()) * 4;
+    p2p_gather_kernel<<<unsigned(grid), 256, 0, s>>>(a);
+    return 1;
+}
+
 int launch_copy(const CopyArgs& a, cudaStream_t s) {
     if (a.total_units == 0 || a.nseg == 0) return 0;
     // local copies: flat grid (one CTA per unit); peer pushes over NVLink: a
@@ -1269,9 +1312,11 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
                          P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
                          aligned16(U.base) && aligned16(P.base);
         if (vec) {
-            // strip height: 16 rows, lowered (>= 4) until the grid has about 8
+            // strip height: 8 rows, lowered (>= 4) until the grid has about 8
             // waves of resident CTAs, so the last-wave tail stays small on the
-            // thin chunks of many-GPU runs
+            // thin chunks of many-GPU runs (r02 sweep, tools/wave_strip.py:
+            // 16384 rows 478 us at h = 8 vs 494 at 16; neighbouring strips'
+            // halo rows are L2 hits, so short strips cost no DRAM re-reads)
             static int occ = 0;
             if (occ == 0) {
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
@@ -1282,6 +1327,12 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             const int64_t resident = int64_t(num_sms()) * occ;
             int64_t h = (rows * cols) / (resident * 8);
             h = h < 4 ? 4 : (h > kWaveRows ? kWaveRows : h);
+            static int force = -1;
+            if (force < 0) {
+                const char* e = getenv("CEL_WAVE_STRIP");           // A/B of the strip height
+                force = e ? atoi(e) : 0;
+            }
+            if (force > 0) h = force;
             KArgs b = a;
             b.strip = int(h);
             dim3 grid(unsigned(cols), unsigned((rows + h - 1) / h));

@@ -78,6 +78,22 @@ int launch_copy_tma(const TmaCopyArgs& a, cudaStream_t s);
 int launch_mc_gather(const char* src, char* mc_dst, uint64_t bytes, unsigned long long* mc_flag, unsigned* ctr,
                      cudaStream_t s);
 
+// P2P all-gather (SURVEY §8 a7 / §8(e) "P2P stores over NVSwitch"): one
+// source's chunk stored into every receiver's allocation (peer pointers:
+// another GPU's memory over NVLink, IPC-mapped in multi-process runs); the
+// last CTA then adds 1 (system scope) to each receiver's gather counter.
+constexpr int kMaxGatherDst = 15;
+struct P2PGatherArgs {
+    const char* src;
+    char* dst[kMaxGatherDst];
+    unsigned long long* counter[kMaxGatherDst];
+    int ndst;
+    uint64_t bytes;            // multiple of 4; src and every dst 16-byte aligned, or 4-byte with vec4 = 0
+    int vec4;
+    unsigned* ctr;             // zeroed word of the source device: CTAs done
+};
+int launch_p2p_gather(const P2PGatherArgs& a, cudaStream_t s);
+
 // ---- accessor (allocation pointer interpolated into the accessor)
 struct DBox {
     int64_t lo[3], hi[3];

@@ -30,3 +30,5 @@ for mc in 0 1; do
   CEL_COLL_MC=$mc timeout 300 python bench_config.py --workload nbody --gpus 4 --fast-math > gpurun_out/nbody.json 2> gpurun_out/nbody.err
   echo "nbody fast 4 GPUs 1 process MC=$mc rc=$?"; cat gpurun_out/nbody.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print({k: d.get(k) for k in ('value','ms_per_step','coll_groups')}, d['profile_ms'].get('coll'))"
 done
+CEL_DIRECT_SENDS=1 timeout 600 python -m pytest tests/test_gpu_cluster.py -m gpu -q --timeout 180 --timeout-method thread > gpurun_out/pytest_cluster_direct.log 2>&1
+echo "cluster tests with direct sends rc=$?"; tail -3 gpurun_out/pytest_cluster_direct.log
