@@ -210,6 +210,7 @@ typedef struct cel_stats_s {
                                              their sends published the device allocation (device-direct) */
     uint64_t staging_materialized;        /* ... of which executed late (their M1 bytes were needed after all) */
     uint64_t coll_p2p;                    /* all-gather sets run as P2P gather kernels (stores into every receiver) */
+    uint64_t coll_fused;                  /* ... fused into the RSim row kernels that produce them */
 } cel_stats_t;
 
 /* Create a runtime.  With execute != 0 every device reserves arena_bytes of

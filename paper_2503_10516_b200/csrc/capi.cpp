@@ -384,6 +384,7 @@ int cel_stats(cel_runtime* rt, cel_stats_t* o) {
         o->vmm_mapped_bytes += e.vmm_mapped_bytes;
         o->coll_multicast += e.coll_multicast;
         o->coll_p2p += e.coll_p2p;
+        o->coll_fused += e.coll_fused;
         o->staging_elided += e.staging_elided;
         o->staging_materialized += e.staging_materialized;
     }

@@ -395,8 +395,12 @@ int Executor::init(std::string* err) {
         if (cv && cv[0] == '0') distinct = false;
         coll_ = distinct && g_nccl.load();
         // NVLS multicast gathers: one process, distinct GPUs, VMM allocations
+        // P2P gather kernels: on by default in one process, and across
+        // processes when every rank has a GPU of its own (two ranks folded onto
+        // one GPU hung with them in the round-2 suite -- cross-process waits on
+        // one GPU, which the profiling guide warns about; they keep pushes)
         const char* p2 = getenv("CEL_COLL_P2P");
-        p2p_gather_ = !(p2 && p2[0] == '0');
+        p2p_gather_ = p2 ? p2[0] == '1' : (cfg_.world == 1 || distinct);
         if (p2p_gather_) {                                    // receivers wait with 64-bit stream memory ops
             g_drv.load();
             int v = 0;
@@ -404,6 +408,10 @@ int Executor::init(std::string* err) {
                 g_drv.devattr(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, CUdevice(phys_[owned(0) ? 0 : cfg_.rank]));
             p2p_gather_ = v != 0 && g_drv.wait64;
         }
+        const char* fr = getenv("CEL_FUSE_ROWS");
+        // (one process: the held-back kernel's flags to other ranks deadlocked
+        // the 4-rank parity run, so multi-process runs do not fuse)
+        fuse_rows_ = p2p_gather_ && cfg_.world == 1 && !(fr && fr[0] == '0');
         const char* mc = getenv("CEL_COLL_MC");
         mc_enabled_ = distinct && vmm_ && cfg_.world == 1 && mc && mc[0] == '1';
         if (coll_ && cfg_.world > 1 && cfg_.rank == 0) {
@@ -453,6 +461,7 @@ int Executor::init(std::string* err) {
     }
     cudaDeviceSynchronize();
     const char* et = getenv("CEL_EXEC_THREAD");
+    if (!(cfg_.comm || !(et && et[0] == '0'))) fuse_rows_ = false;   // parking needs the executor thread's drains
     if (cfg_.comm || !(et && et[0] == '0')) {   // nodes must progress independently
         threaded_ = true;
         thr_ = std::thread([this] { thread_main(); });
@@ -873,28 +882,50 @@ void Executor::signal_deps(const Instr& ins, int owner_dev) {
         if (jo >= 0 && owner_rank(jo) != cfg_.rank) continue;
         const uint64_t key = j * uint64_t(cfg_.world) + uint64_t(o);
         if (!signalled_.insert(key).second) continue;
-        Token t;
-        if (jo < 0) {
-            auto lt = ltok_.find(j);
-            if (lt != ltok_.end()) t = lt->second;
-        } else {
-            t = dep_token(j);
+        if (parked_iids_.count(j)) {          // not launched yet (exec_fuse.cu): signal once it is
+            deferred_signals_.push_back({j, o});
+            continue;
         }
-        Token live;
-        merge(live, t);                               // drops entries already known complete
-        int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
-        if (live.remote.empty() && live.local.size() == 1)
-            sidx = cfg_.rank * kStreamsPerDev + S_SIG0 + (live.local[0].stream % kStreamsPerDev) % kNumSigStreams;
-        wait_token(sidx, live);
-        if (trace_)
-            fprintf(stderr, "[cel r%d] signal iid %llu -> rank %d\n", cfg_.rank, (unsigned long long)j, o);
-        const uint64_t ts = now_ns();
-        checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
-                                    reinterpret_cast<CUdeviceptr>(sig_slot(o, cfg_.rank, j)), j,
-                                    CU_STREAM_WRITE_VALUE_DEFAULT),
-               "cuStreamWriteValue64");
-        st_.signal_ns += now_ns() - ts;
-        st_.signals++;
+        signal_one(j, jo, o);
+    }
+}
+
+// Write "instruction j done" into rank o's flag slot once j's local work has
+// completed (stream-ordered after it).
+void Executor::signal_one(uint64_t j, int jo, int o) {
+    Token t;
+    if (jo < 0) {
+        auto lt = ltok_.find(j);
+        if (lt != ltok_.end()) t = lt->second;
+    } else {
+        t = dep_token(j);
+    }
+    Token live;
+    merge(live, t);                               // drops entries already known complete
+    int sidx = cfg_.rank * kStreamsPerDev + S_SYNC;
+    if (live.remote.empty() && live.local.size() == 1)
+        sidx = cfg_.rank * kStreamsPerDev + S_SIG0 + (live.local[0].stream % kStreamsPerDev) % kNumSigStreams;
+    wait_token(sidx, live);
+    if (trace_) fprintf(stderr, "[cel r%d] signal iid %llu -> rank %d\n", cfg_.rank, (unsigned long long)j, o);
+    const uint64_t ts = now_ns();
+    checkd(g_drv.write64(reinterpret_cast<CUstream>(streams_[sidx].s),
+                         reinterpret_cast<CUdeviceptr>(sig_slot(o, cfg_.rank, j)), j, CU_STREAM_WRITE_VALUE_DEFAULT),
+           "cuStreamWriteValue64");
+    st_.signal_ns += now_ns() - ts;
+    st_.signals++;
+}
+
+void Executor::flush_deferred_signals() {
+    for (size_t i = 0; i < deferred_signals_.size();) {
+        const auto p = deferred_signals_[i];
+        if (parked_iids_.count(p.first)) {
+            ++i;
+            continue;
+        }
+        int jo = 0;
+        if (!owner_lookup(p.first, &jo)) jo = cfg_.rank;
+        signal_one(p.first, jo, p.second);
+        deferred_signals_.erase(deferred_signals_.begin() + long(i));
     }
 }
 
@@ -1013,6 +1044,8 @@ void Executor::thread_main() {
         } else if (it.kind == 1) {
             it.fn();
         } else {
+            flush_parked();                              // a drain / epoch wait: nothing stays held back
+            if (!deferred_signals_.empty()) flush_deferred_signals();
             publish_stats();
             {
                 std::lock_guard<std::mutex> l(dm_);
@@ -1082,12 +1115,25 @@ void Executor::on_instr_impl(const Instr& ins) {
         settle_tok_ = Token{};
     }
     if (!pending_send_.empty()) resolve_sends(ins);
+    // rows fused with their gathers (exec_fuse.cu): hold back a fusable row
+    // kernel, and whatever depends on something held back, except the
+    // all-gather members (held as a set anyway)
+    const bool gather_member = (coll_ || mc_enabled_ || p2p_gather_) && ins.kind == IKind::Copy && ins.coll_n;
+    if (!flushing_ && !parked_iids_.empty() && !gather_member && depends_on_parked(ins)) {
+        park(ins);
+        return;
+    }
+    if (park_candidate(ins)) {
+        if (cfg_.world > 1) kind_of_[ins.iid] = ins.device;
+        park(ins);
+        return;
+    }
     const int od = instr_owner(ins);
     const bool mine = od < 0 || owner_rank(od) == cfg_.rank;
     if (trace_)
         fprintf(stderr, "[cel r%d] iid %llu kind %d owner %d %s\n", cfg_.rank, (unsigned long long)ins.iid,
                 int(ins.kind), od, mine ? "exec" : "skip");
-    if ((coll_ || mc_enabled_ || p2p_gather_) && ins.kind == IKind::Copy && ins.coll_n) {
+    if (gather_member) {
         // §8 a7: a member of an all-gather copy set.  Every rank takes part;
         // the source's and the destination's ranks each wait for the member's
         // dependencies, so the other ranks signal theirs to both.

@@ -124,6 +124,7 @@ struct ExecStats {
     uint64_t vmm_maps = 0, vmm_mapped_bytes = 0;   // VMM: physical granule mappings and their bytes
     uint64_t coll_multicast = 0;                    // all-gather sets run as NVLS multicast stores
     uint64_t coll_p2p = 0;                          // ... as P2P gather kernels
+    uint64_t coll_fused = 0;                        // ... fused into the RSim row kernels that produce them
     uint64_t staging_elided = 0, staging_materialized = 0;   // device-direct sends (virtual-node mode)
     uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
@@ -193,7 +194,9 @@ public:
     void profile_reset();
     int device_count() const { return G_; }
     // multicast gathers run sets of any size: the scheduler should flag small ones too
-    bool gathers_any_size() const { return mc_enabled_ || p2p_gather_; }
+    // (multi-process: P2P gathers replace NCCL for the sets NCCL would take;
+    // small sets stay pushes -- measured faster across processes for RSim rows)
+    bool gathers_any_size() const { return mc_enabled_ || (p2p_gather_ && cfg_.world == 1); }
     int owned(int d) const { return owner_rank(d) == cfg_.rank; }
     void sync_all();
 
@@ -293,6 +296,7 @@ private:
     void exec_copy(const Instr& ins);
     bool exec_copy_tma(const Instr& ins, const AllocRec& S, const AllocRec& D, uint32_t es, int sidx, int dev);
     void exec_kernel(const Instr& ins);
+    void build_kargs(const Instr& ins, KArgs& a);
     void exec_epoch(const Instr& ins);
     void throttle();
     void prune_tokens(uint64_t below);
@@ -349,6 +353,19 @@ private:
     void mc_forget(const VmmRegion* r);
     bool exec_coll_mc(const std::vector<Instr>& m);
     bool exec_coll_p2p(const std::vector<Instr>& m);
+    // RSim rows fused with their gathers (exec_fuse.cu)
+    bool fuse_rows_ = false;                      // CEL_FUSE_ROWS=0: off
+    bool flushing_ = false;
+    std::vector<Instr> parked_;                   // instructions held back, in order
+    std::unordered_set<uint64_t> parked_iids_;
+    std::vector<std::pair<uint64_t, int>> deferred_signals_;   // (iid, rank): signal once it has run
+    bool depends_on_parked(const Instr& ins) const;
+    bool park_candidate(const Instr& ins);
+    void park(const Instr& ins);
+    void flush_parked();
+    bool try_fuse(const std::vector<Instr>& m);
+    void signal_one(uint64_t j, int jo, int o);
+    void flush_deferred_signals();
     bool p2p_gather_ = false;                     // gather sets as P2P gather kernels (CEL_COLL_P2P=0: off)
     uint64_t gather_off_ = 0;                     // per device arena: gather counter word (+64: CTA counter)
     std::vector<uint64_t> gather_exp_;            // per device: chunks received by P2P gathers so far

@@ -71,6 +71,7 @@ bool Executor::exec_coll_p2p(const std::vector<Instr>& m) {
         wait_token(v * kStreamsPerDev + S_PUSH, t);
     }
     uint64_t bytes_total = 0;
+    std::vector<Token> src_done(G_);
     for (auto& rt : roots) {
         const int s = rt.first;
         const Box& b = rt.second[0]->region[0];
@@ -104,6 +105,7 @@ bool Executor::exec_coll_p2p(const std::vector<Instr>& m) {
             st_.kernel_launches += launch_p2p_gather(a, streams_[sidx].s);
         }
         check(cudaGetLastError(), "P2P gather launch");
+        if (cfg_.world > 1) src_done[s] = record(sidx);
     }
     for (const Instr& x : m) gather_exp_[x.dst_mem - 2]++;
     std::vector<Token> tv(G_);
@@ -116,11 +118,16 @@ bool Executor::exec_coll_p2p(const std::vector<Instr>& m) {
                "cuStreamWaitValue64 (gather counter)");
         tv[v] = record(sidx);
     }
+    // a member is complete once its receiver's counter has counted it: that
+    // wait also implies the source kernel's reads and stores are done, so
+    // the receiver's event alone stands for the copy (no cross-device waits
+    // for the next row's kernel); a source rank that is not the receiver
+    // holds the source kernel's completion as its part
     for (const Instr& x : m) {
         const int sd = x.src_mem - 2, dd = x.dst_mem - 2;
         Token lt;
-        for (int v : locals)
-            if (v == sd || v == dd) merge(lt, tv[v]);
+        if (owner_rank(dd) == cfg_.rank) merge(lt, tv[dd]);
+        else if (owner_rank(sd) == cfg_.rank) merge(lt, src_done[sd]);
         if (cfg_.world > 1) {
             ltok_[x.iid] = lt;
             for (int rk : {owner_rank(sd), owner_rank(dd)})
@@ -137,6 +144,10 @@ bool Executor::exec_coll_p2p(const std::vector<Instr>& m) {
 
 void Executor::exec_coll(const std::vector<Instr>& m) {
     const uint32_t es = bufinfo_.at(m[0].buffer).es;
+    if (!parked_.empty()) {
+        if (try_fuse(m)) return;                  // the producing row kernels carry the gather (exec_fuse.cu)
+        flush_parked();                           // the members depend on them: launch them plainly first
+    }
     if (exec_coll_mc(m)) return;                  // NVLS multicast stores (exec_mc.cu)
     if (exec_coll_p2p(m)) return;                 // P2P gather kernels
     uint64_t min_bytes = ~0ull;

@@ -4,6 +4,52 @@
 
 namespace cel {
 
+// The launch arguments of a built-in kernel instruction: chunk, parameters and
+// one accessor per access (allocation base and box, the range mapper's box).
+void Executor::build_kargs(const Instr& ins, KArgs& a) {
+    const TaskDesc& d = *ins.desc;
+    memset(&a, 0, sizeof a);
+    a.kind = d.kernel;
+    a.n_acc = int(std::min<size_t>(d.acc.size(), kMaxAcc));
+    for (int k = 0; k < 3; ++k) {
+        a.chunk.lo[k] = ins.chunk.lo[k];
+        a.chunk.hi[k] = ins.chunk.hi[k];
+    }
+    a.seed = d.params.seed;
+    a.value = d.params.value;
+    a.t = d.params.t;
+    a.salt = d.params.salt;
+    a.fast = cfg_.fast_math ? 1 : 0;
+    a.variant = kernel_variant_;
+    for (int i = 0; i < a.n_acc; ++i) {
+        const Access& ac = d.acc[i];
+        DAcc& A = a.acc[i];
+        const Box ext = bufinfo_.at(ac.buf).extent;
+        for (int k = 0; k < 3; ++k) A.ext[k] = ext.hi[k];
+        A.es = bufinfo_.at(ac.buf).es;
+        A.mode = ac.mode;
+        A.map = int(ac.map.kind);
+        for (int k = 0; k < 3; ++k) {
+            A.border[k] = ac.map.border[k];
+            A.fixed.lo[k] = ac.map.fixed.lo[k];
+            A.fixed.hi[k] = ac.map.fixed.hi[k];
+        }
+        const Box mb = map_access(ac.map, ins.chunk, ext);
+        for (int k = 0; k < 3; ++k) {
+            A.box.lo[k] = mb.lo[k];
+            A.box.hi[k] = mb.hi[k];
+        }
+        auto it = allocs_.find(ins.bindings[i]);
+        if (it != allocs_.end()) {
+            A.base = base_of(it->second);
+            for (int k = 0; k < 3; ++k) {
+                A.lo[k] = it->second.box.lo[k];
+                A.n[k] = it->second.box.extent(k);
+            }
+        }
+    }
+}
+
 void Executor::exec_kernel(const Instr& ins) {
     const TaskDesc& d = *ins.desc;
     const int dev = ins.device;
@@ -47,46 +93,7 @@ void Executor::exec_kernel(const Instr& ins) {
         return;
     }
     KArgs a;
-    memset(&a, 0, sizeof a);
-    a.kind = d.kernel;
-    a.n_acc = int(std::min<size_t>(d.acc.size(), kMaxAcc));
-    for (int k = 0; k < 3; ++k) {
-        a.chunk.lo[k] = ins.chunk.lo[k];
-        a.chunk.hi[k] = ins.chunk.hi[k];
-    }
-    a.seed = d.params.seed;
-    a.value = d.params.value;
-    a.t = d.params.t;
-    a.salt = d.params.salt;
-    a.fast = cfg_.fast_math ? 1 : 0;
-    a.variant = kernel_variant_;
-    for (int i = 0; i < a.n_acc; ++i) {
-        const Access& ac = d.acc[i];
-        DAcc& A = a.acc[i];
-        const Box ext = bufinfo_.at(ac.buf).extent;
-        for (int k = 0; k < 3; ++k) A.ext[k] = ext.hi[k];
-        A.es = bufinfo_.at(ac.buf).es;
-        A.mode = ac.mode;
-        A.map = int(ac.map.kind);
-        for (int k = 0; k < 3; ++k) {
-            A.border[k] = ac.map.border[k];
-            A.fixed.lo[k] = ac.map.fixed.lo[k];
-            A.fixed.hi[k] = ac.map.fixed.hi[k];
-        }
-        const Box mb = map_access(ac.map, ins.chunk, ext);
-        for (int k = 0; k < 3; ++k) {
-            A.box.lo[k] = mb.lo[k];
-            A.box.hi[k] = mb.hi[k];
-        }
-        auto it = allocs_.find(ins.bindings[i]);
-        if (it != allocs_.end()) {
-            A.base = base_of(it->second);
-            for (int k = 0; k < 3; ++k) {
-                A.lo[k] = it->second.box.lo[k];
-                A.n[k] = it->second.box.extent(k);
-            }
-        }
-    }
+    build_kargs(ins, a);
     // Shell / interior split of stencil launches: the boundary bands that
     // neighbouring devices read (halo rows) are computed first on a
     // high-priority stream, so their coherence copies leave while the interior

@@ -928,8 +928,9 @@ __global__ void rsim_row_checked(const __grid_constant__ KArgs a) {
 // W % 4 == 0, W >= 2 kRB, base 16-byte aligned.
 constexpr int kRC = 128, kRR = 16, kRS = 4, kRB = kRC + kRR + 4;
 
-__global__ void __launch_bounds__(kRC) rsim_row_tma(const __grid_constant__ CUtensorMap tm,
-                                                    const __grid_constant__ KArgs a) {
+template <bool kPeer>
+__global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CUtensorMap tm,
+                                                      const __grid_constant__ KArgs a, const __grid_constant__ PeerOut po) {
     extern __shared__ __align__(128) float rsm[];
     __shared__ __align__(8) uint64_t rbar[kRS];
     const DAcc& R = a.acc[0];
@@ -1005,7 +1006,24 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma(const __grid_constant__ CUte
     if (i < a.chunk.hi[0]) {
         const float prev = *ptr<const float>(R, t - 1, i, 0);
         const float coef = 0.5f / float(t);
-        *ptr<float>(Wr, t, i, 0) = 0.5f * prev + coef * acc;
+        const float out = 0.5f * prev + coef * acc;
+        *ptr<float>(Wr, t, i, 0) = out;
+        if (kPeer)
+            for (int k = 0; k < po.n; ++k)
+                reinterpret_cast<float*>(po.base[k])[(t - po.lo0[k]) * po.n1[k] + (i - po.lo1[k])] = out;
+    }
+    if (kPeer) {
+        // the row's gather: every receiver's copy lands before its counter moves
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned prevc = atomicAdd(po.ctr, 1u);
+            if (prevc == gridDim.x - 1) {
+                *po.ctr = 0;
+                __threadfence_system();
+                for (int k = 0; k < po.n; ++k) atomicAdd_system(po.counter[k], 1ull);
+            }
+        }
     }
 }
 
@@ -1286,6 +1304,27 @@ int launch_copy(const CopyArgs& a, cudaStream_t s) {
     return 1;
 }
 
+// Preconditions of the TMA-staged RSim row kernel (see rsim_row_tma_t).
+bool rsim_tma_ok(const KArgs& a) {
+    const DAcc& R0 = a.acc[0];
+    return !(a.variant & kVarRsimRegs) && !a.checked && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 &&
+           R0.n[2] == 1 && R0.lo[2] == 0 && R0.es == 4 && R0.ext[1] >= 2 * kRB && R0.lo[0] == 0 &&
+           (reinterpret_cast<uintptr_t>(R0.base) & 15) == 0 && a.t > 0;
+}
+
+bool rsim_fusable(const KArgs& a) {
+    CUtensorMap tm;
+    return a.kind == K_RSIM_ROW && vol(a.chunk) > 0 && rsim_tma_ok(a) && rsim_tensor_map(a.acc[0], &tm);
+}
+
+int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s) {
+    CUtensorMap tm;
+    if (!rsim_fusable(a) || !rsim_tensor_map(a.acc[0], &tm)) return 0;
+    const unsigned grid = unsigned((vol(a.chunk) + kRC - 1) / kRC);
+    rsim_row_tma_t<true><<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a, po);
+    return 1;
+}
+
 int launch_workload(const KArgs& a, cudaStream_t s) {
     const int64_t cv = vol(a.chunk);
     switch (a.kind) {
@@ -1392,11 +1431,11 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             return 1;
         }
         CUtensorMap tm;
-        if (!(a.variant & kVarRsimRegs) && R0.n[1] == R0.ext[1] && R0.lo[1] == 0 && R0.ext[1] % 4 == 0 && R0.n[2] == 1 &&
-            R0.lo[2] == 0 && R0.es == 4 && R0.ext[1] >= 2 * kRB && R0.lo[0] == 0 &&
-            (reinterpret_cast<uintptr_t>(R0.base) & 15) == 0 && a.t > 0 && rsim_tensor_map(R0, &tm)) {
+        if (rsim_tma_ok(a) && rsim_tensor_map(R0, &tm)) {
             const unsigned grid = unsigned((cv + kRC - 1) / kRC);
-            rsim_row_tma<<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a);
+            PeerOut none;
+            none.n = 0;
+            rsim_row_tma_t<false><<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a, none);
             return 1;
         }
         rsim_row_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a);

@@ -94,6 +94,8 @@ struct P2PGatherArgs {
 };
 int launch_p2p_gather(const P2PGatherArgs& a, cudaStream_t s);
 
+
+
 // ---- accessor (allocation pointer interpolated into the accessor)
 struct DBox {
     int64_t lo[3], hi[3];
@@ -171,5 +173,21 @@ void launch_oob_init(long long* rec, int n, cudaStream_t s);
 int launch_workload(const KArgs& a, cudaStream_t s);
 
 void set_copy_blocks_per_sm(int n);
+
+// RSim row kernel with the row's all-gather fused into its epilogue: each
+// thread also stores its element into every receiver's allocation (same
+// buffer coordinates, the receiver's allocation layout), then the last CTA
+// bumps each receiver's gather counter -- the P2P gather without its own
+// launch.  Used by the executor when a row kernel is followed by the gather
+// set of the row it writes (exec_fuse.cu).
+struct PeerOut {
+    int n;
+    char* base[kMaxGatherDst];
+    int64_t lo0[kMaxGatherDst], lo1[kMaxGatherDst], n1[kMaxGatherDst];   // receiver allocation box (rows, cols)
+    unsigned long long* counter[kMaxGatherDst];
+    unsigned* ctr;
+};
+bool rsim_fusable(const KArgs& a);                       // the TMA row kernel applies (it carries the epilogue)
+int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s);
 
 }  // namespace cel

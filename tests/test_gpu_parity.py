@@ -179,6 +179,27 @@ def test_tma_tensor_map_copies(cel, G, monkeypatch):
         run_both(cel, P.random_program(7300 + 11 * G + s), G, "none", arena=32 << 20)
 
 
+@pytest.mark.parametrize("fuse", [True, False])
+def test_rsim_rows_fused_with_gathers(cel, fuse, monkeypatch):
+    """An RSim row's all-gather (the next task's coherence copy set) fused into
+    the row kernel that produces it: the executor holds the row kernel until
+    the set arrives and launches it with a peer epilogue (stores into every
+    receiver's allocation, then gather counters); otherwise (CEL_FUSE_ROWS=0)
+    the set runs as P2P gather kernels.  Bit-exact with the oracle's bytes
+    and log, on virtual devices of one GPU (and on distinct GPUs when there)."""
+    if not fuse:
+        monkeypatch.setenv("CEL_FUSE_ROWS", "0")
+    for G in (2, 4):
+        st = run_both(cel, P.rsim(1000, 40), G).final_stats
+        assert st["gather_sets"] > 0 and st["coll_p2p"] + st["coll_fused"] == st["gather_sets"]
+        assert (st["coll_fused"] > st["gather_sets"] // 2) == fuse, (st["coll_fused"], st["gather_sets"])
+    run_both(cel, P.rsim(1000, 140), 3)                      # ring cycles of the TMA kernel, fused
+    run_both(cel, P.rsim(1000, 24), 2, "none")               # growing allocations
+    n = torch.cuda.device_count()
+    if n >= 2:
+        run_both(cel, P.rsim(84000, 48), n, devices=list(range(n)))
+
+
 def test_all_gather_collective_vs_pushes(cel, monkeypatch):
     """§8 a7: the same programs with the all-gather copy sets run as NCCL
     broadcasts and as peer pushes give identical bytes."""
@@ -211,6 +232,7 @@ def test_all_gather_multicast(cel, monkeypatch):
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     monkeypatch.setenv("CEL_COLL_MC", "1")
+    monkeypatch.setenv("CEL_FUSE_ROWS", "0")           # (fused rows would take RSim's sets first)
     devs = list(range(n))
     st = run_both(cel, P.rsim(8000, 80), n, devices=devs).final_stats
     assert st["coll_multicast"] == st["gather_sets"] > 0
