@@ -488,31 +488,6 @@ constexpr int kWaveRows = 8;                  // strip height cap of the automat
 // vector path: 128 threads x float4 = 512 columns per CTA, a strip of kWaveRows
 // rows marched top to bottom with a 3-row register window; west/east
 // neighbours come from warp shuffles (scalar loads only at warp edges).
-// kV (A/B of cache hints, CEL_WAVE_VAR): 0 plain; 1 streaming (evict-first)
-// load of up and store of the result; 2 = 1 plus u rows without L1 allocation
-template <int kV>
-__device__ __forceinline__ float4 ld_up(const float* p) {
-    if (kV >= 1) return __ldcs(reinterpret_cast<const float4*>(p));
-    return *reinterpret_cast<const float4*>(p);
-}
-template <int kV>
-__device__ __forceinline__ void st_up(float* p, const float4& v) {
-    if (kV >= 1) __stcs(reinterpret_cast<float4*>(p), v);
-    else *reinterpret_cast<float4*>(p) = v;
-}
-template <int kV>
-__device__ __forceinline__ float4 ld_u(const float* p) {
-    if (kV >= 2) {
-        float4 r;
-        asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-                     : "l"(p));
-        return r;
-    }
-    return __ldg(reinterpret_cast<const float4*>(p));
-}
-
-template <int kV>
 __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a) {
     const DAcc& U = a.acc[0];
     const DAcc& P = a.acc[1];
@@ -533,8 +508,8 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 prev = z4, cur = z4;
     if (valid) {
-        prev = ld_u<kV>(urow(rs > 0 ? rs - 1 : 0) + uoff);
-        cur = ld_u<kV>(urow(rs) + uoff);
+        prev = __ldg(reinterpret_cast<const float4*>(urow(rs > 0 ? rs - 1 : 0) + uoff));
+        cur = __ldg(reinterpret_cast<const float4*>(urow(rs) + uoff));
     }
     const bool need_e = valid && (lane == 31 || c + 4 >= c1);
     const bool need_w = valid && lane == 0;
@@ -546,8 +521,8 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
         float4 nxt = z4, up = z4;
         float* prow = pb + (r - P.lo[0]) * P.n[1] + poff;
         if (valid) {
-            nxt = ld_u<kV>(urow(rn) + uoff);
-            up = ld_up<kV>(prow);
+            nxt = __ldg(reinterpret_cast<const float4*>(urow(rn) + uoff));
+            up = *reinterpret_cast<const float4*>(prow);
         }
         float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
         float e = __shfl_down_sync(0xffffffffu, cur.x, 1);
@@ -558,7 +533,7 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
         o.y = wave1(cur.y, up.y, prev.y, nxt.y, cur.x, cur.z);
         o.z = wave1(cur.z, up.z, prev.z, nxt.z, cur.y, cur.w);
         o.w = wave1(cur.w, up.w, prev.w, nxt.w, cur.z, e);
-        if (valid) st_up<kV>(prow, o);
+        if (valid) *reinterpret_cast<float4*>(prow) = o;
         prev = cur;
         cur = nxt;
     }
@@ -1383,7 +1358,7 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             // halo rows are L2 hits, so short strips cost no DRAM re-reads)
             static int occ = 0;
             if (occ == 0) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec<0>, 128, 0);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
                 if (occ < 1) occ = 1;
             }
             const int64_t cols = (w / 4 + 127) / 128;
@@ -1400,17 +1375,7 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             KArgs b = a;
             b.strip = int(h);
             dim3 grid(unsigned(cols), unsigned((rows + h - 1) / h));
-            static int wv = -1;
-            if (wv < 0) {
-                const char* e = getenv("CEL_WAVE_VAR");
-                wv = e ? atoi(e) : 0;
-            }
-            if (wv == 2)
-                wave5_vec<2><<<grid, 128, 0, s>>>(b);
-            else if (wv == 1)
-                wave5_vec<1><<<grid, 128, 0, s>>>(b);
-            else
-                wave5_vec<0><<<grid, 128, 0, s>>>(b);
+            wave5_vec<<<grid, 128, 0, s>>>(b);
         } else {
             wave5_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);
         }
