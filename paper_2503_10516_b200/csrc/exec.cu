@@ -172,7 +172,7 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     const char* rv = getenv("CEL_RSIM");
     if (rv && rv[0] == '0') kernel_variant_ |= kVarRsimRegs;
     const char* ds = getenv("CEL_DIRECT_SENDS");
-    direct_sends_ = cfg_.comm && ds && ds[0] == '1';
+    direct_sends_ = cfg_.comm && !(ds && ds[0] == '0');
     const char* cmb = getenv("CEL_COLL_MIN_BYTES");
     if (cmb && cmb[0]) coll_min_bytes_ = strtoull(cmb, nullptr, 10);
     const char* cv = getenv("CEL_COPY");
@@ -1371,6 +1371,8 @@ void Executor::exec_epoch(const Instr& ins) {
     }
     host_drop_.clear();
     if (pending_send_.empty()) msg_tok_.clear();
+    for (auto it = elided_iids_.begin(); it != elided_iids_.end();)
+        it = (*it < ins.iid && !pending_send_.count(*it) && !staged_.count(*it)) ? elided_iids_.erase(it) : std::next(it);
     Token mine;
     for (int r = 0; r < cfg_.world; ++r)
         if (r != cfg_.rank) mine.remote.push_back({r, ins.iid});

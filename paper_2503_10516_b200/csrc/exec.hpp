@@ -487,7 +487,8 @@ private:
         bool consumed = false;                     // a send published its source
     };
     std::map<uint64_t, Staged> staged_;
-    bool direct_sends_ = false;                    // CEL_DIRECT_SENDS=1 (opt-in: see DESIGN.md §2)
+    std::unordered_set<uint64_t> elided_iids_;     // every staging copy elided (pruned at epochs)
+    bool direct_sends_ = false;                    // virtual-node mode; CEL_DIRECT_SENDS=0 stages through M1
     bool materializing_ = false;                   // exec_copy of an elided copy that is needed after all
     int64_t direct_src_ = -1;                      // settle_staged -> exec_transfer: device source of this send
     uint64_t direct_staged_ = 0;                   // ... and the elided copy that staged it

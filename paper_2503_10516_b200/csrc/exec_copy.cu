@@ -129,6 +129,7 @@ void Executor::exec_copy(const Instr& ins) {
         // a push's staging copy: elided; its sends publish the device
         // allocation (settle_staged / exec_transfer)
         staged_[ins.iid] = Staged{ins, deps, false};
+        elided_iids_.insert(ins.iid);
         tok_[ins.iid] = deps;
         st_.staging_elided++;
         return;

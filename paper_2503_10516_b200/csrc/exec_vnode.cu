@@ -193,9 +193,15 @@ void Executor::resolve_sends(const Instr& ins) {
         // inputs (its token until resolved), not the first send's pull: waiting
         // for that pull could deadlock when both go to one receiver, whose
         // receive waits for every send of its region to be posted
-        auto sg = staged_.find(j);
-        if (ins.kind == IKind::Send && sg != staged_.end() && sg->second.ins.dst_aid == ins.src_aid) continue;
-        if (ins.kind == IKind::Send && j == direct_staged_) continue;
+        // an elided staging copy waits for the pulls that read its source
+        // allocation only for instructions that may write that allocation:
+        // sends, receives and copies into M1 need the copy's inputs (its token),
+        // and waiting for a pull there could deadlock when the receiver's
+        // receive waits for a send this node posts later
+        if (elided_iids_.count(j) && (ins.kind == IKind::Send || ins.kind == IKind::Receive ||
+                                       ins.kind == IKind::SplitReceive || ins.kind == IKind::AwaitReceive ||
+                                       (ins.kind == IKind::Copy && ins.dst_mem == 1)))
+            continue;
         const std::vector<uint64_t> msgs = it->second;
         pending_send_.erase(it);
         Token t = tok_.count(j) ? tok_[j] : Token{};

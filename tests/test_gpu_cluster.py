@@ -110,15 +110,15 @@ def test_degenerate_shapes(cel):
 
 @pytest.mark.parametrize("direct", [True, False])
 def test_device_direct_sends(cel, direct, monkeypatch):
-    """SURVEY NEXT-1 as written (the paper's RDMA future work), opt-in
-    CEL_DIRECT_SENDS=1: a push's staging copy into M1 is not executed; its
+    """SURVEY NEXT-1 as written (the paper's RDMA future work; default
+    in virtual-node mode, CEL_DIRECT_SENDS=0 turns it off): a push's staging
+    copy into M1 is not executed; its
     sends publish the device allocation and the receiver pulls from it
     (NVLink between GPUs); a send spanning several devices' staged boxes, or
     any other use of the staged M1 bytes, executes the copies first.  Logs
     unchanged (the graph still has the staging copy), bytes bit-exact on the
     configs' stencil, N-body, RSim and 3-D programs (random programs: below)."""
-    if direct:
-        monkeypatch.setenv("CEL_DIRECT_SENDS", "1")
+    monkeypatch.setenv("CEL_DIRECT_SENDS", "1" if direct else "0")
     n = torch.cuda.device_count()
     devs2 = [0, 1 % n]
     for prog, N, D, devs in ((P.wavesim(1024, 7, rows=300), 2, 1, devs2), (P.nbody(2048, 2), 2, 1, devs2),
