@@ -59,11 +59,15 @@ def run(nodes, D, workload, steps, warmup, n):
     st1 = rt.stats()
     rt.shutdown()
     d = {k: st1[k] - st0[k] for k in ("n_send", "n_receive", "n_split_receive", "n_await_receive", "pulls",
-                                       "pull_bytes", "copies_coherence", "bytes_coherence", "bytes_d2d_peer")}
+                                       "pull_bytes", "copies_coherence", "bytes_coherence", "bytes_d2d_peer",
+                                       "staging_elided", "staging_materialized")}
     return {"nodes": nodes, "devices_per_node": D, "gpus": G, "workload": workload, "n": n, "steps": steps,
             "steps_per_s": steps / dt, "ms_per_step": dt * 1e3 / steps,
             "sends_per_step": d["n_send"] / steps, "pull_bytes_per_step": d["pull_bytes"] / steps,
-            "pull_GBps": d["pull_bytes"] / dt / 1e9, "peer_bytes_per_step": d["bytes_d2d_peer"] / steps}
+            "pull_GBps": d["pull_bytes"] / dt / 1e9, "peer_bytes_per_step": d["bytes_d2d_peer"] / steps,
+            "staging_copies_elided_per_step": d["staging_elided"] / steps,
+            "staging_copies_executed_late_per_step": d["staging_materialized"] / steps,
+            "direct_sends": os.environ.get("CEL_DIRECT_SENDS", "1") != "0"}
 
 
 def main():
