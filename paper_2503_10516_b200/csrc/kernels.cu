@@ -257,6 +257,10 @@ __global__ void __launch_bounds__(32) copy_kernel_tmap(const __grid_constant__ T
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     };
     const uint64_t first = blockIdx.x, step = gridDim.x;
+    // bring this launch's descriptors into the TMA unit's cache up front (they
+    // live in the kernel parameters: a cold fetch at the first load of each)
+    for (int q = 0; q < 2 * a.nseg; ++q)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&a.map[q])) : "memory");
     for (int k = 0; k < kTmStages; ++k) {
         const uint64_t t = first + uint64_t(k) * step;
         if (t >= a.total_tiles) break;
