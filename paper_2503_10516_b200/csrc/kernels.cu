@@ -197,8 +197,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
         : "memory");
 }
 
-constexpr int kTmStages = 6;                 // x 16 KiB tiles in flight per CTA
-constexpr int kTmPend = 3;                   // of which up to 3 stores still reading shared memory
+// kTmStages x 16 KiB tiles in flight per CTA, of which kTmPend stores may
+// still be reading shared memory (6 / 3, 2 CTAs per SM)
 constexpr uint32_t kTmTileBytes = 16384;
 
 // One elected thread per CTA streams tiles: TMA tensor load into a stage of the
@@ -206,6 +206,7 @@ constexpr uint32_t kTmTileBytes = 16384;
 // store of the stage into the destination map.  A stage is refilled one tile
 // later than the store that drains it, so a store and kTmStages - 1 loads are
 // in flight at any time.  Tiles t = blockIdx.x + k * gridDim.x.
+template <int kTmStages, int kTmPend>
 __global__ void __launch_bounds__(32) copy_kernel_tmap(const __grid_constant__ TmaCopyArgs a) {
     extern __shared__ __align__(128) unsigned char tbuf[];
     __shared__ __align__(8) uint64_t tbar[kTmStages];
@@ -1270,13 +1271,13 @@ int launch_copy_tma(const TmaCopyArgs& a, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev >= 0 && dev < 64 && !attr_set[dev]) {   // function attributes are per device
-        cudaFuncSetAttribute(copy_kernel_tmap, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kTmStages * kTmTileBytes));
+        cudaFuncSetAttribute(copy_kernel_tmap<6, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(6 * kTmTileBytes));
         attr_set[dev] = true;
     }
-    // two CTAs per SM (2 x 96 KiB of stages), persistent over the tiles
+    // persistent over the tiles, 2 CTAs per SM x 6 stages (3 x 4 measured the same)
     int64_t grid = int64_t(num_sms()) * 2;
     if (int64_t(a.total_tiles) < grid) grid = int64_t(a.total_tiles);
-    copy_kernel_tmap<<<unsigned(grid), 32, kTmStages * kTmTileBytes, s>>>(a);
+    copy_kernel_tmap<6, 3><<<unsigned(grid), 32, 6 * kTmTileBytes, s>>>(a);
     return 1;
 }
 
