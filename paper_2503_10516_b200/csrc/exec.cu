@@ -179,8 +179,6 @@ Executor::Executor(const ExecConfig& cfg, Scheduler* sched) : cfg_(cfg), sched_(
     tma_copy_ = cv && cv[0] == 't';
     const char* fp = getenv("CEL_FORCE_PEER");
     force_peer_ = fp && fp[0] == '1';
-    const char* sc = getenv("CEL_SHELL_ON_COMPUTE");
-    shell_on_compute_ = sc && sc[0] == '1';
     const char* ns = getenv("CEL_NO_SPLIT");
     split_ = !(ns && ns[0] == '1');
     const char* ng = getenv("CEL_NO_GROW");

@@ -452,7 +452,6 @@ private:
     std::vector<uint32_t> host_drop_;
     bool trace_ = false;
     bool split_ = true;
-    bool shell_on_compute_ = false;              // CEL_SHELL_ON_COMPUTE=1 (A/B)
     bool peer_dma_ = true;                        // small contiguous pushes on a copy engine (CEL_PEER_DMA=0: off)
     uint64_t peer_dma_max_ = 4ull << 20;
     int kernel_variant_ = 0;                      // KArgs::variant (CEL_JACOBI=l, CEL_RSIM=0 for A/B)

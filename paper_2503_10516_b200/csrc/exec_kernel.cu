@@ -170,11 +170,12 @@ void Executor::exec_kernel(const Instr& ins) {
         tok_[ins.iid] = record(sidx);
         return;
     }
-    // shell launches: every dependency (they read the incoming halos); on the
-    // high-priority halo stream, or (CEL_SHELL_ON_COMPUTE=1, A/B) ahead of the
-    // interior on the compute stream, which saves the interior's cross-stream
-    // wait for the previous step's shell but makes it wait for the halos
-    const int hidx = shell_on_compute_ ? sidx : dev * kStreamsPerDev + S_HALO;
+    // shell launches: every dependency (they read the incoming halos), on the
+    // high-priority halo stream.  (Measured and rejected in round 2: shells
+    // ahead of the interior on the compute stream -- no cross-stream wait for
+    // the interior, but it then waits for the halos: 6.9k vs 7.5k steps/s at
+    // 4 B200, 3.97k vs 4.04k at 2.)
+    const int hidx = dev * kStreamsPerDev + S_HALO;
     wait_token(hidx, deps);
     std::vector<Box> shell;
     subtract_into(ins.chunk, interior, shell);

@@ -14,10 +14,13 @@ COLORS = {"wave5": "#4e79a7", "shell": "#f28e2b", "copy_peer": "#e15759", "copy"
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    argv = sys.argv[1:]
     window = 600.0
-    if "--window-us" in sys.argv:
-        window = float(sys.argv[sys.argv.index("--window-us") + 1])
+    if "--window-us" in argv:
+        i = argv.index("--window-us")
+        window = float(argv[i + 1])
+        argv = argv[:i] + argv[i + 2:]
+    args = argv
     out, files = args[0], args[1:]
     recs = []
     for f in files:
