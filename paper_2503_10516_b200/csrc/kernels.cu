@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <tuple>
 
@@ -951,6 +952,12 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CU
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&rbar[k])) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // programmatic dependent launch: the next row's kernel may be scheduled
+    // now (its prologue above overlaps this kernel's tail); everything below
+    // reads rows the previous kernel wrote, so wait for it to have completed
+    // (a no-op when the launch was not programmatic)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     auto issue = [&](int g) {
         const int st = g % kRS;
@@ -1317,6 +1324,29 @@ bool rsim_tma_ok(const KArgs& a) {
            (reinterpret_cast<uintptr_t>(R0.base) & 15) == 0 && a.t > 0;
 }
 
+// Launch the TMA RSim row kernel, programmatically dependent on the previous
+// kernel of the stream (CEL_PDL=0: ordinary stream order).
+template <bool kPeer>
+void launch_rsim_tma(const CUtensorMap& tm, const KArgs& a, const PeerOut& po, unsigned grid, cudaStream_t s) {
+    static int pdl = -1;
+    if (pdl < 0) {
+        const char* e = getenv("CEL_PDL");
+        pdl = (e && e[0] == '0') ? 0 : 1;
+    }
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kRC);
+    cfg.dynamicSmemBytes = size_t(kRS) * kRR * kRB * sizeof(float);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, rsim_row_tma_t<kPeer>, tm, a, po);
+}
+
 bool rsim_fusable(const KArgs& a) {
     CUtensorMap tm;
     return a.kind == K_RSIM_ROW && vol(a.chunk) > 0 && rsim_tma_ok(a) && rsim_tensor_map(a.acc[0], &tm);
@@ -1326,7 +1356,7 @@ int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s) {
     CUtensorMap tm;
     if (!rsim_fusable(a) || !rsim_tensor_map(a.acc[0], &tm)) return 0;
     const unsigned grid = unsigned((vol(a.chunk) + kRC - 1) / kRC);
-    rsim_row_tma_t<true><<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a, po);
+    launch_rsim_tma<true>(tm, a, po, grid, s);
     return 1;
 }
 
@@ -1439,8 +1469,8 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         if (rsim_tma_ok(a) && rsim_tensor_map(R0, &tm)) {
             const unsigned grid = unsigned((cv + kRC - 1) / kRC);
             PeerOut none;
-            none.n = 0;
-            rsim_row_tma_t<false><<<grid, kRC, size_t(kRS) * kRR * kRB * sizeof(float), s>>>(tm, a, none);
+            memset(&none, 0, sizeof none);
+            launch_rsim_tma<false>(tm, a, none, grid, s);
             return 1;
         }
         rsim_row_kernel<16><<<grid_for(cv, 128), 128, 0, s>>>(a);
