@@ -512,6 +512,9 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
     const int64_t poff = c - P.lo[1];
     auto urow = [&](int64_t r) { return ub + (r - U.lo[0]) * U.n[1]; };
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    // programmatic dependent launch (see launch_wave5): the previous step wrote u
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     float4 prev = z4, cur = z4;
     if (valid) {
         prev = __ldg(reinterpret_cast<const float4*>(urow(rs > 0 ? rs - 1 : 0) + uoff));
@@ -1410,7 +1413,22 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             KArgs b = a;
             b.strip = int(h);
             dim3 grid(unsigned(cols), unsigned((rows + h - 1) / h));
-            wave5_vec<<<grid, 128, 0, s>>>(b);
+            static int pdl = -1;
+            if (pdl < 0) {
+                const char* e = getenv("CEL_PDL");
+                pdl = (e && e[0] == '0') ? 0 : 1;
+            }
+            cudaLaunchConfig_t cfg;
+            memset(&cfg, 0, sizeof cfg);
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(128);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = pdl ? 1 : 0;
+            cudaLaunchKernelEx(&cfg, wave5_vec, b);
         } else {
             wave5_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);
         }
