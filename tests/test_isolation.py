@@ -81,3 +81,17 @@ def test_workloads_and_oracle_are_independent():
         if f.endswith(".py"):
             mods = imported(ast.parse(open(os.path.join(ROOT, "oracle", f)).read()))
             assert not mods & {"workloads", "paper_2503_10516_b200"}, f
+
+
+def test_only_test_infrastructure_imports_the_oracle():
+    """Outside oracle/ and tests/, only bench.py's CPU arms (checked above)
+    and __graft_entry__.smoke() import the oracle: tools/ and workloads/ do not."""
+    for d in ("tools", "workloads", "paper_2503_10516_b200"):
+        for dirpath, _, files in os.walk(os.path.join(ROOT, d)):
+            for f in files:
+                if f.endswith(".py"):
+                    p = os.path.join(dirpath, f)
+                    assert oracle_imports(ast.parse(open(p).read())) == [], p
+    tree = ast.parse(open(os.path.join(ROOT, "__graft_entry__.py")).read())
+    for fn, line in oracle_imports(tree):
+        assert fn == "smoke", line

@@ -2,7 +2,7 @@
 every kernel family, resize copies, d2d copies between virtual devices, the
 shell/interior split, TMA Jacobi, H2D/D2H."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 from paper_2503_10516_b200 import cel
 from oracle.scheduler import Runtime as ORt

@@ -1,7 +1,7 @@
 """Run one program on virtual devices of GPU 0 and compare with the oracle
 (debug helper: one program per process, so a sticky CUDA error names it).
 
-  python tools/tma_debug.py <case> [G]      env: CEL_COPY=tma etc. as needed
+  python tests/tools/tma_debug.py <case> [G]      env: CEL_COPY=tma etc. as needed
 """
 import json
 import os
@@ -9,7 +9,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 from oracle.scheduler import Runtime as OracleRuntime  # noqa: E402
 from oracle.simulate import simulate  # noqa: E402

@@ -2,7 +2,7 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 export CUDA_LAUNCH_BLOCKING=1 CEL_EXEC_THREAD=0
 for c in "jac36 4" "jac20 5" "ws2d_axes 2" "ws2d_axes 4" "ws2d_box 2 none" "ws2d_box 4 none" "rand0 2 none" "rand1 4 none" "rand2 2 none" "rand3 4 none"; do
-  CEL_COPY=tma CEL_NO_GROW=1 timeout 120 python tools/tma_debug.py $c 2>&1 | tail -2
+  CEL_COPY=tma CEL_NO_GROW=1 timeout 120 python tests/tools/tma_debug.py $c 2>&1 | tail -2
 done
 unset CUDA_LAUNCH_BLOCKING CEL_EXEC_THREAD
 for v in 0 1; do

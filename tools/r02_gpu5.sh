@@ -2,7 +2,7 @@
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
 export CUDA_LAUNCH_BLOCKING=1 CEL_EXEC_THREAD=0
 for c in "ws2d_axes 4" "ws2d_box 4 none" "rand1 4 none" "rand4 4 none" "rand5 3 none" "rand6 4 auto" "rand7 4 none"; do
-  CEL_COPY=tma CEL_NO_GROW=1 timeout 120 python tools/tma_debug.py $c 2>&1 | tail -1
+  CEL_COPY=tma CEL_NO_GROW=1 timeout 120 python tests/tools/tma_debug.py $c 2>&1 | tail -1
 done
 unset CUDA_LAUNCH_BLOCKING CEL_EXEC_THREAD
 for cfg in "CEL_ROW_ALIGN=16" "CEL_ROW_ALIGN=128" "CEL_ROW_ALIGN=128 CEL_NO_VMM=1"; do

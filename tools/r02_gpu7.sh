@@ -13,7 +13,7 @@ done <<'SHAPES'
 SHAPES
 export CUDA_LAUNCH_BLOCKING=1 CEL_EXEC_THREAD=0
 for c in "ws2d_axes 4" "ws2d_box 4 none" "rand1 4 none" "rand5 3 none"; do
-  CEL_COPY=tma CEL_NO_GROW=1 timeout 120 python tools/tma_debug.py $c 2>&1 | tail -1
+  CEL_COPY=tma CEL_NO_GROW=1 timeout 120 python tests/tools/tma_debug.py $c 2>&1 | tail -1
 done
 unset CUDA_LAUNCH_BLOCKING CEL_EXEC_THREAD
 timeout 1800 python -m pytest tests -m gpu -q --timeout 900 -x > gpurun_out/pytest.log 2>&1
