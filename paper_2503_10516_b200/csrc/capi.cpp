@@ -323,6 +323,8 @@ int cel_stats(cel_runtime* rt, cel_stats_t* o) {
     if (!o) return fail(CEL_E_INVALID, "null argument");
     memset(o, 0, sizeof *o);
     SchedStats s = sched0(rt).stats();
+    o->memo_hits = sched0(rt).memo_hits();
+    o->memo_misses = sched0(rt).memo_misses();
     if (rt->cluster)            // virtual-node mode: totals over the nodes
         for (int k = 1; k < rt->cluster->nodes(); ++k) {
             const SchedStats& x = rt->cluster->node(k).stats();

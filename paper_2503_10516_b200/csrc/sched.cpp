@@ -150,10 +150,14 @@ Box map_access(const Mapper& m, const Box& chunk, const Box& ext) {
     return b;
 }
 
+Scheduler::~Scheduler() = default;
+
 Scheduler::Scheduler(int n_devices, int lookahead, int horizon_step, bool checks, InstrSink* sink, FILE* log)
     : G_(n_devices), mode_(lookahead), checks_(checks), sink_(sink), log_(log), horizon_step_(horizon_step) {
     const char* cm = getenv("CEL_COLL_MIN_BYTES");
     if (cm && cm[0]) coll_min_bytes_ = strtoull(cm, nullptr, 10);
+    const char* mm = getenv("CEL_SCHED_MEMO");
+    if (mm && mm[0] == '0') memo_on_ = false;
     cp_[0] = 0;
     // init epoch: tid 0 / iid 0
     Instr e;
@@ -166,7 +170,6 @@ Scheduler::Scheduler(int n_devices, int lookahead, int horizon_step, bool checks
     if (sink_) sink_->on_instr(e);
 }
 
-Scheduler::~Scheduler() = default;
 
 uint32_t Scheduler::elem_size(uint32_t bid) const { return bufs_.at(bid)->elem_size; }
 Box Scheduler::extent(uint32_t bid) const { return bufs_.at(bid)->extent; }
@@ -341,11 +344,23 @@ int Scheduler::task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string*
     if (shut_) return E_STATE;
     Cmd c;
     c.kind = 0;
-    const int rc = prepare(desc, c, err);
-    if (rc != E_OK) return rc;
     std::map<uint32_t, Region> reads, writes;
-    for (auto& kv : c.reads) reads[kv.first.second] = runion(reads[kv.first.second], kv.second);
-    for (auto& kv : c.writes) writes[kv.first.second] = runion(writes[kv.first.second], kv.second);
+    std::vector<int64_t> key;
+    uint64_t h = 0;
+    if (memo_on_) {   // sched_memo.cpp: a shape seen before reuses its prepare() result
+        shape_key(desc, key);
+        h = memo_hash(key);
+        bool live = true;
+        for (const Access& a : desc.acc) live = live && bufs_.count(a.buf) != 0;
+        if (live) prep_lookup(key, h, c, reads, writes);
+    }
+    if (!c.memo) {
+        const int rc = prepare(desc, c, err);
+        if (rc != E_OK) return rc;
+        for (auto& kv : c.reads) reads[kv.first.second] = runion(reads[kv.first.second], kv.second);
+        for (auto& kv : c.writes) writes[kv.first.second] = runion(writes[kv.first.second], kv.second);
+        if (memo_on_) prep_store(std::move(key), h, c, reads, writes);
+    }
     c.desc = std::make_shared<const TaskDesc>(desc);
     return submit_cmd(std::move(c), reads, writes, tid_out);
 }
@@ -665,13 +680,14 @@ uint64_t Scheduler::emit(Instr& ins, std::vector<uint64_t>& deps) {
     ins.iid = next_iid_++;
     ins.deps = deps;
     // execution front: drop deps, add self
-    std::vector<uint64_t> nf;
-    nf.reserve(front_.size() + 1);
+    std::vector<uint64_t>& nf = front_scratch_;
+    nf.clear();
     std::set_difference(front_.begin(), front_.end(), deps.begin(), deps.end(), std::back_inserter(nf));
     nf.push_back(ins.iid);
     front_.swap(nf);
     st_.n_by_kind[int(ins.kind)]++;
     log_instr(ins);
+    if (recording_) recording_->push_back(ins);
     if (filter_world_ > 1) {
         // all-gather members may run as a collective that every rank takes part
         // in (§8 a7): co-owned, like horizons, so their dependents reach everyone
@@ -1101,7 +1117,29 @@ void Scheduler::transfers(Cmd& c, std::map<Key, Alloc*>& binding, bool readback_
 
 void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Box>& ant) {
     const int64_t tid = c.tid;
+    const uint64_t base = next_iid_;
+    // steady-state fast path (sched_memo.cpp): a recorded compile from the same
+    // state (which fixes the live allocations, so it allocates nothing either)
+    bool memo = memo_on_ && c.memo && c.pushes.empty() && c.awaits.empty() && c.remote_writes.empty();
+    std::vector<int64_t>& sig = sig_scratch_;
+    if (memo) {
+        state_sig(c, base, sig);
+        if (const CompileMemo* m = compile_lookup(*c.memo, sig)) {
+            ++memo_hits_;
+            compile_replay(*m, c, base);
+            return;
+        }
+        ++memo_misses_;
+    }
     std::map<Key, Alloc*> binding = allocate(c, ant);
+    memo = memo && next_iid_ == base;   // record only compiles that allocate nothing
+    std::vector<Instr> rec;
+    SchedStats before;
+    const uint64_t coll_before = next_coll_;
+    if (memo) {
+        before = st_;
+        recording_ = &rec;
+    }
     if (!c.pushes.empty() || !c.awaits.empty()) transfers(c, binding, false);
     // R10 coherence copies; masks as they stood before this task
     std::vector<std::tuple<uint32_t, Region, int>> updates;
@@ -1197,6 +1235,10 @@ void Scheduler::compile_task(Cmd& c, const std::map<std::pair<uint32_t, int>, Bo
         Buf& buf = *bufs_.at(kv.first);
         buf.uptodate.update(kv.second, 0u);
         buf.orig_writer.update(kv.second, NONE);
+    }
+    if (memo) {
+        recording_ = nullptr;
+        compile_store(std::vector<int64_t>(sig), c, base, std::move(rec), before, coll_before);
     }
 }
 

@@ -293,6 +293,8 @@ public:
     void debug_dump(FILE* f) const;
 
 private:
+    struct PrepMemo;                                  // sched_memo.cpp
+    struct CompileMemo;
     struct Alloc {
         int64_t aid;
         uint32_t buffer;
@@ -333,6 +335,7 @@ private:
         // virtual-node mode
         std::vector<Push> pushes;                     // sorted by (target, buffer)
         std::map<uint32_t, Region> awaits, remote_writes;
+        std::shared_ptr<PrepMemo> memo;               // set when its shape was submitted before (sched_memo.cpp)
     };
 
     // task graph (R7)
@@ -395,6 +398,8 @@ private:
     std::map<uint32_t, std::unique_ptr<Buf>> bufs_;
     std::unordered_map<int64_t, std::unique_ptr<Alloc>> allocs_;
     std::vector<uint64_t> front_;                     // sorted
+    std::vector<uint64_t> front_scratch_;
+    std::vector<int64_t> sig_scratch_;                // compile memo signature (sched_memo.cpp)
     uint64_t next_iid_ = 1;
     int64_t fallback_ = 0, pending_h_ = -1;
     int64_t next_aid_ = 1;
@@ -416,6 +421,31 @@ public:
 private:
     uint32_t next_bid_ = 0;
     bool shut_ = false;
+
+    // Steady-state fast path (sched_memo.cpp; DESIGN.md §2 "compile memo").
+    // prepare() results per task shape, and compile_task() results per (task
+    // shape, state of the accessed buffers with instruction ids taken relative
+    // to the next iid): a hit re-emits the recorded instructions with ids
+    // shifted and installs the recorded end state, shifted the same way.
+    std::unordered_map<uint64_t, std::shared_ptr<PrepMemo>> prep_memo_;   // by hash of the shape key
+    bool memo_on_ = true;
+    std::vector<Instr>* recording_ = nullptr;        // emit() copies instructions here while set
+    uint64_t memo_hits_ = 0, memo_misses_ = 0;
+    static void shape_key(const TaskDesc& d, std::vector<int64_t>& key);
+    bool prep_lookup(const std::vector<int64_t>& key, uint64_t h, Cmd& c, std::map<uint32_t, Region>& reads,
+                     std::map<uint32_t, Region>& writes);
+    void prep_store(std::vector<int64_t>&& key, uint64_t h, const Cmd& c, const std::map<uint32_t, Region>& reads,
+                    const std::map<uint32_t, Region>& writes);
+    void state_sig(const Cmd& c, uint64_t base, std::vector<int64_t>& sig) const;
+    static const CompileMemo* compile_lookup(const PrepMemo& p, const std::vector<int64_t>& sig);
+    void compile_replay(const CompileMemo& m, Cmd& c, uint64_t base);
+    void compile_store(std::vector<int64_t>&& sig, const Cmd& c, uint64_t base, std::vector<Instr>&& out,
+                       const SchedStats& before, uint64_t coll_before);
+
+public:
+    uint64_t memo_hits() const { return memo_hits_; }
+    uint64_t memo_misses() const { return memo_misses_; }
+    void set_memo(bool on) { memo_on_ = on; }
 };
 
 // Virtual-node mode (§3.4; mirrors

@@ -14,5 +14,6 @@ int apply_mapper(const Mapper& m, const Box& chunk, const Box& ext, Box* out);  
 int mapper_region(const Mapper& m, const Box& chunk, const Box& ext, Region* out);
 bool is_read(int mode);
 bool is_write(int mode);
+uint64_t memo_hash(const std::vector<int64_t>& v);    // sched_memo.cpp
 }  // namespace detail
 }  // namespace cel

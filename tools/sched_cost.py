@@ -1,4 +1,6 @@
-"""Host cost of IDAG generation per WaveSim step (execute=0: no GPU touched), G = 1, 2, 4, 8."""
+"""Host cost of IDAG generation per WaveSim step (execute=0: no GPU touched), G = 1, 2, 4, 8,
+through the Python binding.  CEL_SCHED_MEMO=0 switches the steady-state compile memo off;
+tools/sched_prof.cpp measures the scheduler alone (no Python)."""
 import sys, time
 sys.path.insert(0, "/root/repo")
 from paper_2503_10516_b200 import cel
@@ -17,5 +19,6 @@ for G in (1, 2, 4, 8):
     for s in range(K): rt.submit_desc(descs[s % 2][0])
     rt.wait()
     dt = time.perf_counter() - t0
-    print(G, "%.1f us/step" % (dt / K * 1e6))
+    st = rt.stats()
+    print(G, "%.1f us/step" % (dt / K * 1e6), "memo hits %d misses %d" % (st["memo_hits"], st["memo_misses"]))
     rt.shutdown()

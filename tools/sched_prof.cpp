@@ -1,0 +1,81 @@
+// Host cost of IDAG generation per WaveSim step, without Python or CUDA: the
+// scheduler alone (sched.cpp) with a counting sink, G devices, optionally the
+// multi-process rank filter.  Build and run (CEL_SCHED_MEMO=0: no memo):
+//   g++ -O2 -std=c++17 -Ipaper_2503_10516_b200/csrc tools/sched_prof.cpp paper_2503_10516_b200/csrc/sched.cpp
+//       paper_2503_10516_b200/csrc/sched_memo.cpp -o /tmp/sched_prof && /tmp/sched_prof 8 [rank]
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "sched.hpp"
+
+using namespace cel;
+
+struct Count : InstrSink {
+    uint64_t n = 0;
+    void on_instr(const Instr&) override { ++n; }
+};
+
+static TaskDesc fill(int64_t n, uint32_t buf) {
+    TaskDesc d;
+    d.dims = 2;
+    const int64_t lo[3] = {0, 0, 0}, hi[3] = {n, n, 1};
+    d.range = Box::make(lo, hi);
+    d.kernel = 0;
+    Access a;
+    a.buf = buf;
+    a.mode = MODE_WRITE;
+    d.acc.push_back(a);
+    return d;
+}
+
+static TaskDesc wave(int64_t n, int k) {
+    TaskDesc d;
+    d.dims = 2;
+    const int64_t lo[3] = {0, 0, 0}, hi[3] = {n, n, 1};
+    d.range = Box::make(lo, hi);
+    d.kernel = 3;
+    const uint32_t u = k % 2 == 0 ? 0 : 1, up = 1 - u;
+    Access r;
+    r.buf = u;
+    r.mode = MODE_READ;
+    r.map.kind = MapKind::Neighborhood;
+    r.map.border[0] = r.map.border[1] = 1;
+    Access w;
+    w.buf = up;
+    w.mode = MODE_READ_WRITE;
+    d.acc.push_back(r);
+    d.acc.push_back(w);
+    return d;
+}
+
+int main(int argc, char** argv) {
+    const int G = argc > 1 ? atoi(argv[1]) : 8;
+    const int rank = argc > 2 ? atoi(argv[2]) : -1;
+    const int K = argc > 3 ? atoi(argv[3]) : 20000;
+    const int64_t n = 16384;
+    Count sink;
+    Scheduler s(G, 1, 4, true, &sink, nullptr);
+    if (rank >= 0) s.set_rank_filter(rank, G);
+    const int64_t ext[3] = {n, n, 1};
+    uint32_t b0, b1;
+    s.buffer_create(2, ext, 4, false, &b0);
+    s.buffer_create(2, ext, 4, false, &b1);
+    std::string err;
+    uint64_t tid;
+    s.task_submit(fill(n, 0), &tid, &err);
+    s.task_submit(fill(n, 1), &tid, &err);
+    const TaskDesc w[2] = {wave(n, 0), wave(n, 1)};
+    for (int k = 0; k < 200; ++k) s.task_submit(w[k % 2], &tid, &err);
+    s.wait();
+    const uint64_t n0 = sink.n;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int k = 0; k < K; ++k) s.task_submit(w[k % 2], &tid, &err);
+    s.wait();
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    printf("G=%d rank=%d: %.2f us/step, %.1f instructions/step, memo %llu hits %llu misses\n", G, rank, dt / K * 1e6,
+           double(sink.n - n0) / K, (unsigned long long)s.memo_hits(), (unsigned long long)s.memo_misses());
+    s.shutdown();
+    return 0;
+}
