@@ -487,7 +487,33 @@ struct RegionMap {
     void map_values(F fn) {
         std::vector<Entry> old;
         old.swap(e);
-        for (auto& p : old) put(fn(p.first), p.second);
+        // a non-decreasing fn (the horizon renaming, R7) keeps the order: equal
+        // new values are adjacent, and their regions (disjoint) merge in one canon
+        bool mono = true;
+        for (size_t i = 1; i < old.size() && mono; ++i) mono = !(fn(old[i].first) < fn(old[i - 1].first));
+        if (!mono) {
+            for (auto& p : old) put(fn(p.first), p.second);
+            return;
+        }
+        e.reserve(old.size());
+        for (size_t i = 0; i < old.size();) {
+            const V v = fn(old[i].first);
+            size_t j = i + 1;
+            while (j < old.size() && fn(old[j].first) == v) ++j;
+            if (j == i + 1) {
+                old[i].first = v;
+                e.push_back(std::move(old[i]));
+            } else {
+                Region all;
+                Box bb;
+                for (size_t k = i; k < j; ++k) {
+                    all.insert(all.end(), old[k].second.begin(), old[k].second.end());
+                    bb = bbox(bb, old[k].bb);
+                }
+                e.push_back(Entry{v, canon(std::move(all)), bb});
+            }
+            i = j;
+        }
     }
 
     // Partition of reg by value, sorted by value.

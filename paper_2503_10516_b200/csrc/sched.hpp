@@ -139,19 +139,26 @@ struct ReaderList {
                 any = true;
             }
         if (!any) return;
-        // merge records of equal id (keeps the list bounded across horizons)
+        // merge records of equal id (keeps the list bounded across horizons):
+        // the boxes of every record of an id gathered, one canon per merged id
         std::vector<Rec> out;
+        std::vector<Region> extra;        // boxes to add to out[i]
         for (Rec& x : recs) {
-            bool merged = false;
-            for (Rec& y : out)
-                if (y.id == x.id) {
-                    y.r = runion(y.r, x.r);
-                    y.bb = bbox(y.bb, x.bb);
-                    merged = true;
-                    break;
-                }
-            if (!merged) out.push_back(std::move(x));
+            size_t k = 0;
+            while (k < out.size() && out[k].id != x.id) ++k;
+            if (k == out.size()) {
+                out.push_back(std::move(x));
+                extra.emplace_back();
+            } else {
+                extra[k].insert(extra[k].end(), x.r.begin(), x.r.end());
+                out[k].bb = bbox(out[k].bb, x.bb);
+            }
         }
+        for (size_t k = 0; k < out.size(); ++k)
+            if (!extra[k].empty()) {
+                extra[k].insert(extra[k].end(), out[k].r.begin(), out[k].r.end());
+                out[k].r = canon(std::move(extra[k]));
+            }
         recs.swap(out);
     }
     template <class F>

@@ -3,6 +3,7 @@
 // multi-process rank filter.  Build and run (CEL_SCHED_MEMO=0: no memo):
 //   g++ -O2 -std=c++17 -Ipaper_2503_10516_b200/csrc tools/sched_prof.cpp paper_2503_10516_b200/csrc/sched.cpp
 //       paper_2503_10516_b200/csrc/sched_memo.cpp -o /tmp/sched_prof && /tmp/sched_prof 8 [rank]
+//   /tmp/sched_prof rsim 4 [rank] [T]      (RSim rows, W = 84,000)
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -50,7 +51,59 @@ static TaskDesc wave(int64_t n, int k) {
     return d;
 }
 
+// RSim row t (programs.rsim_row): read rows [0,t) (fixed), write row t (remap kernel dim 0 -> dim 1)
+static TaskDesc rsim_row(int64_t W, int64_t t) {
+    TaskDesc d;
+    d.dims = 1;
+    const int64_t lo[3] = {0, 0, 0}, hi[3] = {W, 1, 1};
+    d.range = Box::make(lo, hi);
+    d.kernel = 7;
+    Access r;
+    r.buf = 0;
+    r.mode = MODE_READ;
+    r.map.kind = MapKind::Fixed;
+    const int64_t flo[3] = {0, 0, 0}, fhi[3] = {t, W, 1};
+    r.map.fixed = Box::make(flo, fhi);
+    Access w;
+    w.buf = 0;
+    w.mode = MODE_WRITE;
+    w.map.kind = MapKind::Remap;
+    w.map.fixed.lo[0] = t;
+    w.map.fixed.hi[0] = t + 1;
+    w.map.fixed.hi[2] = 1;
+    w.map.from_kernel_dim[1] = 0;
+    d.acc.push_back(r);
+    d.acc.push_back(w);
+    return d;
+}
+
+static int rsim_main(int G, int rank, int T) {
+    const int64_t W = 84000;
+    Count sink;
+    Scheduler s(G, 1, 4, true, &sink, nullptr);
+    if (rank >= 0) s.set_rank_filter(rank, G);
+    const int64_t ext[3] = {T, W, 1};
+    uint32_t b0;
+    s.buffer_create(2, ext, 4, false, &b0);
+    std::string err;
+    uint64_t tid;
+    TaskDesc f = rsim_row(W, 0);
+    f.acc.erase(f.acc.begin());
+    f.kernel = 0;
+    s.task_submit(f, &tid, &err);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int t = 1; t < T; ++t) s.task_submit(rsim_row(W, t), &tid, &err);
+    s.wait();
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    printf("rsim G=%d rank=%d T=%d: %.2f us/row, %.1f instructions/row\n", G, rank, T, dt / (T - 1) * 1e6,
+           double(sink.n) / (T - 1));
+    s.shutdown();
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "rsim")
+        return rsim_main(argc > 2 ? atoi(argv[2]) : 4, argc > 3 ? atoi(argv[3]) : -1, argc > 4 ? atoi(argv[4]) : 1024);
     const int G = argc > 1 ? atoi(argv[1]) : 8;
     const int rank = argc > 2 ? atoi(argv[2]) : -1;
     const int K = argc > 3 ? atoi(argv[3]) : 20000;
