@@ -211,6 +211,8 @@ typedef struct cel_stats_s {
     uint64_t staging_materialized;        /* ... of which executed late (their M1 bytes were needed after all) */
     uint64_t coll_p2p;                    /* all-gather sets run as P2P gather kernels (stores into every receiver) */
     uint64_t coll_fused;                  /* ... fused into the RSim row kernels that produce them */
+    uint64_t halo_fused;                  /* coherence copies stored by the stencil launch that writes their rows */
+    uint64_t halo_in_waits;               /* incoming copies awaited by the reading CTAs of a fused launch */
     uint64_t memo_hits, memo_misses;      /* task compiles replayed from the steady-state memo / recorded into it
                                              (CEL_SCHED_MEMO=0 disables it; the instructions are the same) */
 } cel_stats_t;

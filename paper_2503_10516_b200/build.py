@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libcel.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["sched.cpp", "sched_memo.cpp", "cluster.cpp", "capi.cpp", "exec.cu", "exec_copy.cu", "exec_kernel.cu", "exec_coll.cu", "exec_mc.cu", "exec_fuse.cu", "exec_vnode.cu",
+SOURCES = ["sched.cpp", "sched_memo.cpp", "cluster.cpp", "capi.cpp", "exec.cu", "exec_copy.cu", "exec_kernel.cu", "exec_coll.cu", "exec_mc.cu", "exec_fuse.cu", "exec_halo.cu", "exec_vnode.cu",
            "kernels.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
          "-Xcompiler", "-fPIC,-O3,-Wall", "-I" + os.path.join(ROOT, "include")]

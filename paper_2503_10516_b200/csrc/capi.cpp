@@ -387,6 +387,8 @@ int cel_stats(cel_runtime* rt, cel_stats_t* o) {
         o->coll_multicast += e.coll_multicast;
         o->coll_p2p += e.coll_p2p;
         o->coll_fused += e.coll_fused;
+        o->halo_fused += e.halo_fused;
+        o->halo_in_waits += e.halo_in_waits;
         o->staging_elided += e.staging_elided;
         o->staging_materialized += e.staging_materialized;
     }

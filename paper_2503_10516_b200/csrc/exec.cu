@@ -462,6 +462,18 @@ int Executor::init(std::string* err) {
     cudaDeviceSynchronize();
     const char* et = getenv("CEL_EXEC_THREAD");
     if (!(cfg_.comm || !(et && et[0] == '0'))) fuse_rows_ = false;   // parking needs the executor thread's drains
+    {
+        // halo pushes fused into the stencil (exec_halo.cu): one process per
+        // GPU, every GPU distinct (in-kernel waits across processes sharing
+        // a GPU are unsafe), the executor thread (a drain releases held-back
+        // work), 64-bit flags
+        bool distinct = true;
+        for (int a = 0; a < G_; ++a)
+            for (int b = a + 1; b < G_; ++b)
+                if (phys_[a] == phys_[b]) distinct = false;
+        const char* fh = getenv("CEL_FUSE_HALO");
+        fuse_halo_ = cfg_.world > 1 && G_ >= 2 && distinct && !cfg_.comm && !(et && et[0] == '0') && fh && fh[0] == '1';
+    }
     if (cfg_.comm || !(et && et[0] == '0')) {   // nodes must progress independently
         threaded_ = true;
         thr_ = std::thread([this] { thread_main(); });
@@ -1044,7 +1056,8 @@ void Executor::thread_main() {
         } else if (it.kind == 1) {
             it.fn();
         } else {
-            flush_parked();                              // a drain / epoch wait: nothing stays held back
+            halo_flush();                                // a drain / epoch wait: nothing stays held back
+            flush_parked();
             if (!deferred_signals_.empty()) flush_deferred_signals();
             publish_stats();
             {
@@ -1115,6 +1128,28 @@ void Executor::on_instr_impl(const Instr& ins) {
         settle_tok_ = Token{};
     }
     if (!pending_send_.empty()) resolve_sends(ins);
+    // WaveSim halo exchange fused into the stencil launches (exec_halo.cu)
+    if (fuse_halo_ && !halo_flushing_) {
+        if (halo_parked_) {
+            if (halo_attach(ins)) return;
+            const bool dep = halo_depends(ins);
+            if (ins.kind == IKind::Horizon && dep && halo_deferred_.size() < 4) {
+                halo_deferred_.push_back(ins);           // waits with the held-back kernel
+                halo_iids_.insert(ins.iid);
+                return;
+            }
+            if (dep || ins.kind == IKind::Horizon || ins.kind == IKind::Epoch) {
+                halo_flush();
+                cur_ins_ = &ins;
+            }
+        }
+        if (halo_candidate(ins)) {
+            halo_kernel_ = ins;
+            halo_parked_ = true;
+            halo_iids_.insert(ins.iid);
+            return;
+        }
+    }
     // rows fused with their gathers (exec_fuse.cu): hold back a fusable row
     // kernel, and whatever depends on something held back, except the
     // all-gather members (held as a set anyway)

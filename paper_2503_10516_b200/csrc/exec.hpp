@@ -18,6 +18,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <array>
 #include <deque>
 #include <functional>
 #include <mutex>
@@ -125,6 +126,8 @@ struct ExecStats {
     uint64_t coll_multicast = 0;                    // all-gather sets run as NVLS multicast stores
     uint64_t coll_p2p = 0;                          // ... as P2P gather kernels
     uint64_t coll_fused = 0;                        // ... fused into the RSim row kernels that produce them
+    uint64_t halo_fused = 0;                        // coherence copies stored by the stencil launch that writes them
+    uint64_t halo_in_waits = 0;                     // incoming copies awaited inside the consuming launch
     uint64_t staging_elided = 0, staging_materialized = 0;   // device-direct sends (virtual-node mode)
     uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
@@ -366,6 +369,19 @@ private:
     bool try_fuse(const std::vector<Instr>& m);
     void signal_one(uint64_t j, int jo, int o);
     void flush_deferred_signals();
+    // WaveSim halo exchange fused into the stencil launches (exec_halo.cu)
+    bool fuse_halo_ = false;                      // CEL_FUSE_HALO: multi-process, distinct GPUs
+    bool halo_parked_ = false, halo_flushing_ = false;
+    Instr halo_kernel_;                           // the held-back stencil instruction
+    std::vector<Instr> halo_pushes_;              // its outgoing coherence copies
+    std::vector<Instr> halo_deferred_;            // horizons that arrived in between
+    std::unordered_set<uint64_t> halo_iids_;
+    std::vector<std::array<unsigned, kHaloMax>> halo_ctr_;   // per device: CTA counters' host copies
+    bool halo_candidate(const Instr& ins);
+    bool halo_attach(const Instr& ins);
+    bool halo_depends(const Instr& ins) const;
+    bool halo_launch(const Instr& k, const std::vector<Instr>& pushes);
+    void halo_flush();
     bool p2p_gather_ = false;                     // gather sets as P2P gather kernels (CEL_COLL_P2P=0: off)
     uint64_t gather_off_ = 0;                     // per device arena: gather counter word (+64: CTA counter)
     std::vector<uint64_t> gather_exp_;            // per device: chunks received by P2P gathers so far

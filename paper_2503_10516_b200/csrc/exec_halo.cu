@@ -1,0 +1,200 @@
+// Executor: WaveSim's halo exchange fused into the stencil launches (SURVEY §7
+// step 6 and NEXT-2; §5 WaveSim strong scaling, L490 §3.6: the
+// coherence copies between neighbouring devices are the per-step overhead).
+//
+// Multi-process runs on distinct GPUs.  A wave5 kernel instruction this rank
+// executes is held back until the next instruction that depends on it: the
+// coherence copies that push its boundary rows to the neighbours (emitted at
+// the start of the next task's compilation) attach to it, horizons in between
+// wait with it.  The launch (`launch_wave5_halo`) then
+//   - stores each attached copy's rows from the CTAs that compute them
+//     straight into the receiver's allocation (IPC-mapped peer memory over
+//     NVLink), after the copy's remote dependencies -- readers of the
+//     receiver's rows, whose flags arrive in this GPU's slots -- and the last
+//     such CTA writes the receiver's flag slot with the copy's id: exactly
+//     what the copy and its signal would have done;
+//   - awaits each incoming copy (a neighbour's push into rows this launch
+//     reads) in the CTAs that read those rows, not on the stream: interior
+//     CTAs never wait, and consecutive steps follow each other on the compute
+//     stream with programmatic dependent launch.
+// Same instructions, same dependencies, same flags; the instruction graph and
+// its log are unchanged.  Anything else that depends on the held-back work
+// releases it first; anything the fused launch cannot express (a copy that is
+// not a whole-row band of the chunk, too many flags) runs the ordinary way.
+#include "exec_impl.hpp"
+
+namespace cel {
+
+bool Executor::halo_depends(const Instr& ins) const {
+    for (uint64_t j : ins.deps)
+        if (halo_iids_.count(j)) return true;
+    return false;
+}
+
+// A wave5 instruction this rank launches whose vector kernel applies.
+bool Executor::halo_candidate(const Instr& ins) {
+    if (!fuse_halo_ || halo_flushing_ || ins.kind != IKind::Kernel || !ins.desc || ins.desc->kernel != K_WAVE5)
+        return false;
+    if (owner_rank(ins.device) != cfg_.rank || cfg_.bounds_check) return false;
+    KArgs a;
+    build_kargs(ins, a);
+    unsigned gx = 0, gy = 0;
+    return wave5_strip(a, &gx, &gy) > 0;
+}
+
+// A coherence copy of rows the held-back kernel writes, into another GPU.
+bool Executor::halo_attach(const Instr& ins) {
+    const Instr& k = halo_kernel_;
+    if (ins.kind != IKind::Copy || ins.coll_n || int(halo_pushes_.size()) >= kHaloMax) return false;
+    if (ins.src_mem - 2 != k.device || ins.dst_mem < 2 || owner_rank(ins.dst_mem - 2) == cfg_.rank) return false;
+    if (phys_[ins.dst_mem - 2] == phys_[k.device] || ins.src_aid != k.bindings[1] || ins.region.size() != 1) return false;
+    if (std::find(ins.deps.begin(), ins.deps.end(), k.iid) == ins.deps.end()) return false;
+    for (uint64_t j : ins.deps)
+        if (j != k.iid && halo_iids_.count(j)) return false;
+    const Box& b = ins.region[0];
+    if (b.lo[1] != k.chunk.lo[1] || b.hi[1] != k.chunk.hi[1] || b.lo[0] < k.chunk.lo[0] || b.hi[0] > k.chunk.hi[0] ||
+        b.extent(2) != 1)
+        return false;
+    auto d = allocs_.find(ins.dst_aid);
+    if (d == allocs_.end() || d->second.es != 4 || d->second.box.extent(2) != 1 || d->second.box.extent(1) % 4 ||
+        (b.lo[1] - d->second.box.lo[1]) % 4 || (reinterpret_cast<uintptr_t>(base_of(d->second)) & 15))
+        return false;
+    halo_pushes_.push_back(ins);
+    halo_iids_.insert(ins.iid);
+    return true;
+}
+
+// Launch the held-back kernel with its pushes, or say it cannot.
+bool Executor::halo_launch(const Instr& k, const std::vector<Instr>& pushes) {
+    const int dev = k.device;
+    const int sidx = dev * kStreamsPerDev + S_COMPUTE;
+    KArgs a;
+    build_kargs(k, a);
+    unsigned gx = 0, gy = 0;
+    const int64_t h = wave5_strip(a, &gx, &gy);
+    if (h <= 0) return false;
+    HaloArgs hx;
+    memset(&hx, 0, sizeof hx);
+    Token t;
+    // incoming: the kernel's dependencies on other ranks' copies into the
+    // allocation it reads u from (their rows), awaited by the reading CTAs
+    cur_ins_ = &k;
+    for (uint64_t j : k.deps) {
+        Token dt = dep_token(j);
+        auto ci = copy_info_.find(j);
+        if (dt.local.empty() && dt.remote.size() == 1 && ci != copy_info_.end() && ci->second.dst_aid == k.bindings[0] &&
+            hx.n_in < kHaloMax) {
+            hx.in_flag[hx.n_in] = reinterpret_cast<const unsigned long long*>(sig_slot(dev, dt.remote[0].first, j));
+            hx.in_value[hx.n_in] = j;
+            hx.in_r0[hx.n_in] = ci->second.bb.lo[0];
+            hx.in_r1[hx.n_in] = ci->second.bb.hi[0];
+            hx.n_in++;
+        } else {
+            merge(t, dt);
+        }
+    }
+    // outgoing: each push's other dependencies -- local ones on the stream,
+    // remote ones (the receivers' readers) awaited by the pushing CTAs
+    if (halo_ctr_.empty()) halo_ctr_.assign(size_t(G_), std::array<unsigned, kHaloMax>{});
+    std::array<unsigned, kHaloMax> ctr = halo_ctr_[size_t(dev)];
+    for (const Instr& p : pushes) {
+        cur_ins_ = &p;
+        for (uint64_t j : p.deps) {
+            if (j == k.iid) continue;
+            Token dt = dep_token(j);
+            merge(t, Token{dt.local, {}});
+            for (auto& r : dt.remote) {
+                const unsigned long long* f = reinterpret_cast<const unsigned long long*>(sig_slot(dev, r.first, r.second));
+                bool dup = false;
+                for (int i = 0; i < hx.n_war; ++i) dup = dup || (hx.war_flag[i] == f && hx.war_value[i] >= r.second);
+                if (dup) continue;
+                if (hx.n_war == kHaloMax) return false;
+                hx.war_flag[hx.n_war] = f;
+                hx.war_value[hx.n_war] = r.second;
+                hx.n_war++;
+            }
+        }
+        const int i = hx.n_out;
+        const AllocRec& D = allocs_.at(p.dst_aid);
+        const Box& b = p.region[0];
+        hx.base[i] = base_of(D);
+        hx.lo0[i] = D.box.lo[0];
+        hx.lo1[i] = D.box.lo[1];
+        hx.n1[i] = D.box.extent(1);
+        hx.r0[i] = b.lo[0];
+        hx.r1[i] = b.hi[0];
+        hx.flag[i] = reinterpret_cast<unsigned long long*>(sig_slot(p.dst_mem - 2, cfg_.rank, p.iid));
+        hx.value[i] = p.iid;
+        // CTAs that compute the rows: every column block of each strip they touch
+        const int64_t s0 = (b.lo[0] - k.chunk.lo[0]) / h, s1 = (b.hi[0] - 1 - k.chunk.lo[0]) / h;
+        const unsigned n = unsigned(s1 - s0 + 1) * gx;
+        hx.ctr[i] = reinterpret_cast<unsigned*>(arenas_[dev].base + gather_off_ + 256) + i;
+        hx.ctr_last[i] = ctr[size_t(i)] + n - 1;
+        ctr[size_t(i)] += n;
+        hx.n_out++;
+    }
+    cur_ins_ = &k;
+    set_dev(dev);
+    wait_token(sidx, t);
+    int n = 0;
+    if (cfg_.profile && prof_sample(K_WAVE5)) {
+        Prof pr{K_WAVE5, prof_event(dev), prof_event(dev), dev, k.iid, sidx, now_ns()};
+        cudaEventRecord(pr.a, streams_[sidx].s);
+        n = launch_wave5_halo(a, hx, streams_[sidx].s);
+        cudaEventRecord(pr.b, streams_[sidx].s);
+        prof_pending_.push_back(pr);
+    } else {
+        n = launch_wave5_halo(a, hx, streams_[sidx].s);
+    }
+    check(cudaGetLastError(), "fused wave5 halo launch");
+    if (n != 1) {
+        if (!err_) {
+            errmsg_ = "fused wave5 halo launch: kernel no longer applicable";
+            err_ = E_STATE;
+        }
+        return true;
+    }
+    halo_ctr_[size_t(dev)] = ctr;
+    st_.kernel_launches += 1;
+    st_.workload_launches += 1;
+    st_.halo_fused += pushes.size();
+    st_.halo_in_waits += uint64_t(hx.n_in);
+    const Token done = record(sidx);
+    tok_[k.iid] = done;
+    kind_of_[k.iid] = dev;
+    for (const Instr& p : pushes) {
+        tok_[p.iid] = done;
+        kind_of_[p.iid] = dev;
+        copy_info_[p.iid] = CopyInfo{p.src_aid, p.dst_aid, rbbox(p.region), p.region};
+        // the launch wrote the receiver's flag: no stream write for it later
+        signalled_.insert(p.iid * uint64_t(cfg_.world) + uint64_t(owner_rank(p.dst_mem - 2)));
+        st_.bytes_copy[2] += rvolume(p.region) * 4;
+    }
+    if (grown_) {
+        note_use(k);
+        for (const Instr& p : pushes) note_use(p);
+    }
+    return true;
+}
+
+// Release the held-back kernel: fused with its pushes when expressible, else
+// the ordinary path; then the horizons that waited with it.
+void Executor::halo_flush() {
+    if (!halo_parked_) return;
+    halo_parked_ = false;
+    Instr k = std::move(halo_kernel_);
+    std::vector<Instr> pushes, deferred;
+    pushes.swap(halo_pushes_);
+    deferred.swap(halo_deferred_);
+    halo_iids_.clear();
+    halo_flushing_ = true;
+    if (!halo_launch(k, pushes)) {
+        on_instr_impl(k);
+        for (const Instr& p : pushes) on_instr_impl(p);
+    }
+    for (const Instr& x : deferred) on_instr_impl(x);
+    halo_flushing_ = false;
+    cur_ins_ = nullptr;
+}
+
+}  // namespace cel

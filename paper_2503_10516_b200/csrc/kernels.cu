@@ -494,7 +494,28 @@ constexpr int kWaveRows = 8;                  // strip height cap of the automat
 // vector path: 128 threads x float4 = 512 columns per CTA, a strip of kWaveRows
 // rows marched top to bottom with a 3-row register window; west/east
 // neighbours come from warp shuffles (scalar loads only at warp edges).
-__global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a) {
+// kHalo: the halo exchange fused in (HaloArgs, exec_halo.cu).
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// spin until *f >= v; a flag that never comes traps after ~2^34 cycles (a
+// failed launch instead of a hung GPU)
+__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long v) {
+    const long long t0 = clock64();
+    while (ld_acquire_sys(f) < v) {
+        __nanosleep(64);
+        if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
+
+template <bool kHalo>
+__device__ __forceinline__ void wave5_body(const KArgs& a, const HaloArgs* hxp) {
+    const HaloArgs& hx = *hxp;   // dereferenced only when kHalo
     const DAcc& U = a.acc[0];
     const DAcc& P = a.acc[1];
     const int64_t r0 = a.chunk.lo[0], r1 = a.chunk.hi[0];
@@ -515,6 +536,23 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
     // programmatic dependent launch (see launch_wave5): the previous step wrote u
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    unsigned outs = 0;                              // bit i: this strip computes rows of outgoing copy i
+    if (kHalo) {
+        bool wait_in = false;
+        for (int i = 0; i < hx.n_in; ++i)
+            if (hx.in_r0[i] < re + 1 && rs - 1 < hx.in_r1[i]) wait_in = true;
+        for (int i = 0; i < hx.n_out; ++i)
+            if (hx.r0[i] < re && rs < hx.r1[i]) outs |= 1u << i;
+        if (wait_in || (outs && hx.n_war)) {
+            if (threadIdx.x == 0) {
+                for (int i = 0; i < hx.n_in; ++i)
+                    if (hx.in_r0[i] < re + 1 && rs - 1 < hx.in_r1[i]) wait_flag(hx.in_flag[i], hx.in_value[i]);
+                if (outs)
+                    for (int i = 0; i < hx.n_war; ++i) wait_flag(hx.war_flag[i], hx.war_value[i]);
+            }
+            __syncthreads();
+        }
+    }
     float4 prev = z4, cur = z4;
     if (valid) {
         prev = __ldg(reinterpret_cast<const float4*>(urow(rs > 0 ? rs - 1 : 0) + uoff));
@@ -530,7 +568,13 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
         float4 nxt = z4, up = z4;
         float* prow = pb + (r - P.lo[0]) * P.n[1] + poff;
         if (valid) {
-            nxt = __ldg(reinterpret_cast<const float4*>(urow(rn) + uoff));
+            // u comes from the previous step (possibly another GPU's stores
+            // that landed under a flag): plain loads, not the read-only path
+            if (kHalo) {
+                nxt = *reinterpret_cast<const float4*>(urow(rn) + uoff);
+            } else {
+                nxt = __ldg(reinterpret_cast<const float4*>(urow(rn) + uoff));
+            }
             up = *reinterpret_cast<const float4*>(prow);
         }
         float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
@@ -542,10 +586,41 @@ __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a
         o.y = wave1(cur.y, up.y, prev.y, nxt.y, cur.x, cur.z);
         o.z = wave1(cur.z, up.z, prev.z, nxt.z, cur.y, cur.w);
         o.w = wave1(cur.w, up.w, prev.w, nxt.w, cur.z, e);
-        if (valid) *reinterpret_cast<float4*>(prow) = o;
+        if (valid) {
+            *reinterpret_cast<float4*>(prow) = o;
+            if (kHalo && outs)
+                for (int i = 0; i < hx.n_out; ++i)
+                    if (((outs >> i) & 1u) && hx.r0[i] <= r && r < hx.r1[i])
+                        *reinterpret_cast<float4*>(reinterpret_cast<float*>(hx.base[i]) +
+                                                   (r - hx.lo0[i]) * hx.n1[i] + (c - hx.lo1[i])) = o;
+        }
         prev = cur;
         cur = nxt;
     }
+    if (kHalo && outs) {
+        // every thread's peer stores precede thread 0's system fence (bar.sync,
+        // then a cumulative fence); the last CTA of copy i publishes its flag
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence_system();
+            for (int i = 0; i < hx.n_out; ++i)
+                if ((outs >> i) & 1u) {
+                    const unsigned old = atomicAdd(hx.ctr[i], 1u);
+                    if (old == hx.ctr_last[i]) {
+                        __threadfence_system();
+                        st_release_sys(hx.flag[i], hx.value[i]);
+                    }
+                }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a) {
+    wave5_body<false>(a, nullptr);
+}
+
+__global__ void __launch_bounds__(128) wave5_halo(const __grid_constant__ KArgs a, const __grid_constant__ HaloArgs hx) {
+    wave5_body<true>(a, &hx);
 }
 
 // ------------------------------------------------------------------ C5 Jacobi 7-point
@@ -1363,6 +1438,60 @@ int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s) {
     return 1;
 }
 
+int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy) {
+    const DAcc& U = a.acc[0];
+    const DAcc& P = a.acc[1];
+    const int64_t c0 = a.chunk.lo[1], w = a.chunk.hi[1] - c0;
+    const bool vec = !a.checked && U.es == 4 && P.es == 4 && U.n[2] == 1 && P.n[2] == 1 && U.n[1] % 4 == 0 &&
+                     P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
+                     aligned16(U.base) && aligned16(P.base);
+    const int64_t rows = a.chunk.hi[0] - a.chunk.lo[0];
+    if (!vec || rows <= 0 || w <= 0) return 0;
+    // strip height: 8 rows, lowered (>= 4) until the grid has about 8 waves
+    // of resident CTAs, so the last-wave tail stays small on the thin chunks
+    // of many-GPU runs (r02 sweep, tools/wave_strip.py: 16384 rows 478 us at
+    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits, so
+    // short strips cost no DRAM re-reads)
+    static int occ = 0;
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
+        if (occ < 1) occ = 1;
+    }
+    const int64_t cols = (w / 4 + 127) / 128;
+    const int64_t resident = int64_t(num_sms()) * occ;
+    int64_t h = (rows * cols) / (resident * 8);
+    h = h < 4 ? 4 : (h > kWaveRows ? kWaveRows : h);
+    static int force = -1;
+    if (force < 0) {
+        const char* e = getenv("CEL_WAVE_STRIP");           // A/B of the strip height
+        force = e ? atoi(e) : 0;
+    }
+    if (force > 0) h = force;
+    *gx = unsigned(cols);
+    *gy = unsigned((rows + h - 1) / h);
+    return h;
+}
+
+int launch_wave5_halo(const KArgs& a, const HaloArgs& hx, cudaStream_t s) {
+    unsigned gx = 0, gy = 0;
+    const int64_t h = wave5_strip(a, &gx, &gy);
+    if (h <= 0) return 0;
+    KArgs b = a;
+    b.strip = int(h);
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(gx, gy);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, wave5_halo, b, hx);
+    return 1;
+}
+
 int launch_workload(const KArgs& a, cudaStream_t s) {
     const int64_t cv = vol(a.chunk);
     switch (a.kind) {
@@ -1382,37 +1511,11 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
         return 1;
     case K_WAVE5: {
         if (cv == 0) return 0;
-        const DAcc& U = a.acc[0];
-        const DAcc& P = a.acc[1];
-        const int64_t c0 = a.chunk.lo[1], w = a.chunk.hi[1] - c0;
-        const bool vec = !a.checked && U.es == 4 && P.es == 4 && U.n[2] == 1 && P.n[2] == 1 && U.n[1] % 4 == 0 &&
-                         P.n[1] % 4 == 0 && (c0 - U.lo[1]) % 4 == 0 && (c0 - P.lo[1]) % 4 == 0 && w % 4 == 0 &&
-                         aligned16(U.base) && aligned16(P.base);
-        if (vec) {
-            // strip height: 8 rows, lowered (>= 4) until the grid has about 8
-            // waves of resident CTAs, so the last-wave tail stays small on the
-            // thin chunks of many-GPU runs (r02 sweep, tools/wave_strip.py:
-            // 16384 rows 478 us at h = 8 vs 494 at 16; neighbouring strips'
-            // halo rows are L2 hits, so short strips cost no DRAM re-reads)
-            static int occ = 0;
-            if (occ == 0) {
-                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
-                if (occ < 1) occ = 1;
-            }
-            const int64_t cols = (w / 4 + 127) / 128;
-            const int64_t rows = a.chunk.hi[0] - a.chunk.lo[0];
-            const int64_t resident = int64_t(num_sms()) * occ;
-            int64_t h = (rows * cols) / (resident * 8);
-            h = h < 4 ? 4 : (h > kWaveRows ? kWaveRows : h);
-            static int force = -1;
-            if (force < 0) {
-                const char* e = getenv("CEL_WAVE_STRIP");           // A/B of the strip height
-                force = e ? atoi(e) : 0;
-            }
-            if (force > 0) h = force;
+        unsigned gx = 0, gy = 0;
+        const int64_t h = wave5_strip(a, &gx, &gy);
+        if (h > 0) {
             KArgs b = a;
             b.strip = int(h);
-            dim3 grid(unsigned(cols), unsigned((rows + h - 1) / h));
             static int pdl = -1;
             if (pdl < 0) {
                 const char* e = getenv("CEL_PDL");
@@ -1420,7 +1523,7 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             }
             cudaLaunchConfig_t cfg;
             memset(&cfg, 0, sizeof cfg);
-            cfg.gridDim = grid;
+            cfg.gridDim = dim3(gx, gy);
             cfg.blockDim = dim3(128);
             cfg.stream = s;
             cudaLaunchAttribute attr[1];

@@ -190,4 +190,34 @@ struct PeerOut {
 bool rsim_fusable(const KArgs& a);                       // the TMA row kernel applies (it carries the epilogue)
 int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s);
 
+// WaveSim halo exchange fused into the stencil (exec_halo.cu; SURVEY §7 step
+// 6, NEXT-2).  Outgoing: coherence copies of rows this launch writes, stored
+// by the CTAs that compute them straight into the receiver's allocation (peer
+// memory over NVLink), after the copies' remote dependencies (war flags); the
+// last CTA of each copy writes the receiver's flag slot.  Incoming: copies
+// into rows the launch reads, awaited by the CTAs that read them (flag slots
+// in this device's memory), not by the stream.
+constexpr int kHaloMax = 4;
+struct HaloArgs {
+    int n_out;
+    char* base[kHaloMax];                          // receiver allocation
+    int64_t lo0[kHaloMax], lo1[kHaloMax], n1[kHaloMax];   // its box origin (rows, cols), row pitch (elements)
+    int64_t r0[kHaloMax], r1[kHaloMax];            // rows copied, all chunk columns
+    unsigned long long* flag[kHaloMax];            // receiver's signal slot for the copy (peer memory)
+    unsigned long long value[kHaloMax];            // the copy's instruction id
+    unsigned* ctr[kHaloMax];                       // this device's CTA counter of copy i
+    unsigned ctr_last[kHaloMax];                   // counter value before the last CTA's increment
+    int n_war;
+    const unsigned long long* war_flag[kHaloMax];  // remote dependencies of the outgoing copies
+    unsigned long long war_value[kHaloMax];
+    int n_in;
+    const unsigned long long* in_flag[kHaloMax];   // incoming copies: flag slot, instruction id,
+    unsigned long long in_value[kHaloMax];
+    int64_t in_r0[kHaloMax], in_r1[kHaloMax];      // rows they write
+};
+// strip height and grid of the vectorised wave5 launch for this chunk (0 rows
+// if the vector kernel does not apply)
+int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy);
+int launch_wave5_halo(const KArgs& a, const HaloArgs& h, cudaStream_t s);
+
 }  // namespace cel

@@ -78,6 +78,9 @@ def main():
                     close()
                 rt.shutdown = keep_stats
                 res = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
+                if rank == 0 and stats.get("halo_fused"):
+                    print("  halo copies fused into the stencil %d, incoming awaited in-kernel %d"
+                          % (stats["halo_fused"], stats["halo_in_waits"]), flush=True)
                 if rank == 0 and stats.get("gather_sets"):
                     print("  all-gather sets %d, run as NCCL groups %d" % (stats["gather_sets"], stats["coll_groups"]),
                           flush=True)
