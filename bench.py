@@ -450,6 +450,11 @@ def main():
     if world == 1 and G > 1:
         border_rows = 2 * (G - 1) / G
     interior_rows = rows_here - border_rows
+    halo_fused = st1.get("halo_fused", 0) - st0.get("halo_fused", 0)
+    if halo_fused:
+        # halo exchange fused into the stencil (exec_halo.cu): one launch per
+        # step covers the whole chunk, the boundary rows included
+        interior_rows = rows_here
     avg_s = (wms / wcnt) / 1e3 if wcnt else float("nan")         # sampled launches: unbiased average
     alg_bytes = ALG_BYTES_PER_CELL * interior_rows * n
     achieved = alg_bytes / avg_s / 1e9 if wcnt else None
@@ -513,7 +518,7 @@ def main():
         "config": arm_config(G, world, n),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "wave5_vec", "alg_bytes_per_launch": alg_bytes,
+                     "kernel": "wave5_halo" if halo_fused else "wave5_vec", "alg_bytes_per_launch": alg_bytes,
                      "avg_launch_ms": avg_s * 1e3 if wcnt else None,
                      "shell_ms_per_step": shell_ms / args.steps,
                      "peak_source": peak_kind + " hbm_gbs",
@@ -522,6 +527,7 @@ def main():
         "e2e": e2e,
         "copy": copies,
         "gpu_launches": launches,
+        "halo_fused_per_step": halo_fused / args.steps,
         "host_submit_us_per_step": (th1 - th0) / kh * 1e6,
         "host_us_per_step_by_part": {k[8:] if k.startswith("exec_ns_") else k: (sh1[k] - sh0[k]) / kh / 1e3
                                      for k in ("exec_ns_copy", "exec_ns_kernel", "exec_ns_alloc", "exec_ns_free",

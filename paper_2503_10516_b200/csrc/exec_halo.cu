@@ -45,6 +45,12 @@ bool Executor::halo_candidate(const Instr& ins) {
 // A coherence copy of rows the held-back kernel writes, into another GPU.
 bool Executor::halo_attach(const Instr& ins) {
     const Instr& k = halo_kernel_;
+    static int mode = -1;                          // CEL_HALO_MODE bit 1 off: pushes stay copies (A/B)
+    if (mode < 0) {
+        const char* e = getenv("CEL_HALO_MODE");
+        mode = e ? atoi(e) : 3;
+    }
+    if (!(mode & 1)) return false;
     if (ins.kind != IKind::Copy || ins.coll_n || int(halo_pushes_.size()) >= kHaloMax) return false;
     if (ins.src_mem - 2 != k.device || ins.dst_mem < 2 || owner_rank(ins.dst_mem - 2) == cfg_.rank) return false;
     if (phys_[ins.dst_mem - 2] == phys_[k.device] || ins.src_aid != k.bindings[1] || ins.region.size() != 1) return false;
@@ -78,11 +84,17 @@ bool Executor::halo_launch(const Instr& k, const std::vector<Instr>& pushes) {
     Token t;
     // incoming: the kernel's dependencies on other ranks' copies into the
     // allocation it reads u from (their rows), awaited by the reading CTAs
+    // (CEL_HALO_MODE bit 2 off: by the stream, for A/B)
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("CEL_HALO_MODE");
+        mode = e ? atoi(e) : 3;
+    }
     cur_ins_ = &k;
     for (uint64_t j : k.deps) {
         Token dt = dep_token(j);
         auto ci = copy_info_.find(j);
-        if (dt.local.empty() && dt.remote.size() == 1 && ci != copy_info_.end() && ci->second.dst_aid == k.bindings[0] &&
+        if ((mode & 2) && dt.local.empty() && dt.remote.size() == 1 && ci != copy_info_.end() && ci->second.dst_aid == k.bindings[0] &&
             hx.n_in < kHaloMax) {
             hx.in_flag[hx.n_in] = reinterpret_cast<const unsigned long long*>(sig_slot(dev, dt.remote[0].first, j));
             hx.in_value[hx.n_in] = j;

@@ -513,50 +513,28 @@ __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned 
     }
 }
 
-template <bool kHalo>
-__device__ __forceinline__ void wave5_body(const KArgs& a, const HaloArgs* hxp) {
-    const HaloArgs& hx = *hxp;   // dereferenced only when kHalo
-    const DAcc& U = a.acc[0];
-    const DAcc& P = a.acc[1];
-    const int64_t r0 = a.chunk.lo[0], r1 = a.chunk.hi[0];
-    const int64_t c0 = a.chunk.lo[1], c1 = a.chunk.hi[1];
+// One CTA's strip: rows [rs, re) of its 512 columns.  kPlain: u through
+// plain (coherent) loads -- rows another GPU stored while this kernel ran,
+// under a flag -- instead of the read-only path.
+template <bool kPlain>
+__device__ __forceinline__ void wave5_rows(const DAcc& U, const DAcc& P, int64_t rs, int64_t re, int64_t c, int64_t c1,
+                                           bool valid) {
     const int64_t E0 = U.ext[0], E1 = U.ext[1];
     const int lane = threadIdx.x & 31;
-    const int64_t c = c0 + (int64_t(blockIdx.x) * 128 + threadIdx.x) * 4;
-    const bool valid = c < c1;
-    const int64_t h = a.strip > 0 ? a.strip : kWaveRows;
-    const int64_t rs = r0 + int64_t(blockIdx.y) * h;
-    const int64_t re = rs + h < r1 ? rs + h : r1;
     const float* ub = reinterpret_cast<const float*>(U.base);
     float* pb = reinterpret_cast<float*>(P.base);
     const int64_t uoff = c - U.lo[1];
     const int64_t poff = c - P.lo[1];
     auto urow = [&](int64_t r) { return ub + (r - U.lo[0]) * U.n[1]; };
+    auto ld4 = [&](const float* q) {
+        return kPlain ? *reinterpret_cast<const float4*>(q) : __ldg(reinterpret_cast<const float4*>(q));
+    };
+    auto ld1 = [&](const float* q) { return kPlain ? *q : __ldg(q); };
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    // programmatic dependent launch (see launch_wave5): the previous step wrote u
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    unsigned outs = 0;                              // bit i: this strip computes rows of outgoing copy i
-    if (kHalo) {
-        bool wait_in = false;
-        for (int i = 0; i < hx.n_in; ++i)
-            if (hx.in_r0[i] < re + 1 && rs - 1 < hx.in_r1[i]) wait_in = true;
-        for (int i = 0; i < hx.n_out; ++i)
-            if (hx.r0[i] < re && rs < hx.r1[i]) outs |= 1u << i;
-        if (wait_in || (outs && hx.n_war)) {
-            if (threadIdx.x == 0) {
-                for (int i = 0; i < hx.n_in; ++i)
-                    if (hx.in_r0[i] < re + 1 && rs - 1 < hx.in_r1[i]) wait_flag(hx.in_flag[i], hx.in_value[i]);
-                if (outs)
-                    for (int i = 0; i < hx.n_war; ++i) wait_flag(hx.war_flag[i], hx.war_value[i]);
-            }
-            __syncthreads();
-        }
-    }
     float4 prev = z4, cur = z4;
     if (valid) {
-        prev = __ldg(reinterpret_cast<const float4*>(urow(rs > 0 ? rs - 1 : 0) + uoff));
-        cur = __ldg(reinterpret_cast<const float4*>(urow(rs) + uoff));
+        prev = ld4(urow(rs > 0 ? rs - 1 : 0) + uoff);
+        cur = ld4(urow(rs) + uoff);
     }
     const bool need_e = valid && (lane == 31 || c + 4 >= c1);
     const bool need_w = valid && lane == 0;
@@ -568,51 +546,103 @@ __device__ __forceinline__ void wave5_body(const KArgs& a, const HaloArgs* hxp) 
         float4 nxt = z4, up = z4;
         float* prow = pb + (r - P.lo[0]) * P.n[1] + poff;
         if (valid) {
-            // u comes from the previous step (possibly another GPU's stores
-            // that landed under a flag): plain loads, not the read-only path
-            if (kHalo) {
-                nxt = *reinterpret_cast<const float4*>(urow(rn) + uoff);
-            } else {
-                nxt = __ldg(reinterpret_cast<const float4*>(urow(rn) + uoff));
-            }
+            nxt = ld4(urow(rn) + uoff);
             up = *reinterpret_cast<const float4*>(prow);
         }
         float w = __shfl_up_sync(0xffffffffu, cur.w, 1);
         float e = __shfl_down_sync(0xffffffffu, cur.x, 1);
-        if (need_w) w = __ldg(urow(r) + (cw - U.lo[1]));
-        if (need_e) e = __ldg(urow(r) + (ce - U.lo[1]));
+        if (need_w) w = ld1(urow(r) + (cw - U.lo[1]));
+        if (need_e) e = ld1(urow(r) + (ce - U.lo[1]));
         float4 o;
         o.x = wave1(cur.x, up.x, prev.x, nxt.x, w, cur.y);
         o.y = wave1(cur.y, up.y, prev.y, nxt.y, cur.x, cur.z);
         o.z = wave1(cur.z, up.z, prev.z, nxt.z, cur.y, cur.w);
         o.w = wave1(cur.w, up.w, prev.w, nxt.w, cur.z, e);
-        if (valid) {
-            *reinterpret_cast<float4*>(prow) = o;
-            if (kHalo && outs)
-                for (int i = 0; i < hx.n_out; ++i)
-                    if (((outs >> i) & 1u) && hx.r0[i] <= r && r < hx.r1[i])
-                        *reinterpret_cast<float4*>(reinterpret_cast<float*>(hx.base[i]) +
-                                                   (r - hx.lo0[i]) * hx.n1[i] + (c - hx.lo1[i])) = o;
-        }
+        if (valid) *reinterpret_cast<float4*>(prow) = o;
         prev = cur;
         cur = nxt;
     }
-    if (kHalo && outs) {
-        // every thread's peer stores precede thread 0's system fence (bar.sync,
-        // then a cumulative fence); the last CTA of copy i publishes its flag
+}
+
+// Forward rows [ra, rb) of this thread's columns (just written to P: L1 / L2
+// hits) into every outgoing copy that holds them, then count the CTA in: the
+// last CTA of copy i publishes the receiver's flag.  bar.sync, then thread
+// 0's cumulative system fence, order every thread's peer stores before it.
+__device__ __forceinline__ void wave5_push(const DAcc& P, const HaloArgs& hx, int64_t ra, int64_t rb, int64_t c,
+                                           bool valid) {
+    unsigned outs = 0;
+    for (int i = 0; i < hx.n_out; ++i)
+        if (hx.r0[i] < rb && ra < hx.r1[i]) outs |= 1u << i;
+    if (!outs) return;
+    if (hx.n_war) {                         // the receivers' readers of those rows are done
+        if (threadIdx.x == 0)
+            for (int i = 0; i < hx.n_war; ++i) wait_flag(hx.war_flag[i], hx.war_value[i]);
         __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence_system();
-            for (int i = 0; i < hx.n_out; ++i)
-                if ((outs >> i) & 1u) {
-                    const unsigned old = atomicAdd(hx.ctr[i], 1u);
-                    if (old == hx.ctr_last[i]) {
-                        __threadfence_system();
-                        st_release_sys(hx.flag[i], hx.value[i]);
-                    }
-                }
+    }
+    if (valid) {
+        const float* pb = reinterpret_cast<const float*>(P.base);
+        for (int i = 0; i < hx.n_out; ++i) {
+            if (!((outs >> i) & 1u)) continue;
+            const int64_t a = ra > hx.r0[i] ? ra : hx.r0[i], b = rb < hx.r1[i] ? rb : hx.r1[i];
+            for (int64_t r = a; r < b; ++r)
+                *reinterpret_cast<float4*>(reinterpret_cast<float*>(hx.base[i]) + (r - hx.lo0[i]) * hx.n1[i] +
+                                           (c - hx.lo1[i])) =
+                    *reinterpret_cast<const float4*>(pb + (r - P.lo[0]) * P.n[1] + (c - P.lo[1]));
         }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int i = 0; i < hx.n_out; ++i)
+            if ((outs >> i) & 1u) {
+                const unsigned old = atomicAdd(hx.ctr[i], 1u);
+                if (old == hx.ctr_last[i]) {
+                    __threadfence_system();
+                    st_release_sys(hx.flag[i], hx.value[i]);
+                }
+            }
+    }
+}
+
+template <bool kHalo>
+__device__ __forceinline__ void wave5_body(const KArgs& a, const HaloArgs* hxp) {
+    const DAcc& U = a.acc[0];
+    const DAcc& P = a.acc[1];
+    const int64_t r0 = a.chunk.lo[0], r1 = a.chunk.hi[0];
+    const int64_t c0 = a.chunk.lo[1], c1 = a.chunk.hi[1];
+    const int64_t c = c0 + (int64_t(blockIdx.x) * 128 + threadIdx.x) * 4;
+    const bool valid = c < c1;
+    const int64_t h = a.strip > 0 ? a.strip : kWaveRows;
+    // halo launches visit the last strip second (CTAs start roughly in
+    // blockIdx order): both boundary strips -- the ones that exchange rows
+    // with the neighbours -- run first, so pushes leave early and the
+    // neighbours' flags are set by the time their boundary strips look
+    int64_t sy = blockIdx.y;
+    if (kHalo && gridDim.y > 2) sy = blockIdx.y == 0 ? 0 : (blockIdx.y == 1 ? int64_t(gridDim.y) - 1 : int64_t(blockIdx.y) - 1);
+    const int64_t rs = r0 + sy * h;
+    const int64_t re = rs + h < r1 ? rs + h : r1;
+    // programmatic dependent launch (see launch_wave5): the previous step wrote u
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!kHalo) {
+        wave5_rows<false>(U, P, rs, re, c, c1, valid);
+        return;
+    }
+    const HaloArgs& hx = *hxp;
+    // incoming rows this strip reads: wait for their flags first
+    bool wait_in = false;
+    for (int i = 0; i < hx.n_in; ++i)
+        if (hx.in_r0[i] < re + 1 && rs - 1 < hx.in_r1[i]) wait_in = true;
+    if (wait_in) {
+        if (threadIdx.x == 0)
+            for (int i = 0; i < hx.n_in; ++i)
+                if (hx.in_r0[i] < re + 1 && rs - 1 < hx.in_r1[i]) wait_flag(hx.in_flag[i], hx.in_value[i]);
+        __syncthreads();
+        wave5_rows<true>(U, P, rs, re, c, c1, valid);
+    } else {
+        wave5_rows<false>(U, P, rs, re, c, c1, valid);
+    }
+    wave5_push(P, hx, rs, re, c, valid);
 }
 
 __global__ void __launch_bounds__(128) wave5_vec(const __grid_constant__ KArgs a) {
@@ -1448,10 +1478,11 @@ int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy) {
     const int64_t rows = a.chunk.hi[0] - a.chunk.lo[0];
     if (!vec || rows <= 0 || w <= 0) return 0;
     // strip height: 8 rows, lowered (>= 4) until the grid has about 8 waves
-    // of resident CTAs, so the last-wave tail stays small on the thin chunks
-    // of many-GPU runs (r02 sweep, tools/wave_strip.py: 16384 rows 478 us at
-    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits, so
-    // short strips cost no DRAM re-reads)
+    // of resident CTAs (r02 sweep, tools/wave_strip.py: 16384 rows 478 us at
+    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits).  (A
+    // launch-time model picking h = 5 for 4096-row chunks to fill the last
+    // wave -- 15 waves instead of 9.2 -- measured 2% slower at 4 B200:
+    // short strips cost more than their partial last wave saves.)
     static int occ = 0;
     if (occ == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
