@@ -52,7 +52,7 @@ def test_multiprocess_gpu():
 @pytest.mark.parametrize("fuse", ["1", "0"])
 def test_multiprocess_halo_fused(fuse):
     """WaveSim's halo exchange fused into the stencil launches (exec_halo.cu,
-    CEL_FUSE_HALO): ranks on distinct GPUs push boundary rows from the
+    CEL_FUSE_HALO, on by default): ranks on distinct GPUs push boundary rows from the
     computing CTAs into the neighbours' memory and await incoming rows in the
     reading CTAs; the readbacks equal the oracle's bytes and the instruction
     logs its log, with the fused path taken (or, fuse=0, not)."""
