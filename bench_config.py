@@ -127,7 +127,9 @@ def main():
             submit(s)
     rt.wait()
     st0 = rt.stats()
-    rt.profile_enable(True)
+    prof_on = not os.environ.get("CEL_BENCH_NOPROF")     # per-launch events cost host time (RSim: host-bound)
+    if prof_on:
+        rt.profile_enable(True)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -161,6 +163,9 @@ def main():
             "exec_us_per_step": {k[8:]: (st1[k] - st0[k]) / 1e3 / steps for k in
                                  ("exec_ns_alloc", "exec_ns_free", "exec_ns_copy", "exec_ns_kernel", "exec_ns_horizon",
                                   "exec_ns_epoch")},
+            "host_us_per_step": {k: (st1[k] - st0[k]) / 1e3 / steps for k in ("signal_ns", "remote_wait_ns")},
+            "per_step": {k: (st1[k] - st0[k]) / steps for k in ("signals", "remote_waits", "event_waits",
+                                                                   "kernel_launches", "copy_launches", "memcpy_calls")},
             "coll_p2p": st1["coll_p2p"] - st0["coll_p2p"],
             "gpu_launches": st1["kernel_launches"] - st0["kernel_launches"],
             "collective": bool(args.collective),
