@@ -381,6 +381,7 @@ private:
     bool halo_attach(const Instr& ins);
     bool halo_depends(const Instr& ins) const;
     bool halo_launch(const Instr& k, const std::vector<Instr>& pushes);
+    bool halo_launch_rsim(const Instr& k, const std::vector<Instr>& pushes);
     void halo_flush();
     bool p2p_gather_ = false;                     // gather sets as P2P gather kernels (CEL_COLL_P2P=0: off)
     uint64_t gather_off_ = 0;                     // per device arena: gather counter word (+64: CTA counter)

@@ -31,13 +31,15 @@ bool Executor::halo_depends(const Instr& ins) const {
     return false;
 }
 
-// A wave5 instruction this rank launches whose vector kernel applies.
+// A wave5 instruction this rank launches whose vector kernel applies, or an
+// RSim row whose TMA kernel applies (its row goes to every other rank).
 bool Executor::halo_candidate(const Instr& ins) {
-    if (!fuse_halo_ || halo_flushing_ || ins.kind != IKind::Kernel || !ins.desc || ins.desc->kernel != K_WAVE5)
-        return false;
+    if (!fuse_halo_ || halo_flushing_ || ins.kind != IKind::Kernel || !ins.desc) return false;
+    if (ins.desc->kernel != K_WAVE5 && ins.desc->kernel != K_RSIM_ROW) return false;
     if (owner_rank(ins.device) != cfg_.rank || cfg_.bounds_check) return false;
     KArgs a;
     build_kargs(ins, a);
+    if (ins.desc->kernel == K_RSIM_ROW) return rsim_fusable(a);
     unsigned gx = 0, gy = 0;
     return wave5_strip(a, &gx, &gy) > 0;
 }
@@ -51,13 +53,25 @@ bool Executor::halo_attach(const Instr& ins) {
         mode = e ? atoi(e) : 3;
     }
     if (!(mode & 1)) return false;
-    if (ins.kind != IKind::Copy || ins.coll_n || int(halo_pushes_.size()) >= kHaloMax) return false;
+    if (ins.kind != IKind::Copy || ins.coll_n) return false;
+    if (k.desc->kernel == K_WAVE5 && int(halo_pushes_.size()) >= kHaloMax) return false;
     if (ins.src_mem - 2 != k.device || ins.dst_mem < 2 || owner_rank(ins.dst_mem - 2) == cfg_.rank) return false;
     if (phys_[ins.dst_mem - 2] == phys_[k.device] || ins.src_aid != k.bindings[1] || ins.region.size() != 1) return false;
     if (std::find(ins.deps.begin(), ins.deps.end(), k.iid) == ins.deps.end()) return false;
     for (uint64_t j : ins.deps)
         if (j != k.iid && halo_iids_.count(j)) return false;
     const Box& b = ins.region[0];
+    if (k.desc->kernel == K_RSIM_ROW) {
+        // the row the kernel writes, to another rank's allocation of whole rows
+        const Box w = map_access(k.desc->acc[1].map, k.chunk, bufinfo_.at(k.desc->acc[1].buf).extent);
+        auto d = allocs_.find(ins.dst_aid);
+        if (!(b == w) || int(halo_pushes_.size()) >= kMaxGatherDst || d == allocs_.end() || d->second.es != 4 ||
+            d->second.box.extent(2) != 1)
+            return false;
+        halo_pushes_.push_back(ins);
+        halo_iids_.insert(ins.iid);
+        return true;
+    }
     if (b.lo[1] != k.chunk.lo[1] || b.hi[1] != k.chunk.hi[1] || b.lo[0] < k.chunk.lo[0] || b.hi[0] > k.chunk.hi[0] ||
         b.extent(2) != 1)
         return false;
@@ -70,8 +84,141 @@ bool Executor::halo_attach(const Instr& ins) {
     return true;
 }
 
+// An RSim row with its pushes to the other ranks (`rsim_row_tma_t<true>` in
+// flag mode): every thread stores its element into each receiver's
+// allocation, the last CTA writes the receivers' flag slots; the incoming
+// copies of the rows the kernel reads are awaited by the kernel.  One launch
+// per row instead of a launch, G - 1 copies, G - 1 flag writes and G - 1
+// stream waits.
+bool Executor::halo_launch_rsim(const Instr& k, const std::vector<Instr>& pushes) {
+    const int dev = k.device;
+    const int sidx = dev * kStreamsPerDev + S_COMPUTE;
+    Stream& cs = streams_[sidx];
+    KArgs a;
+    build_kargs(k, a);
+    if (!rsim_fusable(a)) return false;
+    PeerOut po;
+    memset(&po, 0, sizeof po);
+    po.flags = 1;
+    Token t;
+    std::vector<uint64_t> newly;
+    static int mode = -1;                          // CEL_HALO_MODE bit 2 off: incoming copies awaited by the stream
+    if (mode < 0) {
+        const char* e = getenv("CEL_HALO_MODE");
+        mode = e ? atoi(e) : 3;
+    }
+    cur_ins_ = &k;
+    for (uint64_t j : k.deps) {
+        Token dt = dep_token(j);
+        auto ci = copy_info_.find(j);
+        if ((mode & 2) && dt.local.empty() && dt.remote.size() == 1 && ci != copy_info_.end() &&
+            ci->second.dst_aid == k.bindings[0]) {
+            // the flag is the remote entry's (an elided copy's token is its
+            // own dependencies': the id to wait for is not always j)
+            const uint64_t rj = dt.remote[0].second;
+            const uint64_t key = (uint64_t(dt.remote[0].first) << 56) ^ rj;
+            if (cs.waited_remote.count(key)) continue;     // an earlier launch on this stream waited for it
+            if (po.n_in == kMaxGatherDst) return false;
+            po.in_flag[po.n_in] = reinterpret_cast<const unsigned long long*>(sig_slot(dev, dt.remote[0].first, rj));
+            po.in_value[po.n_in] = rj;
+            po.n_in++;
+            newly.push_back(key);
+        } else {
+            merge(t, dt);
+        }
+    }
+    for (const Instr& p : pushes) {
+        cur_ins_ = &p;
+        for (uint64_t j : p.deps) {
+            if (j == k.iid) continue;
+            Token dt = dep_token(j);
+            merge(t, Token{dt.local, {}});
+            for (auto& r : dt.remote) {
+                const uint64_t key = (uint64_t(r.first) << 56) ^ r.second;
+                if (cs.waited_remote.count(key)) continue;
+                const unsigned long long* f = reinterpret_cast<const unsigned long long*>(sig_slot(dev, r.first, r.second));
+                bool dup = false;
+                for (int i = 0; i < po.n_wait; ++i) dup = dup || po.wait_flag[i] == f;
+                if (dup) continue;
+                if (po.n_wait == kMaxGatherDst) return false;
+                po.wait_flag[po.n_wait] = f;
+                po.wait_value[po.n_wait] = r.second;
+                po.n_wait++;
+                newly.push_back(key);
+            }
+        }
+        const AllocRec& D = allocs_.at(p.dst_aid);
+        po.base[po.n] = base_of(D);
+        po.lo0[po.n] = D.box.lo[0];
+        po.lo1[po.n] = D.box.lo[1];
+        po.n1[po.n] = D.box.extent(1);
+        po.flag[po.n] = reinterpret_cast<unsigned long long*>(sig_slot(p.dst_mem - 2, cfg_.rank, p.iid));
+        po.value[po.n] = p.iid;
+        po.n++;
+    }
+    po.ctr = reinterpret_cast<unsigned*>(arenas_[dev].base + gather_off_ + 128);
+    if (trace_) {
+        const AllocRec& R = allocs_.at(k.bindings[0]);
+        const AllocRec& Wa = allocs_.at(k.bindings[1]);
+        fprintf(stderr, "[cel r%d] rsim fused iid %llu t %u R aid %lld box [%lld,%lld)x[%lld,%lld) abs %lld W aid %lld abs %lld in %d war %d out %d\n",
+                cfg_.rank, (unsigned long long)k.iid, a.t, (long long)k.bindings[0], (long long)R.box.lo[0], (long long)R.box.hi[0],
+                (long long)R.box.lo[1], (long long)R.box.hi[1], (long long)R.absorbed_into, (long long)k.bindings[1],
+                (long long)Wa.absorbed_into, po.n_in, po.n_wait, po.n);
+        for (const Instr& p : pushes) {
+            const AllocRec& D = allocs_.at(p.dst_aid);
+            fprintf(stderr, "[cel r%d]   push iid %llu -> dev %d aid %lld box [%lld,%lld)x[%lld,%lld) abs %lld region [%lld,%lld)x[%lld,%lld)\n",
+                    cfg_.rank, (unsigned long long)p.iid, p.dst_mem - 2, (long long)p.dst_aid, (long long)D.box.lo[0],
+                    (long long)D.box.hi[0], (long long)D.box.lo[1], (long long)D.box.hi[1], (long long)D.absorbed_into,
+                    (long long)p.region[0].lo[0], (long long)p.region[0].hi[0], (long long)p.region[0].lo[1],
+                    (long long)p.region[0].hi[1]);
+        }
+    }
+    cur_ins_ = &k;
+    set_dev(dev);
+    wait_token(sidx, t);
+    int n = 0;
+    if (cfg_.profile && prof_sample(K_RSIM_ROW)) {
+        Prof pr{K_RSIM_ROW, prof_event(dev), prof_event(dev), dev, k.iid, sidx, now_ns()};
+        cudaEventRecord(pr.a, cs.s);
+        n = launch_rsim_fused(a, po, cs.s);
+        cudaEventRecord(pr.b, cs.s);
+        prof_pending_.push_back(pr);
+    } else {
+        n = launch_rsim_fused(a, po, cs.s);
+    }
+    check(cudaGetLastError(), "fused RSim row launch (flags)");
+    if (n != 1) {
+        if (!err_) {
+            errmsg_ = "fused RSim row: kernel no longer applicable";
+            err_ = E_STATE;
+        }
+        return true;
+    }
+    for (uint64_t key : newly) cs.waited_remote.insert(key);
+    st_.kernel_launches += 1;
+    st_.workload_launches += 1;
+    st_.halo_fused += pushes.size();
+    st_.halo_in_waits += uint64_t(po.n_in);
+    const Token done = record(sidx);
+    tok_[k.iid] = done;
+    kind_of_[k.iid] = dev;
+    for (const Instr& p : pushes) {
+        tok_[p.iid] = done;
+        kind_of_[p.iid] = dev;
+        copy_info_[p.iid] = CopyInfo{p.src_aid, p.dst_aid, rbbox(p.region), p.region};
+        signalled_.insert(p.iid * uint64_t(cfg_.world) + uint64_t(owner_rank(p.dst_mem - 2)));
+        st_.bytes_copy[2] += rvolume(p.region) * 4;
+    }
+    if (grown_) {
+        note_use(k);
+        for (const Instr& p : pushes) note_use(p);
+    }
+    return true;
+}
+
 // Launch the held-back kernel with its pushes, or say it cannot.
 bool Executor::halo_launch(const Instr& k, const std::vector<Instr>& pushes) {
+    if (k.desc->kernel == K_RSIM_ROW) return halo_launch_rsim(k, pushes);
     const int dev = k.device;
     const int sidx = dev * kStreamsPerDev + S_COMPUTE;
     KArgs a;
@@ -96,8 +243,9 @@ bool Executor::halo_launch(const Instr& k, const std::vector<Instr>& pushes) {
         auto ci = copy_info_.find(j);
         if ((mode & 2) && dt.local.empty() && dt.remote.size() == 1 && ci != copy_info_.end() && ci->second.dst_aid == k.bindings[0] &&
             hx.n_in < kHaloMax) {
-            hx.in_flag[hx.n_in] = reinterpret_cast<const unsigned long long*>(sig_slot(dev, dt.remote[0].first, j));
-            hx.in_value[hx.n_in] = j;
+            const uint64_t rj = dt.remote[0].second;     // the remote entry's id (see halo_launch_rsim)
+            hx.in_flag[hx.n_in] = reinterpret_cast<const unsigned long long*>(sig_slot(dev, dt.remote[0].first, rj));
+            hx.in_value[hx.n_in] = rj;
             hx.in_r0[hx.n_in] = ci->second.bb.lo[0];
             hx.in_r1[hx.n_in] = ci->second.bb.hi[0];
             hx.n_in++;

@@ -1066,6 +1066,8 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CU
     // (a no-op when the launch was not programmatic)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (kPeer && po.n_in && threadIdx.x == 0)        // rows other GPUs stored under a flag (TMA reads them from L2)
+        for (int k = 0; k < po.n_in; ++k) wait_flag(po.in_flag[k], po.in_value[k]);
     __syncthreads();
     auto issue = [&](int g) {
         const int st = g % kRS;
@@ -1123,6 +1125,11 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CU
         __syncthreads();
     }
     const int64_t i = i0 + j;
+    if (kPeer && po.n_wait) {                        // the receivers' readers of row t are done
+        if (threadIdx.x == 0)
+            for (int k = 0; k < po.n_wait; ++k) wait_flag(po.wait_flag[k], po.wait_value[k]);
+        __syncthreads();
+    }
     if (i < a.chunk.hi[0]) {
         const float prev = *ptr<const float>(R, t - 1, i, 0);
         const float coef = 0.5f / float(t);
@@ -1132,7 +1139,19 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CU
             for (int k = 0; k < po.n; ++k)
                 reinterpret_cast<float*>(po.base[k])[(t - po.lo0[k]) * po.n1[k] + (i - po.lo1[k])] = out;
     }
-    if (kPeer) {
+    if (kPeer && po.flags) {
+        // every receiver's row lands before its flag: the last CTA publishes them
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned prevc = atomicAdd(po.ctr, 1u);
+            if (prevc == gridDim.x - 1) {
+                *po.ctr = 0;
+                __threadfence_system();
+                for (int k = 0; k < po.n; ++k) st_release_sys(po.flag[k], po.value[k]);
+            }
+        }
+    } else if (kPeer) {
         // the row's gather: every receiver's copy lands before its counter moves
         __threadfence_system();
         __syncthreads();

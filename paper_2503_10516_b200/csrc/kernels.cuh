@@ -186,6 +186,19 @@ struct PeerOut {
     int64_t lo0[kMaxGatherDst], lo1[kMaxGatherDst], n1[kMaxGatherDst];   // receiver allocation box (rows, cols)
     unsigned long long* counter[kMaxGatherDst];
     unsigned* ctr;
+    // flag mode (exec_halo.cu, one process per GPU): the outputs are plain
+    // coherence copies -- the last CTA writes each receiver's flag slot with
+    // the copy's id instead of bumping a gather counter -- and the incoming
+    // copies of the rows this kernel reads are awaited in the kernel
+    int flags;
+    unsigned long long* flag[kMaxGatherDst];
+    unsigned long long value[kMaxGatherDst];
+    int n_wait;                                    // flags awaited before the (remote) writes: WAR dependencies
+    const unsigned long long* wait_flag[kMaxGatherDst];
+    unsigned long long wait_value[kMaxGatherDst];
+    int n_in;                                      // incoming copies: awaited before any load
+    const unsigned long long* in_flag[kMaxGatherDst];
+    unsigned long long in_value[kMaxGatherDst];
 };
 bool rsim_fusable(const KArgs& a);                       // the TMA row kernel applies (it carries the epilogue)
 int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s);

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--execute", type=int, default=1)
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--modes", default="auto,none")
     ap.add_argument("--fold", type=int, default=0,
                     help="k > 0: ranks share k GPUs (rank r on GPU r %% k): CUDA IPC and flags within one GPU")
     args = ap.parse_args()
@@ -39,7 +40,7 @@ def main():
     from paper_2503_10516_b200 import cel
     progs = [P.c1_chain(4096), P.wavesim(1024, 9, rows=700), P.nbody(3000, 2), P.nbody(500, 2, host_init=True),
              P.rsim(3000, 20), P.jacobi3d(40, 3)]
-    modes = ["auto", "none"]
+    modes = args.modes.split(",")
     if args.only:
         progs = [p for p in progs if p["name"] == args.only]
     if not args.quick:
