@@ -282,6 +282,87 @@ inline void canon_dim(Region& bs, int d, Region& out) {
 }
 }  // namespace detail
 
+namespace detail {
+// canon_dim for boxes that all share one dim-2 range (1-D and 2-D buffers):
+// the same dissection -- dim-0 slabs cut where the set of dim-1 intervals
+// changes, each slab's merged dim-1 intervals -- on the stack.  false: too
+// many boxes for the fixed arrays (the caller takes the general path).
+inline bool canon_2d(const Region& bs, Region& out) {
+    constexpr int kN = 16;
+    const int n = int(bs.size());
+    if (n > kN) return false;
+    int64_t cuts[2 * kN];
+    int nc = 0;
+    for (const Box& b : bs) {
+        cuts[nc++] = b.lo[0];
+        cuts[nc++] = b.hi[0];
+    }
+    std::sort(cuts, cuts + nc);
+    nc = int(std::unique(cuts, cuts + nc) - cuts);
+    const int64_t z0 = bs[0].lo[2], z1 = bs[0].hi[2];
+    int64_t pa[kN], pb[kN], ca[kN], cb[kN];
+    int np = 0;
+    int64_t s0 = 0, s1 = 0;
+    auto flush = [&]() {
+        for (int i = 0; i < np; ++i) {
+            Box b;
+            b.lo[0] = s0; b.hi[0] = s1;
+            b.lo[1] = pa[i]; b.hi[1] = pb[i];
+            b.lo[2] = z0; b.hi[2] = z1;
+            out.push_back(b);
+        }
+        np = 0;
+    };
+    for (int k = 0; k + 1 < nc; ++k) {
+        const int64_t lo = cuts[k], hi = cuts[k + 1];
+        int m = 0;
+        for (const Box& b : bs)
+            if (b.lo[0] <= lo && hi <= b.hi[0]) {
+                // insertion by start, then merge
+                int p = m++;
+                while (p > 0 && ca[p - 1] > b.lo[1]) {
+                    ca[p] = ca[p - 1];
+                    cb[p] = cb[p - 1];
+                    --p;
+                }
+                ca[p] = b.lo[1];
+                cb[p] = b.hi[1];
+            }
+        int w = 0;
+        for (int i = 0; i < m; ++i) {
+            if (w > 0 && ca[i] <= cb[w - 1]) {
+                if (cb[i] > cb[w - 1]) cb[w - 1] = cb[i];
+            } else {
+                ca[w] = ca[i];
+                cb[w] = cb[i];
+                ++w;
+            }
+        }
+        m = w;
+        if (m == 0) {
+            flush();
+            continue;
+        }
+        bool same = np == m && s1 == lo;
+        for (int i = 0; same && i < m; ++i) same = pa[i] == ca[i] && pb[i] == cb[i];
+        if (same) {
+            s1 = hi;
+        } else {
+            flush();
+            for (int i = 0; i < m; ++i) {
+                pa[i] = ca[i];
+                pb[i] = cb[i];
+            }
+            np = m;
+            s0 = lo;
+            s1 = hi;
+        }
+    }
+    flush();
+    return true;
+}
+}  // namespace detail
+
 inline Region canon(Region boxes) {
     boxes.erase(std::remove_if(boxes.begin(), boxes.end(), [](const Box& b) { return b.empty(); }), boxes.end());
     Region out;
@@ -311,6 +392,14 @@ inline Region canon(Region boxes) {
         }
         return out;
     }
+    bool flat = true;                             // one dim-2 range: the stack path
+    for (const Box& b : boxes)
+        if (b.lo[2] != f.lo[2] || b.hi[2] != f.hi[2]) {
+            flat = false;
+            break;
+        }
+    if (flat && detail::canon_2d(boxes, out)) return out;
+    out.clear();
     detail::canon_dim(boxes, 0, out);
     return out;
 }
