@@ -69,6 +69,13 @@ inline Box intersect(const Box& a, const Box& b) {
     return r.normalized();
 }
 
+// a and b share a point (both non-empty): the intersection test of the hot
+// scans, without building the intersection
+inline bool overlaps(const Box& a, const Box& b) {
+    return a.lo[0] < b.hi[0] && b.lo[0] < a.hi[0] && a.lo[1] < b.hi[1] && b.lo[1] < a.hi[1] && a.lo[2] < b.hi[2] &&
+           b.lo[2] < a.hi[2] && !a.empty() && !b.empty();
+}
+
 inline Box bbox(const Box& a, const Box& b) {
     if (a.empty()) return b.normalized();
     if (b.empty()) return a;
@@ -461,8 +468,7 @@ inline Region rdiff_nobb(const Region& a, const Region& b) {
     for (const Box& y : b) {
         nxt.clear();
         for (const Box& x : cur) {
-            Box i = intersect(x, y);
-            if (i.empty()) {
+            if (!overlaps(x, y)) {
                 nxt.push_back(x);
             } else {
                 changed = true;
@@ -490,7 +496,7 @@ inline Box rbbox(const Region& r) {
 
 inline bool rintersects(const Region& a, const Box& b) {
     for (const Box& x : a)
-        if (!intersect(x, b).empty()) return true;
+        if (overlaps(x, b)) return true;
     return false;
 }
 
@@ -530,7 +536,7 @@ struct RegionMap {
         size_t w = 0;
         for (size_t i = 0; i < e.size(); ++i) {
             Entry& p = e[i];
-            if (!intersect(p.bb, rb).empty()) {
+            if (overlaps(p.bb, rb)) {
                 Region rr = rdiff_nobb(p.second, reg);
                 if (rr.empty()) continue;
                 if (rr.size() != p.second.size() || !(rr == p.second)) {
@@ -555,7 +561,7 @@ struct RegionMap {
         size_t w = 0;
         for (size_t i = 0; i < e.size(); ++i) {
             Entry& p = e[i];
-            if (!intersect(p.bb, rb).empty()) {
+            if (overlaps(p.bb, rb)) {
                 Region in = rinter(p.second, reg);
                 if (!in.empty()) {
                     Region out = rdiff_nobb(p.second, reg);
@@ -611,7 +617,7 @@ struct RegionMap {
         if (reg.empty()) return out;
         const Box rb = rbbox(reg);
         for (auto& p : e) {
-            if (intersect(p.bb, rb).empty()) continue;
+            if (!overlaps(p.bb, rb)) continue;
             Region i = rinter(p.second, reg);
             if (!i.empty()) out.push_back({std::move(i), p.first});
         }
@@ -624,12 +630,12 @@ struct RegionMap {
         if (reg.empty()) return;
         const Box rb = rbbox(reg);
         for (auto& p : e) {
-            if (intersect(p.bb, rb).empty()) continue;
+            if (!overlaps(p.bb, rb)) continue;
             bool hit = false;
             for (const Box& x : p.second) {
-                if (intersect(x, rb).empty()) continue;
+                if (!overlaps(x, rb)) continue;
                 for (const Box& y : reg)
-                    if (!intersect(x, y).empty()) {
+                    if (overlaps(x, y)) {
                         hit = true;
                         break;
                     }

@@ -99,11 +99,11 @@ struct ReaderList {
         if (w.empty()) return;
         const Box wb = rbbox(w);
         for (const Rec& x : recs) {
-            if (intersect(x.bb, wb).empty()) continue;
+            if (!overlaps(x.bb, wb)) continue;
             bool hit = false;
             for (const Box& a : x.r) {
                 for (const Box& b : w)
-                    if (!intersect(a, b).empty()) {
+                    if (overlaps(a, b)) {
                         hit = true;
                         break;
                     }
@@ -118,7 +118,7 @@ struct ReaderList {
         size_t k = 0;
         for (size_t i = 0; i < recs.size(); ++i) {
             Rec& x = recs[i];
-            if (!intersect(x.bb, wb).empty()) {
+            if (overlaps(x.bb, wb)) {
                 Region rest = rdiff_nobb(x.r, w);
                 if (rest.empty()) continue;
                 if (!(rest == x.r)) {
