@@ -359,7 +359,10 @@ int Scheduler::task_submit(const TaskDesc& desc, uint64_t* tid_out, std::string*
         if (rc != E_OK) return rc;
         for (auto& kv : c.reads) reads[kv.first.second] = runion(reads[kv.first.second], kv.second);
         for (auto& kv : c.writes) writes[kv.first.second] = runion(writes[kv.first.second], kv.second);
-        if (memo_on_) prep_store(std::move(key), h, c, reads, writes);
+        // a shape's second submission stores its prepare() result (most
+        // programs repeat shapes; RSim's never do, and pays only a hash)
+        if (memo_on_ && !prep_seen_.insert(h).second) prep_store(std::move(key), h, c, reads, writes);
+        if (prep_seen_.size() > 4096) prep_seen_.clear();
     }
     c.desc = std::make_shared<const TaskDesc>(desc);
     return submit_cmd(std::move(c), reads, writes, tid_out);

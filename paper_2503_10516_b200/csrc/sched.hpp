@@ -12,6 +12,7 @@
 #include <string>
 #include <tuple>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "geom.hpp"
@@ -435,6 +436,7 @@ private:
     // to the next iid): a hit re-emits the recorded instructions with ids
     // shifted and installs the recorded end state, shifted the same way.
     std::unordered_map<uint64_t, std::shared_ptr<PrepMemo>> prep_memo_;   // by hash of the shape key
+    std::unordered_set<uint64_t> prep_seen_;                               // shape hashes submitted once
     bool memo_on_ = true;
     std::vector<Instr>* recording_ = nullptr;        // emit() copies instructions here while set
     uint64_t memo_hits_ = 0, memo_misses_ = 0;
