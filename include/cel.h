@@ -213,6 +213,7 @@ typedef struct cel_stats_s {
     uint64_t coll_fused;                  /* ... fused into the RSim row kernels that produce them */
     uint64_t halo_fused;                  /* coherence copies stored by the stencil launch that writes their rows */
     uint64_t halo_in_waits;               /* incoming copies awaited by the reading CTAs of a fused launch */
+    uint64_t halo_chained;                /* fused RSim rows that waited for the previous row's local stores, not its grid */
     uint64_t memo_hits, memo_misses;      /* task compiles replayed from the steady-state memo / recorded into it
                                              (CEL_SCHED_MEMO=0 disables it; the instructions are the same) */
 } cel_stats_t;

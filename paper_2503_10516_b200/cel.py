@@ -85,7 +85,7 @@ class cel_stats(C.Structure):
         "signal_ns", "remote_wait_ns", "copies_elided", "bytes_elided", "coll_groups", "coll_copies",
         "gather_sets", "n_send", "n_receive", "n_split_receive", "n_await_receive", "pulls", "pull_bytes",
         "coll_allgathers", "tma_copy_launches", "vmm_maps", "vmm_mapped_bytes", "coll_multicast", "staging_elided",
-        "staging_materialized", "coll_p2p", "coll_fused", "halo_fused", "halo_in_waits", "memo_hits", "memo_misses")]
+        "staging_materialized", "coll_p2p", "coll_fused", "halo_fused", "halo_in_waits", "halo_chained", "memo_hits", "memo_misses")]
 
 
 _P = C.c_void_p

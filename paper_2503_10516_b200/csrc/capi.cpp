@@ -389,6 +389,7 @@ int cel_stats(cel_runtime* rt, cel_stats_t* o) {
         o->coll_fused += e.coll_fused;
         o->halo_fused += e.halo_fused;
         o->halo_in_waits += e.halo_in_waits;
+        o->halo_chained += e.halo_chained;
         o->staging_elided += e.staging_elided;
         o->staging_materialized += e.staging_materialized;
     }

@@ -732,6 +732,7 @@ void Executor::wait_token(int sidx, const Token& t) {
         if (e.stream == sidx || e.seq <= streams_[e.stream].done) continue;
         check(cudaStreamWaitEvent(s.s, e.ev, 0), "cudaStreamWaitEvent");
         st_.event_waits++;
+        s.waits++;
     }
     for (auto& r : t.remote) {
         // a flag this stream already waited for is satisfied for everything
@@ -751,6 +752,7 @@ void Executor::wait_token(int sidx, const Token& t) {
                "cuStreamWaitValue64");
         st_.remote_wait_ns += now_ns() - tw;
         st_.remote_waits++;
+        s.waits++;
     }
 }
 

@@ -128,6 +128,7 @@ struct ExecStats {
     uint64_t coll_fused = 0;                        // ... fused into the RSim row kernels that produce them
     uint64_t halo_fused = 0;                        // coherence copies stored by the stencil launch that writes them
     uint64_t halo_in_waits = 0;                     // incoming copies awaited inside the consuming launch
+    uint64_t halo_chained = 0;                      // fused RSim rows chained to the previous row's local stores
     uint64_t staging_elided = 0, staging_materialized = 0;   // device-direct sends (virtual-node mode)
     uint64_t memcpy_calls = 0;         // cudaMemcpy3DAsync (H2D / D2H)
     uint64_t bytes_copy[6] = {};       // 0 resize, 1 d2d same GPU, 2 d2d peer, 3 h2d, 4 d2h, 5 other
@@ -211,6 +212,7 @@ private:
         uint64_t done = 0;
         std::deque<std::pair<uint64_t, cudaEvent_t>> inflight;
         std::unordered_set<uint64_t> waited_remote;   // (rank, iid) flags already waited on this stream
+        uint64_t waits = 0;                           // waits enqueued (event / flag)
     };
     struct FreeRange {
         uint64_t len;
@@ -377,6 +379,11 @@ private:
     std::vector<Instr> halo_deferred_;            // horizons that arrived in between
     std::unordered_set<uint64_t> halo_iids_;
     std::vector<std::array<unsigned, kHaloMax>> halo_ctr_;   // per device: CTA counters' host copies
+    struct RsimChain {                            // per device: fused RSim rows (exec_halo.cu)
+        unsigned ctr = 0, done = 0;               // the device counters' values after the last launch
+        uint64_t seq = ~0ull, waits = ~0ull;      // compute stream state right after it
+    };
+    std::vector<RsimChain> rsim_chain_;
     bool halo_candidate(const Instr& ins);
     bool halo_attach(const Instr& ins);
     bool halo_depends(const Instr& ins) const;

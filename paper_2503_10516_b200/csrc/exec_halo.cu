@@ -121,6 +121,10 @@ bool Executor::halo_launch_rsim(const Instr& k, const std::vector<Instr>& pushes
             if (po.n_in == kMaxGatherDst) return false;
             po.in_flag[po.n_in] = reinterpret_cast<const unsigned long long*>(sig_slot(dev, dt.remote[0].first, rj));
             po.in_value[po.n_in] = rj;
+            // rows the awaited copy may have written: its own region, or -- an
+            // elided copy standing for its dependencies -- any row
+            const int64_t r0 = (rj == j) ? ci->second.bb.lo[0] : 0;
+            po.in_row0 = po.n_in == 0 ? r0 : std::min(po.in_row0, r0);
             po.n_in++;
             newly.push_back(key);
         } else {
@@ -157,6 +161,7 @@ bool Executor::halo_launch_rsim(const Instr& k, const std::vector<Instr>& pushes
         po.n++;
     }
     po.ctr = reinterpret_cast<unsigned*>(arenas_[dev].base + gather_off_ + 128);
+    po.done = reinterpret_cast<unsigned*>(arenas_[dev].base + gather_off_ + 192);
     if (trace_) {
         const AllocRec& R = allocs_.at(k.bindings[0]);
         const AllocRec& Wa = allocs_.at(k.bindings[1]);
@@ -176,6 +181,21 @@ bool Executor::halo_launch_rsim(const Instr& k, const std::vector<Instr>& pushes
     cur_ins_ = &k;
     set_dev(dev);
     wait_token(sidx, t);
+    // row chain: when the previous operation on the compute stream was a
+    // fused row and this one needs no other wait, wait for the previous row's
+    // local stores (its CTAs' count) instead of its grid, whose tail waits for
+    // the NVLink stores' acknowledgements (CEL_RSIM_CHAIN=0: off)
+    static int chain_env = -1;
+    if (chain_env < 0) {
+        const char* e = getenv("CEL_RSIM_CHAIN");
+        chain_env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (rsim_chain_.empty()) rsim_chain_.resize(size_t(G_));
+    RsimChain& rc = rsim_chain_[size_t(dev)];
+    const unsigned grid = unsigned((k.chunk.volume() + 127) / 128);
+    po.ctr_last = rc.ctr + grid - 1;
+    po.done_wait = rc.done;
+    po.chain = chain_env && rc.done > 0 && cs.seq == rc.seq && cs.waits == rc.waits ? 1 : 0;
     int n = 0;
     if (cfg_.profile && prof_sample(K_RSIM_ROW)) {
         Prof pr{K_RSIM_ROW, prof_event(dev), prof_event(dev), dev, k.iid, sidx, now_ns()};
@@ -195,11 +215,16 @@ bool Executor::halo_launch_rsim(const Instr& k, const std::vector<Instr>& pushes
         return true;
     }
     for (uint64_t key : newly) cs.waited_remote.insert(key);
+    rc.ctr += grid;
+    rc.done += grid;
     st_.kernel_launches += 1;
     st_.workload_launches += 1;
     st_.halo_fused += pushes.size();
     st_.halo_in_waits += uint64_t(po.n_in);
     const Token done = record(sidx);
+    rc.seq = cs.seq;
+    rc.waits = cs.waits;
+    st_.halo_chained += uint64_t(po.chain);
     tok_[k.iid] = done;
     kind_of_[k.iid] = dev;
     for (const Instr& p : pushes) {

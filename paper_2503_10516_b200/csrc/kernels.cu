@@ -503,6 +503,19 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned ld_acquire_gpu32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// spin until *f >= v (32-bit counter, wrap-safe); traps like wait_flag
+__device__ __forceinline__ void wait_flag32(const unsigned* f, unsigned v) {
+    const long long t0 = clock64();
+    while (int(ld_acquire_gpu32(f) - v) < 0) {
+        __nanosleep(32);
+        if (clock64() - t0 > (1ll << 34)) __trap();
+    }
+}
 // spin until *f >= v; a flag that never comes traps after ~2^34 cycles (a
 // failed launch instead of a hung GPU)
 __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long v) {
@@ -1065,11 +1078,27 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CU
     // reads rows the previous kernel wrote, so wait for it to have completed
     // (a no-op when the launch was not programmatic)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (kPeer && po.n_in && threadIdx.x == 0)        // rows other GPUs stored under a flag (TMA reads them from L2)
-        for (int k = 0; k < po.n_in; ++k) wait_flag(po.in_flag[k], po.in_value[k]);
+    if (kPeer && po.chain) {
+        if (threadIdx.x == 0) {
+            wait_flag32(po.done, po.done_wait);
+            // the rows were written by generic-proxy stores; TMA reads them
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     __syncthreads();
+    // incoming rows (other GPUs' stores under a flag; TMA reads them from L2)
+    // are the newest ones (row t - 1 in steady state): the producer waits for
+    // their flags only before issuing the first stage that holds a row at or
+    // after po.in_row0, so the older rows stream meanwhile
+    bool in_done = !(kPeer && po.n_in);
     auto issue = [&](int g) {
+        if (kPeer && !in_done && int64_t(g + 1) * kRR > po.in_row0) {
+            for (int k = 0; k < po.n_in; ++k) wait_flag(po.in_flag[k], po.in_value[k]);
+            asm volatile("fence.proxy.async.global;" ::: "memory");   // generic-proxy stores, TMA reads
+            in_done = true;
+        }
         const int st = g % kRS;
         const int64_t s0 = int64_t(g) * kRR;
         const int nr = int(t - s0 < kRR ? t - s0 : kRR);
@@ -1130,23 +1159,31 @@ __global__ void __launch_bounds__(kRC) rsim_row_tma_t(const __grid_constant__ CU
             for (int k = 0; k < po.n_wait; ++k) wait_flag(po.wait_flag[k], po.wait_value[k]);
         __syncthreads();
     }
+    float out = 0.f;
     if (i < a.chunk.hi[0]) {
-        const float prev = *ptr<const float>(R, t - 1, i, 0);
+        const float prev = (kPeer && po.chain) ? __ldcg(ptr<const float>(R, t - 1, i, 0)) : *ptr<const float>(R, t - 1, i, 0);
         const float coef = 0.5f / float(t);
-        const float out = 0.5f * prev + coef * acc;
+        out = 0.5f * prev + coef * acc;
         *ptr<float>(Wr, t, i, 0) = out;
-        if (kPeer)
-            for (int k = 0; k < po.n; ++k)
-                reinterpret_cast<float*>(po.base[k])[(t - po.lo0[k]) * po.n1[k] + (i - po.lo1[k])] = out;
     }
+    if (kPeer && po.flags && po.done) {
+        // the row is stored locally: the next row's CTAs may read it
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(po.done, 1u);
+        }
+    }
+    if (kPeer && i < a.chunk.hi[0])
+        for (int k = 0; k < po.n; ++k)
+            reinterpret_cast<float*>(po.base[k])[(t - po.lo0[k]) * po.n1[k] + (i - po.lo1[k])] = out;
     if (kPeer && po.flags) {
         // every receiver's row lands before its flag: the last CTA publishes them
         __threadfence_system();
         __syncthreads();
         if (threadIdx.x == 0) {
             const unsigned prevc = atomicAdd(po.ctr, 1u);
-            if (prevc == gridDim.x - 1) {
-                *po.ctr = 0;
+            if (prevc == po.ctr_last) {
                 __threadfence_system();
                 for (int k = 0; k < po.n; ++k) st_release_sys(po.flag[k], po.value[k]);
             }

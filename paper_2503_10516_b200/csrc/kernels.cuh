@@ -196,9 +196,18 @@ struct PeerOut {
     int n_wait;                                    // flags awaited before the (remote) writes: WAR dependencies
     const unsigned long long* wait_flag[kMaxGatherDst];
     unsigned long long wait_value[kMaxGatherDst];
-    int n_in;                                      // incoming copies: awaited before any load
+    int n_in;                                      // incoming copies: awaited before loading rows >= in_row0
     const unsigned long long* in_flag[kMaxGatherDst];
     unsigned long long in_value[kMaxGatherDst];
+    int64_t in_row0;                               // the lowest row they write
+    unsigned ctr_last;                             // flag mode: CTA counter value before the last CTA's increment
+    // row chain (flag mode): every CTA counts itself into *done once its row
+    // is stored locally; a chained launch waits for *done >= done_wait (the
+    // previous row's CTAs) instead of for the whole previous grid, so this
+    // row runs while the previous one's CTAs wait for their NVLink stores
+    unsigned* done;
+    unsigned done_wait;
+    int chain;
 };
 bool rsim_fusable(const KArgs& a);                       // the TMA row kernel applies (it carries the epilogue)
 int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s);

@@ -80,8 +80,8 @@ def main():
                 rt.shutdown = keep_stats
                 res = [r[1] for r in run_program(rt, prog) if r[0] == "read"]
                 if rank == 0 and stats.get("halo_fused"):
-                    print("  halo copies fused into the stencil %d, incoming awaited in-kernel %d"
-                          % (stats["halo_fused"], stats["halo_in_waits"]), flush=True)
+                    print("  halo copies fused into the stencil %d, incoming awaited in-kernel %d, chained rows %d"
+                          % (stats["halo_fused"], stats["halo_in_waits"], stats["halo_chained"]), flush=True)
                 if rank == 0 and stats.get("gather_sets"):
                     print("  all-gather sets %d, run as NCCL groups %d" % (stats["gather_sets"], stats["coll_groups"]),
                           flush=True)

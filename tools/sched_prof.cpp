@@ -4,7 +4,12 @@
 //   g++ -O2 -std=c++17 -Ipaper_2503_10516_b200/csrc tools/sched_prof.cpp paper_2503_10516_b200/csrc/sched.cpp
 //       paper_2503_10516_b200/csrc/sched_memo.cpp -o /tmp/sched_prof && /tmp/sched_prof 8 [rank]
 //   /tmp/sched_prof rsim 4 [rank] [T]      (RSim rows, W = 84,000)
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -15,7 +20,94 @@ using namespace cel;
 
 struct Count : InstrSink {
     uint64_t n = 0;
-    void on_instr(const Instr&) override { ++n; }
+    bool copy = getenv("CEL_PROF_COPY") != nullptr;
+    void on_instr(const Instr& ins) override {
+        ++n;
+        if (copy) {
+            Instr x = ins;                           // the hand-off's copy alone
+            asm volatile("" ::"r"(&x) : "memory");
+        }
+    }
+};
+
+// the executor's hand-off without CUDA: copy into a mutex-guarded deque that
+// a consumer thread drains (CEL_PROF_QUEUE=1)
+struct QueueSink : InstrSink {
+    std::mutex m;
+    std::condition_variable cv;
+    std::deque<Instr> q;
+    std::vector<Instr> pool;                      // CEL_PROF_POOL=1: the executor's recycling
+    bool pooled = getenv("CEL_PROF_POOL") != nullptr;
+    bool stop = false, sleeping = false;
+    bool batched = getenv("CEL_PROF_QUEUE")[0] == '2';
+    std::atomic<size_t> size{0};
+    uint64_t n = 0;
+    std::thread th;
+    QueueSink() {
+        th = std::thread([this] {
+            std::deque<Instr> batch;
+            for (;;) {
+                {
+                    std::unique_lock<std::mutex> l(m);
+                    if (q.empty()) {
+                        l.unlock();
+                        for (int i = 0; i < 20000 && size.load(std::memory_order_acquire) == 0 && !stop; ++i) {
+                        }
+                        l.lock();
+                        while (q.empty() && !stop) {
+                            sleeping = true;
+                            cv.wait(l);
+                            sleeping = false;
+                        }
+                        if (q.empty() && stop) return;
+                    }
+                    if (batched) {
+                        batch.swap(q);
+                    } else {
+                        batch.push_back(std::move(q.front()));
+                        q.pop_front();
+                    }
+                    size.store(q.size(), std::memory_order_release);
+                }
+                while (!batch.empty()) {
+                    Instr x = std::move(batch.front());
+                    batch.pop_front();
+                    ++n;
+                    if (pooled) {
+                        std::lock_guard<std::mutex> g(m);
+                        if (pool.size() < 4096) pool.push_back(std::move(x));
+                    }
+                }
+            }
+        });
+    }
+    ~QueueSink() {
+        {
+            std::lock_guard<std::mutex> g(m);
+            stop = true;
+        }
+        cv.notify_one();
+        th.join();
+    }
+    void on_instr(const Instr& ins) override {
+        bool wake;
+        Instr x;
+        if (pooled) {
+            std::lock_guard<std::mutex> g(m);
+            if (!pool.empty()) {
+                x = std::move(pool.back());
+                pool.pop_back();
+            }
+        }
+        x = ins;
+        {
+            std::lock_guard<std::mutex> g(m);
+            q.push_back(std::move(x));
+            size.store(q.size(), std::memory_order_release);
+            wake = sleeping;
+        }
+        if (wake) cv.notify_one();
+    }
 };
 
 static TaskDesc fill(int64_t n, uint32_t buf) {
@@ -79,8 +171,11 @@ static TaskDesc rsim_row(int64_t W, int64_t t) {
 
 static int rsim_main(int G, int rank, int T) {
     const int64_t W = 84000;
-    Count sink;
-    Scheduler s(G, 1, 4, true, &sink, nullptr);
+    Count count;
+    QueueSink* qs = getenv("CEL_PROF_QUEUE") ? new QueueSink : nullptr;
+    InstrSink* sk = qs ? static_cast<InstrSink*>(qs) : static_cast<InstrSink*>(&count);
+    struct { uint64_t n = 0; } sink;
+    Scheduler s(G, 1, 4, true, sk, nullptr);
     if (rank >= 0) s.set_rank_filter(rank, G);
     const int64_t ext[3] = {T, W, 1};
     uint32_t b0;
@@ -95,9 +190,11 @@ static int rsim_main(int G, int rank, int T) {
     for (int t = 1; t < T; ++t) s.task_submit(rsim_row(W, t), &tid, &err);
     s.wait();
     const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    printf("rsim G=%d rank=%d T=%d: %.2f us/row, %.1f instructions/row\n", G, rank, T, dt / (T - 1) * 1e6,
-           double(sink.n) / (T - 1));
+    sink.n = count.n;
+    printf("rsim G=%d rank=%d T=%d%s: %.2f us/row, %.1f instructions/row\n", G, rank, T, qs ? " (queue sink)" : "",
+           dt / (T - 1) * 1e6, double(sink.n) / (T - 1));
     s.shutdown();
+    delete qs;
     return 0;
 }
 
