@@ -666,6 +666,16 @@ __global__ void __launch_bounds__(128) wave5_halo(const __grid_constant__ KArgs 
     wave5_body<true>(a, &hx);
 }
 
+// The same kernels held to 32 registers: 16 CTAs per SM instead of 12, for
+// thin chunks (see wave5_strip)
+__global__ void __launch_bounds__(128, 16) wave5_vec16(const __grid_constant__ KArgs a) {
+    wave5_body<false>(a, nullptr);
+}
+
+__global__ void __launch_bounds__(128, 16) wave5_halo16(const __grid_constant__ KArgs a, const __grid_constant__ HaloArgs hx) {
+    wave5_body<true>(a, &hx);
+}
+
 // ------------------------------------------------------------------ C5 Jacobi 7-point
 __device__ __forceinline__ float jac1(float c, float zm, float zp, float ym, float yp, float xm, float xp) {
     return 0.25f * c + 0.125f * (((zm + zp) + (ym + yp)) + (xm + xp));
@@ -1524,7 +1534,7 @@ int launch_rsim_fused(const KArgs& a, const PeerOut& po, cudaStream_t s) {
     return 1;
 }
 
-int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy) {
+int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy, bool* occ16_out) {
     const DAcc& U = a.acc[0];
     const DAcc& P = a.acc[1];
     const int64_t c0 = a.chunk.lo[1], w = a.chunk.hi[1] - c0;
@@ -1535,25 +1545,34 @@ int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy) {
     if (!vec || rows <= 0 || w <= 0) return 0;
     // strip height: 8 rows, lowered (>= 4) until the grid has about 8 waves
     // of resident CTAs (r02 sweep, tools/wave_strip.py: 16384 rows 478 us at
-    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits).  (A
-    // launch-time model picking h = 5 for 4096-row chunks to fill the last
-    // wave -- 15 waves instead of 9.2 -- measured 2% slower at 4 B200:
-    // short strips cost more than their partial last wave saves.)
-    static int occ = 0;
+    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits).  Thin
+    // chunks -- fewer than 8 waves of 8-row strips at 16 CTAs/SM, e.g. 4096
+    // rows at 4 GPUs -- run the 32-register variant at 16 CTAs/SM with the
+    // lower strip: 7812-7826 vs 7574-7664 steps/s at 4 B200; at 16384 rows it
+    // is 4% slower than 12 CTAs/SM (2002 vs 2082), so full chunks keep 12.
+    // (A launch-time model picking h = 5 for 4096 rows at 12 CTAs/SM measured
+    // 2% slower: short strips cost more than a partial last wave.)
+    static int occ = 0, occ16 = 0, force = -1;      // force: CEL_WAVE_OCC=12 / 16 (A/B), else -1
     if (occ == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wave5_vec, 128, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ16, wave5_vec16, 128, 0);
         if (occ < 1) occ = 1;
+        if (occ16 < occ) occ16 = occ;
+        const char* e = getenv("CEL_WAVE_OCC");
+        force = e ? (atoi(e) == 16 ? 16 : 12) : -1;
     }
     const int64_t cols = (w / 4 + 127) / 128;
-    const int64_t resident = int64_t(num_sms()) * occ;
-    int64_t h = (rows * cols) / (resident * 8);
+    const int64_t h16 = (rows * cols) / (int64_t(num_sms()) * occ16 * 8);
+    const bool use16 = force == 16 || (force < 0 && occ16 > occ && h16 < kWaveRows);
+    int64_t h = use16 ? h16 : (rows * cols) / (int64_t(num_sms()) * occ * 8);
     h = h < 4 ? 4 : (h > kWaveRows ? kWaveRows : h);
-    static int force = -1;
-    if (force < 0) {
+    if (occ16_out) *occ16_out = use16;
+    static int strip_force = -1;
+    if (strip_force < 0) {
         const char* e = getenv("CEL_WAVE_STRIP");           // A/B of the strip height
-        force = e ? atoi(e) : 0;
+        strip_force = e ? atoi(e) : 0;
     }
-    if (force > 0) h = force;
+    if (strip_force > 0) h = strip_force;
     *gx = unsigned(cols);
     *gy = unsigned((rows + h - 1) / h);
     return h;
@@ -1561,7 +1580,8 @@ int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy) {
 
 int launch_wave5_halo(const KArgs& a, const HaloArgs& hx, cudaStream_t s) {
     unsigned gx = 0, gy = 0;
-    const int64_t h = wave5_strip(a, &gx, &gy);
+    bool o16 = false;
+    const int64_t h = wave5_strip(a, &gx, &gy, &o16);
     if (h <= 0) return 0;
     KArgs b = a;
     b.strip = int(h);
@@ -1575,7 +1595,8 @@ int launch_wave5_halo(const KArgs& a, const HaloArgs& hx, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, wave5_halo, b, hx);
+    if (o16) cudaLaunchKernelEx(&cfg, wave5_halo16, b, hx);
+    else cudaLaunchKernelEx(&cfg, wave5_halo, b, hx);
     return 1;
 }
 
@@ -1599,7 +1620,8 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
     case K_WAVE5: {
         if (cv == 0) return 0;
         unsigned gx = 0, gy = 0;
-        const int64_t h = wave5_strip(a, &gx, &gy);
+        bool o16 = false;
+        const int64_t h = wave5_strip(a, &gx, &gy, &o16);
         if (h > 0) {
             KArgs b = a;
             b.strip = int(h);
@@ -1618,7 +1640,8 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             attr[0].val.programmaticStreamSerializationAllowed = 1;
             cfg.attrs = attr;
             cfg.numAttrs = pdl ? 1 : 0;
-            cudaLaunchKernelEx(&cfg, wave5_vec, b);
+            if (o16) cudaLaunchKernelEx(&cfg, wave5_vec16, b);
+            else cudaLaunchKernelEx(&cfg, wave5_vec, b);
         } else {
             wave5_scalar<<<grid_for(cv, 256), 256, 0, s>>>(a);
         }

@@ -239,7 +239,7 @@ struct HaloArgs {
 };
 // strip height and grid of the vectorised wave5 launch for this chunk (0 rows
 // if the vector kernel does not apply)
-int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy);
+int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy, bool* occ16 = nullptr);
 int launch_wave5_halo(const KArgs& a, const HaloArgs& h, cudaStream_t s);
 
 }  // namespace cel
