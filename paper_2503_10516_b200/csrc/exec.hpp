@@ -227,7 +227,7 @@ private:
         // grow [off, off + old_bytes) in place to new_bytes if the range right
         // after it is free; tok receives that range's completion token
         bool extend(uint64_t off, uint64_t old_bytes, uint64_t new_bytes, Token* tok);
-        void release(uint64_t off, uint64_t bytes, Token tok);
+        Token& release(uint64_t off, uint64_t bytes, Token tok);   // the coalesced free range's token
     };
     // VMM allocation: its own reserved VA range,
     // physical memory mapped in granules as the allocation grows in place
