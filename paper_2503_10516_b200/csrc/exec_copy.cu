@@ -141,9 +141,13 @@ void Executor::exec_copy(const Instr& ins) {
         const AllocRec& D = allocs_.at(ins.dst_aid);
         if (S.dev == D.dev && base_of(S) == base_of(D) && S.box.lo[0] == D.box.lo[0] && S.box.lo[1] == D.box.lo[1] &&
             S.box.lo[2] == D.box.lo[2] && S.box.extent(1) == D.box.extent(1) && S.box.extent(2) == D.box.extent(2)) {
-            // in-place growth: source and destination bytes coincide
+            // in-place growth: source and destination bytes coincide.  The
+            // copy's token is its dependencies'; a long one (other ranks'
+            // flags pile up along a chain of elided copies) folds into one
+            // event, or every later merge of it grows with the program
             st_.copies_elided++;
             st_.bytes_elided += rvolume(ins.region) * es;
+            if (deps.remote.size() > 8 || deps.local.size() > 16) deps = materialize(S.dev >= 0 ? S.dev : D.dev, deps);
             tok_[ins.iid] = deps;
             return;
         }
