@@ -1545,11 +1545,13 @@ int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy, bool* occ16_out)
     if (!vec || rows <= 0 || w <= 0) return 0;
     // strip height: 8 rows, lowered (>= 4) until the grid has about 8 waves
     // of resident CTAs (r02 sweep, tools/wave_strip.py: 16384 rows 478 us at
-    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits).  Thin
-    // chunks -- fewer than 8 waves of 8-row strips at 16 CTAs/SM, e.g. 4096
-    // rows at 4 GPUs -- run the 32-register variant at 16 CTAs/SM with the
-    // lower strip: 7812-7826 vs 7574-7664 steps/s at 4 B200; at 16384 rows it
-    // is 4% slower than 12 CTAs/SM (2002 vs 2082), so full chunks keep 12.
+    // h = 8 vs 494 at 16; neighbouring strips' halo rows are L2 hits).
+    // Chunks of fewer than ~20 waves of 8-row strips at 16 CTAs/SM (the
+    // multi-GPU chunks: 8192 / 5462 / 4096 rows at 2 / 3 / 4 GPUs) run the
+    // 32-register variant at 16 CTAs/SM, with the lower strip when that gives
+    // fewer than 8 waves: 4029 vs 3995 steps/s at 2 B200, 5892 vs 5834 at 3,
+    // 7812-7826 vs 7574-7664 at 4; the full 16384-row chunk (27.7 waves)
+    // keeps 12 CTAs/SM, where 16 is 4% slower (2002 vs 2082).
     // (A launch-time model picking h = 5 for 4096 rows at 12 CTAs/SM measured
     // 2% slower: short strips cost more than a partial last wave.)
     static int occ = 0, occ16 = 0, force = -1;      // force: CEL_WAVE_OCC=12 / 16 (A/B), else -1
@@ -1563,7 +1565,7 @@ int64_t wave5_strip(const KArgs& a, unsigned* gx, unsigned* gy, bool* occ16_out)
     }
     const int64_t cols = (w / 4 + 127) / 128;
     const int64_t h16 = (rows * cols) / (int64_t(num_sms()) * occ16 * 8);
-    const bool use16 = force == 16 || (force < 0 && occ16 > occ && h16 < kWaveRows);
+    const bool use16 = force == 16 || (force < 0 && occ16 > occ && h16 < 20);
     int64_t h = use16 ? h16 : (rows * cols) / (int64_t(num_sms()) * occ * 8);
     h = h < 4 ? 4 : (h > kWaveRows ? kWaveRows : h);
     if (occ16_out) *occ16_out = use16;
