@@ -40,6 +40,9 @@ def main():
     from paper_2503_10516_b200 import cel
     progs = [P.c1_chain(4096), P.wavesim(1024, 9, rows=700), P.nbody(3000, 2), P.nbody(500, 2, host_init=True),
              P.rsim(3000, 20), P.jacobi3d(40, 3)]
+    w2 = P.wavesim(512, 7, rows=300, split="2d", mapper="neighborhood_axes")
+    w2["name"] = "wavesim2d"
+    progs.append(w2)
     modes = args.modes.split(",")
     if args.only:
         progs = [p for p in progs if p["name"] == args.only]
