@@ -206,6 +206,10 @@ void Executor::exec_copy(const Instr& ins) {
                 // cudaMemcpy2DAsync rejects pitches above the device limit: those boxes
                 // stay on the copy kernel instead of poisoning the runtime
                 if (m.height > 1 && (m.spitch > max_pitch_ || m.dpitch > max_pitch_ || m.width > max_pitch_)) ok = false;
+                // narrow rows (a column halo of a 2-D tile: one element per row)
+                // are a descriptor per row for the copy engine: the copy kernel
+                // moves them a thread per row
+                if (m.height > 1 && m.width < 512) ok = false;
                 plan.push_back(m);
                 total += b.volume() * es;
             }
