@@ -143,6 +143,73 @@ static TaskDesc wave(int64_t n, int k) {
     return d;
 }
 
+// the hand-off as a ring of reused slots (CEL_PROF_QUEUE=3): the producer
+// copy-assigns into a free slot under the lock (vectors keep their capacity,
+// nothing is allocated per instruction), the consumer reads its slot in place
+struct RingSink : InstrSink {
+    static constexpr size_t kCap = 16384;
+    std::vector<Instr> ring = std::vector<Instr>(kCap);
+    size_t head = 0, tail = 0;
+    std::mutex m;
+    std::condition_variable cv, full;
+    bool stop = false, sleeping = false;
+    std::atomic<size_t> size{0};
+    uint64_t n = 0;
+    std::thread th;
+    RingSink() {
+        th = std::thread([this] {
+            for (;;) {
+                size_t h;
+                {
+                    std::unique_lock<std::mutex> l(m);
+                    if (head == tail) {
+                        l.unlock();
+                        for (int i = 0; i < 20000 && size.load(std::memory_order_acquire) == 0 && !stop; ++i) {
+                        }
+                        l.lock();
+                        while (head == tail && !stop) {
+                            sleeping = true;
+                            cv.wait(l);
+                            sleeping = false;
+                        }
+                        if (head == tail && stop) return;
+                    }
+                    h = head;
+                }
+                const Instr& x = ring[h];
+                asm volatile("" ::"r"(&x), "r"(x.deps.size()) : "memory");
+                ++n;
+                {
+                    std::lock_guard<std::mutex> g(m);
+                    head = (h + 1) % kCap;
+                    size.store((tail + kCap - head) % kCap, std::memory_order_release);
+                }
+                full.notify_one();
+            }
+        });
+    }
+    ~RingSink() {
+        {
+            std::lock_guard<std::mutex> g(m);
+            stop = true;
+        }
+        cv.notify_one();
+        th.join();
+    }
+    void on_instr(const Instr& ins) override {
+        bool wake;
+        {
+            std::unique_lock<std::mutex> l(m);
+            while ((tail + 1) % kCap == head) full.wait(l);
+            ring[tail] = ins;
+            tail = (tail + 1) % kCap;
+            size.store((tail + kCap - head) % kCap, std::memory_order_release);
+            wake = sleeping;
+        }
+        if (wake) cv.notify_one();
+    }
+};
+
 // RSim row t (programs.rsim_row): read rows [0,t) (fixed), write row t (remap kernel dim 0 -> dim 1)
 static TaskDesc rsim_row(int64_t W, int64_t t) {
     TaskDesc d;
@@ -172,8 +239,10 @@ static TaskDesc rsim_row(int64_t W, int64_t t) {
 static int rsim_main(int G, int rank, int T) {
     const int64_t W = 84000;
     Count count;
-    QueueSink* qs = getenv("CEL_PROF_QUEUE") ? new QueueSink : nullptr;
-    InstrSink* sk = qs ? static_cast<InstrSink*>(qs) : static_cast<InstrSink*>(&count);
+    const char* qe = getenv("CEL_PROF_QUEUE");
+    QueueSink* qs = qe && qe[0] != '3' ? new QueueSink : nullptr;
+    RingSink* rs = qe && qe[0] == '3' ? new RingSink : nullptr;
+    InstrSink* sk = qs ? static_cast<InstrSink*>(qs) : rs ? static_cast<InstrSink*>(rs) : static_cast<InstrSink*>(&count);
     struct { uint64_t n = 0; } sink;
     Scheduler s(G, 1, 4, true, sk, nullptr);
     if (rank >= 0) s.set_rank_filter(rank, G);
@@ -191,10 +260,12 @@ static int rsim_main(int G, int rank, int T) {
     s.wait();
     const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     sink.n = count.n;
-    printf("rsim G=%d rank=%d T=%d%s: %.2f us/row, %.1f instructions/row\n", G, rank, T, qs ? " (queue sink)" : "",
+    printf("rsim G=%d rank=%d T=%d%s: %.2f us/row, %.1f instructions/row\n", G, rank, T,
+           qs ? " (queue sink)" : rs ? " (ring sink)" : "",
            dt / (T - 1) * 1e6, double(sink.n) / (T - 1));
     s.shutdown();
     delete qs;
+    delete rs;
     return 0;
 }
 
