@@ -172,17 +172,21 @@ def main():
             "coll_groups": st1["coll_groups"] - st0["coll_groups"],
             "coll_allgathers": st1["coll_allgathers"] - st0["coll_allgathers"],
             "profile_ms": {k: {"ms": v[0], "launches": v[1]} for k, v in prof.items()}}
-    if args.workload == "jacobi3d":
+    if args.workload == "jacobi3d" and km > 0:   # (per-launch profiling off, CEL_BENCH_NOPROF: no roofline)
         cells = 1024 ** 3 / G
         line["roofline"] = {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_kind,
                             "achieved": 8 * cells / (km / 1e3 / steps) / 1e9,
                             "note": "rank-0 chunk; kernel time = interior + shell launch durations (they overlap, so this is a lower bound)"}
         line["roofline"]["frac"] = line["roofline"]["achieved"] / peak
-    elif args.workload == "nbody":
+    elif args.workload == "jacobi3d":
+        pass
+    elif args.workload == "nbody" and km > 0:
         inter = (1 << 20) * (1 << 20) / G * steps
         line["roofline"] = {"bound": "alu", "unit": "TFLOP/s", "peak": FP32_NOMINAL_TFLOPS,
                             "achieved": 20 * inter / (km / 1e3) / 1e12, "fast_math": args.fast_math}
         line["roofline"]["frac"] = line["roofline"]["achieved"] / FP32_NOMINAL_TFLOPS
+        line["interactions_per_s"] = (1 << 40) * steps / (ms / 1e3)
+    elif args.workload == "nbody":
         line["interactions_per_s"] = (1 << 40) * steps / (ms / 1e3)
     elif args.workload == "wavesim":
         line["split"] = args.split
