@@ -513,16 +513,16 @@ __device__ __forceinline__ void wait_flag32(const unsigned* f, unsigned v) {
     const long long t0 = clock64();
     while (int(ld_acquire_gpu32(f) - v) < 0) {
         __nanosleep(32);
-        if (clock64() - t0 > (1ll << 34)) __trap();
+        if (clock64() - t0 > (1ll << 37)) __trap();
     }
 }
-// spin until *f >= v; a flag that never comes traps after ~2^34 cycles (a
+// spin until *f >= v; a flag that never comes traps after ~2^37 cycles (~70 s: a
 // failed launch instead of a hung GPU)
 __device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long v) {
     const long long t0 = clock64();
     while (ld_acquire_sys(f) < v) {
         __nanosleep(64);
-        if (clock64() - t0 > (1ll << 34)) __trap();
+        if (clock64() - t0 > (1ll << 37)) __trap();
     }
 }
 
