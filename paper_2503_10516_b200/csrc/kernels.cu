@@ -784,6 +784,10 @@ __global__ void __launch_bounds__(512) jacobi7_tma(const __grid_constant__ CUten
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
+    // programmatic dependent launch (as wave5): the next step's prologue may
+    // overlap this grid's tail; the input planes come from the previous step
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __syncthreads();
     auto issue = [&](int i) {       // plane i (0 -> zs-1), clamped to the buffer extent
         int64_t z = zs - 1 + i;
@@ -1668,7 +1672,23 @@ int launch_workload(const KArgs& a, cudaStream_t s) {
             }
             dim3 grid{unsigned((w + kJBX - 1) / kJBX), unsigned((a.chunk.hi[1] - a.chunk.lo[1] + kJBY - 1) / kJBY),
                       unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kJZS - 1) / kJZS)};
-            jacobi7_tma<<<grid, 32 * kJBY, kJStages * kJStride * sizeof(float), s>>>(tm, a);
+            static int pdl = -1;
+            if (pdl < 0) {
+                const char* e = getenv("CEL_PDL");
+                pdl = (e && e[0] == '0') ? 0 : 1;
+            }
+            cudaLaunchConfig_t cfg;
+            memset(&cfg, 0, sizeof cfg);
+            cfg.gridDim = grid;
+            cfg.blockDim = dim3(32 * kJBY);
+            cfg.dynamicSmemBytes = size_t(kJStages) * kJStride * sizeof(float);
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = pdl ? 1 : 0;
+            cudaLaunchKernelEx(&cfg, jacobi7_tma, tm, a);
         } else if (vec) {
             dim3 grid(unsigned((w / 4 + 127) / 128), unsigned(a.chunk.hi[1] - a.chunk.lo[1]),
                       unsigned((a.chunk.hi[0] - a.chunk.lo[0] + kJacZ - 1) / kJacZ));
